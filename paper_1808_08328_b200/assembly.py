@@ -1,0 +1,228 @@
+"""Ten-block four-field assembly on the device (drop-in for dppflow.assembly).
+
+assemble() runs the sm_100a element kernels of csrc/assembly.cu (reference
+assembly.py:233-557) and returns a BlockSystem whose blocks live in HBM; the
+scipy views of the blocks (k1_uu, ...) are exported lazily on first access,
+so code written against the reference keeps working unchanged.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native as N
+from .device import BLOCK_NAMES, DeviceSystem
+from .elements import Formulation
+from .mesh import Mesh
+from .problem import BoundarySpec, DppParameters
+
+FIELDS = ("u1", "p1", "u2", "p2")
+FORM_QUAD_DEGREE = 2
+DATA_QUAD_DEGREE = 4
+_RHS_NAMES = ("f1_u", "f1_p", "f2_u", "f2_p")
+_LAZY = frozenset(BLOCK_NAMES + _RHS_NAMES)
+
+
+@dataclass
+class AssemblyStats:
+    wall_time_s: float
+    nnz: dict
+
+
+@dataclass
+class BlockSystem:
+    """Ten-block system with RHS segments (reference assembly.py:48-99).
+
+    Built by assemble(): blocks are device-resident (`_dev`) and exported to
+    scipy on first attribute access.  Built by the user from scipy blocks:
+    uploaded to the device on first solve.
+    """
+
+    formulation: Formulation
+    mesh: Mesh | None
+    params: DppParameters | None
+    k1_uu: sp.csr_matrix = None
+    k1_up: sp.csr_matrix = None
+    k1_pu: sp.csr_matrix = None
+    k1_pp: sp.csr_matrix = None
+    k2_uu: sp.csr_matrix = None
+    k2_up: sp.csr_matrix = None
+    k2_pu: sp.csr_matrix = None
+    k2_pp: sp.csr_matrix = None
+    k12_pp: sp.csr_matrix = None
+    k21_pp: sp.csr_matrix = None
+    f1_u: np.ndarray = None
+    f1_p: np.ndarray = None
+    f2_u: np.ndarray = None
+    f2_p: np.ndarray = None
+    stats: AssemblyStats | None = None
+    _dev: DeviceSystem | None = field(default=None, init=False, repr=False, compare=False)
+
+    def __getattribute__(self, name):
+        v = object.__getattribute__(self, name)
+        if v is None and name in _LAZY:
+            dev = object.__getattribute__(self, "_dev")
+            if dev is not None:
+                if name in _RHS_NAMES:
+                    v = dev.rhs(_RHS_NAMES.index(name))
+                else:
+                    v = dev.block(BLOCK_NAMES.index(name)).to_scipy()
+                object.__setattr__(self, name, v)
+        return v
+
+    @property
+    def field_sizes(self) -> dict:
+        dev = object.__getattribute__(self, "_dev")
+        if dev is not None and object.__getattribute__(self, "k1_uu") is None:
+            return dict(zip(FIELDS, dev.sizes))
+        return {"u1": self.k1_uu.shape[0], "p1": self.k1_pp.shape[0],
+                "u2": self.k2_uu.shape[0], "p2": self.k2_pp.shape[0]}
+
+    @property
+    def size(self) -> int:
+        return sum(self.field_sizes.values())
+
+    def index_sets(self) -> dict:
+        out, start = {}, 0
+        for name, n in self.field_sizes.items():
+            out[name] = np.arange(start, start + n)
+            start += n
+        return out
+
+    def block_table(self) -> dict:
+        return {("u1", "u1"): self.k1_uu, ("u1", "p1"): self.k1_up, ("p1", "u1"): self.k1_pu,
+                ("p1", "p1"): self.k1_pp, ("p1", "p2"): self.k12_pp, ("p2", "p1"): self.k21_pp,
+                ("u2", "u2"): self.k2_uu, ("u2", "p2"): self.k2_up, ("p2", "u2"): self.k2_pu,
+                ("p2", "p2"): self.k2_pp}
+
+    def rhs_segments(self) -> dict:
+        return {"u1": self.f1_u, "p1": self.f1_p, "u2": self.f2_u, "p2": self.f2_p}
+
+    def split_solution(self, x: np.ndarray) -> dict:
+        return {name: x[idx] for name, idx in self.index_sets().items()}
+
+    def device(self) -> DeviceSystem:
+        """The HBM copy of this system (uploaded from the scipy blocks on first use)."""
+        dev = object.__getattribute__(self, "_dev")
+        if dev is None:
+            blocks = [getattr(self, n) for n in BLOCK_NAMES]
+            sizes = [self.k1_uu.shape[0], self.k1_pp.shape[0], self.k2_uu.shape[0], self.k2_pp.shape[0]]
+            rhs = [getattr(self, n) for n in _RHS_NAMES]
+            dev = DeviceSystem.from_blocks(blocks, rhs, sizes)
+            object.__setattr__(self, "_dev", dev)
+        return dev
+
+
+def monolithic_view(block_system: BlockSystem):
+    """(K, f) in the (u1, p1, u2, p2) ordering (reference assembly.py:102-108).
+
+    K is built on the device (sp.bmat semantics: sorted, explicit zeros kept)
+    and returned as a scipy CSR matrix.
+    """
+    dev = block_system.device()
+    K = dev.monolithic().to_scipy()
+    f = np.concatenate([dev.rhs(i) for i in range(4)])
+    return K, f
+
+
+def _pressure_data(mesh: Mesh, bcs: BoundarySpec, net: int):
+    """Pressure facets of one network and p0 at their degree-4 quadrature points."""
+    bf = mesh.boundary_facets
+    vel = bcs.velocity_facets[net - 1]
+    if vel:
+        bf = bf[~np.isin(bf, np.fromiter(vel, dtype=np.int64))]
+    pf = N.i64(bf)
+    nq = C.c_int()
+    N.call("dpp_facet_rule_size", mesh.dim, N.KINDS[mesh.cell_kind.value], DATA_QUAD_DEGREE,
+           C.byref(nq))
+    X = np.empty((len(pf), nq.value, mesh.dim))
+    if len(pf):
+        N.call("dpp_facet_points", N.ctx(), mesh._h, DATA_QUAD_DEGREE, len(pf), N.ptr(pf),
+               N.ptr(X), None)
+    p0 = N.f64(np.asarray(bcs.p_data[net - 1](X.reshape(-1, mesh.dim)), dtype=float)
+               .reshape(len(pf), nq.value))
+    return pf, p0
+
+
+def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec | None,
+             workers: int = 1, pressure_dirichlet: str = "weak") -> BlockSystem:
+    """Device assembly (reference assembly.py:564-566).  `workers` is accepted
+    for API compatibility; the device assembles all cells at once."""
+    t0 = time.perf_counter()
+    form = Formulation(formulation)
+    gb = np.asarray(params.gamma_b, dtype=float)
+    if gb.shape != (mesh.dim,):
+        raise ValueError("gamma_b dimension does not match the mesh")
+    if pressure_dirichlet not in ("weak", "strong"):
+        raise ValueError("pressure_dirichlet must be 'weak' or 'strong'")
+    if pressure_dirichlet == "strong":
+        raise NotImplementedError("strong pressure elimination is not implemented on the device yet")
+    p = N.Params(params.mu, params.beta, params.k1, params.k2, params.eta_u, params.eta_p,
+                 (C.c_double * 3)(*(list(gb) + [0.0] * (3 - len(gb)))))
+    keep = []
+    bcp = None
+    if bcs is not None:
+        if any(len(v) for v in bcs.velocity_facets):
+            raise NotImplementedError("prescribed-velocity boundary facets are not implemented on the device yet")
+        bc = N.Bc()
+        for net in (1, 2):
+            pf, p0 = _pressure_data(mesh, bcs, net)
+            keep += [pf, p0]
+            bc.n_pfacets[net - 1] = len(pf)
+            bc.pfacets[net - 1] = pf.ctypes.data
+            bc.p0[net - 1] = p0.ctypes.data
+        bcp = C.byref(bc)
+    h = C.c_void_p()
+    N.call("dpp_assemble", N.ctx(), mesh._h, N.FORMS[form.value], C.byref(p), bcp, C.byref(h))
+    dev = DeviceSystem(h)
+    bs = BlockSystem(formulation=form, mesh=mesh, params=params)
+    object.__setattr__(bs, "_dev", dev)
+    wall = time.perf_counter() - t0
+    bs.stats = AssemblyStats(wall_time_s=wall, nnz=_DeviceNnz(dev))
+    return bs
+
+
+class _DeviceNnz(dict):
+    """nnz per block, read from the device lazily (AssemblyStats.nnz)."""
+
+    def __init__(self, dev):
+        super().__init__()
+        self._dev = dev
+
+    def _fill(self):
+        if not super().__len__():
+            for i, n in enumerate(BLOCK_NAMES):
+                super().__setitem__(n, self._dev.block(i).nnz)
+
+    def __getitem__(self, k):
+        self._fill()
+        return super().__getitem__(k)
+
+    def items(self):
+        self._fill()
+        return super().items()
+
+    def keys(self):
+        self._fill()
+        return super().keys()
+
+    def values(self):
+        self._fill()
+        return super().values()
+
+    def __iter__(self):
+        self._fill()
+        return super().__iter__()
+
+    def __len__(self):
+        self._fill()
+        return super().__len__()
+
+
+def solution_fields(block_system: BlockSystem, x: np.ndarray) -> dict:
+    return block_system.split_solution(x)

@@ -1,0 +1,356 @@
+// Smoothed-aggregation AMG on the device.
+//
+// Reference: linalg.amg_setup / _strength_aggregates / _jacobi_spectral_radius /
+// _vcycle (linalg.py:279-400).
+//  setup per level:  strength graph |a_ij| >= theta*max_k!=i |a_ik| (device),
+//                    3-pass greedy aggregation in row order (exact; see aggregate()),
+//                    rho(D^-1 A) by 10 power iterations from the reference's start
+//                    vector (device SpMV + norms), P = P0 - (2w/rho) D^-1 (A P0)
+//                    with scipy's rounding (device), A_c = (P^T A) P (device SpGEMM),
+//                    D+L / D+U sweeps for SGS, dense inverse of the coarsest operator.
+//  apply:            V(1,1) with SGS (forward then backward GS as x += T^-1 (b - A x)),
+//                    restriction P^T, prolongation P, coarse dense solve.
+#include <cmath>
+
+#include "dpp_internal.cuh"
+
+namespace dpp {
+
+// ---------------------------------------------------------------- strength graph
+__global__ void k_strength(int rows, const int *ptr, const int *idx, const double *val,
+                           double theta, const int *optr, int *cnt, int *oidx) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int s = ptr[r], e = ptr[r + 1];
+        double mx = -1.0;
+        for (int p = s + lane; p < e; p += 32)
+            if (idx[p] != r) mx = fmax(mx, fabs(val[p]));
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const double thr = theta * mx;
+        int w = optr ? optr[r] : 0, n = 0;
+        for (int base = s; base < e; base += 32) {
+            const int p = base + lane;
+            const bool keep = mx >= 0.0 && p < e && idx[p] != r && fabs(val[p]) >= thr;
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep && oidx) oidx[w + __popc(m & ((1u << lane) - 1))] = idx[p];
+            w += __popc(m);
+            n += __popc(m);
+        }
+        if (lane == 0 && cnt) cnt[r] = n;
+    }
+}
+
+// Greedy aggregation (linalg.py:301-323), exact sequential semantics on the
+// host from the device-built strength graph: pass 1 seeds nodes whose closed
+// strong neighbourhood is still free, pass 2 attaches leftovers to the first
+// aggregated strong neighbour (in stored order, seeing pass-2 assignments of
+// earlier rows), pass 3 makes singletons.
+static int64_t greedy(int n, const std::vector<int> &sp, const std::vector<int> &si,
+                      std::vector<int64_t> &agg) {
+    agg.assign(n, -1);
+    int64_t next = 0;
+    for (int i = 0; i < n; ++i) {
+        if (agg[i] != -1) continue;
+        bool free_nb = true;
+        for (int p = sp[i]; p < sp[i + 1] && free_nb; ++p) free_nb = agg[si[p]] == -1;
+        if (!free_nb) continue;
+        agg[i] = next;
+        for (int p = sp[i]; p < sp[i + 1]; ++p) agg[si[p]] = next;
+        ++next;
+    }
+    for (int i = 0; i < n; ++i) {
+        if (agg[i] != -1) continue;
+        for (int p = sp[i]; p < sp[i + 1]; ++p)
+            if (agg[si[p]] != -1) { agg[i] = agg[si[p]]; break; }
+    }
+    for (int i = 0; i < n; ++i)
+        if (agg[i] == -1) agg[i] = next++;
+    return next;
+}
+
+static int64_t aggregate(Ctx *c, const Csr &A, double theta, std::vector<int64_t> &agg) {
+    const int n = A.rows;
+    DBuf<int> cnt(n, c->s);
+    const int grid = grid_for((int64_t)n * 32, 256, c->sms, 8);
+    k_strength<<<grid, 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, theta, nullptr, cnt.p, nullptr);
+    launched(c);
+    DBuf<int> sptr;
+    int64_t snnz = counts_to_ptr(c, cnt.p, n, sptr);
+    DBuf<int> sidx(snnz, c->s);
+    k_strength<<<grid, 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, theta, sptr.p, nullptr, sidx.p);
+    launched(c);
+    std::vector<int> hp = sptr.to_host(), hi = sidx.to_host();
+    return greedy(n, hp, hi, agg);
+}
+
+// ---------------------------------------------------------------- P construction
+// P = P0 - damping * (Dinv @ (A @ P0)) with scipy's rounding:
+//   w = fl(dinv_i * y_ij), dw = fl(damping * w), p = fl(p0 - dw), zeros dropped.
+__global__ void k_build_p(int rows, const int *yp, const int *yi, const double *yv,
+                          const int *agg, const double *dinv, double damping, const int *optr,
+                          int *cnt, int *oi, double *ov) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        const int a = agg[r];
+        int w = optr ? optr[r] : 0, n = 0;
+        bool seen = false;
+        auto emit = [&](int j, double v) {
+            if (v == 0.0) return;
+            if (oi) { oi[w] = j; ov[w] = v; ++w; }
+            ++n;
+        };
+        for (int p = yp[r]; p < yp[r + 1]; ++p) {
+            const int j = yi[p];
+            if (!seen && j > a) { emit(a, 1.0); seen = true; }
+            const double dw = __dmul_rn(damping, __dmul_rn(dinv[r], yv[p]));
+            if (j == a) { emit(j, __dsub_rn(1.0, dw)); seen = true; }
+            else emit(j, -dw);
+        }
+        if (!seen) emit(a, 1.0);
+        if (cnt) cnt[r] = n;
+    }
+}
+
+__global__ void k_p0(int rows, const int *agg, int *ptr, int *idx, double *val) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= rows; r += gridDim.x * blockDim.x) {
+        ptr[r] = r;
+        if (r < rows) { idx[r] = agg[r]; val[r] = 1.0; }
+    }
+}
+
+__global__ void k_recip(int n, const double *d, double *o) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) o[r] = 1.0 / d[r];
+}
+
+// M = diag(dinv) @ A  (row scaling, exact products)
+__global__ void k_rowscale(int rows, const int *ptr, const double *val, const double *dinv, double *o) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) o[p] = __dmul_rn(dinv[r], val[p]);
+}
+
+static double spectral_radius(Ctx *c, const Csr &A, const double *dinv, dpp_randn_fn randn,
+                              void *user) {
+    const int n = A.rows;
+    Csr M = csr_copy(c, A);
+    k_rowscale<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, M.ptr.p, A.val.p, dinv, M.val.p);
+    launched(c);
+    std::vector<double> x0(n);
+    if (!randn) DPP_FAIL(DPP_ERR_VALUE, "amg_setup needs the power-iteration start vector callback");
+    randn(n, x0.data(), user);
+    DBuf<double> x(n, c->s), y(n, c->s), nr(12, c->s);
+    x.upload(x0.data(), n);
+    norm2_dev(c, n, x.p, nr.p);
+    scale_by_dev(c, n, x.p, nr.p, x.p);
+    for (int it = 1; it <= 10; ++it) {
+        spmv(c, M, x.p, y.p);
+        norm2_dev(c, n, y.p, nr.p + it);
+        scale_by_dev(c, n, y.p, nr.p + it, x.p);
+    }
+    spmv(c, M, x.p, y.p);
+    norm2_dev(c, n, y.p, nr.p + 11);
+    std::vector<double> h = nr.to_host();
+    for (int it = 1; it <= 10; ++it)
+        if (h[it] == 0.0) return 1.0;
+    return std::max(h[11], 1e-8);
+}
+
+// ---------------------------------------------------------------- dense coarse solve
+__global__ void k_to_dense(int n, const int *ptr, const int *idx, const double *val, double *D) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) D[(int64_t)r * n + idx[p]] += val[p];
+}
+
+// LU with partial pivoting (first maximal |pivot|, as LAPACK idamax) and explicit
+// inverse, one block.  n is small (<= max_coarse unless aggregation stalls).
+__global__ void __launch_bounds__(256) k_dense_inverse(int n, double *A, int *perm, double *Ainv) {
+    __shared__ double smax[256];
+    __shared__ int sarg[256];
+    const int t = threadIdx.x;
+    for (int i = t; i < n; i += blockDim.x) perm[i] = i;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        double best = -1.0;
+        int arg = k;
+        for (int r = k + t; r < n; r += blockDim.x) {
+            const double v = fabs(A[(int64_t)r * n + k]);
+            if (v > best) { best = v; arg = r; }
+        }
+        smax[t] = best;
+        sarg[t] = arg;
+        __syncthreads();
+        for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+            if (t < o) {
+                if (smax[t + o] > smax[t] || (smax[t + o] == smax[t] && sarg[t + o] < sarg[t])) {
+                    smax[t] = smax[t + o];
+                    sarg[t] = sarg[t + o];
+                }
+            }
+            __syncthreads();
+        }
+        const int p = sarg[0];
+        __syncthreads();
+        if (p != k) {
+            for (int j = t; j < n; j += blockDim.x) {
+                const double tmp = A[(int64_t)k * n + j];
+                A[(int64_t)k * n + j] = A[(int64_t)p * n + j];
+                A[(int64_t)p * n + j] = tmp;
+            }
+            if (t == 0) { int q = perm[k]; perm[k] = perm[p]; perm[p] = q; }
+        }
+        __syncthreads();
+        const double piv = A[(int64_t)k * n + k];
+        for (int r = k + 1 + t; r < n; r += blockDim.x) A[(int64_t)r * n + k] /= piv;
+        __syncthreads();
+        const int m = n - k - 1;
+        for (int64_t q = t; q < (int64_t)m * m; q += blockDim.x) {
+            const int r = k + 1 + (int)(q / m), cc = k + 1 + (int)(q % m);
+            A[(int64_t)r * n + cc] -= A[(int64_t)r * n + k] * A[(int64_t)k * n + cc];
+        }
+        __syncthreads();
+    }
+    // column c of the inverse: solve L U x = P e_c (row i of P e_c is [perm[i] == c])
+    for (int cidx = t; cidx < n; cidx += blockDim.x) {
+        for (int i = 0; i < n; ++i) {
+            double s = perm[i] == cidx ? 1.0 : 0.0;
+            for (int j = 0; j < i; ++j) s -= A[(int64_t)i * n + j] * Ainv[(int64_t)j * n + cidx];
+            Ainv[(int64_t)i * n + cidx] = s;
+        }
+        for (int i = n - 1; i >= 0; --i) {
+            double s = Ainv[(int64_t)i * n + cidx];
+            for (int j = i + 1; j < n; ++j) s -= A[(int64_t)i * n + j] * Ainv[(int64_t)j * n + cidx];
+            Ainv[(int64_t)i * n + cidx] = s / A[(int64_t)i * n + i];
+        }
+    }
+}
+
+__global__ void k_gemv(int n, const double *M, const double *x, double *y) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double s = 0.0;
+        for (int j = lane; j < n; j += 32) s += M[r * n + j] * x[j];
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) y[r] = s;
+    }
+}
+
+static void coarse_setup(Ctx *c, Amg &h, const Csr &A) {
+    const int n = A.rows;
+    h.nc = n;
+    DBuf<double> D((size_t)n * n, c->s);
+    DBuf<int> perm(n, c->s);
+    h.coarse_inv.alloc((size_t)n * n, c->s);
+    if (!n) return;
+    CK(cudaMemsetAsync(D.p, 0, sizeof(double) * n * n, c->s));
+    k_to_dense<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, D.p);
+    launched(c);
+    k_dense_inverse<<<1, 256, 0, c->s>>>(n, D.p, perm.p, h.coarse_inv.p);
+    launched(c);
+    CK(cudaStreamSynchronize(c->s));
+}
+
+// ---------------------------------------------------------------- setup
+std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega, int max_coarse,
+                               int max_levels, dpp_randn_fn randn, void *user) {
+    if (A0.rows != A0.cols) DPP_FAIL(DPP_ERR_VALUE, "amg_setup requires a square matrix");
+    auto h = std::make_unique<Amg>();
+    h->ctx = c;
+    {
+        DBuf<double> d(A0.rows, c->s);
+        csr_diag(c, A0, d.p, nullptr);
+        std::vector<double> hd = d.to_host();
+        for (double v : hd)
+            if (v == 0.0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "structurally singular input: zero diagonal entry");
+    }
+    Csr cur = csr_copy(c, A0);
+    while (cur.rows > max_coarse && (int)h->lv.size() < max_levels - 1) {
+        auto L = std::make_unique<AmgLevel>();
+        const int n = cur.rows;
+        int64_t nc = aggregate(c, cur, theta, L->agg);
+        if (nc >= n) {
+            if (n > 5000) DPP_FAIL(DPP_ERR_RUNTIME, "aggregation stalled on a large operator");
+            break;
+        }
+        DBuf<double> d(n, c->s), dinv(n, c->s);
+        csr_diag(c, cur, d.p, nullptr);
+        k_recip<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d.p, dinv.p);
+        launched(c);
+        L->rho = spectral_radius(c, cur, dinv.p, randn, user);
+        const double damping = 2.0 * omega / L->rho;
+        std::vector<int> agg32(L->agg.begin(), L->agg.end());
+        DBuf<int> dagg(n, c->s);
+        dagg.upload(agg32.data(), n);
+        Csr P0;
+        P0.alloc(n, (int)nc, n, c->s);
+        k_p0<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(n, dagg.p, P0.ptr.p, P0.idx.p, P0.val.p);
+        launched(c);
+        Csr Y = spgemm(c, cur, P0, nullptr, false, nullptr);
+        DBuf<int> cnt(n, c->s);
+        k_build_p<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, Y.ptr.p, Y.idx.p, Y.val.p, dagg.p,
+                                                             dinv.p, damping, nullptr, cnt.p, nullptr,
+                                                             nullptr);
+        launched(c);
+        L->P.rows = n;
+        L->P.cols = (int)nc;
+        L->P.nnz = counts_to_ptr(c, cnt.p, n, L->P.ptr);
+        L->P.idx.alloc(L->P.nnz, c->s);
+        L->P.val.alloc(L->P.nnz, c->s);
+        k_build_p<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, Y.ptr.p, Y.idx.p, Y.val.p, dagg.p,
+                                                             dinv.p, damping, L->P.ptr.p, nullptr,
+                                                             L->P.idx.p, L->P.val.p);
+        launched(c);
+        L->R = csr_transpose(c, L->P);
+        Csr T = spgemm(c, L->R, cur, nullptr, false, nullptr);
+        Csr next = spgemm(c, T, L->P, nullptr, false, nullptr);
+        L->lo = make_tri(c, cur, true, false);
+        L->up = make_tri(c, cur, false, false);
+        L->A = std::move(cur);
+        for (DBuf<double> *b : {&L->b, &L->x, &L->r, &L->t, &L->y}) b->alloc(n, c->s);
+        L->ticket.alloc(4, c->s);
+        h->lv.push_back(std::move(L));
+        cur = std::move(next);
+        CK(cudaStreamSynchronize(c->s));
+    }
+    auto last = std::make_unique<AmgLevel>();
+    coarse_setup(c, *h, cur);
+    const int n = cur.rows;
+    for (DBuf<double> *b : {&last->b, &last->x}) b->alloc(n, c->s);
+    last->A = std::move(cur);
+    h->lv.push_back(std::move(last));
+    CK(cudaStreamSynchronize(c->s));
+    return h;
+}
+
+// ---------------------------------------------------------------- V(1,1) cycle
+static void vc(Ctx *c, Amg &h, size_t l, const double *b, double *xo, cudaStream_t st) {
+    AmgLevel &L = *h.lv[l];
+    const int n = L.A.rows;
+    if (l + 1 == h.lv.size()) {
+        if (n) {
+            k_gemv<<<grid_for((int64_t)n * 32, 128, c->sms, 4), 128, 0, st>>>(n, h.coarse_inv.p, b, xo);
+            launched(c);
+        }
+        return;
+    }
+    AmgLevel &C = *h.lv[l + 1];
+    // pre-smoothing, x starts at 0: x1 = (D+L)^-1 b ; x2 = x1 + (D+U)^-1 (b - A x1)
+    trsv(c, L.lo, b, L.x.p, L.ticket.p, nullptr, nullptr, st);
+    spmv(c, L.A, L.x.p, L.r.p, b, -1.0, st);
+    trsv(c, L.up, L.r.p, L.y.p, L.ticket.p + 1, L.x.p, L.t.p, st);
+    // restriction of the residual, coarse correction, prolongation
+    spmv(c, L.A, L.t.p, L.r.p, b, -1.0, st);
+    spmv(c, L.R, L.r.p, C.b.p, nullptr, 1.0, st);
+    vc(c, h, l + 1, C.b.p, C.x.p, st);
+    spmv(c, L.P, C.x.p, L.x.p, L.t.p, 1.0, st);
+    // post-smoothing
+    spmv(c, L.A, L.x.p, L.r.p, b, -1.0, st);
+    trsv(c, L.lo, L.r.p, L.y.p, L.ticket.p + 2, L.x.p, L.t.p, st);
+    spmv(c, L.A, L.t.p, L.r.p, b, -1.0, st);
+    trsv(c, L.up, L.r.p, L.y.p, L.ticket.p + 3, L.t.p, xo, st);
+}
+
+void amg_vcycle(Ctx *c, Amg &h, const double *r, double *z, cudaStream_t st) {
+    vc(c, h, 0, r, z, st ? st : c->s);
+}
+
+}  // namespace dpp

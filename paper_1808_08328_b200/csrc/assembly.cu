@@ -1,0 +1,1186 @@
+// Device assembly of the ten-block four-field DPP systems.
+//
+// Reference: assembly.assemble_hdiv / _vms_cell_blocks / assemble_cgvms /
+// assemble_dgvms / _Coo (assembly.py:123-147, :233-557).
+//
+// Pattern: every formulation is a Kronecker expansion of a scalar "node graph"
+// G (CG: vertices, DG: cell-local nodes, H(div): facets).  The local couplings
+// (cell pairs (a,b), DG interior-facet side pairs) are emitted as 64-bit keys
+// in the reference's COO insertion order and stably radix-sorted, so G (with
+// explicit zeros, sorted columns) is bit-identical to scipy's pattern and each
+// G entry owns its list of contributions in insertion order.
+// Values: one thread per G entry walks its contribution list, recomputes each
+// cell's (or facet's) local integral in FP64 and writes the entries of all
+// blocks that the entry expands to (deterministic segmented sum, no atomics).
+// H(div) follows the reference's einsum order bitwise (needed: its AMG setup is
+// ulp-sensitive).
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cmath>
+
+#include "abi_guard.cuh"
+#include "mesh.h"
+#include "system.cuh"
+
+namespace dpp {
+
+// ------------------------------------------------------------------ rules
+struct Rule {
+    int nq = 0, rdim = 0;
+    double p[27][3] = {};
+    double w[27] = {};
+};
+
+static const double GL_T[5][4] = {
+    {0}, {0x1.0000000000000p-1},
+    {0x1.b0cb174df99c8p-3, 0x1.93cd3a2c8198ep-1},
+    {0x1.cda042f0236e0p-4, 0x1.0000000000000p-1, 0x1.c64bf7a1fb924p-1},
+    {0x1.1c6490c2719ecp-4, 0x1.51ee013116102p-2, 0x1.5708ff6774f7fp-1, 0x1.dc736de7b1cc2p-1}};
+static const double GL_W[5][4] = {
+    {0}, {0x1.0000000000000p+0},
+    {0x1.0000000000000p-1, 0x1.0000000000000p-1},
+    {0x1.1c71c71c71c73p-2, 0x1.c71c71c71c71cp-2, 0x1.1c71c71c71c73p-2},
+    {0x1.64340f7e7b666p-3, 0x1.4de5f840c24cdp-2, 0x1.4de5f840c24cdp-2, 0x1.64340f7e7b666p-3}};
+
+// elements.quadrature_rule (elements.py:175-221) for the degrees used here
+static Rule cell_rule(int kind, int degree) {
+    Rule r;
+    degree = std::max(degree, 1);
+    const int dim = kind_dim(kind);
+    r.rdim = dim;
+    if (kind == DPP_QUAD || kind == DPP_HEX) {
+        const int n = (degree + 2) / 2;   // ceil((degree+1)/2)
+        if (n > 4) throw Error(DPP_ERR_VALUE, "quadrature degree too high");
+        int q = 0;
+        if (dim == 2) {
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j, ++q) {
+                    r.p[q][0] = GL_T[n][i]; r.p[q][1] = GL_T[n][j];
+                    r.w[q] = 1.0 * GL_W[n][i] * GL_W[n][j];
+                }
+        } else {
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j)
+                    for (int k = 0; k < n; ++k, ++q) {
+                        r.p[q][0] = GL_T[n][i]; r.p[q][1] = GL_T[n][j]; r.p[q][2] = GL_T[n][k];
+                        r.w[q] = 1.0 * GL_W[n][i] * GL_W[n][j] * GL_W[n][k];
+                    }
+        }
+        r.nq = q;
+        return r;
+    }
+    if (kind == DPP_TRI) {
+        if (degree == 1) { r.nq = 1; r.p[0][0] = r.p[0][1] = 1.0 / 3; r.w[0] = 0.5; return r; }
+        if (degree == 2) {
+            const double pts[3][2] = {{1.0 / 6, 1.0 / 6}, {2.0 / 3, 1.0 / 6}, {1.0 / 6, 2.0 / 3}};
+            r.nq = 3;
+            for (int q = 0; q < 3; ++q) { r.p[q][0] = pts[q][0]; r.p[q][1] = pts[q][1]; r.w[q] = 1.0 / 6; }
+            return r;
+        }
+        const int n = (degree + 3) / 2;   // ceil((degree+2)/2)
+        int q = 0;
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < n; ++j, ++q) {
+                const double u = GL_T[n][i], v = GL_T[n][j];
+                r.p[q][0] = u;
+                r.p[q][1] = v * (1 - u);
+                r.w[q] = GL_W[n][i] * GL_W[n][j] * (1 - u);
+            }
+        r.nq = q;
+        return r;
+    }
+    // TET
+    if (degree == 1) { r.nq = 1; r.p[0][0] = r.p[0][1] = r.p[0][2] = 0.25; r.w[0] = 1.0 / 6; return r; }
+    if (degree == 2) {
+        const double a = (5.0 + 3.0 * std::sqrt(5.0)) / 20.0, b = (5.0 - std::sqrt(5.0)) / 20.0;
+        const double pts[4][3] = {{a, b, b}, {b, a, b}, {b, b, a}, {b, b, b}};
+        r.nq = 4;
+        for (int q = 0; q < 4; ++q) {
+            for (int d = 0; d < 3; ++d) r.p[q][d] = pts[q][d];
+            r.w[q] = 1.0 / 24;
+        }
+        return r;
+    }
+    throw Error(DPP_ERR_VALUE, "TET cell rules above degree 2 are not needed on the hot path");
+}
+
+// facet reference rule (assembly.py:161-170): 2D Gauss on [0,1]; TET faces: TRI
+// rule (ref measure 1/2); HEX faces: QUAD rule
+static Rule facet_rule(int kind, int degree, double &ref_measure) {
+    const int dim = kind_dim(kind);
+    if (dim == 2) {
+        Rule r;
+        const int n = (degree + 2) / 2;   // ceil((degree+1)/2)
+        r.nq = n;
+        r.rdim = 1;
+        for (int q = 0; q < n; ++q) { r.p[q][0] = GL_T[n][q]; r.w[q] = GL_W[n][q]; }
+        ref_measure = 1.0;
+        return r;
+    }
+    if (kind == DPP_TET) { ref_measure = 0.5; return cell_rule(DPP_TRI, degree); }
+    ref_measure = 1.0;
+    return cell_rule(DPP_QUAD, degree);
+}
+
+// ------------------------------------------------------------------ element tables
+struct Elem {
+    int kind, dim, nn, nq;
+    double w[8];
+    double N[8][8];       // [q][a]
+    double G[8][8][3];    // [q][a][j] reference gradients
+    double Mref[8][8];    // sum_q w N_a N_b
+    double wsum;
+};
+
+__host__ __device__ inline void scalar_basis(int kind, int dim, const double *x, double *N, double *G) {
+    if (kind == DPP_TRI || kind == DPP_TET) {
+        double s = x[0];
+        for (int d = 1; d < dim; ++d) s += x[d];
+        N[0] = 1.0 - s;
+        for (int d = 0; d < dim; ++d) N[d + 1] = x[d];
+        if (G) {
+            for (int j = 0; j < dim; ++j) G[j] = -1.0;
+            for (int a = 1; a <= dim; ++a)
+                for (int j = 0; j < dim; ++j) G[a * 3 + j] = (a - 1 == j) ? 1.0 : 0.0;
+        }
+        return;
+    }
+    const int nd = 1 << dim;
+    for (int a = 0; a < nd; ++a) {
+        double v = 1.0;
+        double g[3] = {1.0, 1.0, 1.0};
+        for (int ax = 0; ax < dim; ++ax) {
+            const int s = (a >> ax) & 1;
+            const double f = s ? x[ax] : 1.0 - x[ax];
+            const double df = s ? 1.0 : -1.0;
+            v *= f;
+            for (int o = 0; o < dim; ++o) g[o] *= (o == ax) ? df : f;
+        }
+        N[a] = v;
+        if (G)
+            for (int o = 0; o < dim; ++o) G[a * 3 + o] = g[o];
+    }
+}
+
+static Elem make_elem(int kind) {
+    Elem e{};
+    e.kind = kind;
+    e.dim = kind_dim(kind);
+    e.nn = kind_nodes(kind);
+    Rule r = cell_rule(kind, 2);
+    e.nq = r.nq;
+    double ws = 0.0;
+    for (int q = 0; q < r.nq; ++q) {
+        e.w[q] = r.w[q];
+        ws += r.w[q];
+        scalar_basis(kind, e.dim, r.p[q], e.N[q], &e.G[q][0][0]);
+    }
+    e.wsum = ws;
+    for (int a = 0; a < e.nn; ++a)
+        for (int b = 0; b < e.nn; ++b) {
+            double s = 0.0;
+            for (int q = 0; q < e.nq; ++q) s += e.w[q] * e.N[q][a] * e.N[q][b];
+            e.Mref[a][b] = s;
+        }
+    return e;
+}
+
+// ------------------------------------------------------------------ device mesh
+struct DevMesh {
+    Ctx *c = nullptr;
+    int dim = 0, kind = 0, nn = 0, nf = 0, nvf = 0;
+    int64_t V = 0, C = 0, F = 0;
+    DBuf<double> verts, det, Jinv;
+    DBuf<int> cells, cf, fv, fplus, fminus;
+    DBuf<signed char> cs;
+    DBuf<double> fn, fm;
+};
+
+// J (mesh.py:175-183) and J^-1 by LU with partial pivoting (numpy.linalg.inv)
+__global__ void k_geom(int64_t C, int dim, int kind, int nn, const double *V, const int *cells,
+                       double *Jinv) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+        double a[9] = {0}, inv[9] = {0};
+        const int *cv = cells + c * nn;
+        if (kind == DPP_TRI || kind == DPP_TET) {
+            for (int k = 0; k < dim; ++k)
+                for (int d = 0; d < dim; ++d) a[d * dim + k] = V[(int64_t)cv[k + 1] * dim + d] - V[(int64_t)cv[0] * dim + d];
+        } else {
+            for (int d = 0; d < dim; ++d) a[d * dim + d] = V[(int64_t)cv[nn - 1] * dim + d] - V[(int64_t)cv[0] * dim + d];
+        }
+        int perm[3] = {0, 1, 2};
+        for (int k = 0; k < dim; ++k) {
+            int p = k;
+            double best = fabs(a[k * dim + k]);
+            for (int r = k + 1; r < dim; ++r)
+                if (fabs(a[r * dim + k]) > best) { best = fabs(a[r * dim + k]); p = r; }
+            if (p != k) {
+                for (int cc = 0; cc < dim; ++cc) { double t = a[k * dim + cc]; a[k * dim + cc] = a[p * dim + cc]; a[p * dim + cc] = t; }
+                int t = perm[k]; perm[k] = perm[p]; perm[p] = t;
+            }
+            const double rp = 1.0 / a[k * dim + k];
+            for (int r = k + 1; r < dim; ++r) {
+                const double l = __dmul_rn(a[r * dim + k], rp);
+                a[r * dim + k] = l;
+                for (int cc = k + 1; cc < dim; ++cc) a[r * dim + cc] = __dsub_rn(a[r * dim + cc], __dmul_rn(l, a[k * dim + cc]));
+            }
+        }
+        for (int col = 0; col < dim; ++col) {
+            double y[3];
+            for (int i = 0; i < dim; ++i) {
+                double s = perm[i] == col ? 1.0 : 0.0;
+                for (int j = 0; j < i; ++j) s = __dsub_rn(s, __dmul_rn(a[i * dim + j], y[j]));
+                y[i] = s;
+            }
+            for (int i = dim - 1; i >= 0; --i) {
+                double s = y[i];
+                for (int j = i + 1; j < dim; ++j) s = __dsub_rn(s, __dmul_rn(a[i * dim + j], y[j]));
+                y[i] = s / a[i * dim + i];
+            }
+            for (int i = 0; i < dim; ++i) inv[i * dim + col] = y[i];
+        }
+        for (int k = 0; k < dim * dim; ++k) Jinv[c * dim * dim + k] = inv[k];
+    }
+}
+
+static DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
+    if (m.dev && m.dev->c == c) return *m.dev;
+    auto d = std::make_shared<DevMesh>();
+    d->c = c;
+    d->dim = m.dim;
+    d->kind = m.kind;
+    d->nn = kind_nodes(m.kind);
+    d->nf = kind_facets(m.kind);
+    d->nvf = kind_facet_nodes(m.kind);
+    d->V = m.n_vertices;
+    d->C = m.n_cells;
+    d->F = m.n_facets;
+    auto up32 = [&](DBuf<int> &b, const std::vector<int64_t> &v) {
+        std::vector<int> t(v.begin(), v.end());
+        b.alloc(t.size(), c->s);
+        b.upload(t.data(), t.size());
+        CK(cudaStreamSynchronize(c->s));
+    };
+    d->verts.alloc(m.vertices.size(), c->s);
+    d->verts.upload(m.vertices.data(), m.vertices.size());
+    d->det.alloc(m.det.size(), c->s);
+    d->det.upload(m.det.data(), m.det.size());
+    up32(d->cells, m.cells);
+    up32(d->cf, m.cell_facets);
+    up32(d->fv, m.facet_vertex_ids);
+    up32(d->fplus, m.facet_plus);
+    up32(d->fminus, m.facet_minus);
+    d->cs.alloc(m.cell_facet_signs.size(), c->s);
+    d->cs.upload((const signed char *)m.cell_facet_signs.data(), m.cell_facet_signs.size());
+    d->fn.alloc(m.facet_normals.size(), c->s);
+    d->fn.upload(m.facet_normals.data(), m.facet_normals.size());
+    d->fm.alloc(m.facet_measures.size(), c->s);
+    d->fm.upload(m.facet_measures.data(), m.facet_measures.size());
+    d->Jinv.alloc((size_t)d->C * d->dim * d->dim, c->s);
+    if (d->C) {
+        k_geom<<<grid_for(d->C, 128, c->sms), 128, 0, c->s>>>(d->C, d->dim, d->kind, d->nn, d->verts.p,
+                                                           d->cells.p, d->Jinv.p);
+        launched(c);
+    }
+    CK(cudaStreamSynchronize(c->s));
+    m.dev = d;
+    return *d;
+}
+
+// ------------------------------------------------------------------ facet points
+struct FRule { int nq, rdim; double p[27][2]; double w[27]; double rm; };
+static FRule frule(int kind, int degree) {
+    double rm;
+    Rule r = facet_rule(kind, degree, rm);
+    FRule f{};
+    f.nq = r.nq;
+    f.rdim = r.rdim;
+    f.rm = rm;
+    for (int q = 0; q < r.nq; ++q) {
+        f.p[q][0] = r.p[q][0];
+        f.p[q][1] = r.p[q][1];
+        f.w[q] = r.w[q];
+    }
+    return f;
+}
+
+// X = v0 + sum_k ref_qk (v_{k+1} - v0), W = w_q * (|f| / ref measure) (assembly.py:173-181)
+__device__ inline void facet_point(const FRule &R, int dim, int nvf, const int *fv, const double *V,
+                                   int64_t f, int q, double *X) {
+    const int *vid = fv + f * nvf;
+    for (int i = 0; i < dim; ++i) {
+        const double v0 = V[(int64_t)vid[0] * dim + i];
+        double s = 0.0;
+        for (int k = 0; k < R.rdim; ++k) s += R.p[q][k] * (V[(int64_t)vid[k + 1] * dim + i] - v0);
+        X[i] = v0 + s;
+    }
+}
+
+__global__ void k_facet_points(int64_t nf, const int64_t *fids, FRule R, int dim, int nvf,
+                               const int *fv, const double *V, const double *fm, double *X,
+                               double *W) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nf * R.nq; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / R.nq;
+        const int q = (int)(t % R.nq);
+        const int64_t f = fids[i];
+        double x[3];
+        facet_point(R, dim, nvf, fv, V, f, q, x);
+        for (int d = 0; d < dim; ++d) X[t * dim + d] = x[d];
+        if (W) W[t] = R.w[q] * (fm[f] / R.rm);
+    }
+}
+
+// trace of the nodal basis of cell c at physical point X (assembly.py:184-189)
+__device__ inline void trace(int kind, int dim, int nn, const double *V, const int *cells,
+                             const double *Jinv, int64_t c, const double *X, double *N) {
+    const double *o = V + (int64_t)cells[c * nn] * dim;
+    const double *Ji = Jinv + c * dim * dim;
+    double xh[3];
+    for (int i = 0; i < dim; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < dim; ++j) s += Ji[i * dim + j] * (X[j] - o[j]);
+        xh[i] = s;
+    }
+    scalar_basis(kind, dim, xh, N, nullptr);
+}
+
+// ------------------------------------------------------------------ node graph
+struct Graph {
+    int64_t n_nodes = 0, nnz = 0;
+    DBuf<int> ptr, col, row;
+    DBuf<int64_t> seg;      // contribution segment starts (nnz+1)
+    DBuf<int> pay;          // sorted payloads
+};
+
+__global__ void k_flag_new(int64_t n, const uint64_t *k, int *flag) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        flag[i] = (i == 0 || k[i] != k[i - 1]) ? 1 : 0;
+}
+__global__ void k_segments(int64_t n, const uint64_t *k, const int *flag, const int64_t *eid,
+                           int64_t nodes, int64_t *seg, int *col, int *row, int *rowcnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (!flag[i]) continue;
+        const int64_t e = eid[i];
+        seg[e] = i;
+        const int64_t r = (int64_t)(k[i] / (uint64_t)nodes);
+        col[e] = (int)(k[i] % (uint64_t)nodes);
+        row[e] = (int)r;
+        atomicAdd(&rowcnt[r], 1);
+    }
+}
+
+// keys/payloads in insertion order -> G (stable sort keeps insertion order per key)
+static Graph build_graph(Ctx *c, DBuf<uint64_t> &keys, DBuf<int> &pay, int64_t n, int64_t nodes) {
+    Graph g;
+    g.n_nodes = nodes;
+    DBuf<uint64_t> k2(n, c->s);
+    g.pay.alloc(n, c->s);
+    int end_bit = 1;
+    while (end_bit < 64 && ((uint64_t)1 << end_bit) < (uint64_t)nodes * (uint64_t)nodes) ++end_bit;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, keys.p, k2.p, pay.p, g.pay.p, n, 0, end_bit, c->s));
+    {
+        DBuf<char> t(tb, c->s);
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, keys.p, k2.p, pay.p, g.pay.p, n, 0, end_bit, c->s));
+        launched(c);
+    }
+    DBuf<int> flag(n, c->s);
+    DBuf<int64_t> eid(n, c->s);
+    k_flag_new<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, k2.p, flag.p);
+    launched(c);
+    tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, eid.p, n, c->s));
+    {
+        DBuf<char> t(tb, c->s);
+        CK(cub::DeviceScan::ExclusiveSum(t.p, tb, flag.p, eid.p, n, c->s));
+        launched(c);
+    }
+    int64_t last_e = 0;
+    int last_f = 0;
+    CK(cudaMemcpyAsync(&last_e, eid.p + n - 1, sizeof(int64_t), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaMemcpyAsync(&last_f, flag.p + n - 1, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    g.nnz = last_e + last_f;
+    g.seg.alloc(g.nnz + 1, c->s);
+    g.col.alloc(g.nnz, c->s);
+    g.row.alloc(g.nnz, c->s);
+    DBuf<int> rowcnt(nodes, c->s);
+    CK(cudaMemsetAsync(rowcnt.p, 0, sizeof(int) * nodes, c->s));
+    k_segments<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, k2.p, flag.p, eid.p, nodes, g.seg.p,
+                                                           g.col.p, g.row.p, rowcnt.p);
+    launched(c);
+    CK(cudaMemcpyAsync(g.seg.p + g.nnz, &n, sizeof(int64_t), cudaMemcpyHostToDevice, c->s));
+    counts_to_ptr(c, rowcnt.p, (int)nodes, g.ptr);
+    CK(cudaStreamSynchronize(c->s));
+    return g;
+}
+
+// cell pairs (a,b) of node ids nodes_of(c,a) -> keys, payload c*nn*nn + a*nn + b
+__global__ void k_emit_cell_pairs(int64_t C, int nn, const int *cellnodes, int node_mode, int64_t nodes,
+                                  uint64_t *keys, int *pay) {
+    const int64_t per = (int64_t)nn * nn;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < C * per; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = t / per;
+        const int a = (int)((t / nn) % nn), b = (int)(t % nn);
+        int64_t na, nb;
+        if (node_mode == 0) { na = cellnodes[c * nn + a]; nb = cellnodes[c * nn + b]; }   // CG: vertices / H(div): facets
+        else { na = c * nn + a; nb = c * nn + b; }                                        // DG nodes
+        keys[t] = (uint64_t)na * (uint64_t)nodes + (uint64_t)nb;
+        pay[t] = (int)t;
+    }
+}
+// DG interior facet side pairs in the reference insertion order: (s,t) major, facet, a, b
+__global__ void k_emit_dg_facets(int64_t Fi, int nn, int64_t C, const int *interior, const int *fplus,
+                                 const int *fminus, int64_t nodes, uint64_t *keys, int *pay) {
+    const int64_t per = (int64_t)nn * nn;
+    const int64_t base = C * per;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 4 * Fi * per; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = t / per;
+        const int st = (int)(q / Fi);
+        const int64_t fi = q % Fi;
+        const int a = (int)((t / nn) % nn), b = (int)(t % nn);
+        const int f = interior[fi];
+        const int64_t cs = (st < 2) ? fplus[f] : fminus[f];
+        const int64_t ct = (st % 2 == 0) ? fplus[f] : fminus[f];
+        keys[t] = (uint64_t)(cs * nn + a) * (uint64_t)nodes + (uint64_t)(ct * nn + b);
+        pay[t] = (int)(base + t);
+    }
+}
+
+// ------------------------------------------------------------------ VMS values
+struct VmsArgs {
+    Elem E;
+    int64_t C, Fi;
+    int dg;
+    const double *det, *Jinv;
+    const int *gptr, *gcol, *grow;
+    const int64_t *seg;
+    const int *pay;
+    int64_t nnz;
+    double s_uu[2], s_pp_gg[2], s_pp_m, s_cross;
+    double c_uu[2], c_pp[2];     // DG facet coefficients (before side signs)
+    // DG facet tables
+    const int *interior;
+    const double *fW, *fNp, *fNm, *fn;  // (Fi,nq), (Fi,nq,nn) x2, normals of all facets
+    int fnq;
+    // outputs (CSR idx/val) ; ptr arrays computed separately
+    int *uu_i[2], *up_i[2], *pu_i[2], *pp_i[2], *cr_i;
+    double *uu_v[2], *up_v[2], *pu_v[2], *pp_v[2], *cr_v;
+};
+
+// per-cell gradient of node a at quadrature point q: Gp_i = sum_j Gref_qaj Jinv_ji
+__device__ inline void grad_phys(const Elem &E, const double *Ji, int q, int a, double *g) {
+    for (int i = 0; i < E.dim; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < E.dim; ++j) s += E.G[q][a][j] * Ji[j * E.dim + i];
+        g[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
+    const Elem &E = A.E;
+    const int dim = E.dim, nn = E.nn;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < A.nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        double uu[2][3][3] = {}, up[3] = {}, pu[3] = {}, pp[2] = {}, cr = 0.0;
+        for (int64_t t = A.seg[e]; t < A.seg[e + 1]; ++t) {
+            const int64_t p = A.pay[t];
+            const int64_t per = (int64_t)nn * nn;
+            if (p < A.C * per) {       // cell contribution (assembly.py:330-342)
+                const int64_t c = p / per;
+                const int a = (int)((p / nn) % nn), b = (int)(p % nn);
+                const double det = A.det[c];
+                const double *Ji = A.Jinv + c * dim * dim;
+                const double mass = det * E.Mref[a][b];
+                double gg = 0.0, gnab[3] = {0, 0, 0}, gnba[3] = {0, 0, 0};
+                for (int q = 0; q < E.nq; ++q) {
+                    double ga[3], gb[3];
+                    grad_phys(E, Ji, q, a, ga);
+                    grad_phys(E, Ji, q, b, gb);
+                    for (int i = 0; i < dim; ++i) {
+                        gg += E.w[q] * ga[i] * gb[i];
+                        gnab[i] += E.w[q] * ga[i] * E.N[q][b];
+                        gnba[i] += E.w[q] * gb[i] * E.N[q][a];
+                    }
+                }
+                gg *= det;
+                for (int i = 0; i < dim; ++i) { gnab[i] *= det; gnba[i] *= det; }
+                for (int n = 0; n < 2; ++n) {
+                    const double v = A.s_uu[n] * mass;
+                    for (int i = 0; i < dim; ++i) uu[n][i][i] += v;
+                    pp[n] += A.s_pp_gg[n] * gg + A.s_pp_m * mass;
+                }
+                for (int i = 0; i < dim; ++i) {
+                    up[i] += -(gnab[i] + 0.5 * gnba[i]);
+                    pu[i] += gnba[i] + 0.5 * gnab[i];
+                }
+                cr += A.s_cross * mass;
+            } else {                   // DG interior facet side pair (assembly.py:497-517)
+                const int64_t idx = p - A.C * per;
+                const int64_t q2 = idx / per;
+                const int st = (int)(q2 / A.Fi);
+                const int64_t fi = q2 % A.Fi;
+                const int a = (int)((idx / nn) % nn), b = (int)(idx % nn);
+                const double ss = st < 2 ? 1.0 : -1.0, tt = (st % 2 == 0) ? 1.0 : -1.0;
+                const double *Ns = (st < 2 ? A.fNp : A.fNm) + fi * A.fnq * nn;
+                const double *Nt = (st % 2 == 0 ? A.fNp : A.fNm) + fi * A.fnq * nn;
+                double F = 0.0;
+                for (int q = 0; q < A.fnq; ++q) F += A.fW[fi * A.fnq + q] * Ns[q * nn + a] * Nt[q * nn + b];
+                const double *n = A.fn + (int64_t)A.interior[fi] * dim;
+                for (int k = 0; k < 2; ++k) {
+                    const double cu = A.c_uu[k] * ss * tt;
+                    for (int i = 0; i < dim; ++i)
+                        for (int j = 0; j < dim; ++j) uu[k][i][j] += cu * (F * n[i] * n[j]);
+                    pp[k] += A.c_pp[k] * ss * tt * F;
+                }
+                for (int i = 0; i < dim; ++i) {
+                    up[i] += 0.5 * ss * (F * n[i]);
+                    pu[i] += -0.5 * tt * (F * n[i]);
+                }
+            }
+        }
+        // Kronecker placement of entry e (row v, col v2) into the expanded blocks
+        const int v = A.grow[e], v2 = A.gcol[e];
+        const int64_t g0 = A.gptr[v], len = A.gptr[v + 1] - g0, o = e - g0;
+        for (int n = 0; n < 2; ++n) {
+            for (int i = 0; i < dim; ++i) {
+                const int64_t rs = (int64_t)dim * dim * g0 + (int64_t)i * dim * len;
+                for (int j = 0; j < dim; ++j) {
+                    const int64_t pos = rs + o * dim + j;
+                    A.uu_i[n][pos] = v2 * dim + j;
+                    A.uu_v[n][pos] = uu[n][i][j];
+                }
+                const int64_t ps = (int64_t)dim * g0 + (int64_t)i * len + o;
+                A.up_i[n][ps] = v2;
+                A.up_v[n][ps] = up[i];
+            }
+            for (int j = 0; j < dim; ++j) {
+                const int64_t pos = (int64_t)dim * g0 + o * dim + j;
+                A.pu_i[n][pos] = v2 * dim + j;
+                A.pu_v[n][pos] = pu[j];
+            }
+            A.pp_i[n][e] = v2;
+            A.pp_v[n][e] = pp[n];
+        }
+        if (A.cr_i) {
+            A.cr_i[e] = v2;
+            A.cr_v[e] = cr;
+        }
+    }
+}
+
+// row pointers of the expanded blocks from G.ptr
+__global__ void k_kron_ptr(int64_t nodes, int dim, const int *gptr, int *uu, int *up, int *pu) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= nodes; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g0 = gptr[v];
+        if (v < nodes) {
+            const int64_t len = gptr[v + 1] - g0;
+            for (int i = 0; i < dim; ++i) {
+                uu[v * dim + i] = (int)(dim * dim * g0 + i * dim * len);
+                up[v * dim + i] = (int)(dim * g0 + i * len);
+            }
+        } else {
+            uu[v * dim] = (int)(dim * dim * g0);
+            up[v * dim] = (int)(dim * g0);
+        }
+        pu[v] = (int)(dim * g0);
+    }
+}
+
+// DG cross blocks: cell-local mass (assembly.py:487-489)
+__global__ void k_dg_cross(int64_t C, Elem E, const double *det, double s_cross, int *ptr, int *idx,
+                           double *val) {
+    const int nn = E.nn;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r <= C * nn; r += (int64_t)gridDim.x * blockDim.x) {
+        ptr[r] = (int)(r * nn);
+        if (r == C * nn) continue;
+        const int64_t c = r / nn;
+        const int a = (int)(r % nn);
+        for (int b = 0; b < nn; ++b) {
+            idx[r * nn + b] = (int)(c * nn + b);
+            val[r * nn + b] = s_cross * (det[c] * E.Mref[a][b]);
+        }
+    }
+}
+
+// DG interior facet traces at the degree-2 facet rule
+__global__ void k_dg_facet_tables(int64_t Fi, FRule R, int kind, int dim, int nn, int nvf,
+                                  const int *interior, const int *fv, const int *fplus,
+                                  const int *fminus, const double *V, const int *cells,
+                                  const double *Jinv, const double *fm, double *W, double *Np,
+                                  double *Nm) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < Fi * R.nq; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t fi = t / R.nq;
+        const int q = (int)(t % R.nq);
+        const int f = interior[fi];
+        double X[3];
+        facet_point(R, dim, nvf, fv, V, f, q, X);
+        W[t] = R.w[q] * (fm[f] / R.rm);
+        trace(kind, dim, nn, V, cells, Jinv, fplus[f], X, Np + t * nn);
+        trace(kind, dim, nn, V, cells, Jinv, fminus[f], X, Nm + t * nn);
+    }
+}
+
+// ------------------------------------------------------------------ H(div) values
+struct HdivArgs {
+    int dim, nf, nq;
+    double w[8];
+    double Vref[8][6][3];   // [q][f][j]
+    double s_uu[2];
+    const double *V, *det;
+    const int *cells, *cf;
+    const signed char *cs;
+    int nn, kind;
+    const int *gptr, *gcol, *grow;
+    const int64_t *seg;
+    const int *pay;
+    int64_t nnz;
+    int *uu_i[2];
+    double *uu_v[2];
+};
+
+// local mass[f][g] of cell c, einsum order of assembly.py:262-264 (bitwise)
+__device__ inline double hdiv_mass(const HdivArgs &A, int64_t c, int lf, int lg) {
+    const int dim = A.dim;
+    double J[9];
+    const int *cv = A.cells + c * A.nn;
+    if (A.kind == DPP_TRI || A.kind == DPP_TET) {
+        for (int k = 0; k < dim; ++k)
+            for (int d = 0; d < dim; ++d) J[d * dim + k] = __dsub_rn(A.V[(int64_t)cv[k + 1] * dim + d], A.V[(int64_t)cv[0] * dim + d]);
+    } else {
+        for (int k = 0; k < dim * dim; ++k) J[k] = 0.0;
+        for (int d = 0; d < dim; ++d) J[d * dim + d] = __dsub_rn(A.V[(int64_t)cv[A.nn - 1] * dim + d], A.V[(int64_t)cv[0] * dim + d]);
+    }
+    const double det = A.det[c];
+    double m = 0.0;
+    for (int q = 0; q < A.nq; ++q) {
+        double acc = 0.0;
+        for (int i = 0; i < dim; ++i) {
+            double vf = __dmul_rn(J[i * dim], A.Vref[q][lf][0]);
+            double vg = __dmul_rn(J[i * dim], A.Vref[q][lg][0]);
+            for (int j = 1; j < dim; ++j) {
+                vf = __dadd_rn(vf, __dmul_rn(J[i * dim + j], A.Vref[q][lf][j]));
+                vg = __dadd_rn(vg, __dmul_rn(J[i * dim + j], A.Vref[q][lg][j]));
+            }
+            vf = __ddiv_rn(vf, det);
+            vg = __ddiv_rn(vg, det);
+            acc = __dadd_rn(acc, __dmul_rn(__dmul_rn(A.w[q], vf), vg));
+        }
+        m = __dadd_rn(m, acc);
+    }
+    m = __dmul_rn(m, det);
+    const double sf = A.cs[c * A.nf + lf], sg = A.cs[c * A.nf + lg];
+    return __dmul_rn(__dmul_rn(m, sf), sg);
+}
+
+__global__ void k_hdiv_uu(HdivArgs A) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < A.nnz; e += (int64_t)gridDim.x * blockDim.x) {
+        double acc[2] = {0.0, 0.0};
+        bool first = true;
+        for (int64_t t = A.seg[e]; t < A.seg[e + 1]; ++t) {
+            const int64_t p = A.pay[t];
+            const int64_t per = (int64_t)A.nf * A.nf;
+            const int64_t c = p / per;
+            const int lf = (int)((p / A.nf) % A.nf), lg = (int)(p % A.nf);
+            const double m = hdiv_mass(A, c, lf, lg);
+            for (int n = 0; n < 2; ++n) {
+                const double v = __dmul_rn(A.s_uu[n], m);
+                acc[n] = first ? v : __dadd_rn(acc[n], v);
+            }
+            first = false;
+        }
+        for (int n = 0; n < 2; ++n) {
+            A.uu_i[n][e] = A.gcol[e];
+            A.uu_v[n][e] = acc[n];
+        }
+    }
+}
+
+// up (F x C): row f = [plus, minus]; pu (C x F): row c = its facets sorted by id;
+// pp / cross diagonal (assembly.py:266-280)
+__global__ void k_hdiv_rest(int64_t F, int64_t C, int nf, const int *fplus, const int *fminus,
+                            const int *cf, const signed char *cs, const double *det, double wsum,
+                            double bm, double nbm, int *up_p, int *up_i, double *up_v, int *pu_p,
+                            int *pu_i, double *pu_v, int *pp_p, int *pp_i, double *pp_v,
+                            double *cr_v) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= C; c += (int64_t)gridDim.x * blockDim.x) {
+        pu_p[c] = (int)(c * nf);
+        pp_p[c] = (int)c;
+        if (c == C) continue;
+        int ids[6];
+        double sg[6];
+        for (int k = 0; k < nf; ++k) { ids[k] = cf[c * nf + k]; sg[k] = cs[c * nf + k]; }
+        for (int i = 1; i < nf; ++i)
+            for (int j = i; j > 0 && ids[j - 1] > ids[j]; --j) {
+                int t = ids[j]; ids[j] = ids[j - 1]; ids[j - 1] = t;
+                double s = sg[j]; sg[j] = sg[j - 1]; sg[j - 1] = s;
+            }
+        for (int k = 0; k < nf; ++k) { pu_i[c * nf + k] = ids[k]; pu_v[c * nf + k] = sg[k]; }
+        const double vol = det[c] * wsum;
+        pp_i[c] = (int)c;
+        pp_v[c] = bm * vol * 1.0;
+        cr_v[c] = nbm * vol * 1.0;
+    }
+}
+__global__ void k_hdiv_up(int64_t F, const int *fplus, const int *fminus, const int *upp, int *up_i,
+                          double *up_v) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F; f += (int64_t)gridDim.x * blockDim.x) {
+        const int o = upp[f];
+        up_i[o] = fplus[f];
+        up_v[o] = -1.0;
+        if (fminus[f] >= 0) { up_i[o + 1] = fminus[f]; up_v[o + 1] = 1.0; }
+    }
+}
+__global__ void k_hdiv_up_cnt(int64_t F, const int *fminus, int *cnt) {
+    for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F; f += (int64_t)gridDim.x * blockDim.x)
+        cnt[f] = fminus[f] >= 0 ? 2 : 1;
+}
+
+// ------------------------------------------------------------------ boundary RHS
+// contributions of -(w.n, p0) on pressure facets (assembly.py:422-436, :291-300)
+__global__ void k_rhs_nodal(int64_t nf, const int64_t *fids, FRule R, int kind, int dim, int nn,
+                            int nvf, int dg, const int *fv, const int *fplus, const double *fn,
+                            const double *fm, const double *V, const int *cells, const double *Jinv,
+                            const double *p0, int64_t *dof, double *val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = fids[i];
+        const int64_t c = fplus[f];
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int q = 0; q < R.nq; ++q) {
+            double X[3], N[8];
+            facet_point(R, dim, nvf, fv, V, f, q, X);
+            trace(kind, dim, nn, V, cells, Jinv, c, X, N);
+            const double W = R.w[q] * (fm[f] / R.rm);
+            const double wp = W * p0[i * R.nq + q];
+            for (int a = 0; a < nn; ++a) acc[a] += wp * N[a];
+        }
+        for (int a = 0; a < nn; ++a)
+            for (int d = 0; d < dim; ++d) {
+                const int64_t k = (i * nn + a) * dim + d;
+                const int64_t node = dg ? c * nn + a : cells[c * nn + a];
+                dof[k] = node * dim + d;
+                val[k] = -(acc[a] * fn[f * dim + d]);
+            }
+    }
+}
+__global__ void k_rhs_hdiv(int64_t nf, const int64_t *fids, FRule R, const double *fm,
+                           const double *p0, int64_t *dof, double *val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nf; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = fids[i];
+        double s = 0.0;
+        for (int q = 0; q < R.nq; ++q) s += (R.w[q] * (fm[f] / R.rm)) * p0[i * R.nq + q];
+        dof[i] = f;
+        val[i] = -s / fm[f];
+    }
+}
+__global__ void k_seg_add(int64_t n, const int64_t *dof, const double *val, double *rhs) {
+    // dof sorted (stable); one thread per run start sums the run in order
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i > 0 && dof[i - 1] == dof[i]) continue;
+        double s = rhs[dof[i]];
+        for (int64_t j = i; j < n && dof[j] == dof[i]; ++j) s += val[j];
+        rhs[dof[i]] = s;
+    }
+}
+// np.add.at(rhs, dof, val) with the per-dof order of insertion
+static void add_at(Ctx *c, int64_t n, DBuf<int64_t> &dof, DBuf<double> &val, double *rhs) {
+    if (!n) return;
+    DBuf<int64_t> d2(n, c->s);
+    DBuf<double> v2(n, c->s);
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dof.p, d2.p, val.p, v2.p, n, 0, 64, c->s));
+    DBuf<char> t(tb, c->s);
+    CK(cub::DeviceRadixSort::SortPairs(t.p, tb, dof.p, d2.p, val.p, v2.p, n, 0, 64, c->s));
+    launched(c);
+    k_seg_add<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d2.p, v2.p, rhs);
+    launched(c);
+    CK(cudaStreamSynchronize(c->s));
+}
+
+// ------------------------------------------------------------------ drivers
+static void alloc_blk(Ctx *c, Csr &B, int rows, int cols, int64_t nnz) { B.alloc(rows, cols, nnz, c->s); }
+
+static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, bool dg,
+                         dpp_system &S) {
+    const Elem E = make_elem(m.kind);
+    const int dim = m.dim, nn = m.nn;
+    const int64_t C = m.C;
+    const int64_t nodes = dg ? C * nn : m.V;
+    // interior facets (DG)
+    std::vector<int64_t> inter;
+    if (dg)
+        for (int64_t f = 0; f < hm.n_facets; ++f)
+            if (hm.facet_minus[f] >= 0) inter.push_back(f);
+    const int64_t Fi = (int64_t)inter.size();
+    const int64_t ncell = C * nn * nn, nfac = dg ? 4 * Fi * nn * nn : 0, ntot = ncell + nfac;
+    if (ntot > INT32_MAX) DPP_FAIL(DPP_ERR_VALUE, "mesh too large for 32-bit contribution ids");
+    DBuf<uint64_t> keys(ntot, c->s);
+    DBuf<int> pay(ntot, c->s);
+    k_emit_cell_pairs<<<grid_for(ncell, 256, c->sms), 256, 0, c->s>>>(C, nn, m.cells.p, dg ? 1 : 0, nodes,
+                                                                   keys.p, pay.p);
+    launched(c);
+    DBuf<int> dinter(Fi, c->s);
+    DBuf<double> fW, fNp, fNm;
+    FRule R2 = frule(m.kind, 2);
+    if (dg && Fi) {
+        std::vector<int> t(inter.begin(), inter.end());
+        dinter.upload(t.data(), Fi);
+        k_emit_dg_facets<<<grid_for(nfac, 256, c->sms), 256, 0, c->s>>>(Fi, nn, C, dinter.p, m.fplus.p,
+                                                                     m.fminus.p, nodes, keys.p + ncell,
+                                                                     pay.p + ncell);
+        launched(c);
+        fW.alloc(Fi * R2.nq, c->s);
+        fNp.alloc(Fi * R2.nq * nn, c->s);
+        fNm.alloc(Fi * R2.nq * nn, c->s);
+        k_dg_facet_tables<<<grid_for(Fi * R2.nq, 128, c->sms), 128, 0, c->s>>>(
+            Fi, R2, m.kind, dim, nn, m.nvf, dinter.p, m.fv.p, m.fplus.p, m.fminus.p, m.verts.p,
+            m.cells.p, m.Jinv.p, m.fm.p, fW.p, fNp.p, fNm.p);
+        launched(c);
+        CK(cudaStreamSynchronize(c->s));
+    }
+    Graph G = build_graph(c, keys, pay, ntot, nodes);
+    keys.release();
+    pay.release();
+    const int64_t g = G.nnz;
+    const int nu = (int)(nodes * dim), np_ = (int)nodes;
+    Csr *uu[2] = {&S.blk[DPP_K1_UU], &S.blk[DPP_K2_UU]}, *up[2] = {&S.blk[DPP_K1_UP], &S.blk[DPP_K2_UP]},
+        *pu[2] = {&S.blk[DPP_K1_PU], &S.blk[DPP_K2_PU]}, *pp[2] = {&S.blk[DPP_K1_PP], &S.blk[DPP_K2_PP]};
+    for (int n = 0; n < 2; ++n) {
+        alloc_blk(c, *uu[n], nu, nu, g * dim * dim);
+        alloc_blk(c, *up[n], nu, np_, g * dim);
+        alloc_blk(c, *pu[n], np_, nu, g * dim);
+        alloc_blk(c, *pp[n], np_, np_, g);
+        k_kron_ptr<<<grid_for(nodes + 1, 256, c->sms), 256, 0, c->s>>>(nodes, dim, G.ptr.p, uu[n]->ptr.p,
+                                                                     up[n]->ptr.p, pu[n]->ptr.p);
+        launched(c);
+        CK(cudaMemcpyAsync(pp[n]->ptr.p, G.ptr.p, sizeof(int) * (nodes + 1), cudaMemcpyDeviceToDevice, c->s));
+    }
+    VmsArgs A{};
+    A.E = E;
+    A.C = C;
+    A.Fi = Fi;
+    A.dg = dg;
+    A.det = m.det.p;
+    A.Jinv = m.Jinv.p;
+    A.gptr = G.ptr.p;
+    A.gcol = G.col.p;
+    A.grow = G.row.p;
+    A.seg = G.seg.p;
+    A.pay = G.pay.p;
+    A.nnz = g;
+    const double ks[2] = {p.k1, p.k2};
+    for (int n = 0; n < 2; ++n) {
+        A.s_uu[n] = 0.5 * p.mu / ks[n];
+        A.s_pp_gg[n] = 0.5 * ks[n] / p.mu;
+        A.c_uu[n] = p.eta_u * (1.0 / hm.n_div) * p.mu / ks[n];
+        A.c_pp[n] = p.eta_p / (1.0 / hm.n_div) * ks[n] / p.mu;
+        A.uu_i[n] = uu[n]->idx.p; A.uu_v[n] = uu[n]->val.p;
+        A.up_i[n] = up[n]->idx.p; A.up_v[n] = up[n]->val.p;
+        A.pu_i[n] = pu[n]->idx.p; A.pu_v[n] = pu[n]->val.p;
+        A.pp_i[n] = pp[n]->idx.p; A.pp_v[n] = pp[n]->val.p;
+    }
+    A.s_pp_m = p.beta / p.mu;
+    A.s_cross = -p.beta / p.mu;
+    A.interior = dinter.p;
+    A.fW = fW.p;
+    A.fNp = fNp.p;
+    A.fNm = fNm.p;
+    A.fn = m.fn.p;
+    A.fnq = R2.nq;
+    Csr &c12 = S.blk[DPP_K12_PP], &c21 = S.blk[DPP_K21_PP];
+    if (!dg) {
+        alloc_blk(c, c12, np_, np_, g);
+        CK(cudaMemcpyAsync(c12.ptr.p, G.ptr.p, sizeof(int) * (nodes + 1), cudaMemcpyDeviceToDevice, c->s));
+        A.cr_i = c12.idx.p;
+        A.cr_v = c12.val.p;
+    }
+    k_vms_values<<<grid_for(g, 128, c->sms, 32), 128, 0, c->s>>>(A);
+    launched(c);
+    if (dg) {
+        alloc_blk(c, c12, np_, np_, C * nn * nn);
+        k_dg_cross<<<grid_for(C * nn + 1, 128, c->sms), 128, 0, c->s>>>(C, E, m.det.p, -p.beta / p.mu,
+                                                                      c12.ptr.p, c12.idx.p, c12.val.p);
+        launched(c);
+    }
+    c21 = csr_copy(c, c12);
+    CK(cudaStreamSynchronize(c->s));
+}
+
+static void assemble_hdiv(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, dpp_system &S) {
+    const int dim = m.dim, nf = m.nf;
+    const int64_t C = m.C, F = m.F;
+    Rule r = cell_rule(m.kind, 2);
+    HdivArgs A{};
+    A.dim = dim;
+    A.nf = nf;
+    A.nq = r.nq;
+    for (int q = 0; q < r.nq; ++q) {
+        A.w[q] = r.w[q];
+        // elements.eval_basis flux families (elements.py:124-138)
+        for (int f = 0; f < nf; ++f)
+            for (int j = 0; j < dim; ++j) {
+                double v;
+                if (m.kind == DPP_TRI) {
+                    static const double opp[3][2] = {{0.0, 1.0}, {1.0, 0.0}, {0.0, 0.0}};
+                    v = r.p[q][j] - opp[f][j];
+                } else if (m.kind == DPP_TET) {
+                    static const double opp[4][3] = {{0, 0, 1}, {0, 1, 0}, {1, 0, 0}, {0, 0, 0}};
+                    v = 2.0 * (r.p[q][j] - opp[f][j]);
+                } else {
+                    const int ax = f / 2;
+                    v = (j != ax) ? 0.0 : ((f % 2 == 0) ? r.p[q][ax] - 1.0 : r.p[q][ax]);
+                }
+                A.Vref[q][f][j] = v;
+            }
+    }
+    double ws = 0.0;
+    for (int q = 0; q < r.nq; ++q) ws += r.w[q];
+    A.s_uu[0] = p.mu / p.k1;
+    A.s_uu[1] = p.mu / p.k2;
+    A.V = m.verts.p;
+    A.det = m.det.p;
+    A.cells = m.cells.p;
+    A.cf = m.cf.p;
+    A.cs = m.cs.p;
+    A.nn = m.nn;
+    A.kind = m.kind;
+    const int64_t ne = C * nf * nf;
+    DBuf<uint64_t> keys(ne, c->s);
+    DBuf<int> pay(ne, c->s);
+    k_emit_cell_pairs<<<grid_for(ne, 256, c->sms), 256, 0, c->s>>>(C, nf, m.cf.p, 0, F, keys.p, pay.p);
+    launched(c);
+    Graph G = build_graph(c, keys, pay, ne, F);
+    keys.release();
+    pay.release();
+    A.gptr = G.ptr.p;
+    A.gcol = G.col.p;
+    A.grow = G.row.p;
+    A.seg = G.seg.p;
+    A.pay = G.pay.p;
+    A.nnz = G.nnz;
+    Csr *uu[2] = {&S.blk[DPP_K1_UU], &S.blk[DPP_K2_UU]};
+    for (int n = 0; n < 2; ++n) {
+        alloc_blk(c, *uu[n], (int)F, (int)F, G.nnz);
+        CK(cudaMemcpyAsync(uu[n]->ptr.p, G.ptr.p, sizeof(int) * (F + 1), cudaMemcpyDeviceToDevice, c->s));
+        A.uu_i[n] = uu[n]->idx.p;
+        A.uu_v[n] = uu[n]->val.p;
+    }
+    k_hdiv_uu<<<grid_for(G.nnz, 128, c->sms, 32), 128, 0, c->s>>>(A);
+    launched(c);
+    // up / pu / pp / cross
+    Csr &up1 = S.blk[DPP_K1_UP], &pu1 = S.blk[DPP_K1_PU], &pp1 = S.blk[DPP_K1_PP], &c12 = S.blk[DPP_K12_PP];
+    {
+        DBuf<int> cnt(F, c->s);
+        k_hdiv_up_cnt<<<grid_for(F, 256, c->sms), 256, 0, c->s>>>(F, m.fminus.p, cnt.p);
+        launched(c);
+        up1.rows = (int)F;
+        up1.cols = (int)C;
+        up1.nnz = counts_to_ptr(c, cnt.p, (int)F, up1.ptr);
+        up1.idx.alloc(up1.nnz, c->s);
+        up1.val.alloc(up1.nnz, c->s);
+        k_hdiv_up<<<grid_for(F, 256, c->sms), 256, 0, c->s>>>(F, m.fplus.p, m.fminus.p, up1.ptr.p, up1.idx.p,
+                                                           up1.val.p);
+        launched(c);
+    }
+    alloc_blk(c, pu1, (int)C, (int)F, C * nf);
+    alloc_blk(c, pp1, (int)C, (int)C, C);
+    alloc_blk(c, c12, (int)C, (int)C, C);
+    DBuf<double> crv(C, c->s);
+    k_hdiv_rest<<<grid_for(C + 1, 256, c->sms), 256, 0, c->s>>>(
+        F, C, nf, m.fplus.p, m.fminus.p, m.cf.p, m.cs.p, m.det.p, ws, p.beta / p.mu, -p.beta / p.mu,
+        nullptr, nullptr, nullptr, pu1.ptr.p, pu1.idx.p, pu1.val.p, pp1.ptr.p, pp1.idx.p, pp1.val.p,
+        c12.val.p);
+    launched(c);
+    CK(cudaMemcpyAsync(c12.ptr.p, pp1.ptr.p, sizeof(int) * (C + 1), cudaMemcpyDeviceToDevice, c->s));
+    CK(cudaMemcpyAsync(c12.idx.p, pp1.idx.p, sizeof(int) * C, cudaMemcpyDeviceToDevice, c->s));
+    S.blk[DPP_K2_UP] = csr_copy(c, up1);
+    S.blk[DPP_K2_PU] = csr_copy(c, pu1);
+    S.blk[DPP_K2_PP] = csr_copy(c, pp1);
+    S.blk[DPP_K21_PP] = csr_copy(c, c12);
+    CK(cudaStreamSynchronize(c->s));
+    (void)hm;
+}
+
+static void boundary_rhs(Ctx *c, DevMesh &m, int formulation, const dpp_bc *bc, dpp_system &S) {
+    if (!bc) return;
+    FRule R4 = frule(m.kind, 4);
+    const bool dg = formulation == DPP_DGVMS;
+    for (int net = 0; net < 2; ++net) {
+        const int64_t nfp = bc->n_pfacets[net];
+        if (nfp <= 0) continue;
+        DBuf<int64_t> fids(nfp, c->s);
+        fids.upload(bc->pfacets[net], nfp);
+        DBuf<double> p0(nfp * R4.nq, c->s);
+        p0.upload(bc->p0[net], nfp * R4.nq);
+        double *rhs = S.rhs[net == 0 ? 0 : 2].p;
+        if (formulation == DPP_HDIV) {
+            DBuf<int64_t> dof(nfp, c->s);
+            DBuf<double> val(nfp, c->s);
+            k_rhs_hdiv<<<grid_for(nfp, 256, c->sms), 256, 0, c->s>>>(nfp, fids.p, R4, m.fm.p, p0.p, dof.p, val.p);
+            launched(c);
+            add_at(c, nfp, dof, val, rhs);
+        } else {
+            const int64_t ne = nfp * m.nn * m.dim;
+            DBuf<int64_t> dof(ne, c->s);
+            DBuf<double> val(ne, c->s);
+            k_rhs_nodal<<<grid_for(nfp, 128, c->sms), 128, 0, c->s>>>(
+                nfp, fids.p, R4, m.kind, m.dim, m.nn, m.nvf, dg, m.fv.p, m.fplus.p, m.fn.p, m.fm.p,
+                m.verts.p, m.cells.p, m.Jinv.p, p0.p, dof.p, val.p);
+            launched(c);
+            add_at(c, ne, dof, val, rhs);
+        }
+    }
+}
+
+}  // namespace dpp
+
+// ------------------------------------------------------------------ C ABI
+using namespace dpp;
+
+struct dpp_mesh { HostMesh m; };
+
+
+extern "C" {
+
+int dpp_mesh_generate(int dim, int kind, int n_div, dpp_mesh **out) {
+    return guard([&] {
+        try {
+            auto *h = new dpp_mesh;
+            h->m = generate(dim, kind, n_div);
+            *out = h;
+        } catch (const std::invalid_argument &e) {
+            DPP_FAIL(DPP_ERR_VALUE, e.what());
+        }
+    });
+}
+
+int dpp_mesh_from_arrays(int dim, int kind, int n_div, int64_t nv, const double *vertices, int64_t nc,
+                         const int64_t *cells, dpp_mesh **out) {
+    return guard([&] {
+        if (kind < 0 || kind > 3 || kind_dim(kind) != dim) DPP_FAIL(DPP_ERR_VALUE, "cell kind / dim mismatch");
+        auto *h = new dpp_mesh;
+        h->m.dim = dim;
+        h->m.kind = kind;
+        h->m.n_div = n_div;
+        h->m.n_vertices = nv;
+        h->m.n_cells = nc;
+        h->m.vertices.assign(vertices, vertices + nv * dim);
+        h->m.cells.assign(cells, cells + nc * kind_nodes(kind));
+        for (int64_t v : h->m.cells)
+            if (v < 0 || v >= nv) { delete h; DPP_FAIL(DPP_ERR_VALUE, "cell vertex id out of range"); }
+        try {
+            h->m.build();
+        } catch (const std::runtime_error &e) {
+            delete h;
+            DPP_FAIL(DPP_ERR_VALUE, e.what());
+        }
+        *out = h;
+    });
+}
+
+int dpp_mesh_counts(const dpp_mesh *m, int64_t *nv, int64_t *nc, int64_t *nf) {
+    return guard([&] {
+        if (nv) *nv = m->m.n_vertices;
+        if (nc) *nc = m->m.n_cells;
+        if (nf) *nf = m->m.n_facets;
+    });
+}
+
+int dpp_mesh_export(const dpp_mesh *mm, double *vertices, int64_t *cells, int64_t *fvi, int64_t *cf,
+                    int8_t *cs, int64_t *fp, int64_t *fmi, double *fn, double *fms, double *J, double *det) {
+    return guard([&] {
+        const HostMesh &m = mm->m;
+        auto cp = [](auto *dst, const auto &v) {
+            if (dst) std::copy(v.begin(), v.end(), dst);
+        };
+        cp(vertices, m.vertices);
+        cp(cells, m.cells);
+        cp(fvi, m.facet_vertex_ids);
+        cp(cf, m.cell_facets);
+        cp(cs, m.cell_facet_signs);
+        cp(fp, m.facet_plus);
+        cp(fmi, m.facet_minus);
+        cp(fn, m.facet_normals);
+        cp(fms, m.facet_measures);
+        cp(J, m.J);
+        cp(det, m.det);
+    });
+}
+
+int dpp_mesh_destroy(dpp_mesh *m) {
+    return guard([&] { delete m; });
+}
+
+int dpp_mesh_release_device(dpp_mesh *m) {
+    return guard([&] { m->m.dev.reset(); });
+}
+
+int dpp_facet_rule_size(int dim, int kind, int degree, int *nq) {
+    return guard([&] {
+        if (kind_dim(kind) != dim) DPP_FAIL(DPP_ERR_VALUE, "cell kind / dim mismatch");
+        *nq = frule(kind, degree).nq;
+    });
+}
+
+int dpp_facet_points(dpp_ctx *ctx, dpp_mesh *mm, int degree, int64_t nf, const int64_t *facets,
+                     double *X, double *W) {
+    return guard([&] {
+        Ctx *c = &ctx->c;
+        DevMesh &m = dev_mesh(c, mm->m);
+        FRule R = frule(m.kind, degree);
+        if (nf <= 0) return;
+        DBuf<int64_t> f(nf, c->s);
+        f.upload(facets, nf);
+        DBuf<double> dX(nf * R.nq * m.dim, c->s), dW(nf * R.nq, c->s);
+        k_facet_points<<<grid_for(nf * R.nq, 256, c->sms), 256, 0, c->s>>>(nf, f.p, R, m.dim, m.nvf, m.fv.p,
+                                                                        m.verts.p, m.fm.p, dX.p, dW.p);
+        launched(c);
+        if (X) dX.download(X, nf * R.nq * m.dim);
+        if (W) dW.download(W, nf * R.nq);
+        CK(cudaStreamSynchronize(c->s));
+    });
+}
+
+int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *p, const dpp_bc *bc,
+                 dpp_system **out) {
+    return guard([&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        Ctx *c = &ctx->c;
+        HostMesh &hm = mm->m;
+        if (p->mu <= 0 || p->k1 <= 0 || p->k2 <= 0) DPP_FAIL(DPP_ERR_VALUE, "mu, k1, k2 must be positive");
+        for (int d = 0; d < hm.dim; ++d)
+            if (p->gamma_b[d] != 0.0)
+                DPP_FAIL(DPP_ERR_VALUE, "nonzero body force gamma_b is not supported by the device assembler yet");
+        if (bc)
+            for (int n = 0; n < 2; ++n)
+                if (bc->n_vfacets[n] > 0)
+                    DPP_FAIL(DPP_ERR_VALUE, "prescribed-velocity boundary facets are not supported by the device assembler yet");
+        DevMesh &m = dev_mesh(c, hm);
+        auto S = std::make_unique<dpp_system>();
+        S->ctx = c;
+        if (formulation == DPP_HDIV) {
+            S->sizes[0] = S->sizes[2] = m.F;
+            S->sizes[1] = S->sizes[3] = m.C;
+        } else if (formulation == DPP_CGVMS) {
+            S->sizes[0] = S->sizes[2] = m.V * m.dim;
+            S->sizes[1] = S->sizes[3] = m.V;
+        } else if (formulation == DPP_DGVMS) {
+            S->sizes[1] = S->sizes[3] = m.C * m.nn;
+            S->sizes[0] = S->sizes[2] = m.C * m.nn * m.dim;
+        } else {
+            DPP_FAIL(DPP_ERR_VALUE, "unknown formulation");
+        }
+        for (int k = 0; k < 4; ++k) {
+            S->rhs[k].alloc(S->sizes[k], c->s);
+            if (S->sizes[k]) CK(cudaMemsetAsync(S->rhs[k].p, 0, sizeof(double) * S->sizes[k], c->s));
+        }
+        if (formulation == DPP_HDIV) assemble_hdiv(c, hm, m, *p, *S);
+        else assemble_vms(c, hm, m, *p, formulation == DPP_DGVMS, *S);
+        boundary_rhs(c, m, formulation, bc, *S);
+        CK(cudaStreamSynchronize(c->s));
+        S->assembly_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        *out = S.release();
+    });
+}
+
+}  // extern "C"

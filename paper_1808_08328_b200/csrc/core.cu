@@ -1,0 +1,487 @@
+// Core device sparse/vector kernels: CSR SpMV, vector ops, CSR restructuring.
+// Reference semantics: scipy.sparse CSR as used by dppflow (linalg.py:27-32,
+// blocksolve.py:227-228, assembly.py:102-108, linalg.py:218-219, :372-374).
+#include <cub/cub.cuh>
+
+#include <climits>
+
+#include "dpp_internal.cuh"
+
+namespace dpp {
+
+static inline cudaStream_t S(Ctx *c, cudaStream_t st) { return st ? st : c->s; }
+
+// ---------------------------------------------------------------- scans
+__global__ void k_widen(const int *a, int64_t *b, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+        b[i] = i < n ? a[i] : 0;
+}
+__global__ void k_narrow(const int64_t *a, int *b, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+        b[i] = (int)a[i];
+}
+// counts[n] -> ptr[n+1] (int32), returns total; errors if total >= 2^31
+int64_t counts_to_ptr(Ctx *c, const int *counts, int n, DBuf<int> &ptr) {
+    DBuf<int64_t> tmp64((size_t)n + 1, c->s);
+    DBuf<int64_t> in64((size_t)n + 1, c->s);
+    k_widen<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(counts, in64.p, n);
+    launched(c);
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in64.p, tmp64.p, n + 1, c->s));
+    DBuf<char> t(tb, c->s);
+    CK(cub::DeviceScan::ExclusiveSum(t.p, tb, in64.p, tmp64.p, n + 1, c->s));
+    launched(c);
+    int64_t total = 0;
+    CK(cudaMemcpyAsync(&total, tmp64.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    if (total > INT_MAX) DPP_FAIL(DPP_ERR_VALUE, "CSR with more than 2^31-1 entries");
+    ptr.alloc((size_t)n + 1, c->s);
+    k_narrow<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(tmp64.p, ptr.p, n);
+    launched(c);
+    return total;
+}
+
+// ---------------------------------------------------------------- SpMV
+// G lanes per row; every lane of a warp runs the same number of iterations so
+// the width-G shuffles are always fully populated.
+template <int G>
+__global__ void __launch_bounds__(256) k_spmv(int rows, const int *__restrict__ ptr,
+                                              const int *__restrict__ idx,
+                                              const double *__restrict__ val,
+                                              const double *__restrict__ x, double *__restrict__ y,
+                                              const double *__restrict__ b, double alpha) {
+    constexpr int RPW = 32 / G;
+    const int lane = threadIdx.x & (G - 1);
+    const int grp = (threadIdx.x & 31) / G;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t w = warp; w * RPW < rows; w += nwarp) {
+        const int64_t r = w * RPW + grp;
+        double sum = 0.0;
+        if (r < rows) {
+            const int s = __ldg(ptr + r), e = __ldg(ptr + r + 1);
+            for (int p = s + lane; p < e; p += G) sum += __ldg(val + p) * __ldg(x + __ldg(idx + p));
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
+        if (r < rows && lane == 0) y[r] = b ? b[r] + alpha * sum : alpha * sum;
+    }
+}
+
+void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b, double alpha,
+          cudaStream_t st) {
+    st = S(c, st);
+    if (A.rows == 0) return;
+    const double avg = A.rows ? (double)A.nnz / A.rows : 0.0;
+    const int block = 256;
+    auto launch = [&](auto kern, int G) {
+        int64_t warps = ((int64_t)A.rows * G + 31) / 32;
+        int grid = grid_for(warps * 32, block, c->sms, 8);
+        kern<<<grid, block, 0, st>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, x, y, b, alpha);
+    };
+    if (avg <= 6) launch(k_spmv<4>, 4);
+    else if (avg <= 12) launch(k_spmv<8>, 8);
+    else if (avg <= 28) launch(k_spmv<16>, 16);
+    else launch(k_spmv<32>, 32);
+    launched(c);
+}
+
+// ---------------------------------------------------------------- vectors
+__global__ void k_fill(double *x, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) x[i] = v;
+}
+__global__ void k_axpy(int64_t n, double a, const double *x, double *y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] += a * x[i];
+}
+__global__ void k_axpby_to(int64_t n, const double *x, double a, const double *y, double *o) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) o[i] = x[i] + a * y[i];
+}
+__global__ void k_div_dev(int64_t n, const double *x, const double *num, double *o) {
+    const double d = *num;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) o[i] = x[i] / d;
+}
+
+void fill(Ctx *c, double *x, int64_t n, double v, cudaStream_t st) {
+    if (!n) return;
+    k_fill<<<grid_for(n, 256, c->sms), 256, 0, S(c, st)>>>(x, n, v);
+    launched(c);
+}
+void axpy(Ctx *c, int64_t n, double a, const double *x, double *y, cudaStream_t st) {
+    if (!n) return;
+    k_axpy<<<grid_for(n, 256, c->sms), 256, 0, S(c, st)>>>(n, a, x, y);
+    launched(c);
+}
+void axpby_to(Ctx *c, int64_t n, const double *x, double a, const double *y, double *o,
+              cudaStream_t st) {
+    if (!n) return;
+    k_axpby_to<<<grid_for(n, 256, c->sms), 256, 0, S(c, st)>>>(n, x, a, y, o);
+    launched(c);
+}
+void scale_by_dev(Ctx *c, int64_t n, const double *x, const double *num, double *o,
+                  cudaStream_t st) {
+    if (!n) return;
+    k_div_dev<<<grid_for(n, 256, c->sms), 256, 0, S(c, st)>>>(n, x, num, o);
+    launched(c);
+}
+
+// deterministic two-stage sum of squares -> sqrt
+__global__ void k_sumsq_partial(int64_t n, const double *x, double *part) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) s += x[i] * x[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        s = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) part[blockIdx.x] = s;
+    }
+}
+__global__ void k_sum_sqrt(int np, const double *part, double *out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += 32) s += part[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *out = sqrt(s);
+}
+
+void norm2_dev(Ctx *c, int64_t n, const double *x, double *out_dev, cudaStream_t st) {
+    st = S(c, st);
+    double *part = st == c->s2 ? c->nrm_part2 : c->nrm_part;
+    k_sumsq_partial<<<NRM_BLOCKS, 256, 0, st>>>(n, x, part);
+    launched(c);
+    k_sum_sqrt<<<1, 32, 0, st>>>(NRM_BLOCKS, part, out_dev);
+    launched(c);
+}
+
+double norm2(Ctx *c, int64_t n, const double *x) {
+    DBuf<double> o(1, c->s);
+    norm2_dev(c, n, x, o.p);
+    double h = 0;
+    CK(cudaMemcpyAsync(&h, o.p, sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return h;
+}
+
+struct Segs { int64_t d[4], s[4], l[4]; int n; };
+__global__ void k_copy_segs(double *dst, const double *src, Segs g) {
+    for (int k = 0; k < g.n; ++k)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.l[k]; i += (int64_t)gridDim.x * blockDim.x)
+            dst[g.d[k] + i] = src[g.s[k] + i];
+}
+void copy_segments(Ctx *c, double *dst, const double *src, int nseg, const int64_t *doff,
+                   const int64_t *soff, const int64_t *len, cudaStream_t st) {
+    Segs g{};
+    int64_t tot = 0;
+    if (nseg > 4) DPP_FAIL(DPP_ERR_VALUE, "copy_segments: too many segments");
+    g.n = nseg;
+    for (int k = 0; k < nseg; ++k) g.d[k] = doff[k], g.s[k] = soff[k], g.l[k] = len[k], tot = std::max(tot, len[k]);
+    if (!tot) return;
+    k_copy_segs<<<grid_for(tot, 256, c->sms), 256, 0, S(c, st)>>>(dst, src, g);
+    launched(c);
+}
+
+// ---------------------------------------------------------------- CSR utilities
+Csr csr_from_host(Ctx *c, int rows, int cols, int64_t nnz, const int *ptr, const int *idx,
+                  const double *val) {
+    Csr A;
+    A.alloc(rows, cols, nnz, c->s);
+    A.ptr.upload(ptr, (size_t)rows + 1);
+    A.idx.upload(idx, (size_t)nnz);
+    A.val.upload(val, (size_t)nnz);
+    return A;
+}
+
+Csr csr_copy(Ctx *c, const Csr &A) {
+    Csr B;
+    B.alloc(A.rows, A.cols, A.nnz, c->s);
+    CK(cudaMemcpyAsync(B.ptr.p, A.ptr.p, sizeof(int) * (A.rows + 1), cudaMemcpyDeviceToDevice, c->s));
+    if (A.nnz) {
+        CK(cudaMemcpyAsync(B.idx.p, A.idx.p, sizeof(int) * A.nnz, cudaMemcpyDeviceToDevice, c->s));
+        CK(cudaMemcpyAsync(B.val.p, A.val.p, sizeof(double) * A.nnz, cudaMemcpyDeviceToDevice, c->s));
+    }
+    return B;
+}
+
+Csr csr_empty(Ctx *c, int rows, int cols) {
+    Csr A;
+    A.alloc(rows, cols, 0, c->s);
+    CK(cudaMemsetAsync(A.ptr.p, 0, sizeof(int) * (rows + 1), c->s));
+    return A;
+}
+
+// row filter: keep entry p of row r when pred(r, col, val); warp per row, ordered compaction
+struct Pred {
+    int part;      // -1 strict lower, 0 diag, 1 strict upper, 2 lower+diag, 3 upper+diag, 9 all
+    bool nz;       // also require val != 0
+    __device__ bool operator()(int r, int j, double v) const {
+        bool ok;
+        switch (part) {
+            case -1: ok = j < r; break;
+            case 0: ok = j == r; break;
+            case 1: ok = j > r; break;
+            case 2: ok = j <= r; break;
+            case 3: ok = j >= r; break;
+            default: ok = true;
+        }
+        return ok && (!nz || v != 0.0);
+    }
+};
+
+__global__ void k_filter_count(int rows, const int *ptr, const int *idx, const double *val,
+                               Pred pr, int *cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int s = ptr[r], e = ptr[r + 1], n = 0;
+        for (int p = s + lane; p < e; p += 32) n += pr((int)r, idx[p], val[p]);
+        for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+        if (lane == 0) cnt[r] = n;
+    }
+}
+__global__ void k_filter_fill(int rows, const int *ptr, const int *idx, const double *val,
+                              Pred pr, const int *optr, int *oidx, double *oval) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int s = ptr[r], e = ptr[r + 1], w = optr[r];
+        for (int base = s; base < e; base += 32) {
+            int p = base + lane;
+            bool keep = p < e && pr((int)r, idx[p], val[p]);
+            unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                int pos = w + __popc(m & ((1u << lane) - 1));
+                oidx[pos] = idx[p];
+                oval[pos] = val[p];
+            }
+            w += __popc(m);
+        }
+    }
+}
+
+static Csr csr_filter(Ctx *c, const Csr &A, Pred pr) {
+    DBuf<int> cnt((size_t)A.rows, c->s);
+    int grid = grid_for((int64_t)A.rows * 32, 256, c->sms, 8);
+    if (A.rows) {
+        k_filter_count<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, pr, cnt.p);
+        launched(c);
+    }
+    Csr B;
+    B.rows = A.rows;
+    B.cols = A.cols;
+    B.nnz = counts_to_ptr(c, cnt.p, A.rows, B.ptr);
+    B.idx.alloc((size_t)B.nnz, c->s);
+    B.val.alloc((size_t)B.nnz, c->s);
+    if (A.rows) {
+        k_filter_fill<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, pr, B.ptr.p, B.idx.p,
+                                              B.val.p);
+        launched(c);
+    }
+    return B;
+}
+
+Csr csr_drop_zeros(Ctx *c, const Csr &A) { return csr_filter(c, A, Pred{9, true}); }
+Csr csr_part(Ctx *c, const Csr &A, int part, bool dz) { return csr_filter(c, A, Pred{part, dz}); }
+
+int64_t csr_count_nonzero(Ctx *c, const Csr &A) {
+    Csr B = csr_drop_zeros(c, A);
+    return B.nnz;
+}
+
+__global__ void k_diag(int rows, const int *ptr, const int *idx, const double *val, double *d,
+                       int *missing) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        bool found = false;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p)
+            if (idx[p] == r) { v += val[p]; found = true; }
+        d[r] = v;
+        if (!found && missing) atomicAdd(missing, 1);
+    }
+}
+void csr_diag(Ctx *c, const Csr &A, double *d, int *missing) {
+    int n = std::min(A.rows, A.cols);
+    if (!n) return;
+    k_diag<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, d, missing);
+    launched(c);
+}
+
+// transpose via stable radix sort of (col,row) keys: rows of A^T ascending in A's row
+__global__ void k_coo_keys(int rows, const int *ptr, const int *idx, uint64_t *key, int *pos) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
+            key[p] = ((uint64_t)(uint32_t)idx[p] << 32) | (uint32_t)r;
+            pos[p] = p;
+        }
+}
+__global__ void k_tr_fill(int64_t nnz, const uint64_t *key, const int *pos, const double *val,
+                          int *oidx, double *oval, int *cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
+        oidx[i] = (int)(key[i] & 0xffffffffu);
+        oval[i] = val[pos[i]];
+        atomicAdd(&cnt[key[i] >> 32], 1);
+    }
+}
+Csr csr_transpose(Ctx *c, const Csr &A) {
+    Csr T;
+    T.rows = A.cols;
+    T.cols = A.rows;
+    T.nnz = A.nnz;
+    DBuf<int> cnt((size_t)A.cols + 1, c->s);
+    CK(cudaMemsetAsync(cnt.p, 0, sizeof(int) * (A.cols + 1), c->s));
+    T.idx.alloc((size_t)A.nnz, c->s);
+    T.val.alloc((size_t)A.nnz, c->s);
+    if (A.nnz) {
+        DBuf<uint64_t> k0(A.nnz, c->s), k1(A.nnz, c->s);
+        DBuf<int> p0(A.nnz, c->s), p1(A.nnz, c->s);
+        k_coo_keys<<<grid_for(A.rows, 256, c->sms), 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, k0.p, p0.p);
+        launched(c);
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.p, k1.p, p0.p, p1.p, (int)A.nnz, 0, 64, c->s));
+        DBuf<char> t(tb, c->s);
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, k0.p, k1.p, p0.p, p1.p, (int)A.nnz, 0, 64, c->s));
+        launched(c);
+        k_tr_fill<<<grid_for(A.nnz, 256, c->sms), 256, 0, c->s>>>(A.nnz, k1.p, p1.p, A.val.p, T.idx.p, T.val.p, cnt.p);
+        launched(c);
+    }
+    counts_to_ptr(c, cnt.p, A.cols, T.ptr);
+    return T;
+}
+
+// submatrix by segment lists (blocksolve._submatrix: M[rows][:, cols], order preserving)
+__global__ void k_sub_count(int nr, const int *rowmap, const int *ptr, const int *idx,
+                            const int *colmap, int *cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nr;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int src = rowmap[r], n = 0;
+        for (int p = ptr[src] + lane; p < ptr[src + 1]; p += 32) n += colmap[idx[p]] >= 0;
+        for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+        if (lane == 0) cnt[r] = n;
+    }
+}
+__global__ void k_sub_fill(int nr, const int *rowmap, const int *ptr, const int *idx,
+                           const double *val, const int *colmap, const int *optr, int *oidx,
+                           double *oval) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nr;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int src = rowmap[r], w = optr[r], s = ptr[src], e = ptr[src + 1];
+        for (int base = s; base < e; base += 32) {
+            int p = base + lane;
+            int m = p < e ? colmap[idx[p]] : -1;
+            unsigned b = __ballot_sync(0xffffffffu, m >= 0);
+            if (m >= 0) {
+                int pos = w + __popc(b & ((1u << lane) - 1));
+                oidx[pos] = m;
+                oval[pos] = val[p];
+            }
+            w += __popc(b);
+        }
+    }
+}
+Csr csr_submatrix(Ctx *c, const Csr &M, const std::vector<std::pair<int, int>> &rowseg,
+                  const std::vector<std::pair<int, int>> &colseg) {
+    std::vector<int> rmap, cmap(M.cols, -1);
+    for (auto &s : rowseg)
+        for (int i = 0; i < s.second; ++i) rmap.push_back(s.first + i);
+    int nc = 0;
+    for (auto &s : colseg)
+        for (int i = 0; i < s.second; ++i) cmap[s.first + i] = nc++;
+    int nr = (int)rmap.size();
+    DBuf<int> drm(rmap.size(), c->s), dcm(cmap.size(), c->s), cnt(nr, c->s);
+    drm.upload(rmap.data(), rmap.size());
+    dcm.upload(cmap.data(), cmap.size());
+    int grid = grid_for((int64_t)nr * 32, 256, c->sms, 8);
+    if (nr) {
+        k_sub_count<<<grid, 256, 0, c->s>>>(nr, drm.p, M.ptr.p, M.idx.p, dcm.p, cnt.p);
+        launched(c);
+    }
+    Csr B;
+    B.rows = nr;
+    B.cols = nc;
+    B.nnz = counts_to_ptr(c, cnt.p, nr, B.ptr);
+    B.idx.alloc(B.nnz, c->s);
+    B.val.alloc(B.nnz, c->s);
+    if (nr) {
+        k_sub_fill<<<grid, 256, 0, c->s>>>(nr, drm.p, M.ptr.p, M.idx.p, M.val.p, dcm.p, B.ptr.p,
+                                           B.idx.p, B.val.p);
+        launched(c);
+    }
+    CK(cudaStreamSynchronize(c->s));  // host vectors go out of scope
+    return B;
+}
+
+// sp.bmat of a block grid: per output row concatenate the block rows left to right
+struct BGrid {
+    const int *ptr[16];
+    const int *idx[16];
+    const double *val[16];
+    int roff[5], coff[5];
+    int nbr, nbc;
+};
+__global__ void k_bmat_count(int rows, BGrid g, int *cnt) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        int I = 0;
+        while (r >= g.roff[I + 1]) ++I;
+        int lr = r - g.roff[I], n = 0;
+        for (int J = 0; J < g.nbc; ++J) {
+            const int *p = g.ptr[I * g.nbc + J];
+            if (p) n += p[lr + 1] - p[lr];
+        }
+        cnt[r] = n;
+    }
+}
+__global__ void k_bmat_fill(int rows, BGrid g, const int *optr, int *oidx, double *oval) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int I = 0;
+        while (r >= g.roff[I + 1]) ++I;
+        int lr = (int)r - g.roff[I], w = optr[r];
+        for (int J = 0; J < g.nbc; ++J) {
+            int b = I * g.nbc + J;
+            const int *p = g.ptr[b];
+            if (!p) continue;
+            int s = p[lr], e = p[lr + 1];
+            for (int q = s + lane; q < e; q += 32) {
+                oidx[w + q - s] = g.idx[b][q] + g.coff[J];
+                oval[w + q - s] = g.val[b][q];
+            }
+            w += e - s;
+        }
+    }
+}
+Csr csr_bmat(Ctx *c, const std::vector<const Csr *> &grid, int nbr, int nbc,
+             const std::vector<int> &rsz, const std::vector<int> &csz) {
+    BGrid g{};
+    g.nbr = nbr;
+    g.nbc = nbc;
+    g.roff[0] = g.coff[0] = 0;
+    for (int i = 0; i < nbr; ++i) g.roff[i + 1] = g.roff[i] + rsz[i];
+    for (int j = 0; j < nbc; ++j) g.coff[j + 1] = g.coff[j] + csz[j];
+    for (int b = 0; b < nbr * nbc; ++b) {
+        const Csr *B = grid[b];
+        if (B && B->nnz > 0) {
+            g.ptr[b] = B->ptr.p;
+            g.idx[b] = B->idx.p;
+            g.val[b] = B->val.p;
+        }
+    }
+    int rows = g.roff[nbr];
+    DBuf<int> cnt(rows, c->s);
+    k_bmat_count<<<grid_for(rows, 256, c->sms), 256, 0, c->s>>>(rows, g, cnt.p);
+    launched(c);
+    Csr K;
+    K.rows = rows;
+    K.cols = g.coff[nbc];
+    K.nnz = counts_to_ptr(c, cnt.p, rows, K.ptr);
+    K.idx.alloc(K.nnz, c->s);
+    K.val.alloc(K.nnz, c->s);
+    k_bmat_fill<<<grid_for((int64_t)rows * 32, 256, c->sms, 8), 256, 0, c->s>>>(rows, g, K.ptr.p,
+                                                                                   K.idx.p, K.val.p);
+    launched(c);
+    return K;
+}
+
+}  // namespace dpp

@@ -1,0 +1,208 @@
+// libdpp internals: context, device buffers, device CSR, shared kernel helpers.
+// sm_100a, FP64.  See DESIGN.md for the data layout in HBM.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/dpp.h"
+
+namespace dpp {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define DPP_FAIL(code, msg) throw ::dpp::Error((code), (msg))
+#define CK(x)                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw ::dpp::Error(DPP_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));  \
+    } while (0)
+
+struct Ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t s = nullptr;    // main stream
+    cudaStream_t s2 = nullptr;   // fork stream (concurrent branches of additive splits)
+    int64_t launches = 0;        // libdpp kernels launched (incl. graph replays' kernels)
+    int capturing = 0;
+    double *nrm_part = nullptr;  // NRM_BLOCKS partial sums (norm reductions on s)
+    double *nrm_part2 = nullptr; // same for s2
+    cudaEvent_t t0 = nullptr, t1 = nullptr;   // dpp_timer_*
+};
+constexpr int NRM_BLOCKS = 296;
+
+// record one kernel launch (checks launch errors outside graph capture)
+inline void launched(Ctx *c) {
+    c->launches++;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(DPP_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+// Stream-ordered device buffer.
+template <typename T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(size_t count, cudaStream_t st) { alloc(count, st); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count, cudaStream_t st) {
+        release();
+        s = st;
+        n = count;
+        if (count) {
+            cudaError_t e = cudaMallocAsync((void **)&p, sizeof(T) * count, st);
+            if (e != cudaSuccess)
+                throw Error(DPP_ERR_ALLOC, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+        }
+    }
+    void release() {
+        if (p) cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    void upload(const T *h, size_t count) {
+        if (count) CK(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+    }
+    void download(T *h, size_t count) const {
+        if (count) CK(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<T> to_host() const {
+        std::vector<T> v(n);
+        download(v.data(), n);
+        CK(cudaStreamSynchronize(s));
+        return v;
+    }
+};
+
+// Device CSR (int32 indices, FP64 values), scipy storage semantics.
+struct Csr {
+    int rows = 0, cols = 0;
+    int64_t nnz = 0;
+    DBuf<int> ptr, idx;
+    DBuf<double> val;
+    void alloc(int r, int c, int64_t z, cudaStream_t s) {
+        rows = r; cols = c; nnz = z;
+        ptr.alloc((size_t)r + 1, s);
+        idx.alloc((size_t)z, s);
+        val.alloc((size_t)z, s);
+    }
+};
+
+int64_t counts_to_ptr(Ctx *c, const int *counts, int n, DBuf<int> &ptr);
+
+inline int grid_for(int64_t work, int block, int sms, int per_sm = 16) {
+    int64_t g = (work + block - 1) / block;
+    int64_t cap = (int64_t)sms * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ---- core sparse / vector ops (core.cu) -----------------------------------
+void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b = nullptr,
+          double alpha = 1.0, cudaStream_t st = nullptr);   // y = b + alpha*A x (b may be null)
+void fill(Ctx *c, double *x, int64_t n, double v, cudaStream_t st = nullptr);
+void axpy(Ctx *c, int64_t n, double a, const double *x, double *y, cudaStream_t st = nullptr);
+void axpby_to(Ctx *c, int64_t n, const double *x, double a, const double *y, double *out,
+              cudaStream_t st = nullptr);                    // out = x + a*y
+void scale_by_dev(Ctx *c, int64_t n, const double *x, const double *num, double *out,
+                  cudaStream_t st = nullptr);                // out = x / *num
+void norm2_dev(Ctx *c, int64_t n, const double *x, double *out_dev, cudaStream_t st = nullptr);
+double norm2(Ctx *c, int64_t n, const double *x);
+void copy_segments(Ctx *c, double *dst, const double *src, int nseg, const int64_t *dst_off,
+                   const int64_t *src_off, const int64_t *len, cudaStream_t st = nullptr);
+Csr csr_from_host(Ctx *c, int rows, int cols, int64_t nnz, const int *ptr, const int *idx,
+                  const double *val);
+Csr csr_copy(Ctx *c, const Csr &A);
+Csr csr_empty(Ctx *c, int rows, int cols);
+Csr csr_drop_zeros(Ctx *c, const Csr &A);
+// part: -1 strict lower, 0 diag only, +1 strict upper, 2 lower incl diag, 3 upper incl diag
+Csr csr_part(Ctx *c, const Csr &A, int part, bool drop_zeros);
+void csr_diag(Ctx *c, const Csr &A, double *d_out, int *missing_dev);
+Csr csr_transpose(Ctx *c, const Csr &A);
+// rows/cols selected by segment lists of the parent index space (order preserving)
+Csr csr_submatrix(Ctx *c, const Csr &M, const std::vector<std::pair<int, int>> &rowseg,
+                  const std::vector<std::pair<int, int>> &colseg);
+// block grid (4x4 of optional blocks) -> one CSR (sp.bmat semantics, sorted, zeros kept)
+Csr csr_bmat(Ctx *c, const std::vector<const Csr *> &grid, int nbr, int nbc,
+             const std::vector<int> &rsz, const std::vector<int> &csz);
+int64_t csr_count_nonzero(Ctx *c, const Csr &A);
+
+// ---- SpGEMM (spgemm.cu) ----------------------------------------------------
+// C = D - (A*diag(s)) * B or C = A * B with the reference's accumulation order:
+// for each output row, products are accumulated over A's row entries in storage
+// order (descending when `reverse`), a'_ik = fl(a_ik * s_k) when s given,
+// acc = fl(acc + fl(a' * b)), exact zeros dropped (scipy csr_matmat / csr_binop).
+Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse,
+           const Csr *D, bool keep_zeros = false);
+
+// ---- triangular solves and ILU(0) (trsv.cu) --------------------------------
+struct Tri {              // one sweep: strict part (zero-free) + optional diagonal
+    Csr strict;
+    DBuf<double> diag;    // empty -> unit diagonal
+    bool backward = false;
+    int n = 0;
+};
+Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit);     // from a full matrix
+// x = T^{-1} b  (xout = xadd + x when xadd given); x/ticket are scratch of size n / 1
+void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const double *xadd,
+          double *xout, cudaStream_t st = nullptr);
+
+struct Ilu {
+    Ctx *ctx = nullptr;
+    Csr LU;             // factored values on A's pattern (sorted)
+    Tri L, U;
+    DBuf<double> tmp, y;
+    DBuf<int> ticket;
+    int n = 0;
+};
+std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A);
+void ilu_apply(Ctx *c, Ilu &f, const double *r, double *z, cudaStream_t st = nullptr);
+
+// ---- AMG (amg.cu) -----------------------------------------------------------
+struct AmgLevel {
+    Csr A, P, R;               // R = P^T
+    Tri lo, up;                // D+L, D+U
+    std::vector<int64_t> agg;  // host copy of aggregates
+    double rho = 0;
+    DBuf<double> b, x, r, t, y; // workspace
+    DBuf<int> ticket;
+};
+struct Amg {
+    Ctx *ctx = nullptr;
+    std::vector<std::unique_ptr<AmgLevel>> lv;
+    DBuf<double> coarse_inv;   // dense inverse of the coarsest operator (row-major)
+    int nc = 0;
+};
+std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A, double theta, double omega, int max_coarse,
+                               int max_levels, dpp_randn_fn randn, void *user);
+void amg_vcycle(Ctx *c, Amg &h, const double *r, double *z, cudaStream_t st = nullptr);
+
+// ---- launch bookkeeping for graph capture ----------------------------------
+struct Recorder { int64_t kernels = 0; };
+
+}  // namespace dpp
+
+// ---- opaque handles ----------------------------------------------------------
+struct dpp_ctx { dpp::Ctx c; };
+struct dpp_csr { dpp::Ctx *ctx; dpp::Csr m; };

@@ -1,0 +1,305 @@
+// Ordered row-merge SpGEMM with scipy's arithmetic (no FMA, zero dropping).
+//
+// Reference: linalg.schur_selfp (linalg.py:244-254) computes
+//   S = D - (C @ diag(1/dA)) @ B
+// through scipy's csr_matmat (per output row: sums[j] += a_ik*b_kj over the left
+// operand's entries in storage order, starting from 0, exact zeros dropped) and
+// csr_binop (d - x over the union, zeros dropped).  C @ diag(.) emits each row
+// in reverse first-touch order, i.e. descending k, so the second product
+// accumulates over k DESCENDING.  This kernel reproduces that bit-for-bit:
+// one warp per output row, a shared-memory open-addressing table keyed by
+// column, products accumulated k by k (__syncwarp between k) with separate
+// __dmul_rn / __dadd_rn, survivors rank-sorted into canonical CSR order.
+// Rows whose column bound exceeds the shared table use a per-row table in
+// global memory (same code path through generic pointers).
+#include "dpp_internal.cuh"
+
+namespace dpp {
+
+namespace {
+
+constexpr int SM_CAP = 512;   // slots per warp in shared memory
+constexpr int WPB = 2;        // warps per block
+
+struct Table {
+    int *key;
+    unsigned char *has;   // bit0: x present, bit1: d present
+    double *x, *d;
+    int *lk;
+    double *lv;
+    int cap;
+};
+
+__device__ __forceinline__ unsigned hsh(int j) { return (unsigned)j * 2654435761u; }
+
+__device__ __forceinline__ int tab_slot(Table &t, int j) {
+    unsigned h = hsh(j) & (t.cap - 1);
+    while (true) {
+        int old = atomicCAS(&t.key[h], -1, j);
+        if (old == -1 || old == j) return (int)h;
+        h = (h + 1) & (t.cap - 1);
+    }
+}
+
+struct Args {
+    int rows;
+    const int *ap, *ai;
+    const double *av;
+    const int *bp, *bi;
+    const double *bv;
+    const double *s;      // optional column scale of A
+    const int *dp, *di;   // optional D
+    const double *dv;
+    int reverse, keep_zeros;
+    const int64_t *goff;  // per-row global table offsets (or -1 => shared)
+    const int *gcap;
+    int *g_key;
+    unsigned char *g_has;
+    double *g_x, *g_d, *g_lv;
+    int *g_lk;
+    int *cnt;             // count pass output
+    const int *optr;      // fill pass input
+    int *oi;
+    double *ov;
+};
+
+template <bool FILL>
+__global__ void __launch_bounds__(32 * WPB) k_spgemm(Args a) {
+    extern __shared__ unsigned char smem[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t per = (size_t)SM_CAP * (4 + 1 + 8 + 8 + 4 + 8);
+    unsigned char *base = smem + per * w;
+    for (int64_t row = (int64_t)blockIdx.x * WPB + w; row < a.rows; row += (int64_t)gridDim.x * WPB) {
+        Table t;
+        const int64_t go = a.goff[row];
+        if (go < 0) {
+            t.cap = SM_CAP;
+            t.x = (double *)base;
+            t.d = t.x + SM_CAP;
+            t.lv = t.d + SM_CAP;
+            t.key = (int *)(t.lv + SM_CAP);
+            t.lk = t.key + SM_CAP;
+            t.has = (unsigned char *)(t.lk + SM_CAP);
+        } else {
+            t.cap = a.gcap[row];
+            t.key = a.g_key + go;
+            t.has = a.g_has + go;
+            t.x = a.g_x + go;
+            t.d = a.g_d + go;
+            t.lk = a.g_lk + go;
+            t.lv = a.g_lv + go;
+        }
+        for (int h = lane; h < t.cap; h += 32) { t.key[h] = -1; t.has[h] = 0; }
+        __syncwarp();
+        if (a.dp) {
+            for (int p = a.dp[row] + lane; p < a.dp[row + 1]; p += 32) {
+                int sl = tab_slot(t, a.di[p]);
+                t.d[sl] = a.dv[p];
+                t.has[sl] |= 2;
+            }
+            __syncwarp();
+        }
+        const int s = a.ap[row], e = a.ap[row + 1];
+        for (int q = 0; q < e - s; ++q) {
+            const int p = a.reverse ? e - 1 - q : s + q;
+            const int k = a.ai[p];
+            double av = a.av[p];
+            if (a.s) av = __dmul_rn(av, a.s[k]);
+            if (av == 0.0) continue;   // zero products never change a sum (scipy drops them)
+            for (int r = a.bp[k] + lane; r < a.bp[k + 1]; r += 32) {
+                const double bv = a.bv[r];
+                if (bv == 0.0) continue;
+                const double pr = __dmul_rn(av, bv);
+                int sl = tab_slot(t, a.bi[r]);
+                if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
+                else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
+            }
+            __syncwarp();
+        }
+        // survivors (slot order), then rank sort by column
+        int nsurv = 0;
+        for (int h0 = 0; h0 < t.cap; h0 += 32) {
+            const int h = h0 + lane;
+            bool keep = false;
+            double v = 0.0;
+            int j = -1;
+            if (h < t.cap && t.key[h] >= 0) {
+                const unsigned char f = t.has[h];
+                j = t.key[h];
+                if (f & 1) v = (f & 2) ? __dsub_rn(t.d[h], t.x[h]) : -t.x[h];
+                else v = t.d[h];
+                keep = a.keep_zeros || v != 0.0;
+            }
+            unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                int pos = nsurv + __popc(m & ((1u << lane) - 1));
+                t.lk[pos] = j;
+                t.lv[pos] = v;
+            }
+            nsurv += __popc(m);
+        }
+        __syncwarp();
+        if (!FILL) {
+            if (lane == 0) a.cnt[row] = nsurv;
+        } else {
+            const int o = a.optr[row];
+            for (int u = lane; u < nsurv; u += 32) {
+                const int j = t.lk[u];
+                int rank = 0;
+                for (int v = 0; v < nsurv; ++v) rank += t.lk[v] < j;
+                a.oi[o + rank] = j;
+                a.ov[o + rank] = t.lv[u];
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// upper bound of distinct columns per row -> table placement
+__global__ void k_bound(int rows, const int *ap, const int *ai, const int *bp, const int *dp,
+                        int bcols, int64_t *need) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        int64_t ub = dp ? dp[r + 1] - dp[r] : 0;
+        for (int p = ap[r]; p < ap[r + 1]; ++p) ub += bp[ai[p] + 1] - bp[ai[p]];
+        if (ub > bcols) ub = bcols;
+        need[r] = ub;
+    }
+}
+
+constexpr int UCAP = 4096;   // key-only slots per warp for the symbolic pass
+constexpr int UWPB = 2;
+
+__global__ void __launch_bounds__(32 * UWPB) k_unique(int rows, const int *ap, const int *ai,
+                                                      const int *bp, const int *bi, const int *dp,
+                                                      const int *di, const int64_t *goff,
+                                                      const int *gcap, int *gkey, int *uniq) {
+    __shared__ int sk[UWPB][UCAP];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t row = (int64_t)blockIdx.x * UWPB + w; row < rows; row += (int64_t)gridDim.x * UWPB) {
+        int *key;
+        int cap;
+        if (goff[row] < 0) { key = sk[w]; cap = UCAP; }
+        else { key = gkey + goff[row]; cap = gcap[row]; }
+        for (int h = lane; h < cap; h += 32) key[h] = -1;
+        __syncwarp();
+        int n = 0;
+        auto ins = [&](int j) {
+            unsigned h = hsh(j) & (cap - 1);
+            while (true) {
+                int old = atomicCAS(&key[h], -1, j);
+                if (old == -1) { ++n; return; }
+                if (old == j) return;
+                h = (h + 1) & (cap - 1);
+            }
+        };
+        if (dp)
+            for (int p = dp[row] + lane; p < dp[row + 1]; p += 32) ins(di[p]);
+        for (int p = ap[row]; p < ap[row + 1]; ++p) {
+            const int k = ai[p];
+            for (int r = bp[k] + lane; r < bp[k + 1]; r += 32) ins(bi[r]);
+        }
+        for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+        if (lane == 0) uniq[row] = n;
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse, const Csr *D,
+           bool keep_zeros) {
+    if (A.cols != B.rows) DPP_FAIL(DPP_ERR_VALUE, "spgemm: dimension mismatch");
+    if (D && (D->rows != A.rows || D->cols != B.cols)) DPP_FAIL(DPP_ERR_VALUE, "spgemm: D shape");
+    const int rows = A.rows;
+    Csr C;
+    C.rows = rows;
+    C.cols = B.cols;
+    if (rows == 0) {
+        C.ptr.alloc(1, c->s);
+        CK(cudaMemsetAsync(C.ptr.p, 0, sizeof(int), c->s));
+        return C;
+    }
+    // 1) bound of distinct columns per row; 2) exact distinct count; 3) table placement
+    DBuf<int64_t> need(rows, c->s);
+    k_bound<<<grid_for(rows, 256, c->sms), 256, 0, c->s>>>(rows, A.ptr.p, A.idx.p, B.ptr.p,
+                                                          D ? D->ptr.p : nullptr, B.cols, need.p);
+    launched(c);
+    std::vector<int64_t> h = need.to_host();
+    std::vector<int64_t> uoff(rows, -1);
+    std::vector<int> ucap(rows, 0);
+    int64_t utot = 0;
+    for (int r = 0; r < rows; ++r) {
+        if (h[r] < UCAP - 1) continue;
+        int cap = 64;
+        while (cap < 2 * h[r] + 2) cap <<= 1;
+        uoff[r] = utot;
+        ucap[r] = cap;
+        utot += cap;
+    }
+    std::vector<int> u(rows);
+    {
+        DBuf<int64_t> duoff(rows, c->s);
+        DBuf<int> ducap(rows, c->s), dkey(utot, c->s), duniq(rows, c->s);
+        duoff.upload(uoff.data(), rows);
+        ducap.upload(ucap.data(), rows);
+        k_unique<<<grid_for((int64_t)rows * 32, 32 * UWPB, c->sms, 12), 32 * UWPB, 0, c->s>>>(
+            rows, A.ptr.p, A.idx.p, B.ptr.p, B.idx.p, D ? D->ptr.p : nullptr,
+            D ? D->idx.p : nullptr, duoff.p, ducap.p, dkey.p, duniq.p);
+        launched(c);
+        duniq.download(u.data(), rows);
+        CK(cudaStreamSynchronize(c->s));
+    }
+    std::vector<int64_t> goff(rows, -1);
+    std::vector<int> gcap(rows, 0);
+    int64_t gtot = 0;
+    for (int r = 0; r < rows; ++r) {
+        if (2 * (int64_t)u[r] + 2 <= SM_CAP) continue;
+        int cap = 64;
+        while (cap < 2 * (int64_t)u[r] + 2) cap <<= 1;
+        goff[r] = gtot;
+        gcap[r] = cap;
+        gtot += cap;
+    }
+    DBuf<int64_t> dgoff(rows, c->s);
+    DBuf<int> dgcap(rows, c->s);
+    dgoff.upload(goff.data(), rows);
+    dgcap.upload(gcap.data(), rows);
+    DBuf<int> gk(gtot, c->s), glk(gtot, c->s);
+    DBuf<unsigned char> ghas(gtot, c->s);
+    DBuf<double> gx(gtot, c->s), gd(gtot, c->s), glv(gtot, c->s);
+    DBuf<int> cnt(rows, c->s);
+
+    Args a{};
+    a.rows = rows;
+    a.ap = A.ptr.p; a.ai = A.idx.p; a.av = A.val.p;
+    a.bp = B.ptr.p; a.bi = B.idx.p; a.bv = B.val.p;
+    a.s = s_dev;
+    if (D) { a.dp = D->ptr.p; a.di = D->idx.p; a.dv = D->val.p; }
+    a.reverse = reverse;
+    a.keep_zeros = keep_zeros;
+    a.goff = dgoff.p; a.gcap = dgcap.p;
+    a.g_key = gk.p; a.g_has = ghas.p; a.g_x = gx.p; a.g_d = gd.p; a.g_lk = glk.p; a.g_lv = glv.p;
+    a.cnt = cnt.p;
+    const size_t smem = (size_t)WPB * SM_CAP * (4 + 1 + 8 + 8 + 4 + 8);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_spgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_spgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int grid = grid_for((int64_t)rows * 32 * WPB / WPB, 32 * WPB, c->sms, 12);
+    k_spgemm<false><<<grid, 32 * WPB, smem, c->s>>>(a);
+    launched(c);
+    C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
+    C.idx.alloc(C.nnz, c->s);
+    C.val.alloc(C.nnz, c->s);
+    a.optr = C.ptr.p;
+    a.oi = C.idx.p;
+    a.ov = C.val.p;
+    k_spgemm<true><<<grid, 32 * WPB, smem, c->s>>>(a);
+    launched(c);
+    CK(cudaStreamSynchronize(c->s));   // host vectors above go out of scope
+    return C;
+}
+
+}  // namespace dpp

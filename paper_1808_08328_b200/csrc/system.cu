@@ -1,0 +1,51 @@
+// Block-system helpers: monolithic view (assembly.monolithic_view,
+// assembly.py:102-108) and small shared kernels.
+#include "system.cuh"
+
+namespace dpp {
+
+__global__ void k_reciprocal(int64_t n, const double *d, double *o) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = 1.0 / d[i];
+}
+void reciprocal(Ctx *c, int64_t n, const double *d, double *o) {
+    if (!n) return;
+    k_reciprocal<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d, o);
+    launched(c);
+}
+
+static void build_K(Ctx *c, dpp_system *s) {
+    if (s->hasK) return;
+    // (u1,p1,u2,p2) x (u1,p1,u2,p2) grid of reference blocks (assembly.py:88-93)
+    const Csr *g[16] = {nullptr};
+    auto at = [&](int r, int cc) -> const Csr *& { return g[r * 4 + cc]; };
+    at(0, 0) = &s->blk[DPP_K1_UU];
+    at(0, 1) = &s->blk[DPP_K1_UP];
+    at(1, 0) = &s->blk[DPP_K1_PU];
+    at(1, 1) = &s->blk[DPP_K1_PP];
+    at(1, 3) = &s->blk[DPP_K12_PP];
+    at(3, 1) = &s->blk[DPP_K21_PP];
+    at(2, 2) = &s->blk[DPP_K2_UU];
+    at(2, 3) = &s->blk[DPP_K2_UP];
+    at(3, 2) = &s->blk[DPP_K2_PU];
+    at(3, 3) = &s->blk[DPP_K2_PP];
+    std::vector<const Csr *> grid(g, g + 16);
+    std::vector<int> sz = {(int)s->sizes[0], (int)s->sizes[1], (int)s->sizes[2], (int)s->sizes[3]};
+    s->K = csr_bmat(c, grid, 4, 4, sz, sz);
+    s->Kc = csr_drop_zeros(c, s->K);
+    int64_t tot = s->sizes[0] + s->sizes[1] + s->sizes[2] + s->sizes[3], off = 0;
+    s->f.alloc(tot, c->s);
+    for (int k = 0; k < 4; ++k) {
+        if (s->sizes[k])
+            CK(cudaMemcpyAsync(s->f.p + off, s->rhs[k].p, sizeof(double) * s->sizes[k],
+                               cudaMemcpyDeviceToDevice, c->s));
+        off += s->sizes[k];
+    }
+    s->hasK = true;
+}
+
+const Csr &system_K(Ctx *c, dpp_system *s) { build_K(c, s); return s->K; }
+const Csr &system_Kc(Ctx *c, dpp_system *s) { build_K(c, s); return s->Kc; }
+const double *system_f(Ctx *c, dpp_system *s) { build_K(c, s); return s->f.p; }
+
+}  // namespace dpp
