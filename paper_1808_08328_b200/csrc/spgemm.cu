@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(32 * WPB) k_spgemm(Args a) {
             if (h < t.cap && t.key[h] >= 0) {
                 const unsigned char f = t.has[h];
                 j = t.key[h];
-                if (f & 1) v = (f & 2) ? __dsub_rn(t.d[h], t.x[h]) : -t.x[h];
+                if (!a.dp) v = t.x[h];                                   // C = A B
+                else if (f & 1) v = (f & 2) ? __dsub_rn(t.d[h], t.x[h]) : -t.x[h];   // D - X
                 else v = t.d[h];
                 keep = a.keep_zeros || v != 0.0;
             }

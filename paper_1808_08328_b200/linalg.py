@@ -172,7 +172,8 @@ def diag_lump(A) -> np.ndarray:
     if A.shape[0] != A.shape[1]:
         raise ValueError("diag_lump requires a square matrix")
     d = np.empty(A.shape[0])
-    N.call("dpp_diag", N.ctx(), as_device(A).h, N.ptr(d))
+    dA = as_device(A)          # keep the device copy alive across the call
+    N.call("dpp_diag", N.ctx(), dA.h, N.ptr(d))
     if np.any(d == 0.0):
         raise ZeroPivotError("zero diagonal entry in diag_lump")
     return d
@@ -186,8 +187,8 @@ def schur_selfp(D, C_, diagA: np.ndarray, B) -> sp.csr_matrix:
     if C_.shape[1] != len(diagA) or B.shape[0] != len(diagA) or D.shape != (C_.shape[0], B.shape[1]):
         raise ValueError("schur_selfp: non-conforming block dimensions")
     h = C.c_void_p()
-    N.call("dpp_schur_selfp", N.ctx(), as_device(D).h, as_device(C_).h, N.ptr(diagA),
-           as_device(B).h, C.byref(h))
+    dD, dC, dB = as_device(D), as_device(C_), as_device(B)
+    N.call("dpp_schur_selfp", N.ctx(), dD.h, dC.h, N.ptr(diagA), dB.h, C.byref(h))
     return DeviceCsr(h).to_scipy()
 
 
@@ -252,7 +253,8 @@ def amg_setup(A, *, theta: float = 0.5, omega: float = 2.0 / 3.0, max_coarse: in
     if A.shape[0] != A.shape[1]:
         raise ValueError("amg_setup requires a square matrix")
     h = C.c_void_p()
-    N.call("dpp_amg_create", N.ctx(), as_device(A).h, float(theta), float(omega), int(max_coarse),
+    dA = as_device(A)
+    N.call("dpp_amg_create", N.ctx(), dA.h, float(theta), float(omega), int(max_coarse),
            int(max_levels), N.RANDN, None, C.byref(h))
     return AmgHierarchy(h)
 
