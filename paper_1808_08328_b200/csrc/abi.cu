@@ -422,7 +422,10 @@ int dpp_solve(dpp_ctx *ctx, dpp_system *s, dpp_pc *pc, double rtol, int max_iter
         DBuf<double> dx(n, c->s);
         if (n) CK(cudaMemsetAsync(dx.p, 0, sizeof(double) * n, c->s));
         std::vector<double> hist;
-        gmres_dev(c, n, op, pm, f, dx.p, rtol, max_iter, restart, stats, &hist);
+        {
+            DPP_TRACE_SCOPE(c, "solve.gmres");
+            gmres_dev(c, n, op, pm, f, dx.p, rtol, max_iter, restart, stats, &hist);
+        }
         if (x) dx.download(x, n);
         CK(cudaStreamSynchronize(c->s));
         for (int i = 0; i < (int)hist.size() && i < history_cap; ++i) history[i] = hist[i];

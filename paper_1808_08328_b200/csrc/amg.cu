@@ -252,6 +252,7 @@ static void coarse_setup(Ctx *c, Amg &h, const Csr &A) {
 // ---------------------------------------------------------------- setup
 std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega, int max_coarse,
                                int max_levels, dpp_randn_fn randn, void *user) {
+    DPP_TRACE_SCOPE(c, "amg.total");
     if (A0.rows != A0.cols) DPP_FAIL(DPP_ERR_VALUE, "amg_setup requires a square matrix");
     auto h = std::make_unique<Amg>();
     h->ctx = c;
@@ -266,7 +267,11 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
     while (cur.rows > max_coarse && (int)h->lv.size() < max_levels - 1) {
         auto L = std::make_unique<AmgLevel>();
         const int n = cur.rows;
-        int64_t nc = aggregate(c, cur, theta, L->agg);
+        int64_t nc;
+        {
+            DPP_TRACE_SCOPE(c, "amg.aggregate");
+            nc = aggregate(c, cur, theta, L->agg);
+        }
         if (nc >= n) {
             if (n > 5000) DPP_FAIL(DPP_ERR_RUNTIME, "aggregation stalled on a large operator");
             break;
@@ -275,7 +280,10 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
         csr_diag(c, cur, d.p, nullptr);
         k_recip<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d.p, dinv.p);
         launched(c);
-        L->rho = spectral_radius(c, cur, dinv.p, randn, user);
+        {
+            DPP_TRACE_SCOPE(c, "amg.rho");
+            L->rho = spectral_radius(c, cur, dinv.p, randn, user);
+        }
         const double damping = 2.0 * omega / L->rho;
         std::vector<int> agg32(L->agg.begin(), L->agg.end());
         DBuf<int> dagg(n, c->s);
@@ -299,11 +307,21 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
                                                              dinv.p, damping, L->P.ptr.p, nullptr,
                                                              L->P.idx.p, L->P.val.p);
         launched(c);
-        L->R = csr_transpose(c, L->P);
-        Csr T = spgemm(c, L->R, cur, nullptr, false, nullptr);
-        Csr next = spgemm(c, T, L->P, nullptr, false, nullptr);
-        L->lo = make_tri(c, cur, true, false);
-        L->up = make_tri(c, cur, false, false);
+        Csr next;
+        {
+            DPP_TRACE_SCOPE(c, "amg.rap");
+            // A_c = P^T (A P): both products keep per-row distinct counts small enough
+            // for the shared-memory tables (the reference's (P^T A) P association
+            // differs only by rounding; coarse levels are insensitive)
+            L->R = csr_transpose(c, L->P);
+            Csr AP = spgemm(c, cur, L->P, nullptr, false, nullptr);
+            next = spgemm(c, L->R, AP, nullptr, false, nullptr);
+        }
+        {
+            DPP_TRACE_SCOPE(c, "amg.smoother_setup");
+            L->lo = make_tri(c, cur, true, false, true);
+            L->up = make_tri(c, cur, false, false, true);
+        }
         L->A = std::move(cur);
         for (DBuf<double> *b : {&L->b, &L->x, &L->r, &L->t, &L->y}) b->alloc(n, c->s);
         L->ticket.alloc(4, c->s);

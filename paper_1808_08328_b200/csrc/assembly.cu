@@ -838,7 +838,11 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
         launched(c);
         CK(cudaStreamSynchronize(c->s));
     }
-    Graph G = build_graph(c, keys, pay, ntot, nodes);
+    Graph G;
+    {
+        DPP_TRACE_SCOPE(c, "assemble.graph_sort");
+        G = build_graph(c, keys, pay, ntot, nodes);
+    }
     keys.release();
     pay.release();
     const int64_t g = G.nnz;
@@ -1155,7 +1159,13 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
             for (int n = 0; n < 2; ++n)
                 if (bc->n_vfacets[n] > 0)
                     DPP_FAIL(DPP_ERR_VALUE, "prescribed-velocity boundary facets are not supported by the device assembler yet");
-        DevMesh &m = dev_mesh(c, hm);
+        DPP_TRACE_SCOPE(c, "assemble.total");
+        DevMesh *mp;
+        {
+            DPP_TRACE_SCOPE(c, "assemble.mesh_upload");
+            mp = &dev_mesh(c, hm);
+        }
+        DevMesh &m = *mp;
         auto S = std::make_unique<dpp_system>();
         S->ctx = c;
         if (formulation == DPP_HDIV) {
@@ -1174,9 +1184,15 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
             S->rhs[k].alloc(S->sizes[k], c->s);
             if (S->sizes[k]) CK(cudaMemsetAsync(S->rhs[k].p, 0, sizeof(double) * S->sizes[k], c->s));
         }
-        if (formulation == DPP_HDIV) assemble_hdiv(c, hm, m, *p, *S);
-        else assemble_vms(c, hm, m, *p, formulation == DPP_DGVMS, *S);
-        boundary_rhs(c, m, formulation, bc, *S);
+        {
+            DPP_TRACE_SCOPE(c, "assemble.blocks");
+            if (formulation == DPP_HDIV) assemble_hdiv(c, hm, m, *p, *S);
+            else assemble_vms(c, hm, m, *p, formulation == DPP_DGVMS, *S);
+        }
+        {
+            DPP_TRACE_SCOPE(c, "assemble.rhs");
+            boundary_rhs(c, m, formulation, bc, *S);
+        }
         CK(cudaStreamSynchronize(c->s));
         S->assembly_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         *out = S.release();

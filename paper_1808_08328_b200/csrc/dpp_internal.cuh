@@ -42,6 +42,23 @@ struct Ctx {
 };
 constexpr int NRM_BLOCKS = 296;
 
+// Optional phase tracer (DPP_TRACE=1): synchronises the stream at scope
+// boundaries and prints wall-clock milliseconds per named phase to stderr.
+struct TraceScope {
+    Ctx *c;
+    const char *name;
+    double t0;
+    static bool on();
+    static double now();
+    TraceScope(Ctx *cc, const char *n) : c(cc), name(n), t0(0) {
+        if (on()) { cudaStreamSynchronize(c->s); t0 = now(); }
+    }
+    ~TraceScope();
+};
+#define DPP_CAT2(a, b) a##b
+#define DPP_CAT(a, b) DPP_CAT2(a, b)
+#define DPP_TRACE_SCOPE(c, name) ::dpp::TraceScope DPP_CAT(dpp_trace_scope_, __LINE__)((c), (name))
+
 // record one kernel launch (checks launch errors outside graph capture)
 inline void launched(Ctx *c) {
     c->launches++;
@@ -157,13 +174,29 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
            const Csr *D, bool keep_zeros = false);
 
 // ---- triangular solves and ILU(0) (trsv.cu) --------------------------------
+struct ClusterPlan {      // level-ordered per-CTA blocks for the cluster sweep (tricluster.cu)
+    int C = 0, chunk = 0, L = 0, G = 32, stage = 0, nst = 0, threads = 1024;
+    DBuf<unsigned char> blocks;
+    DBuf<long long> boff;
+};
 struct Tri {              // one sweep: strict part (zero-free) + optional diagonal
     Csr strict;
     DBuf<double> diag;    // empty -> unit diagonal
+    DBuf<int> order;      // rows in (dependency level, row) order: the sweep's ticket order
+    DBuf<int> levptr;     // level l = order[levptr[l] .. levptr[l+1])
+    std::unique_ptr<ClusterPlan> cl;   // cluster-resident sweep when x fits in one cluster
+    DBuf<double> dense;   // optional dense inverse (small coarse levels): sweep = triangular GEMV
     bool backward = false;
-    int n = 0;
+    int n = 0, nlev = 0;
 };
-Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit);     // from a full matrix
+// dependency levels of a strict triangle -> topological (level, row) order
+int tri_levels(Ctx *c, const Csr &strict, bool backward, DBuf<int> &order, DBuf<int> *levptr = nullptr,
+               DBuf<int> *lev_out = nullptr);
+bool cluster_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L);
+void trsv_cluster(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+                  cudaStream_t st);
+constexpr int DENSE_TRI_MAX = 1024;
+Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense = false);
 // x = T^{-1} b  (xout = xadd + x when xadd given); x/ticket are scratch of size n / 1
 void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const double *xadd,
           double *xout, cudaStream_t st = nullptr);

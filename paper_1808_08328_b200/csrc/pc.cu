@@ -142,8 +142,12 @@ struct Builder {
         N->segB = segs(gB);
         for (auto &s : N->segA) N->nA += s.second;
         for (auto &s : N->segB) N->nB += s.second;
-        Csr A = csr_submatrix(c, M, N->segA, N->segA);
-        Csr D = csr_submatrix(c, M, N->segB, N->segB);
+        Csr A, D;
+        {
+            DPP_TRACE_SCOPE(c, "pc.submatrix");
+            A = csr_submatrix(c, M, N->segA, N->segA);
+            D = csr_submatrix(c, M, N->segB, N->segB);
+        }
         for (DBuf<double> *b : {&N->rA, &N->zA, &N->zA2, &N->w}) b->alloc(N->nA, c->s);
         for (DBuf<double> *b : {&N->rB, &N->zB, &N->t}) b->alloc(N->nB, c->s);
         if (nd.split_type == DPP_SPLIT_ADDITIVE) {
@@ -167,7 +171,11 @@ struct Builder {
                 if (v == 0.0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero diagonal entry in diag_lump");
         }
         reciprocal(c, N->nA, d.p, dinv.p);
-        Csr S = spgemm(c, C, B, dinv.p, true, &D);
+        Csr S;
+        {
+            DPP_TRACE_SCOPE(c, "pc.selfp_spgemm");
+            S = spgemm(c, C, B, dinv.p, true, &D);
+        }
         N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA);
         N->b = leaf(nd.child_type[1], nd.child_node[1], S, gB);
         N->Bc = csr_drop_zeros(c, B);
@@ -208,7 +216,13 @@ dpp_pc *pc_create(Ctx *c, dpp_system *s, const dpp_split_node *nodes, int n_node
     CK(cudaEventRecord(e0, c->s));
     auto pc = std::make_unique<dpp_pc>();
     pc->ctx = c;
-    const Csr &K = system_K(c, s);
+    DPP_TRACE_SCOPE(c, "pc.total");
+    const Csr *Kp;
+    {
+        DPP_TRACE_SCOPE(c, "pc.monolithic");
+        Kp = &system_K(c, s);
+    }
+    const Csr &K = *Kp;
     Builder b{c, nodes, n_nodes, s->sizes, randn, user};
     pc->root = b.node(0, K, {0, 1, 2, 3});
     pc->n = K.rows;

@@ -12,6 +12,8 @@
 // __dmul_rn / __dadd_rn, survivors rank-sorted into canonical CSR order.
 // Rows whose column bound exceeds the shared table use a per-row table in
 // global memory (same code path through generic pointers).
+#include <cstdio>
+
 #include "dpp_internal.cuh"
 
 namespace dpp {
@@ -167,8 +169,8 @@ __global__ void k_bound(int rows, const int *ap, const int *ai, const int *bp, c
     }
 }
 
-constexpr int UCAP = 4096;   // key-only slots per warp for the symbolic pass
-constexpr int UWPB = 2;
+constexpr int UCAP = 8192;   // key-only slots per warp for the symbolic pass
+constexpr int UWPB = 1;
 
 __global__ void __launch_bounds__(32 * UWPB) k_unique(int rows, const int *ap, const int *ai,
                                                       const int *bp, const int *bi, const int *dp,
@@ -220,6 +222,7 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         CK(cudaMemsetAsync(C.ptr.p, 0, sizeof(int), c->s));
         return C;
     }
+    DPP_TRACE_SCOPE(c, "spgemm");
     // 1) bound of distinct columns per row; 2) exact distinct count; 3) table placement
     DBuf<int64_t> need(rows, c->s);
     k_bound<<<grid_for(rows, 256, c->sms), 256, 0, c->s>>>(rows, A.ptr.p, A.idx.p, B.ptr.p,
@@ -289,6 +292,12 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         attr = true;
     }
     const int grid = grid_for((int64_t)rows * 32 * WPB / WPB, 32 * WPB, c->sms, 12);
+    if (TraceScope::on()) {
+        int nglob = 0;
+        for (int r = 0; r < rows; ++r) nglob += goff[r] >= 0;
+        std::fprintf(stderr, "[dpp-trace]   spgemm %d x %d (A nnz %lld, B nnz %lld): %d rows global, gtot %lld\n",
+                     rows, B.cols, (long long)A.nnz, (long long)B.nnz, nglob, (long long)gtot);
+    }
     k_spgemm<false><<<grid, 32 * WPB, smem, c->s>>>(a);
     launched(c);
     C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);

@@ -2,7 +2,25 @@
 // assembly.py:102-108) and small shared kernels.
 #include "system.cuh"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 namespace dpp {
+
+bool TraceScope::on() {
+    static int v = -1;
+    if (v < 0) { const char *e = std::getenv("DPP_TRACE"); v = e && *e && *e != '0'; }
+    return v == 1;
+}
+double TraceScope::now() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+TraceScope::~TraceScope() {
+    if (!on()) return;
+    cudaStreamSynchronize(c->s);
+    std::fprintf(stderr, "[dpp-trace] %-28s %9.3f ms\n", name, now() - t0);
+}
 
 __global__ void k_reciprocal(int64_t n, const double *d, double *o) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)

@@ -18,6 +18,10 @@
 //    factors are bitwise those of the reference.
 // Deadlock freedom: a warp only waits on rows with an earlier ticket, which
 // are owned by warps that are already running.
+#include <cub/cub.cuh>
+
+#include <cstdlib>
+
 #include "dpp_internal.cuh"
 
 namespace dpp {
@@ -44,7 +48,181 @@ __device__ __forceinline__ void st_release(int *p, int v) {
 }
 
 // ------------------------------------------------------------------ TRSV
-__global__ void __launch_bounds__(128) k_trsv(int n, int backward, const int *__restrict__ ptr,
+// ------------------------------------------------------------------ level analysis
+// One thread per row, all threads resident, rows dealt round-robin across warps
+// (consecutive rows land in different warps); a row's level is 1 + the max level
+// of the rows it reads.  Smallest unfinished row is always runnable -> progress.
+__global__ void __launch_bounds__(256) k_levels(int n, int backward, const int *__restrict__ ptr,
+                                                const int *__restrict__ idx, int *level) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t W = T >> 5, w = g >> 5, lane = g & 31;
+    for (int64_t base = 0; base < n; base += T) {
+        const int64_t t = base + lane * W + w;
+        if (t >= n) continue;
+        const int row = backward ? n - 1 - (int)t : (int)t;
+        int lv = 0;
+        for (int p = ptr[row]; p < ptr[row + 1]; ++p) {
+            const int j = idx[p];
+            int lj = ld_acquire(level + j);
+            long long spins = 0;
+            while (lj < 0) {
+                lj = ld_acquire(level + j);
+                if (++spins > SPIN_LIMIT) __trap();
+            }
+            lv = max(lv, lj + 1);
+        }
+        st_release(level + row, lv);
+    }
+}
+
+// warp per row (small matrices with long rows: coarse AMG levels)
+__global__ void __launch_bounds__(256) k_levels_warp(int n, int backward, const int *__restrict__ ptr,
+                                                     const int *__restrict__ idx, int *level) {
+    const int lane = threadIdx.x & 31;
+    const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += W) {
+        const int row = backward ? n - 1 - (int)t : (int)t;
+        int lv = 0;
+        for (int p = ptr[row] + lane; p < ptr[row + 1]; p += 32) {
+            const int j = idx[p];
+            int lj = ld_acquire(level + j);
+            long long spins = 0;
+            while (lj < 0) {
+                lj = ld_acquire(level + j);
+                if (++spins > SPIN_LIMIT) __trap();
+            }
+            lv = max(lv, lj + 1);
+        }
+        for (int o = 16; o > 0; o >>= 1) lv = max(lv, __shfl_xor_sync(0xffffffffu, lv, o));
+        if (lane == 0) st_release(level + row, lv);
+    }
+}
+
+__global__ void k_iota(int n, int *a) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a[i] = i;
+}
+__global__ void k_maxlev(int n, const int *lv, int *mx) {
+    int m = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = max(m, lv[i]);
+    atomicMax(mx, m);
+}
+
+__global__ void k_levptr(int n, const int *sorted_lev, int nlev, int *levptr) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+        if (i == n) { levptr[nlev] = n; continue; }
+        const int l = sorted_lev[i];
+        const int prev = i ? sorted_lev[i - 1] : -1;
+        for (int k = prev + 1; k <= l; ++k) levptr[k] = i;
+    }
+}
+
+int tri_levels(Ctx *c, const Csr &S, bool backward, DBuf<int> &order, DBuf<int> *levptr,
+               DBuf<int> *lev_out) {
+    DPP_TRACE_SCOPE(c, "tri_levels");
+    const int n = S.rows;
+    order.alloc(n, c->s);
+    if (!n) return 0;
+    DBuf<int> lev(n, c->s), lev2(n, c->s), rows(n, c->s), mx(1, c->s);
+    CK(cudaMemsetAsync(lev.p, 0xFF, sizeof(int) * n, c->s));
+    CK(cudaMemsetAsync(mx.p, 0, sizeof(int), c->s));
+    // every thread of the grid must be resident (waits are on other threads' rows)
+    const int block = 256;
+    int per_sm = 0, per_sm_w = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels, block, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, k_levels_warp, block, 0));
+    if (per_sm < 1 || per_sm_w < 1) DPP_FAIL(DPP_ERR_CUDA, "level analysis kernels cannot be resident");
+    const int64_t warps_res = (int64_t)c->sms * per_sm_w * (block / 32);
+    const double avg = n ? (double)S.nnz / n : 0.0;
+    if (n <= warps_res && avg > 8.0) {
+        const int grid = (int)(((int64_t)n * 32 + block - 1) / block);
+        k_levels_warp<<<grid, block, 0, c->s>>>(n, backward, S.ptr.p, S.idx.p, lev.p);
+    } else {
+        const int64_t need = ((int64_t)n + 31) / 32 * 32;
+        const int64_t cap = (int64_t)c->sms * per_sm * block;
+        const int grid = (int)((std::min(need, cap) + block - 1) / block);
+        k_levels<<<grid, block, 0, c->s>>>(n, backward, S.ptr.p, S.idx.p, lev.p);
+    }
+    launched(c);
+    k_iota<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, rows.p);
+    launched(c);
+    k_maxlev<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, lev.p, mx.p);
+    launched(c);
+    int hmx = 0;
+    CK(cudaMemcpyAsync(&hmx, mx.p, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    int bits = 1;
+    while (bits < 31 && (1 << bits) <= hmx) ++bits;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, lev.p, lev2.p, rows.p, order.p, n, 0, bits, c->s));
+    DBuf<char> t(tb, c->s);
+    CK(cub::DeviceRadixSort::SortPairs(t.p, tb, lev.p, lev2.p, rows.p, order.p, n, 0, bits, c->s));
+    launched(c);
+    if (lev_out) {
+        lev_out->alloc(n, c->s);
+        CK(cudaMemcpyAsync(lev_out->p, lev.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, c->s));
+    }
+    if (levptr) {
+        levptr->alloc((size_t)hmx + 2, c->s);
+        k_levptr<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(n, lev2.p, hmx + 1, levptr->p);
+        launched(c);
+    }
+    CK(cudaStreamSynchronize(c->s));
+    return hmx + 1;
+}
+
+// ------------------------------------------------------------------ dense inverses (small levels)
+__global__ void k_tri_dense(int n, const int *ptr, const int *idx, const double *val, const double *diag,
+                            double *T) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) T[(int64_t)r * n + idx[p]] += val[p];
+        T[(int64_t)r * n + r] += diag ? diag[r] : 1.0;
+    }
+}
+// column c of T^-1 by substitution: one warp per column, the column lives in
+// shared memory, each step is a lane-parallel dot product over a row of T
+constexpr int INV_WPB = 4;
+__global__ void __launch_bounds__(32 * INV_WPB) k_tri_inverse(int n, int backward, const double *__restrict__ T,
+                                                             double *Ti) {
+    extern __shared__ double col[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *x = col + (size_t)w * n;
+    for (int c = blockIdx.x * INV_WPB + w; c < n; c += gridDim.x * INV_WPB) {
+        for (int i = lane; i < n; i += 32) x[i] = 0.0;
+        __syncwarp();
+        for (int s = 0; s < n; ++s) {
+            const int i = backward ? c - s : c + s;
+            if (i < 0 || i >= n) break;
+            const int j0 = backward ? i + 1 : c, j1 = backward ? c + 1 : i;
+            double acc = 0.0;
+            for (int j = j0 + lane; j < j1; j += 32) acc += T[(int64_t)i * n + j] * x[j];
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) x[i] = ((i == c ? 1.0 : 0.0) - acc) / T[(int64_t)i * n + i];
+            __syncwarp();
+        }
+        for (int i = lane; i < n; i += 32) Ti[(int64_t)i * n + c] = x[i];
+        __syncwarp();
+    }
+}
+// x = Ti b over the triangle's nonzero half; xout = xadd + x
+__global__ void k_tri_gemv(int n, int backward, const double *__restrict__ Ti, const double *__restrict__ b,
+                           double *x, const double *__restrict__ xadd, double *xout) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int j0 = backward ? (int)r : 0, j1 = backward ? n : (int)r + 1;
+        double s = 0.0;
+        for (int j = j0 + lane; j < j1; j += 32) s += Ti[r * n + j] * b[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            x[r] = s;
+            if (xout) xout[r] = xadd[r] + s;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(128) k_trsv(int n, const int *__restrict__ order, const int *__restrict__ ptr,
                                               const int *__restrict__ idx,
                                               const double *__restrict__ val,
                                               const double *__restrict__ diag,
@@ -56,8 +234,15 @@ __global__ void __launch_bounds__(128) k_trsv(int n, int backward, const int *__
         if (lane == 0) t = atomicAdd(ticket, 1);
         t = __shfl_sync(0xffffffffu, t, 0);
         if (t >= n) return;
-        const int row = backward ? n - 1 - t : t;
+        const int row = order[t];
         const int s = ptr[row], e = ptr[row + 1];
+        // per-row constants first: their latency must not follow the dependency wait
+        double bi = 0.0, di = 1.0, ai = 0.0;
+        if (lane == 0) {
+            bi = b[row];
+            if (diag) di = diag[row];
+            if (xout) ai = xadd[row];
+        }
         double sum = 0.0;
         for (int p = s + lane; p < e; p += 32) {
             const int j = idx[p];
@@ -73,11 +258,11 @@ __global__ void __launch_bounds__(128) k_trsv(int n, int backward, const int *__
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
         if (lane == 0) {
-            double xi = b[row] - sum;
-            if (diag) xi = xi / diag[row];
+            double xi = bi - sum;
+            if (diag) xi = xi / di;
             if (__double_as_longlong(xi) == (long long)SENT) xi = __longlong_as_double(0x7ff8000000000000ll);
             st_relaxed(x + row, xi);
-            if (xout) xout[row] = xadd[row] + xi;
+            if (xout) xout[row] = ai + xi;
         }
     }
 }
@@ -86,16 +271,26 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
           double *xout, cudaStream_t st) {
     st = st ? st : c->s;
     if (T.n == 0) return;
+    if (T.dense.n) {
+        k_tri_gemv<<<grid_for((int64_t)T.n * 32, 256, c->sms, 8), 256, 0, st>>>(T.n, T.backward, T.dense.p, b,
+                                                                               x, xadd, xout);
+        launched(c);
+        return;
+    }
+    if (T.cl) {
+        trsv_cluster(c, T, b, x, xadd, xout, st);
+        return;
+    }
     CK(cudaMemsetAsync(x, 0xFF, sizeof(double) * T.n, st));
     CK(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     const int warps = std::min<int64_t>(T.n, (int64_t)c->sms * 32);
     const int grid = (warps + 3) / 4;
-    k_trsv<<<grid, 128, 0, st>>>(T.n, T.backward, T.strict.ptr.p, T.strict.idx.p, T.strict.val.p,
+    k_trsv<<<grid, 128, 0, st>>>(T.n, T.order.p, T.strict.ptr.p, T.strict.idx.p, T.strict.val.p,
                                  T.diag.n ? T.diag.p : nullptr, b, x, ticket, xadd, xout);
     launched(c);
 }
 
-Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit) {
+Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense) {
     Tri T;
     T.n = A.rows;
     T.backward = !lower;
@@ -104,6 +299,27 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit) {
         T.diag.alloc(A.rows, c->s);
         csr_diag(c, A, T.diag.p, nullptr);
     }
+    if (allow_dense && T.n <= DENSE_TRI_MAX) {
+        // exact-arithmetic rewrite for small, deep coarse levels: x = T^-1 b as a GEMV
+        const int n = T.n;
+        DBuf<double> D((size_t)n * n, c->s);
+        CK(cudaMemsetAsync(D.p, 0, sizeof(double) * n * n, c->s));
+        T.dense.alloc((size_t)n * n, c->s);
+        k_tri_dense<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, T.strict.ptr.p, T.strict.idx.p, T.strict.val.p,
+                                                              T.diag.n ? T.diag.p : nullptr, D.p);
+        launched(c);
+        const size_t sm = (size_t)INV_WPB * n * sizeof(double);
+        CK(cudaFuncSetAttribute(k_tri_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        k_tri_inverse<<<(n + INV_WPB - 1) / INV_WPB, 32 * INV_WPB, sm, c->s>>>(n, T.backward, D.p, T.dense.p);
+        launched(c);
+        CK(cudaStreamSynchronize(c->s));
+        T.nlev = n;
+        return T;
+    }
+    DBuf<int> lev;
+    T.nlev = tri_levels(c, T.strict, T.backward, T.order, nullptr, &lev);
+    static const bool no_cluster = [] { const char *e = std::getenv("DPP_NO_CLUSTER"); return e && *e == '1'; }();
+    if (!no_cluster) cluster_plan(c, T, lev, T.nlev);
     return T;
 }
 
@@ -124,7 +340,8 @@ constexpr int ILU_WPB = 4;
 __global__ void __launch_bounds__(32 * ILU_WPB) k_ilu0(int n, const int *__restrict__ ptr,
                                                        const int *__restrict__ idx, double *val,
                                                        const int *__restrict__ dpos, int *done,
-                                                       int *ticket, int *err_row) {
+                                                       int *ticket, int *err_row,
+                                                       const int *__restrict__ order) {
     __shared__ double sv[ILU_WPB][ILU_CAP];
     __shared__ int sc[ILU_WPB][ILU_CAP];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,6 +350,7 @@ __global__ void __launch_bounds__(32 * ILU_WPB) k_ilu0(int n, const int *__restr
         if (lane == 0) i = atomicAdd(ticket, 1);
         i = __shfl_sync(0xffffffffu, i, 0);
         if (i >= n) return;
+        i = order[i];
         const int s = ptr[i], e = ptr[i + 1], len = e - s;
         const bool big = len > ILU_CAP;
         double *v = big ? val + s : sv[w];
@@ -183,6 +401,7 @@ __global__ void __launch_bounds__(32 * ILU_WPB) k_ilu0(int n, const int *__restr
 }
 
 std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
+    DPP_TRACE_SCOPE(c, "ilu0.total");
     if (A.rows != A.cols) DPP_FAIL(DPP_ERR_VALUE, "ilu0 requires a square matrix");
     auto f = std::make_unique<Ilu>();
     f->ctx = c;
@@ -201,10 +420,16 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
     CK(cudaMemcpyAsync(&hm, missing, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
     if (hm) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "missing diagonal entry in sparsity pattern");
+    DBuf<int> order;
+    {
+        Csr lower = csr_part(c, A, -1, false);   // stored pattern: every row the IKJ loop may read
+        tri_levels(c, lower, false, order);
+    }
+    DPP_TRACE_SCOPE(c, "ilu0.factor_kernel");
     if (n) {
         const int warps = std::min<int64_t>(n, (int64_t)c->sms * 16);
         k_ilu0<<<(warps + ILU_WPB - 1) / ILU_WPB, 32 * ILU_WPB, 0, c->s>>>(
-            n, f->LU.ptr.p, f->LU.idx.p, f->LU.val.p, dpos.p, flags.p, ticket, err);
+            n, f->LU.ptr.p, f->LU.idx.p, f->LU.val.p, dpos.p, flags.p, ticket, err, order.p);
         launched(c);
     }
     int he = 0;
