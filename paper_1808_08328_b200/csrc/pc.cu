@@ -9,7 +9,10 @@
 // with S_p = D - C diag(A)^-1 B built by the ordered SpGEMM.  Leaves are
 // bjacobi -> ILU(0) and hypre -> smoothed-aggregation AMG V-cycle.
 // The whole apply is captured once into a CUDA graph and replayed.
+#include <cstdlib>
+#include <exception>
 #include <string>
+#include <thread>
 
 #include "dpp_internal.cuh"
 #include "system.cuh"
@@ -27,7 +30,22 @@ struct PcLeaf {
     void apply(Ctx *c, const double *r, double *z, cudaStream_t st);
 };
 
+// Side stream of an additive node: the second child is built (on a host
+// thread) and applied (in the captured graph) on it.  Declared first in
+// PcNode so it is destroyed last, after every buffer freed on it.
+struct SideStream {
+    cudaStream_t s = nullptr;
+    Ctx ctx;   // view of the parent context whose stream is the side stream
+    ~SideStream() {
+        if (!s) return;
+        cudaStreamSynchronize(s);
+        if (ctx.nrm_part) cudaFree(ctx.nrm_part);
+        cudaStreamDestroy(s);
+    }
+};
+
 struct PcNode {
+    SideStream side_owner;
     int split = 0;
     int n = 0, nA = 0, nB = 0;
     std::vector<std::pair<int, int>> segA, segB;   // (offset, length) in the local space
@@ -40,7 +58,6 @@ struct PcNode {
     ~PcNode() {
         if (ev_fork) cudaEventDestroy(ev_fork);
         if (ev_join) cudaEventDestroy(ev_join);
-        if (side) cudaStreamDestroy(side);
     }
     void apply(Ctx *c, const double *r, double *z, cudaStream_t st);
 };
@@ -151,9 +168,48 @@ struct Builder {
         for (DBuf<double> *b : {&N->rA, &N->zA, &N->zA2, &N->w}) b->alloc(N->nA, c->s);
         for (DBuf<double> *b : {&N->rB, &N->zB, &N->t}) b->alloc(N->nB, c->s);
         if (nd.split_type == DPP_SPLIT_ADDITIVE) {
-            N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA);
-            N->b = leaf(nd.child_type[1], nd.child_node[1], D, gB);
-            CK(cudaStreamCreateWithFlags(&N->side, cudaStreamNonBlocking));
+            // the two children are independent: build B on the side stream from a
+            // second host thread while A is built here (both pore networks of the
+            // scale split, both AMG hierarchies of the field split's Schur leaf)
+            CK(cudaStreamCreateWithFlags(&N->side_owner.s, cudaStreamNonBlocking));
+            N->side = N->side_owner.s;
+            Ctx &sc = N->side_owner.ctx;
+            sc = *c;
+            sc.s = sc.s2 = N->side;
+            sc.launches = 0;
+            sc.t0 = sc.t1 = nullptr;
+            CK(cudaMalloc(&sc.nrm_part, sizeof(double) * NRM_BLOCKS));
+            sc.nrm_part2 = sc.nrm_part;
+            CK(cudaStreamSynchronize(c->s));
+            std::exception_ptr err;
+            static const bool serial = [] { const char *e = std::getenv("DPP_SERIAL_SETUP"); return e && *e == '1'; }();
+            if (serial) {
+                Builder bb = *this;
+                bb.c = &sc;
+                N->b = bb.leaf(nd.child_type[1], nd.child_node[1], D, gB);
+                CK(cudaStreamSynchronize(sc.s));
+            }
+            std::thread tb([&, nd, gB] {
+                if (serial) return;
+                try {
+                    CK(cudaSetDevice(sc.device));
+                    Builder bb = *this;
+                    bb.c = &sc;
+                    N->b = bb.leaf(nd.child_type[1], nd.child_node[1], D, gB);
+                    CK(cudaStreamSynchronize(sc.s));
+                } catch (...) {
+                    err = std::current_exception();
+                }
+            });
+            try {
+                N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA);
+            } catch (...) {
+                tb.join();
+                throw;
+            }
+            tb.join();
+            if (err) std::rethrow_exception(err);
+            c->launches += sc.launches;
             CK(cudaEventCreateWithFlags(&N->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&N->ev_join, cudaEventDisableTiming));
             N->desc = "additive(" + N->a.desc + ", " + N->b.desc + ")";

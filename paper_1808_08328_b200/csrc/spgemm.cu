@@ -20,8 +20,9 @@ namespace dpp {
 
 namespace {
 
-constexpr int SM_CAP = 512;   // slots per warp in shared memory
-constexpr int WPB = 2;        // warps per block
+constexpr int SM_CAP = 512;     // slots per warp in shared memory (rows with <= 255 distinct columns)
+constexpr int WPB = 2;          // warps per block
+constexpr int SM_CAP_L = 4096;  // large rows (<= 2047 distinct columns): one warp per block
 
 struct Table {
     int *key;
@@ -65,23 +66,27 @@ struct Args {
     double *ov;
 };
 
-template <bool FILL>
-__global__ void __launch_bounds__(32 * WPB) k_spgemm(Args a) {
+// CLS: -1 = the row's table is in shared memory of capacity CAP, class chosen
+// by goff: -1 small rows (CAP = SM_CAP), -2 large rows (CAP = SM_CAP_L);
+// goff >= 0 rows use a global table (processed by the small-row launch)
+template <bool FILL, int CAP, int W>
+__global__ void __launch_bounds__(32 * W) k_spgemm(Args a, int cls) {
     extern __shared__ unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t per = (size_t)SM_CAP * (4 + 1 + 8 + 8 + 4 + 8);
+    const size_t per = (size_t)CAP * (4 + 1 + 8 + 8 + 4 + 8);
     unsigned char *base = smem + per * w;
-    for (int64_t row = (int64_t)blockIdx.x * WPB + w; row < a.rows; row += (int64_t)gridDim.x * WPB) {
+    for (int64_t row = (int64_t)blockIdx.x * W + w; row < a.rows; row += (int64_t)gridDim.x * W) {
         Table t;
         const int64_t go = a.goff[row];
+        if (cls == -1 ? go == -2 : go != -2) continue;   // not this launch's class
         if (go < 0) {
-            t.cap = SM_CAP;
+            t.cap = CAP;
             t.x = (double *)base;
-            t.d = t.x + SM_CAP;
-            t.lv = t.d + SM_CAP;
-            t.key = (int *)(t.lv + SM_CAP);
-            t.lk = t.key + SM_CAP;
-            t.has = (unsigned char *)(t.lk + SM_CAP);
+            t.d = t.x + CAP;
+            t.lv = t.d + CAP;
+            t.key = (int *)(t.lv + CAP);
+            t.lk = t.key + CAP;
+            t.has = (unsigned char *)(t.lk + CAP);
         } else {
             t.cap = a.gcap[row];
             t.key = a.g_key + go;
@@ -256,8 +261,10 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
     std::vector<int64_t> goff(rows, -1);
     std::vector<int> gcap(rows, 0);
     int64_t gtot = 0;
+    int nlarge = 0;
     for (int r = 0; r < rows; ++r) {
         if (2 * (int64_t)u[r] + 2 <= SM_CAP) continue;
+        if (2 * (int64_t)u[r] + 2 <= SM_CAP_L) { goff[r] = -2; ++nlarge; continue; }
         int cap = 64;
         while (cap < 2 * (int64_t)u[r] + 2) cap <<= 1;
         goff[r] = gtot;
@@ -285,29 +292,41 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
     a.g_key = gk.p; a.g_has = ghas.p; a.g_x = gx.p; a.g_d = gd.p; a.g_lk = glk.p; a.g_lv = glv.p;
     a.cnt = cnt.p;
     const size_t smem = (size_t)WPB * SM_CAP * (4 + 1 + 8 + 8 + 4 + 8);
+    const size_t smem_l = (size_t)SM_CAP_L * (4 + 1 + 8 + 8 + 4 + 8);
     static bool attr = false;
     if (!attr) {
-        CK(cudaFuncSetAttribute(k_spgemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute(k_spgemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_spgemm<false, SM_CAP, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_spgemm<true, SM_CAP, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_spgemm<false, SM_CAP_L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l));
+        CK(cudaFuncSetAttribute(k_spgemm<true, SM_CAP_L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l));
         attr = true;
     }
     const int grid = grid_for((int64_t)rows * 32 * WPB / WPB, 32 * WPB, c->sms, 12);
+    const int grid_l = std::max(1, std::min(nlarge, c->sms));
     if (TraceScope::on()) {
         int nglob = 0;
         for (int r = 0; r < rows; ++r) nglob += goff[r] >= 0;
-        std::fprintf(stderr, "[dpp-trace]   spgemm %d x %d (A nnz %lld, B nnz %lld): %d rows global, gtot %lld\n",
-                     rows, B.cols, (long long)A.nnz, (long long)B.nnz, nglob, (long long)gtot);
+        std::fprintf(stderr, "[dpp-trace]   spgemm %d x %d (A nnz %lld, B nnz %lld): %d large, %d global, gtot %lld\n",
+                     rows, B.cols, (long long)A.nnz, (long long)B.nnz, nlarge, nglob, (long long)gtot);
     }
-    k_spgemm<false><<<grid, 32 * WPB, smem, c->s>>>(a);
+    k_spgemm<false, SM_CAP, WPB><<<grid, 32 * WPB, smem, c->s>>>(a, -1);
     launched(c);
+    if (nlarge) {
+        k_spgemm<false, SM_CAP_L, 1><<<grid_l, 32, smem_l, c->s>>>(a, -2);
+        launched(c);
+    }
     C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
     C.idx.alloc(C.nnz, c->s);
     C.val.alloc(C.nnz, c->s);
     a.optr = C.ptr.p;
     a.oi = C.idx.p;
     a.ov = C.val.p;
-    k_spgemm<true><<<grid, 32 * WPB, smem, c->s>>>(a);
+    k_spgemm<true, SM_CAP, WPB><<<grid, 32 * WPB, smem, c->s>>>(a, -1);
     launched(c);
+    if (nlarge) {
+        k_spgemm<true, SM_CAP_L, 1><<<grid_l, 32, smem_l, c->s>>>(a, -2);
+        launched(c);
+    }
     CK(cudaStreamSynchronize(c->s));   // host vectors above go out of scope
     return C;
 }

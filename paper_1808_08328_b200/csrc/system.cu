@@ -19,7 +19,14 @@ double TraceScope::now() {
 TraceScope::~TraceScope() {
     if (!on()) return;
     cudaStreamSynchronize(c->s);
-    std::fprintf(stderr, "[dpp-trace] %-28s %9.3f ms\n", name, now() - t0);
+    cudaMemPool_t pool;
+    unsigned long long res = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) {
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    std::fprintf(stderr, "[dpp-trace] %-28s %9.3f ms   pool reserved %7.1f MB used %7.1f MB\n", name,
+                 now() - t0, res / 1048576.0, used / 1048576.0);
 }
 
 __global__ void k_reciprocal(int64_t n, const double *d, double *o) {
