@@ -179,12 +179,18 @@ struct ClusterPlan {      // level-ordered per-CTA blocks for the cluster sweep 
     DBuf<unsigned char> blocks;
     DBuf<long long> boff;
 };
+struct BlockPlan {        // block-sequential sweep with dense diagonal-block inverses (triblock.cu)
+    int nblk = 0, stage = 0, nst = 0;
+    DBuf<unsigned char> blocks;
+    DBuf<long long> boff;
+};
 struct Tri {              // one sweep: strict part (zero-free) + optional diagonal
     Csr strict;
     DBuf<double> diag;    // empty -> unit diagonal
     DBuf<int> order;      // rows in (dependency level, row) order: the sweep's ticket order
     DBuf<int> levptr;     // level l = order[levptr[l] .. levptr[l+1])
     std::unique_ptr<ClusterPlan> cl;   // cluster-resident sweep when x fits in one cluster
+    std::unique_ptr<BlockPlan> bl;     // block-sequential sweep (small n, narrow levels)
     DBuf<double> dense;   // optional dense inverse (small coarse levels): sweep = triangular GEMV
     bool backward = false;
     int n = 0, nlev = 0;
@@ -193,6 +199,9 @@ struct Tri {              // one sweep: strict part (zero-free) + optional diago
 int tri_levels(Ctx *c, const Csr &strict, bool backward, DBuf<int> &order, DBuf<int> *levptr = nullptr,
                DBuf<int> *lev_out = nullptr);
 bool cluster_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L);
+bool block_plan(Ctx *c, Tri &T);
+void trsv_block(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+                cudaStream_t st);
 void trsv_cluster(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
                   cudaStream_t st);
 constexpr int DENSE_TRI_MAX = 1024;

@@ -20,6 +20,7 @@
 // are owned by warps that are already running.
 #include <cub/cub.cuh>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "dpp_internal.cuh"
@@ -277,6 +278,10 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
         launched(c);
         return;
     }
+    if (T.bl) {
+        trsv_block(c, T, b, x, xadd, xout, st);
+        return;
+    }
     if (T.cl) {
         trsv_cluster(c, T, b, x, xadd, xout, st);
         return;
@@ -318,6 +323,12 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense) {
     }
     DBuf<int> lev;
     T.nlev = tri_levels(c, T.strict, T.backward, T.order, nullptr, &lev);
+    // narrow, deep levels (coarse AMG): block-sequential sweep with dense block inverses
+    static const bool no_block = [] { const char *e = std::getenv("DPP_NO_BLOCK"); return e && *e == '1'; }();
+    if (TraceScope::on())
+        std::fprintf(stderr, "[dpp-trace]   make_tri n=%d nnz=%lld levels=%d backward=%d\n", T.n,
+                     (long long)T.strict.nnz, T.nlev, (int)T.backward);
+    if (!no_block && T.n <= 8192 && (int64_t)T.nlev * 64 > T.n && block_plan(c, T)) return T;
     static const bool no_cluster = [] { const char *e = std::getenv("DPP_NO_CLUSTER"); return e && *e == '1'; }();
     if (!no_cluster) cluster_plan(c, T, lev, T.nlev);
     return T;
