@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(CL_THREADS, 1)
             }
 #pragma unroll
             for (int s = G / 2; s > 0; s >>= 1) sum += __shfl_xor_sync(gmask, sum, s, G);
-            if (gl == 0) xs[r] = (xs[r] - sum) / dg[q];
+            if (gl == 0) xs[r] = (xs[r] - sum) * dg[q];   // dg = 1/t_ii (as SuperLU's pre-scaled solve)
         }
     }
     level_barrier(C);
@@ -178,7 +178,7 @@ __global__ void k_block_fill(int n, int chunk, const int *skey, const int *perm,
         if (i == 0) { reinterpret_cast<int *>(B)[0] = nr; reinterpret_cast<int *>(B)[1] = ne; }
         reinterpret_cast<int *>(B + 16)[i] = r - owner * chunk;
         reinterpret_cast<int *>(B + 16 + pad16(4 * nr))[i] = rptr[q + 1] - rptr[q0];
-        reinterpret_cast<double *>(B + 16 + 2 * pad16(4 * nr))[i] = diag ? diag[r] : 1.0;
+        reinterpret_cast<double *>(B + 16 + 2 * pad16(4 * nr))[i] = diag ? 1.0 / diag[r] : 1.0;
         int *ci = reinterpret_cast<int *>(B + 16 + 2 * pad16(4 * nr) + 8 * nr);
         double *vv = reinterpret_cast<double *>(B + 16 + 2 * pad16(4 * nr) + 8 * nr + pad16(4 * ne));
         int w = rptr[q] - rptr[q0];
@@ -253,8 +253,11 @@ static bool try_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     P->stage = (int)stage;
     P->nst = nst;
     const double avg = (double)T.strict.nnz / n;
-    P->G = avg <= 4 ? 4 : avg <= 8 ? 8 : avg <= 16 ? 16 : 32;
-    int threads = 128;
+    // ~4 entries per lane; threads sized to the widest (CTA, level) so idle warps
+    // do not pay the per-level instruction overhead
+    P->G = 2;
+    while (P->G < 32 && P->G * 4 < avg) P->G *= 2;
+    int threads = 64;
     while (threads < CL_THREADS && (threads / P->G) < widest) threads *= 2;
     P->threads = threads;
     P->blocks.alloc((size_t)total, c->s);
@@ -281,13 +284,16 @@ bool cluster_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
             CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_LIMIT));
             CK(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
         };
+        setk((const void *)k_trsv_cluster<2>);
         setk((const void *)k_trsv_cluster<4>);
         setk((const void *)k_trsv_cluster<8>);
         setk((const void *)k_trsv_cluster<16>);
         setk((const void *)k_trsv_cluster<32>);
         attr = true;
     }
-    for (int C = (n + XS_MAX - 1) / XS_MAX; C <= CL_MAX; ++C)
+    // as many CTAs as useful: each keeps >= ~2k rows of x
+    int C0 = std::max((n + XS_MAX - 1) / XS_MAX, std::min(CL_MAX, (n + 2047) / 2048));
+    for (int C = C0; C <= CL_MAX; ++C)
         if (try_plan(c, T, lev, L, C)) return true;
     return false;
 }
@@ -311,6 +317,7 @@ void trsv_cluster(Ctx *c, const Tri &T, const double *b, double *x, const double
     const long long *O = P.boff.p;
     cudaError_t e;
     switch (P.G) {
+        case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_cluster<2>, T.n, P.chunk, P.L, P.C, P.stage, P.nst, B, O, b, x, xadd, xout); break;
         case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_cluster<4>, T.n, P.chunk, P.L, P.C, P.stage, P.nst, B, O, b, x, xadd, xout); break;
         case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_cluster<8>, T.n, P.chunk, P.L, P.C, P.stage, P.nst, B, O, b, x, xadd, xout); break;
         case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_cluster<16>, T.n, P.chunk, P.L, P.C, P.stage, P.nst, B, O, b, x, xadd, xout); break;
