@@ -106,22 +106,50 @@ __global__ void __launch_bounds__(32 * W) k_spgemm(Args a, int cls) {
             }
             __syncwarp();
         }
-        const int s = a.ap[row], e = a.ap[row + 1];
-        for (int q = 0; q < e - s; ++q) {
-            const int p = a.reverse ? e - 1 - q : s + q;
-            const int k = a.ai[p];
-            double av = a.av[p];
-            if (a.s) av = __dmul_rn(av, a.s[k]);
-            if (av == 0.0) continue;   // zero products never change a sum (scipy drops them)
-            for (int r = a.bp[k] + lane; r < a.bp[k + 1]; r += 32) {
-                const double bv = a.bv[r];
-                if (bv == 0.0) continue;
-                const double pr = __dmul_rn(av, bv);
-                int sl = tab_slot(t, a.bi[r]);
-                if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
-                else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
+        // A's row is fetched 32 entries at a time (k, scaled a_ik, B-row bounds in lane
+        // registers); the next k's B entries are prefetched while the current k is
+        // accumulated, so the k-ordered loop does not wait on global memory.
+        const int s = a.ap[row], e = a.ap[row + 1], len = e - s;
+        for (int q0 = 0; q0 < len; q0 += 32) {
+            int bs = 0, be = 0;
+            double aq = 0.0;
+            if (q0 + lane < len) {
+                const int p = a.reverse ? e - 1 - (q0 + lane) : s + q0 + lane;
+                const int kq = a.ai[p];
+                aq = a.av[p];
+                if (a.s) aq = __dmul_rn(aq, a.s[kq]);
+                bs = a.bp[kq];
+                be = a.bp[kq + 1];
             }
-            __syncwarp();
+            const int cnt = min(32, len - q0);
+            int cj = -1;
+            double cb = 0.0;
+            {
+                const int rs = __shfl_sync(0xffffffffu, bs, 0), re = __shfl_sync(0xffffffffu, be, 0);
+                if (rs + lane < re) { cj = a.bi[rs + lane]; cb = a.bv[rs + lane]; }
+            }
+            for (int qq = 0; qq < cnt; ++qq) {
+                const double av = __shfl_sync(0xffffffffu, aq, qq);
+                const int rs = __shfl_sync(0xffffffffu, bs, qq), re = __shfl_sync(0xffffffffu, be, qq);
+                const int ns = __shfl_sync(0xffffffffu, bs, (qq + 1) & 31), ne = __shfl_sync(0xffffffffu, be, (qq + 1) & 31);
+                int nj = -1;
+                double nbv = 0.0;
+                if (qq + 1 < cnt && ns + lane < ne) { nj = a.bi[ns + lane]; nbv = a.bv[ns + lane]; }
+                if (av != 0.0) {   // zero products never change a sum (scipy drops them)
+                    auto acc = [&](int j, double bv) {
+                        if (bv == 0.0) return;
+                        const double pr = __dmul_rn(av, bv);
+                        const int sl = tab_slot(t, j);
+                        if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
+                        else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
+                    };
+                    if (cj >= 0) acc(cj, cb);
+                    for (int r = rs + 32 + lane; r < re; r += 32) acc(a.bi[r], a.bv[r]);
+                    __syncwarp();
+                }
+                cj = nj;
+                cb = nbv;
+            }
         }
         // survivors (slot order), then rank sort by column
         int nsurv = 0;
@@ -202,9 +230,19 @@ __global__ void __launch_bounds__(32 * UWPB) k_unique(int rows, const int *ap, c
         };
         if (dp)
             for (int p = dp[row] + lane; p < dp[row + 1]; p += 32) ins(di[p]);
-        for (int p = ap[row]; p < ap[row + 1]; ++p) {
-            const int k = ai[p];
-            for (int r = bp[k] + lane; r < bp[k + 1]; r += 32) ins(bi[r]);
+        const int s = ap[row], len = ap[row + 1] - s;
+        for (int q0 = 0; q0 < len; q0 += 32) {
+            int bs = 0, be = 0;
+            if (q0 + lane < len) {
+                const int kq = ai[s + q0 + lane];
+                bs = bp[kq];
+                be = bp[kq + 1];
+            }
+            const int cnt = min(32, len - q0);
+            for (int qq = 0; qq < cnt; ++qq) {
+                const int rs = __shfl_sync(0xffffffffu, bs, qq), re = __shfl_sync(0xffffffffu, be, qq);
+                for (int r = rs + lane; r < re; r += 32) ins(bi[r]);
+            }
         }
         for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
         if (lane == 0) uniq[row] = n;

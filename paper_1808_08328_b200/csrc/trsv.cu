@@ -62,16 +62,22 @@ __global__ void __launch_bounds__(256) k_levels(int n, int backward, const int *
         const int64_t t = base + lane * W + w;
         if (t >= n) continue;
         const int row = backward ? n - 1 - (int)t : (int)t;
+        // dependencies in batches of 8 loads in flight; spin only on the ones not ready
         int lv = 0;
-        for (int p = ptr[row]; p < ptr[row + 1]; ++p) {
-            const int j = idx[p];
-            int lj = ld_acquire(level + j);
-            long long spins = 0;
-            while (lj < 0) {
-                lj = ld_acquire(level + j);
-                if (++spins > SPIN_LIMIT) __trap();
+        for (int p0 = ptr[row]; p0 < ptr[row + 1]; p0 += 8) {
+            const int cnt = min(8, ptr[row + 1] - p0);
+            int lj[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) lj[u] = u < cnt ? ld_acquire(level + idx[p0 + u]) : 0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                long long spins = 0;
+                while (lj[u] < 0) {
+                    lj[u] = ld_acquire(level + idx[p0 + u]);
+                    if (++spins > SPIN_LIMIT) __trap();
+                }
+                lv = max(lv, lj[u] + 1);
             }
-            lv = max(lv, lj + 1);
         }
         st_release(level + row, lv);
     }
