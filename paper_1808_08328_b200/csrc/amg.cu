@@ -11,6 +11,9 @@
 //  apply:            V(1,1) with SGS (forward then backward GS as x += T^-1 (b - A x)),
 //                    restriction P^T, prolongation P, coarse dense solve.
 #include <cmath>
+#include <cstdlib>
+#include <exception>
+#include <thread>
 
 #include "dpp_internal.cuh"
 
@@ -264,6 +267,20 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
             if (v == 0.0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "structurally singular input: zero diagonal entry");
     }
     Csr cur = csr_copy(c, A0);
+    // smoother setup (level analysis + sweep plans) of level l runs on a worker
+    // thread / side stream while this thread builds level l+1
+    h->side.ensure(c);
+    std::thread worker;
+    std::exception_ptr werr;
+    auto join_worker = [&] {
+        if (worker.joinable()) worker.join();
+        if (werr) std::rethrow_exception(werr);
+    };
+    static const bool serial = [] { const char *e = std::getenv("DPP_SERIAL_SETUP"); return e && *e == '1'; }();
+    struct Joiner {
+        std::thread &t;
+        ~Joiner() { if (t.joinable()) t.join(); }
+    } joiner{worker};
     while (cur.rows > max_coarse && (int)h->lv.size() < max_levels - 1) {
         auto L = std::make_unique<AmgLevel>();
         const int n = cur.rows;
@@ -317,18 +334,38 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
             Csr AP = spgemm(c, cur, L->P, nullptr, false, nullptr);
             next = spgemm(c, L->R, AP, nullptr, false, nullptr);
         }
-        {
-            DPP_TRACE_SCOPE(c, "amg.smoother_setup");
-            L->lo = make_tri(c, cur, true, false, true);
-            L->up = make_tri(c, cur, false, false, true);
-        }
         L->A = std::move(cur);
         for (DBuf<double> *b : {&L->b, &L->x, &L->r, &L->t, &L->y}) b->alloc(n, c->s);
         L->ticket.alloc(4, c->s);
+        CK(cudaStreamSynchronize(c->s));
+        join_worker();
+        AmgLevel *Lp = L.get();
+        Ctx *sc = &h->side.ctx;
+        auto smoother = [Lp, sc] {
+            DPP_TRACE_SCOPE(sc, "amg.smoother_setup");
+            Lp->lo = make_tri(sc, Lp->A, true, false, true);
+            Lp->up = make_tri(sc, Lp->A, false, false, true);
+            CK(cudaStreamSynchronize(sc->s));
+        };
+        if (serial) {
+            smoother();
+        } else {
+            worker = std::thread([smoother, sc, &werr] {
+                try {
+                    CK(cudaSetDevice(sc->device));
+                    smoother();
+                } catch (...) {
+                    werr = std::current_exception();
+                }
+            });
+        }
         h->lv.push_back(std::move(L));
         cur = std::move(next);
         CK(cudaStreamSynchronize(c->s));
     }
+    join_worker();
+    c->launches += h->side.ctx.launches;
+    h->side.ctx.launches = 0;
     auto last = std::make_unique<AmgLevel>();
     coarse_setup(c, *h, cur);
     const int n = cur.rows;

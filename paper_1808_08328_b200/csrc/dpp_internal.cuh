@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -125,6 +126,20 @@ struct Csr {
     }
 };
 
+// ---- host task parallelism for setup ----------------------------------------
+// A side stream plus a context view bound to it.  Objects built through the
+// view allocate (and later free) on the side stream, so the owner of those
+// objects must also own the SideStream and destroy it last.
+struct SideStream {
+    cudaStream_t s = nullptr;
+    Ctx ctx;
+    void ensure(Ctx *parent);
+    ~SideStream();
+};
+// run side(view) on a host thread with the side stream while main_fn() runs here
+void fork_join(Ctx *c, SideStream &owner, const std::function<void(Ctx *)> &side,
+               const std::function<void()> &main_fn);
+
 int64_t counts_to_ptr(Ctx *c, const int *counts, int n, DBuf<int> &ptr);
 
 inline int grid_for(int64_t work, int block, int sms, int per_sm = 16) {
@@ -231,6 +246,7 @@ struct AmgLevel {
     DBuf<int> ticket;
 };
 struct Amg {
+    SideStream side;           // smoother setup of level l overlaps the Galerkin product of l+1
     Ctx *ctx = nullptr;
     std::vector<std::unique_ptr<AmgLevel>> lv;
     DBuf<double> coarse_inv;   // dense inverse of the coarsest operator (row-major)

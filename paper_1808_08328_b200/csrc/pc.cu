@@ -30,20 +30,6 @@ struct PcLeaf {
     void apply(Ctx *c, const double *r, double *z, cudaStream_t st);
 };
 
-// Side stream of an additive node: the second child is built (on a host
-// thread) and applied (in the captured graph) on it.  Declared first in
-// PcNode so it is destroyed last, after every buffer freed on it.
-struct SideStream {
-    cudaStream_t s = nullptr;
-    Ctx ctx;   // view of the parent context whose stream is the side stream
-    ~SideStream() {
-        if (!s) return;
-        cudaStreamSynchronize(s);
-        if (ctx.nrm_part) cudaFree(ctx.nrm_part);
-        cudaStreamDestroy(s);
-    }
-};
-
 struct PcNode {
     SideStream side_owner;
     int split = 0;
@@ -171,45 +157,15 @@ struct Builder {
             // the two children are independent: build B on the side stream from a
             // second host thread while A is built here (both pore networks of the
             // scale split, both AMG hierarchies of the field split's Schur leaf)
-            CK(cudaStreamCreateWithFlags(&N->side_owner.s, cudaStreamNonBlocking));
+            N->side_owner.ensure(c);
             N->side = N->side_owner.s;
-            Ctx &sc = N->side_owner.ctx;
-            sc = *c;
-            sc.s = sc.s2 = N->side;
-            sc.launches = 0;
-            sc.t0 = sc.t1 = nullptr;
-            CK(cudaMalloc(&sc.nrm_part, sizeof(double) * NRM_BLOCKS));
-            sc.nrm_part2 = sc.nrm_part;
-            CK(cudaStreamSynchronize(c->s));
-            std::exception_ptr err;
-            static const bool serial = [] { const char *e = std::getenv("DPP_SERIAL_SETUP"); return e && *e == '1'; }();
-            if (serial) {
-                Builder bb = *this;
-                bb.c = &sc;
-                N->b = bb.leaf(nd.child_type[1], nd.child_node[1], D, gB);
-                CK(cudaStreamSynchronize(sc.s));
-            }
-            std::thread tb([&, nd, gB] {
-                if (serial) return;
-                try {
-                    CK(cudaSetDevice(sc.device));
-                    Builder bb = *this;
-                    bb.c = &sc;
-                    N->b = bb.leaf(nd.child_type[1], nd.child_node[1], D, gB);
-                    CK(cudaStreamSynchronize(sc.s));
-                } catch (...) {
-                    err = std::current_exception();
-                }
-            });
-            try {
-                N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA);
-            } catch (...) {
-                tb.join();
-                throw;
-            }
-            tb.join();
-            if (err) std::rethrow_exception(err);
-            c->launches += sc.launches;
+            fork_join(c, N->side_owner,
+                      [&](Ctx *sc) {
+                          Builder bb = *this;
+                          bb.c = sc;
+                          N->b = bb.leaf(nd.child_type[1], nd.child_node[1], D, gB);
+                      },
+                      [&] { N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA); });
             CK(cudaEventCreateWithFlags(&N->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&N->ev_join, cudaEventDisableTiming));
             N->desc = "additive(" + N->a.desc + ", " + N->b.desc + ")";
@@ -228,12 +184,19 @@ struct Builder {
         }
         reciprocal(c, N->nA, d.p, dinv.p);
         Csr S;
-        {
-            DPP_TRACE_SCOPE(c, "pc.selfp_spgemm");
-            S = spgemm(c, C, B, dinv.p, true, &D);
-        }
-        N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA);
-        N->b = leaf(nd.child_type[1], nd.child_node[1], S, gB);
+        fork_join(c, N->side_owner,
+                  [&](Ctx *sc) {   // the A-block leaf (ILU(0)) does not need S_p
+                      Builder bb = *this;
+                      bb.c = sc;
+                      N->a = bb.leaf(nd.child_type[0], nd.child_node[0], A, gA);
+                  },
+                  [&] {
+                      {
+                          DPP_TRACE_SCOPE(c, "pc.selfp_spgemm");
+                          S = spgemm(c, C, B, dinv.p, true, &D);
+                      }
+                      N->b = leaf(nd.child_type[1], nd.child_node[1], S, gB);
+                  });
         N->Bc = csr_drop_zeros(c, B);
         N->Cc = csr_drop_zeros(c, C);
         N->desc = "schur-full(" + N->a.desc + ", selfp->" + N->b.desc + ")";

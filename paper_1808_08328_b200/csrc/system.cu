@@ -5,6 +5,8 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
+#include <thread>
 
 namespace dpp {
 
@@ -27,6 +29,56 @@ TraceScope::~TraceScope() {
     }
     std::fprintf(stderr, "[dpp-trace] %-28s %9.3f ms   pool reserved %7.1f MB used %7.1f MB\n", name,
                  now() - t0, res / 1048576.0, used / 1048576.0);
+}
+
+void SideStream::ensure(Ctx *parent) {
+    if (s) return;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    ctx = *parent;
+    ctx.s = ctx.s2 = s;
+    ctx.launches = 0;
+    ctx.t0 = ctx.t1 = nullptr;
+    CK(cudaMalloc(&ctx.nrm_part, sizeof(double) * NRM_BLOCKS));
+    ctx.nrm_part2 = ctx.nrm_part;
+}
+SideStream::~SideStream() {
+    if (!s) return;
+    cudaStreamSynchronize(s);
+    if (ctx.nrm_part) cudaFree(ctx.nrm_part);
+    cudaStreamDestroy(s);
+}
+
+void fork_join(Ctx *c, SideStream &owner, const std::function<void(Ctx *)> &side,
+               const std::function<void()> &main_fn) {
+    owner.ensure(c);
+    CK(cudaStreamSynchronize(c->s));   // inputs produced on the parent stream are ready
+    static const bool serial = [] { const char *e = std::getenv("DPP_SERIAL_SETUP"); return e && *e == '1'; }();
+    if (serial) {
+        side(&owner.ctx);
+        CK(cudaStreamSynchronize(owner.s));
+        main_fn();
+    } else {
+        std::exception_ptr err;
+        std::thread t([&] {
+            try {
+                CK(cudaSetDevice(owner.ctx.device));
+                side(&owner.ctx);
+                CK(cudaStreamSynchronize(owner.s));
+            } catch (...) {
+                err = std::current_exception();
+            }
+        });
+        try {
+            main_fn();
+        } catch (...) {
+            t.join();
+            throw;
+        }
+        t.join();
+        if (err) std::rethrow_exception(err);
+    }
+    c->launches += owner.ctx.launches;
+    owner.ctx.launches = 0;
 }
 
 __global__ void k_reciprocal(int64_t n, const double *d, double *o) {
