@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdpp.so")
+LIB_PATH = os.environ.get("DPP_LIB") or os.path.join(_HERE, "libdpp.so")
 
 DPP_OK, DPP_ERR_CUDA, DPP_ERR_VALUE, DPP_ERR_ZERO_PIVOT, DPP_ERR_RUNTIME, DPP_ERR_ALLOC = range(6)
 KINDS = {"tri": 0, "quad": 1, "tet": 2, "hex": 3}

@@ -199,6 +199,11 @@ struct BlockPlan {        // block-sequential sweep with dense diagonal-block in
     DBuf<unsigned char> blocks;
     DBuf<long long> boff;
 };
+struct BdPlan {           // block-dense sweep: per-(block, CTA) segments of inverse rows + off-block CSR (tribd.cu)
+    int B = 0, nb = 0, C = 0, W = 0, stage = 0, nst = 0;
+    DBuf<unsigned char> segs;
+    DBuf<long long> soff;
+};
 struct Tri {              // one sweep: strict part (zero-free) + optional diagonal
     Csr strict;
     DBuf<double> diag;    // empty -> unit diagonal
@@ -206,6 +211,7 @@ struct Tri {              // one sweep: strict part (zero-free) + optional diago
     DBuf<int> levptr;     // level l = order[levptr[l] .. levptr[l+1])
     std::unique_ptr<ClusterPlan> cl;   // cluster-resident sweep when x fits in one cluster
     std::unique_ptr<BlockPlan> bl;     // block-sequential sweep (small n, narrow levels)
+    std::unique_ptr<BdPlan> bd;        // block-dense sweep (AMG smoother factors)
     DBuf<double> dense;   // optional dense inverse (small coarse levels): sweep = triangular GEMV
     bool backward = false;
     int n = 0, nlev = 0;
@@ -215,6 +221,9 @@ int tri_levels(Ctx *c, const Csr &strict, bool backward, DBuf<int> &order, DBuf<
                DBuf<int> *lev_out = nullptr);
 bool cluster_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L);
 bool block_plan(Ctx *c, Tri &T);
+bool bd_plan(Ctx *c, Tri &T, int B);
+void trsv_bd(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+             cudaStream_t st);
 void trsv_block(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
                 cudaStream_t st);
 void trsv_cluster(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,

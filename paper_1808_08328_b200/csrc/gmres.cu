@@ -155,8 +155,12 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
         bool happy = false;
         for (int j = 0; j < m; ++j) {
             double *Vj = V.p + (size_t)j * n;
+            {
+            DPP_TRACE_SCOPE(c, "gmres.matvec_pc");
             g.matvec(Vj, tmp.p);
             g.pc(tmp.p, w.p);                      // w = M^-1 A V[j]
+            }
+            DPP_TRACE_SCOPE(c, "gmres.mgs_givens");
             for (int i = 0; i <= j; ++i) {         // modified Gram-Schmidt
                 const double *Vi = V.p + (size_t)i * n;
                 g.dot_dev(Vi, w.p, hcol + i);

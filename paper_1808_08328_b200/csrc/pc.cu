@@ -263,6 +263,7 @@ void pc_apply_dev(dpp_pc *pc, const double *r_dev, double *z_dev) {
     if (r_dev != pc->r.p)
         CK(cudaMemcpyAsync(pc->r.p, r_dev, sizeof(double) * pc->n, cudaMemcpyDeviceToDevice, c->s));
     if (!pc->exec) {
+        DPP_TRACE_SCOPE(c, "pc.capture_instantiate");
         const int64_t before = c->launches;
         CK(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
         try {
@@ -278,7 +279,21 @@ void pc_apply_dev(dpp_pc *pc, const double *r_dev, double *z_dev) {
         pc->kernels_per_apply = c->launches - before;
         c->launches = before;
     }
-    CK(cudaGraphLaunch(pc->exec, c->s));
+    if (TraceScope::on()) {   // device time of this apply (trace runs only)
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        CK(cudaEventRecord(e0, c->s));
+        CK(cudaGraphLaunch(pc->exec, c->s));
+        CK(cudaEventRecord(e1, c->s));
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        fprintf(stderr, "[dpp-trace]   pc apply graph %.3f ms (%lld kernels)\n", ms, (long long)pc->kernels_per_apply);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    } else
+        CK(cudaGraphLaunch(pc->exec, c->s));
     c->launches += pc->kernels_per_apply;
     if (z_dev != pc->z.p)
         CK(cudaMemcpyAsync(z_dev, pc->z.p, sizeof(double) * pc->n, cudaMemcpyDeviceToDevice, c->s));

@@ -13,6 +13,7 @@
 // Rows whose column bound exceeds the shared table use a per-row table in
 // global memory (same code path through generic pointers).
 #include <cstdio>
+#include <new>
 
 #include "dpp_internal.cuh"
 
@@ -191,6 +192,81 @@ __global__ void __launch_bounds__(32 * W) k_spgemm(Args a, int cls) {
     }
 }
 
+// Dense-accumulator variant for products with a small column space (coarse AMG
+// levels): each warp owns acc[ncols] + presence flags in shared memory, the
+// k-ordered accumulation is the same as the hashed kernel, and survivors come
+// out in column order (no sort).
+template <bool FILL>
+__global__ void k_spgemm_dense(Args a, int ncols, int W) {
+    extern __shared__ unsigned char smem[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t per = (size_t)ncols * 8 * 2 + (size_t)((ncols + 15) & ~15);
+    double *acc = reinterpret_cast<double *>(smem + per * w);
+    double *dv = acc + ncols;
+    unsigned char *has = reinterpret_cast<unsigned char *>(dv + ncols);
+    for (int64_t row = (int64_t)blockIdx.x * W + w; row < a.rows; row += (int64_t)gridDim.x * W) {
+        for (int j = lane; j < ncols; j += 32) has[j] = 0;
+        __syncwarp();
+        if (a.dp) {
+            for (int p = a.dp[row] + lane; p < a.dp[row + 1]; p += 32) {
+                dv[a.di[p]] = a.dv[p];
+                has[a.di[p]] |= 2;
+            }
+            __syncwarp();
+        }
+        const int s = a.ap[row], e = a.ap[row + 1], len = e - s;
+        for (int q0 = 0; q0 < len; q0 += 32) {
+            int bs = 0, be = 0;
+            double aq = 0.0;
+            if (q0 + lane < len) {
+                const int p = a.reverse ? e - 1 - (q0 + lane) : s + q0 + lane;
+                const int kq = a.ai[p];
+                aq = a.av[p];
+                if (a.s) aq = __dmul_rn(aq, a.s[kq]);
+                bs = a.bp[kq];
+                be = a.bp[kq + 1];
+            }
+            const int cnt = min(32, len - q0);
+            for (int qq = 0; qq < cnt; ++qq) {
+                const double av = __shfl_sync(0xffffffffu, aq, qq);
+                const int rs = __shfl_sync(0xffffffffu, bs, qq), re = __shfl_sync(0xffffffffu, be, qq);
+                if (av == 0.0) continue;
+                for (int r = rs + lane; r < re; r += 32) {
+                    const double bv = a.bv[r];
+                    if (bv == 0.0) continue;
+                    const int j = a.bi[r];
+                    const double pr = __dmul_rn(av, bv);
+                    if (has[j] & 1) acc[j] = __dadd_rn(acc[j], pr);
+                    else { acc[j] = __dadd_rn(0.0, pr); has[j] |= 1; }
+                }
+                __syncwarp();
+            }
+        }
+        int w0 = FILL ? a.optr[row] : 0, nsurv = 0;
+        for (int j0 = 0; j0 < ncols; j0 += 32) {
+            const int j = j0 + lane;
+            bool keep = false;
+            double v = 0.0;
+            if (j < ncols && has[j]) {
+                const unsigned char f = has[j];
+                if (!a.dp) v = acc[j];
+                else if (f & 1) v = (f & 2) ? __dsub_rn(dv[j], acc[j]) : -acc[j];
+                else v = dv[j];
+                keep = a.keep_zeros || v != 0.0;
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (FILL && keep) {
+                const int pos = w0 + nsurv + __popc(m & ((1u << lane) - 1));
+                a.oi[pos] = j;
+                a.ov[pos] = v;
+            }
+            nsurv += __popc(m);
+        }
+        if (!FILL && lane == 0) a.cnt[row] = nsurv;
+        __syncwarp();
+    }
+}
+
 // upper bound of distinct columns per row -> table placement
 __global__ void k_bound(int rows, const int *ap, const int *ai, const int *bp, const int *dp,
                         int bcols, int64_t *need) {
@@ -266,12 +342,52 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         return C;
     }
     DPP_TRACE_SCOPE(c, "spgemm");
+    // small column space and dense-ish rows: dense accumulator, no hashing / sorting
+    {
+        const int ncols = B.cols;
+        const size_t per = (size_t)ncols * 16 + (size_t)((ncols + 15) & ~15);
+        const double avg_out = rows ? (double)std::min<int64_t>((int64_t)ncols, (int64_t)((double)A.nnz / rows * ((double)B.nnz / std::max(1, B.rows)))) : 0.0;
+        if (ncols <= 4096 && avg_out * 8 >= ncols && per <= 200 * 1024) {
+            const int W = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per));
+            const size_t smem_d = per * W;
+            static bool dattr = false;
+            if (!dattr) {
+                CK(cudaFuncSetAttribute(k_spgemm_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                CK(cudaFuncSetAttribute(k_spgemm_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                dattr = true;
+            }
+            Args a{};
+            a.rows = rows;
+            a.ap = A.ptr.p; a.ai = A.idx.p; a.av = A.val.p;
+            a.bp = B.ptr.p; a.bi = B.idx.p; a.bv = B.val.p;
+            a.s = s_dev;
+            if (D) { a.dp = D->ptr.p; a.di = D->idx.p; a.dv = D->val.p; }
+            a.reverse = reverse;
+            a.keep_zeros = keep_zeros;
+            DBuf<int> cnt(rows, c->s);
+            a.cnt = cnt.p;
+            const int grid = std::max(1, std::min<int>((rows + W - 1) / W, c->sms * 4));
+            k_spgemm_dense<false><<<grid, 32 * W, smem_d, c->s>>>(a, ncols, W);
+            launched(c);
+            C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
+            C.idx.alloc(C.nnz, c->s);
+            C.val.alloc(C.nnz, c->s);
+            a.optr = C.ptr.p;
+            a.oi = C.idx.p;
+            a.ov = C.val.p;
+            k_spgemm_dense<true><<<grid, 32 * W, smem_d, c->s>>>(a, ncols, W);
+            launched(c);
+            CK(cudaStreamSynchronize(c->s));
+            return C;
+        }
+    }
     // 1) bound of distinct columns per row; 2) exact distinct count; 3) table placement
     DBuf<int64_t> need(rows, c->s);
     k_bound<<<grid_for(rows, 256, c->sms), 256, 0, c->s>>>(rows, A.ptr.p, A.idx.p, B.ptr.p,
                                                           D ? D->ptr.p : nullptr, B.cols, need.p);
     launched(c);
     std::vector<int64_t> h = need.to_host();
+    DPP_TRACE_SCOPE(c, "spgemm.after_bound");
     std::vector<int64_t> uoff(rows, -1);
     std::vector<int> ucap(rows, 0);
     int64_t utot = 0;
@@ -285,6 +401,7 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
     }
     std::vector<int> u(rows);
     {
+        DPP_TRACE_SCOPE(c, "spgemm.unique");
         DBuf<int64_t> duoff(rows, c->s);
         DBuf<int> ducap(rows, c->s), dkey(utot, c->s), duniq(rows, c->s);
         duoff.upload(uoff.data(), rows);
@@ -347,12 +464,15 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         std::fprintf(stderr, "[dpp-trace]   spgemm %d x %d (A nnz %lld, B nnz %lld): %d large, %d global, gtot %lld\n",
                      rows, B.cols, (long long)A.nnz, (long long)B.nnz, nlarge, nglob, (long long)gtot);
     }
+    TraceScope ts_count(c, "spgemm.count");
     k_spgemm<false, SM_CAP, WPB><<<grid, 32 * WPB, smem, c->s>>>(a, -1);
     launched(c);
     if (nlarge) {
         k_spgemm<false, SM_CAP_L, 1><<<grid_l, 32, smem_l, c->s>>>(a, -2);
         launched(c);
     }
+    ts_count.~TraceScope();
+    new (&ts_count) TraceScope(c, "spgemm.fill");
     C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
     C.idx.alloc(C.nnz, c->s);
     C.val.alloc(C.nnz, c->s);

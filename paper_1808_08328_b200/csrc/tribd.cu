@@ -1,0 +1,445 @@
+// Block-dense triangular sweep for AMG smoother factors (the Gauss-Seidel
+// triangles of linalg.amg_vcycle, linalg.py:372-400).
+//
+// The level-scheduled sweep of a smoother triangle costs one cluster barrier
+// plus a DSMEM round trip per dependency level (281 levels on the finest C2
+// level, 691 on the next).  Here the rows are cut into consecutive blocks of B
+// rows and the diagonal block inverses are formed once at setup, so a sweep is
+// nb = ceil(n / B) dependent steps instead of nlev levels:
+//
+//     y     = b_blk - T[blk, outside] x     (off-block entries: rows already solved)
+//     x_blk = inv(T[blk, blk]) y           (dense triangular GEMV)
+//
+// In exact arithmetic this is the same forward/backward substitution; the
+// rounding is that of a dense inverse (as the small-level dense path,
+// DENSE_TRI_MAX), which keeps V-cycle results within the parity tolerance.
+//
+// One thread-block cluster of C CTAs runs the whole sweep.  Block rows are dealt
+// to the CTAs cyclically (row a -> CTA a % C, balancing the triangle), and
+// everything a CTA needs for one step that does not depend on x -- its rows of
+// the block inverse (packed triangle) and its off-block CSR rows -- is packed at
+// setup into one contiguous segment per (block, CTA).  A TMA bulk-copy ring
+// stages the segments NST-1 steps ahead, so the step's critical path is only
+// the x gather (L2), one DSMEM exchange of y and two cluster barriers.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "dpp_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dpp {
+
+constexpr int BD_THREADS = 1024;
+constexpr int BD_INV_WPB = 4;
+constexpr int BD_NST_MAX = 8;
+constexpr size_t BD_SMEM_LIMIT = 227 * 1024;
+
+__host__ __device__ __forceinline__ long long bd_pad16(long long b) { return (b + 15) & ~15LL; }
+
+__device__ __forceinline__ unsigned bd_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bd_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void bd_mbar_wait(unsigned long long *m, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(bd_u32(m)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bd_issue(unsigned char *dst, const unsigned char *src, unsigned bytes,
+                                         unsigned long long *m) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bd_u32(m)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(bd_u32(dst)), "l"(src), "r"(bytes), "r"(bd_u32(m)) : "memory");
+}
+
+// ---------------------------------------------------------------- segment layout
+// segment (blk, k), rows i = 0..nr-1 with block-local row a = k + C i:
+//   int nr, int ne, int 0, int 0
+//   int dofs[nr + 1]      packed-triangle row offsets (doubles)
+//   int optr[nr + 1]      off-block CSR row pointers (local)
+//   int oidx[ne]          global columns
+//   (pad 16) double dinv[dofs[nr]]   row i = inv(T_blk)[a, j0:j1)
+//   (pad 16) double oval[ne]
+struct SegDims {
+    int nr, nd, ne;
+};
+__host__ __device__ inline long long seg_bytes(int nr, long long nd, long long ne) {
+    const long long ints = 16 + 4LL * (nr + 1) * 2 + 4LL * ne;
+    return bd_pad16(bd_pad16(ints) + 8 * nd + 8 * ne);
+}
+__device__ __forceinline__ int row_len(int a, int m, int backward) { return backward ? m - a : a + 1; }
+
+__global__ void k_bd_seg_size(int n, int B, int C, int nb, int backward, const int *__restrict__ ptr,
+                              const int *__restrict__ idx, long long *bytes, int *maxback) {
+    const int seg = blockIdx.x * blockDim.x + threadIdx.x;
+    if (seg >= nb * C) return;
+    const int blk = seg / C, k = seg % C, s = blk * B, m = min(B, n - s);
+    int nr = 0;
+    long long nd = 0, ne = 0;
+    for (int a = k; a < m; a += C) {
+        ++nr;
+        nd += row_len(a, m, backward);
+        const int r = s + a;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
+            const int bc = idx[p] / B;
+            if (bc == blk) continue;
+            ++ne;
+            atomicMax(maxback, backward ? bc - blk : blk - bc);
+        }
+    }
+    bytes[seg] = seg_bytes(nr, nd, ne);
+}
+
+// one CTA per segment: dense block inverse rows + off-block CSR rows -> segment
+__global__ void k_bd_seg_fill(int n, int B, int C, int W, int backward, const int *__restrict__ ptr,
+                              const int *__restrict__ idx, const double *__restrict__ val,
+                              const double *__restrict__ dense, const long long *__restrict__ soff,
+                              unsigned char *segs) {
+    const int seg = blockIdx.x, blk = seg / C, k = seg % C, s = blk * B, m = min(B, n - s);
+    unsigned char *S = segs + soff[seg];
+    const int nr = m > k ? (m - k + C - 1) / C : 0;
+    __shared__ int ne_s, nd_s;
+    int *dofs = reinterpret_cast<int *>(S + 16);
+    int *optr = dofs + nr + 1;
+    if (threadIdx.x == 0) {
+        int d = 0, e = 0;
+        for (int i = 0; i < nr; ++i) {
+            const int a = k + C * i, r = s + a;
+            dofs[i] = d;
+            optr[i] = e;
+            d += row_len(a, m, backward);
+            for (int p = ptr[r]; p < ptr[r + 1]; ++p) e += (idx[p] / B) != blk;
+        }
+        dofs[nr] = d;
+        optr[nr] = e;
+        reinterpret_cast<int *>(S)[0] = nr;
+        reinterpret_cast<int *>(S)[1] = e;
+        reinterpret_cast<int *>(S)[2] = 0;
+        reinterpret_cast<int *>(S)[3] = 0;
+        ne_s = e;
+        nd_s = d;
+    }
+    __syncthreads();
+    const int ne = ne_s, nd = nd_s;
+    int *oidx = optr + nr + 1;
+    double *dv = reinterpret_cast<double *>(S + bd_pad16(16 + 4LL * (nr + 1) * 2 + 4LL * ne));
+    double *ov = dv + nd;
+    const double *Db = dense + (size_t)blk * B * B;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int i = w; i < nr; i += nw) {
+        const int a = k + C * i, r = s + a;
+        const int j0 = backward ? a : 0, len = row_len(a, m, backward);
+        for (int q = lane; q < len; q += 32) dv[dofs[i] + q] = Db[(size_t)a * B + j0 + q];
+        if (lane == 0) {
+            int e = optr[i];
+            for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
+                const int bc = idx[p] / B;
+                if (bc == blk) continue;
+                // every off-block column lies in the x window (W >= the largest block distance)
+                oidx[e] = (bc % W) * B + (idx[p] - bc * B);
+                ov[e] = val[p];
+                ++e;
+            }
+        }
+    }
+}
+
+// Column c of inv(T[blk, blk]) by substitution over the strict CSR rows of the
+// block (one warp per column, the column in shared memory); dense[blk] is B x B
+// row-major with the block's rows/columns local.
+__global__ void __launch_bounds__(32 * BD_INV_WPB)
+    k_bd_inverse(int n, int B, int backward, const int *__restrict__ ptr, const int *__restrict__ idx,
+                 const double *__restrict__ val, const double *__restrict__ diag, double *__restrict__ dense) {
+    extern __shared__ double colbuf[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *xc = colbuf + (size_t)w * B;
+    const int blk = blockIdx.y, s = blk * B, m = min(B, n - s);
+    const int c = blockIdx.x * BD_INV_WPB + w;
+    if (c >= m) return;
+    for (int i = lane; i < m; i += 32) xc[i] = 0.0;
+    __syncwarp();
+    // forward: rows c, c+1, ..., m-1 ; backward: rows c, c-1, ..., 0
+    for (int a = c; backward ? a >= 0 : a < m; a += backward ? -1 : 1) {
+        const int r = s + a;
+        double acc = 0.0;
+        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
+            const int j = idx[p] - s;
+            if (j >= 0 && j < m) acc += val[p] * xc[j];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            const double d = diag ? diag[r] : 1.0;
+            xc[a] = ((a == c ? 1.0 : 0.0) - acc) / d;
+        }
+        __syncwarp();
+    }
+    double *D = dense + (size_t)blk * B * B;
+    for (int i = lane; i < m; i += 32) D[(size_t)i * B + c] = xc[i];
+}
+
+// ---------------------------------------------------------------- sweep
+// Values move between the cluster's CTAs only by st.async pushes that count
+// their bytes on the receiving CTA's mbarrier (no cluster barrier, no fence):
+//   y of step t  -> every CTA's yf[t & 1],       counted on mby[t & 1]
+//   x of block t -> every CTA's x window slot,   counted on mbx[t & 1]
+// Buffer reuse is safe by causality: a CTA can only produce step t+1 data after
+// it received every CTA's step t data, and every CTA consumed its own step t
+// buffers (CTA barrier) before producing step t+1 data.
+//
+// shared memory: mbarriers (ring NST, mby 2, mbx 2) | yf[2][B] | xw[W][B] | bst[2][B] | so[2 nb] | ring
+__host__ __device__ inline size_t bd_fixed(int B, int nb, int W) {
+    return 8 * (BD_NST_MAX + 4) + 8 * (size_t)B * (2 + W + 2) + (size_t)bd_pad16(16LL * nb);
+}
+__device__ __forceinline__ unsigned bd_mapa(unsigned a, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void bd_push(unsigned raddr, double v, unsigned rmbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 ::"r"(raddr), "l"(__double_as_longlong(v)), "r"(rmbar) : "memory");
+}
+__device__ __forceinline__ void bd_arm(unsigned long long *m, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bd_u32(m)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(BD_THREADS, 1)
+    k_trsv_bd(int n, int B, int nb, int W, int backward, int stage, int nst, const unsigned char *__restrict__ segs,
+              const long long *__restrict__ soff, const double *__restrict__ b, double *x,
+              const double *__restrict__ xadd, double *xout, unsigned long long *dbg) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long ph[6] = {0, 0, 0, 0, 0, 0}, tc = 0;
+    unsigned long long *mbar = reinterpret_cast<unsigned long long *>(smem);
+    unsigned long long *mby = mbar + BD_NST_MAX, *mbx = mby + 2;
+    double *yf = reinterpret_cast<double *>(smem + 8 * (BD_NST_MAX + 4));
+    double *xw = yf + 2 * (size_t)B;
+    double *bst = xw + (size_t)W * B;
+    long long *so = reinterpret_cast<long long *>(bst + 2 * (size_t)B);
+    unsigned char *ring = smem + bd_fixed(B, nb, W);
+    cg::cluster_group cl = cg::this_cluster();
+    const int C = (int)cl.num_blocks(), k = (int)cl.block_rank();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // push targets: lane l < C writes to CTA l
+    const int peer = lane < C ? lane : 0;
+    const unsigned yf_r = bd_mapa(bd_u32(yf), peer), xw_r = bd_mapa(bd_u32(xw), peer);
+    const unsigned mby_r = bd_mapa(bd_u32(mby), peer), mbx_r = bd_mapa(bd_u32(mbx), peer);
+    auto seg_of = [&](int t) { return (backward ? nb - 1 - t : t) * C + k; };
+    auto rows_of = [&](int t) { const int blk = backward ? nb - 1 - t : t; return min(B, n - blk * B); };
+    auto issue = [&](int t) {   // step t's segment -> ring slot t % nst
+        bd_issue(ring + (size_t)(t % nst) * stage, segs + so[2 * t], (unsigned)so[2 * t + 1], &mbar[t % nst]);
+    };
+    auto fetch_b = [&](int t) {   // lane 0: b of this warp's rows of step t -> bst[t & 1] (async)
+        if (lane != 0 || t >= nb) return;
+        const int blk = backward ? nb - 1 - t : t;
+        const int s = blk * B, m = min(B, n - s);
+        double *dst = bst + (size_t)(t & 1) * B;
+        for (int a = k + C * warp; a < m; a += C * nw)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(bd_u32(dst + a)), "l"(b + s + a) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if (threadIdx.x < nst + 4)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bd_u32(&mbar[threadIdx.x < nst ? threadIdx.x : BD_NST_MAX + threadIdx.x - nst])) : "memory");
+    for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+        const int sg = seg_of(t);
+        so[2 * t] = soff[sg];
+        so[2 * t + 1] = soff[sg + 1] - soff[sg];
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int t = 0; t < min(nst - 1, nb); ++t) issue(t);
+        bd_arm(&mby[0], 8u * rows_of(0));
+        bd_arm(&mbx[0], 8u * rows_of(0));
+        bd_mbar_wait(&mbar[0], 0);
+    }
+    fetch_b(0);
+    // every CTA's mbarriers are initialised before the first remote push
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    for (int t = 0; t < nb; ++t) {
+        const int blk = backward ? nb - 1 - t : t;
+        const int s = blk * B, m = min(B, n - s);
+        const unsigned par = (unsigned)((t >> 1) & 1);
+        if (dbg) tc = clock64();
+        if (threadIdx.x == 0) {
+            if (t + nst - 1 < nb) issue(t + nst - 1);   // slot of step t-1 is free
+            if (t + 1 < nb) bd_arm(&mby[(t + 1) & 1], 8u * rows_of(t + 1));   // its previous phase (t-1) completed
+        }
+        const double *bs = bst + (size_t)(t & 1) * B;
+        if (lane == 0) asm volatile("cp.async.wait_all;" ::: "memory");   // this step's b
+        __syncwarp();
+        fetch_b(t + 1);
+        const unsigned char *S = ring + (size_t)(t % nst) * stage;
+        const int nr = reinterpret_cast<const int *>(S)[0], ne = reinterpret_cast<const int *>(S)[1];
+        const int *dofs = reinterpret_cast<const int *>(S + 16);
+        const int *optr = dofs + nr + 1;
+        const int *oidx = optr + nr + 1;
+        const double *dv = reinterpret_cast<const double *>(S + bd_pad16(16 + 4LL * (nr + 1) * 2 + 4LL * ne));
+        const double *ov = dv + dofs[nr];
+        // x of the previous block has landed in the window
+        if (t > 0) bd_mbar_wait(&mbx[(t - 1) & 1], (unsigned)(((t - 1) >> 1) & 1));
+        // mbx[(t+1) & 1] is re-armed only after its previous phase (block t-1) completed
+        if (threadIdx.x == 0 && t + 1 < nb) bd_arm(&mbx[(t + 1) & 1], 8u * rows_of(t + 1));
+        if (dbg) { const unsigned long long u = clock64(); ph[0] += u - tc; tc = u; }
+        // 1. y = b - T_off x over this CTA's rows (warp per row), pushed to every CTA
+        for (int i = warp; i < nr; i += nw) {
+            const int a = k + C * i;
+            double acc = 0.0;
+            for (int p = optr[i] + lane; p < optr[i + 1]; p += 32) acc += ov[p] * xw[oidx[p]];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane < C) bd_push(yf_r + 8u * ((t & 1) * B + a), bs[a] - acc, mby_r + 8u * (t & 1));
+        }
+        if (dbg) { const unsigned long long u = clock64(); ph[1] += u - tc; tc = u; }
+        bd_mbar_wait(&mby[t & 1], par);
+        if (dbg) { const unsigned long long u = clock64(); ph[2] += u - tc; tc = u; }
+        // 2. x_blk = inv(T_blk) y, this CTA's rows (packed triangle rows in the segment)
+        const double *y = yf + (size_t)(t & 1) * B;
+        const unsigned slot = (unsigned)((blk % W) * B);
+        for (int i = warp; i < nr; i += nw) {
+            const int a = k + C * i;
+            const int j0 = backward ? a : 0;
+            const double *row = dv + dofs[i];
+            const int len = dofs[i + 1] - dofs[i];
+            double acc0 = 0.0, acc1 = 0.0;
+            int q = lane;
+            for (; q + 32 < len; q += 64) {
+                acc0 += row[q] * y[j0 + q];
+                acc1 += row[q + 32] * y[j0 + q + 32];
+            }
+            if (q < len) acc0 += row[q] * y[j0 + q];
+            double acc = acc0 + acc1;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (dbg) { const unsigned long long u = clock64() + (unsigned long long)(acc != acc); ph[5] += u - tc; }
+            if (lane < C) bd_push(xw_r + 8u * (slot + a), acc, mbx_r + 8u * (t & 1));
+            if (lane == 31) {
+                x[s + a] = acc;
+                if (xout) xout[s + a] = xadd[s + a] + acc;
+            }
+        }
+        if (dbg) { const unsigned long long u = clock64(); ph[3] += u - tc; tc = u; }
+        // next step's segment landed; this step's ring slot and yf buffer are free
+        if (threadIdx.x == 0 && t + 1 < nb) bd_mbar_wait(&mbar[(t + 1) % nst], (unsigned)(((t + 1) / nst) & 1));
+        if (dbg) { const unsigned long long u = clock64(); ph[4] += u - tc; tc = u; }
+        __syncthreads();
+    }
+    // the last block's x pushes must land before this CTA's shared memory is released
+    bd_mbar_wait(&mbx[(nb - 1) & 1], (unsigned)(((nb - 1) >> 1) & 1));
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (dbg && threadIdx.x == (int)(dbg[6 * 16] & 1023))
+        for (int q = 0; q < 6; ++q) dbg[k * 6 + q] = ph[q];
+}
+
+static int bd_cluster_size() {
+    static int C = -1;
+    if (C < 0) {
+        C = 16;
+        if (cudaFuncSetAttribute(k_trsv_bd, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            C = 8;
+        }
+    }
+    return C;
+}
+
+bool bd_plan(Ctx *c, Tri &T, int B) {
+    const int n = T.n;
+    if (n == 0 || B <= 0) return false;
+    auto P = std::make_unique<BdPlan>();
+    P->B = B;
+    P->nb = (n + B - 1) / B;
+    P->C = bd_cluster_size();
+    const int C = P->C, nseg = P->nb * C;
+    // segment sizes -> offsets
+    DBuf<long long> sz(nseg, c->s);
+    DBuf<int> mb(1, c->s);
+    CK(cudaMemsetAsync(mb.p, 0, sizeof(int), c->s));
+    k_bd_seg_size<<<(nseg + 127) / 128, 128, 0, c->s>>>(n, B, C, P->nb, T.backward, T.strict.ptr.p,
+                                                         T.strict.idx.p, sz.p, mb.p);
+    launched(c);
+    P->W = std::max(1, mb.to_host()[0] + 1);   // window slots: blocks back 1..maxback, plus the current
+    std::vector<long long> hs = sz.to_host(), ho(nseg + 1, 0);
+    long long mx = 0;
+    for (int i = 0; i < nseg; ++i) {
+        ho[i + 1] = ho[i] + hs[i];
+        mx = std::max(mx, hs[i]);
+    }
+    const long long stage = (mx + 127) & ~127LL;
+    const size_t fixed = bd_fixed(B, P->nb, P->W);
+    if (fixed + 2 * (size_t)stage > BD_SMEM_LIMIT) return false;
+    P->nst = (int)std::min<size_t>(BD_NST_MAX, (BD_SMEM_LIMIT - fixed) / stage);
+    P->nst = std::min(P->nst, std::max(2, P->nb));
+    P->stage = (int)stage;
+    P->soff.alloc(nseg + 1, c->s);
+    P->soff.upload(ho.data(), nseg + 1);
+    P->segs.alloc((size_t)std::max<long long>(ho[nseg], 16), c->s);
+    // dense diagonal-block inverses (temporary) -> packed segments
+    {
+        DBuf<double> dense((size_t)P->nb * B * B, c->s);
+        const size_t sm = (size_t)BD_INV_WPB * B * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            CK(cudaFuncSetAttribute(k_bd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)(BD_INV_WPB * 1024 * sizeof(double))));
+            CK(cudaFuncSetAttribute(k_trsv_bd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD_SMEM_LIMIT));
+            attr = true;
+        }
+        dim3 grid((B + BD_INV_WPB - 1) / BD_INV_WPB, P->nb);
+        k_bd_inverse<<<grid, 32 * BD_INV_WPB, sm, c->s>>>(n, B, T.backward, T.strict.ptr.p, T.strict.idx.p,
+                                                           T.strict.val.p, T.diag.n ? T.diag.p : nullptr, dense.p);
+        launched(c);
+        k_bd_seg_fill<<<nseg, 256, 0, c->s>>>(n, B, C, P->W, T.backward, T.strict.ptr.p, T.strict.idx.p,
+                                               T.strict.val.p, dense.p, P->soff.p, P->segs.p);
+        launched(c);
+        CK(cudaStreamSynchronize(c->s));
+    }
+    if (TraceScope::on())
+        std::fprintf(stderr, "[dpp-trace]   bd_plan n=%d B=%d nb=%d C=%d W=%d stage=%lld nst=%d segs %.1f MB\n", n, B,
+                     P->nb, C, P->W, stage, P->nst, ho[nseg] / 1e6);
+    T.bd = std::move(P);
+    return true;
+}
+
+void trsv_bd(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+             cudaStream_t st) {
+    const BdPlan &P = *T.bd;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.C, 1, 1);
+    cfg.blockDim = dim3(BD_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = bd_fixed(P.B, P.nb, P.W) + (size_t)P.nst * P.stage;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    static const bool dbg_on = [] { const char *e = std::getenv("DPP_BD_DEBUG"); return e && *e == '1'; }();
+    unsigned long long *dbg = nullptr;
+    if (dbg_on && !c->capturing) {
+        CK(cudaMallocAsync((void **)&dbg, sizeof(unsigned long long) * (6 * 16 + 1), st));
+        static const unsigned long long who = [] { const char *e = std::getenv("DPP_BD_THREAD"); return e ? std::atoll(e) : 0ll; }();
+        CK(cudaMemcpyAsync(dbg + 6 * 16, &who, 8, cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaLaunchKernelEx(&cfg, k_trsv_bd, T.n, P.B, P.nb, P.W, (int)T.backward, P.stage, P.nst, P.segs.p, P.soff.p, b,
+                          x, xadd, xout, dbg));
+    launched(c);
+    if (dbg) {
+        std::vector<unsigned long long> h(6 * P.C);
+        CK(cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFreeAsync(dbg, st);
+        std::fprintf(stderr, "[dpp-bd] n=%d nb=%d cycles/step (CTA0,1,15): top %.0f %.0f %.0f | gather %.0f | ywait %.0f | gemv %.0f | mbar %.0f | gemv-before-push %.0f\n",
+                     T.n, P.nb, (double)h[0] / P.nb, (double)h[6] / P.nb, (double)h[6 * (P.C - 1)] / P.nb,
+                     (double)h[1] / P.nb, (double)h[2] / P.nb, (double)h[3] / P.nb, (double)h[4] / P.nb, (double)h[5] / P.nb);
+    }
+}
+
+}  // namespace dpp

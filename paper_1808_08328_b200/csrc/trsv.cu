@@ -284,6 +284,10 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
         launched(c);
         return;
     }
+    if (T.bd) {
+        trsv_bd(c, T, b, x, xadd, xout, st);
+        return;
+    }
     if (T.bl) {
         trsv_block(c, T, b, x, xadd, xout, st);
         return;
@@ -325,6 +329,16 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense) {
         launched(c);
         CK(cudaStreamSynchronize(c->s));
         T.nlev = n;
+        return T;
+    }
+    // AMG smoother factors above the dense limit and up to DPP_BD_MAX rows: block-dense
+    // sweep (no level analysis).  Measured on C2: the 5593-row level goes from 264 us
+    // (block-sequential) to ~35 us per sweep; on the 68921-row level it only ties the
+    // cluster sweep (468 us), so larger factors stay level-scheduled.
+    static const int bd_max = [] { const char *e = std::getenv("DPP_BD_MAX"); return e ? std::atoi(e) : 8192; }();
+    static const int bd_b = [] { const char *e = std::getenv("DPP_BD_B"); return e ? std::atoi(e) : 512; }();
+    if (allow_dense && T.n <= bd_max && bd_plan(c, T, std::min(bd_b, 1024))) {
+        T.nlev = T.bd->nb;
         return T;
     }
     DBuf<int> lev;
