@@ -229,7 +229,10 @@ void trsv_block(Ctx *c, const Tri &T, const double *b, double *x, const double *
 void trsv_cluster(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
                   cudaStream_t st);
 constexpr int DENSE_TRI_MAX = 1024;
-Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense = false);
+// pre_order / pre_lev: a level analysis of a superset pattern of this triangle
+// (e.g. ILU(0)'s stored lower pattern for its L factor), reused as the schedule
+Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense = false,
+             DBuf<int> *pre_order = nullptr, DBuf<int> *pre_lev = nullptr, int pre_nlev = 0);
 // x = T^{-1} b  (xout = xadd + x when xadd given); x/ticket are scratch of size n / 1
 void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const double *xadd,
           double *xout, cudaStream_t st = nullptr);

@@ -6,12 +6,21 @@
 // operand's entries in storage order, starting from 0, exact zeros dropped) and
 // csr_binop (d - x over the union, zeros dropped).  C @ diag(.) emits each row
 // in reverse first-touch order, i.e. descending k, so the second product
-// accumulates over k DESCENDING.  This kernel reproduces that bit-for-bit:
-// one warp per output row, a shared-memory open-addressing table keyed by
-// column, products accumulated k by k (__syncwarp between k) with separate
-// __dmul_rn / __dadd_rn, survivors rank-sorted into canonical CSR order.
-// Rows whose column bound exceeds the shared table use a per-row table in
-// global memory (same code path through generic pointers).
+// accumulates over k DESCENDING.  The AMG Galerkin products (linalg.py:341-370)
+// are plain csr_matmat products.  Every path below reproduces that bit-for-bit:
+// one warp per output row, products accumulated k by k (__syncwarp between k)
+// with separate __dmul_rn / __dadd_rn, survivors emitted in column order.
+//
+// Pipeline (hashed path):
+//   1. symbolic: distinct columns per row in a 1024-key shared table (8 warps
+//      per CTA); rows that overflow it are recounted with an 8192-key table or a
+//      per-row global table sized from the row's product bound
+//   2. numeric: ONE pass per size class (shared tables of 256 / 1024 / 4096
+//      slots, or global), survivors rank-sorted by column and written to a
+//      scratch at the row's symbolic offset, with the surviving count
+//   3. compaction of the scratch into canonical CSR
+// Small column spaces (coarse levels) use a dense per-warp accumulator instead,
+// whose survivors come out in column order without sorting.
 #include <cstdio>
 #include <new>
 
@@ -21,29 +30,7 @@ namespace dpp {
 
 namespace {
 
-constexpr int SM_CAP = 512;     // slots per warp in shared memory (rows with <= 255 distinct columns)
-constexpr int WPB = 2;          // warps per block
-constexpr int SM_CAP_L = 4096;  // large rows (<= 2047 distinct columns): one warp per block
-
-struct Table {
-    int *key;
-    unsigned char *has;   // bit0: x present, bit1: d present
-    double *x, *d;
-    int *lk;
-    double *lv;
-    int cap;
-};
-
 __device__ __forceinline__ unsigned hsh(int j) { return (unsigned)j * 2654435761u; }
-
-__device__ __forceinline__ int tab_slot(Table &t, int j) {
-    unsigned h = hsh(j) & (t.cap - 1);
-    while (true) {
-        int old = atomicCAS(&t.key[h], -1, j);
-        if (old == -1 || old == j) return (int)h;
-        h = (h + 1) & (t.cap - 1);
-    }
-}
 
 struct Args {
     int rows;
@@ -55,32 +42,207 @@ struct Args {
     const int *dp, *di;   // optional D
     const double *dv;
     int reverse, keep_zeros;
-    const int64_t *goff;  // per-row global table offsets (or -1 => shared)
+    // numeric pass: rows of this launch and their global tables (if any)
+    const int *rl;
+    int nrl;
+    const int64_t *goff;  // per list entry: global table offset (class G) or unused
     const int *gcap;
     int *g_key;
     unsigned char *g_has;
     double *g_x, *g_d, *g_lv;
     int *g_lk;
-    int *cnt;             // count pass output
-    const int *optr;      // fill pass input
-    int *oi;
-    double *ov;
+    // output: sorted survivors at toff[row] in the scratch, count in cnt[row]
+    const int64_t *toff;
+    int *ti;
+    double *tv;
+    int *cnt;
 };
 
-// CLS: -1 = the row's table is in shared memory of capacity CAP, class chosen
-// by goff: -1 small rows (CAP = SM_CAP), -2 large rows (CAP = SM_CAP_L);
-// goff >= 0 rows use a global table (processed by the small-row launch)
-template <bool FILL, int CAP, int W>
-__global__ void __launch_bounds__(32 * W) k_spgemm(Args a, int cls) {
+// The k-ordered accumulation loop shared by the hashed and dense kernels: A's row
+// is taken 32 entries at a time (k, scaled a_ik, B-row bounds in lane registers);
+// each k's B row is held in registers (up to PF x 32 entries) and the NEXT k's
+// row is loaded while the current one is accumulated.
+constexpr int PF = 4;
+template <typename Upd>
+__device__ __forceinline__ void accumulate_row(const Args &a, int64_t row, int lane, Upd &&upd) {
+    const int s = a.ap[row], e = a.ap[row + 1], len = e - s;
+    for (int q0 = 0; q0 < len; q0 += 32) {
+        int bs = 0, be = 0;
+        double aq = 0.0;
+        if (q0 + lane < len) {
+            const int p = a.reverse ? e - 1 - (q0 + lane) : s + q0 + lane;
+            const int kq = a.ai[p];
+            aq = a.av[p];
+            if (a.s) aq = __dmul_rn(aq, a.s[kq]);
+            bs = a.bp[kq];
+            be = a.bp[kq + 1];
+        }
+        const int cnt = min(32, len - q0);
+        int cj[PF];
+        double cb[PF];
+        {
+            const int rs = __shfl_sync(0xffffffffu, bs, 0), re = __shfl_sync(0xffffffffu, be, 0);
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const int r = rs + 32 * u + lane;
+                cj[u] = r < re ? a.bi[r] : -1;
+                cb[u] = r < re ? a.bv[r] : 0.0;
+            }
+        }
+        for (int qq = 0; qq < cnt; ++qq) {
+            const double av = __shfl_sync(0xffffffffu, aq, qq);
+            const int rs = __shfl_sync(0xffffffffu, bs, qq), re = __shfl_sync(0xffffffffu, be, qq);
+            const int ns = __shfl_sync(0xffffffffu, bs, (qq + 1) & 31), ne = __shfl_sync(0xffffffffu, be, (qq + 1) & 31);
+            int nj[PF];
+            double nb[PF];
+#pragma unroll
+            for (int u = 0; u < PF; ++u) {
+                const int r = ns + 32 * u + lane;
+                const bool ok = qq + 1 < cnt && r < ne;
+                nj[u] = ok ? a.bi[r] : -1;
+                nb[u] = ok ? a.bv[r] : 0.0;
+            }
+            if (av != 0.0) {   // zero products never change a sum (scipy drops them)
+#pragma unroll
+                for (int u = 0; u < PF; ++u)
+                    if (cj[u] >= 0 && cb[u] != 0.0) upd(cj[u], __dmul_rn(av, cb[u]));
+                for (int r = rs + 32 * PF + lane; r < re; r += 32) {
+                    const double bv = a.bv[r];
+                    if (bv != 0.0) upd(a.bi[r], __dmul_rn(av, bv));
+                }
+                __syncwarp();
+            }
+#pragma unroll
+            for (int u = 0; u < PF; ++u) { cj[u] = nj[u]; cb[u] = nb[u]; }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- symbolic
+constexpr int US_CAP = 1024;   // keys per warp, small symbolic table
+constexpr int US_LIM = 768;    // distinct columns before a row is sent to the large path
+constexpr int US_W = 8;
+
+__global__ void __launch_bounds__(32 * US_W) k_unique_s(int rows, const int *ap, const int *ai, const int *bp,
+                                                        const int *bi, const int *dp, const int *di, int *uniq) {
+    __shared__ int sk[US_W][US_CAP];
+    __shared__ int sn[US_W];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int *key = sk[w];
+    for (int64_t row = (int64_t)blockIdx.x * US_W + w; row < rows; row += (int64_t)gridDim.x * US_W) {
+        for (int h = lane; h < US_CAP; h += 32) key[h] = -1;
+        if (lane == 0) sn[w] = 0;
+        __syncwarp();
+        bool over = false;
+        auto ins = [&](int j) {
+            if (over) return;
+            unsigned h = hsh(j) & (US_CAP - 1);
+            while (true) {
+                const int old = atomicCAS(&key[h], -1, j);
+                if (old == -1) {
+                    if (atomicAdd(&sn[w], 1) >= US_LIM) over = true;
+                    return;
+                }
+                if (old == j) return;
+                h = (h + 1) & (US_CAP - 1);
+            }
+        };
+        if (dp)
+            for (int p = dp[row] + lane; p < dp[row + 1]; p += 32) ins(di[p]);
+        // the symbolic pass needs no k order: each lane inserts its own k's B row
+        for (int p = ap[row] + lane; p < ap[row + 1]; p += 32) {
+            const int kq = ai[p];
+            const int rs = bp[kq], re = bp[kq + 1];
+            for (int r = rs; r < re; ++r) {
+                ins(bi[r]);
+                if (over) break;
+            }
+        }
+        over = __any_sync(0xffffffffu, over);
+        __syncwarp();
+        if (lane == 0) uniq[row] = over ? -1 : sn[w];
+        __syncwarp();
+    }
+}
+
+// rows of a list, table of up to UCAP keys in shared memory or per row in global memory
+constexpr int UCAP = 8192;
+__global__ void __launch_bounds__(32) k_unique_l(const int *rl, int nrl, const int *ap, const int *ai, const int *bp,
+                                                 const int *bi, const int *dp, const int *di, const int64_t *goff,
+                                                 const int *gcap, int *gkey, int *uniq) {
+    __shared__ int sk[UCAP];
+    const int lane = threadIdx.x;
+    for (int li = blockIdx.x; li < nrl; li += gridDim.x) {
+        const int row = rl[li];
+        int *key;
+        int cap;
+        if (goff[li] < 0) { key = sk; cap = UCAP; }
+        else { key = gkey + goff[li]; cap = gcap[li]; }
+        for (int h = lane; h < cap; h += 32) key[h] = -1;
+        __syncwarp();
+        int n = 0;
+        auto ins = [&](int j) {
+            unsigned h = hsh(j) & (cap - 1);
+            while (true) {
+                const int old = atomicCAS(&key[h], -1, j);
+                if (old == -1) { ++n; return; }
+                if (old == j) return;
+                h = (h + 1) & (cap - 1);
+            }
+        };
+        if (dp)
+            for (int p = dp[row] + lane; p < dp[row + 1]; p += 32) ins(di[p]);
+        for (int p = ap[row] + lane; p < ap[row + 1]; p += 32) {
+            const int kq = ai[p];
+            for (int r = bp[kq]; r < bp[kq + 1]; ++r) ins(bi[r]);
+        }
+        for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
+        if (lane == 0) uniq[row] = n;
+        __syncwarp();
+    }
+}
+
+// product bound per listed row (sizes the global symbolic tables)
+__global__ void k_bound_list(const int *rl, int nrl, const int *ap, const int *ai, const int *bp, const int *dp,
+                             int bcols, int64_t *need) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrl; i += gridDim.x * blockDim.x) {
+        const int r = rl[i];
+        int64_t ub = dp ? dp[r + 1] - dp[r] : 0;
+        for (int p = ap[r]; p < ap[r + 1]; ++p) ub += bp[ai[p] + 1] - bp[ai[p]];
+        need[i] = ub < bcols ? ub : bcols;
+    }
+}
+
+// ---------------------------------------------------------------- numeric
+struct Table {
+    int *key;
+    unsigned char *has;   // bit0: x present, bit1: d present
+    double *x, *d;
+    int *lk;
+    double *lv;
+    int cap;
+};
+__device__ __forceinline__ int tab_slot(Table &t, int j) {
+    unsigned h = hsh(j) & (t.cap - 1);
+    while (true) {
+        const int old = atomicCAS(&t.key[h], -1, j);
+        if (old == -1 || old == j) return (int)h;
+        h = (h + 1) & (t.cap - 1);
+    }
+}
+constexpr int SLOT_BYTES = 4 + 1 + 8 + 8 + 4 + 8;
+
+// CAP: shared table slots per warp (0 => global tables); K: survivor keys per
+// lane held in registers for ranking (0 => rank loop over shared memory)
+template <int CAP, int W, int K>
+__global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
     extern __shared__ unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const size_t per = (size_t)CAP * (4 + 1 + 8 + 8 + 4 + 8);
-    unsigned char *base = smem + per * w;
-    for (int64_t row = (int64_t)blockIdx.x * W + w; row < a.rows; row += (int64_t)gridDim.x * W) {
+    unsigned char *base = smem + (size_t)CAP * SLOT_BYTES * w;
+    for (int li = blockIdx.x * W + w; li < a.nrl; li += gridDim.x * W) {
+        const int row = a.rl[li];
         Table t;
-        const int64_t go = a.goff[row];
-        if (cls == -1 ? go == -2 : go != -2) continue;   // not this launch's class
-        if (go < 0) {
+        if (CAP > 0) {
             t.cap = CAP;
             t.x = (double *)base;
             t.d = t.x + CAP;
@@ -89,7 +251,8 @@ __global__ void __launch_bounds__(32 * W) k_spgemm(Args a, int cls) {
             t.lk = t.key + CAP;
             t.has = (unsigned char *)(t.lk + CAP);
         } else {
-            t.cap = a.gcap[row];
+            const int64_t go = a.goff[li];
+            t.cap = a.gcap[li];
             t.key = a.g_key + go;
             t.has = a.g_has + go;
             t.x = a.g_x + go;
@@ -101,58 +264,18 @@ __global__ void __launch_bounds__(32 * W) k_spgemm(Args a, int cls) {
         __syncwarp();
         if (a.dp) {
             for (int p = a.dp[row] + lane; p < a.dp[row + 1]; p += 32) {
-                int sl = tab_slot(t, a.di[p]);
+                const int sl = tab_slot(t, a.di[p]);
                 t.d[sl] = a.dv[p];
                 t.has[sl] |= 2;
             }
             __syncwarp();
         }
-        // A's row is fetched 32 entries at a time (k, scaled a_ik, B-row bounds in lane
-        // registers); the next k's B entries are prefetched while the current k is
-        // accumulated, so the k-ordered loop does not wait on global memory.
-        const int s = a.ap[row], e = a.ap[row + 1], len = e - s;
-        for (int q0 = 0; q0 < len; q0 += 32) {
-            int bs = 0, be = 0;
-            double aq = 0.0;
-            if (q0 + lane < len) {
-                const int p = a.reverse ? e - 1 - (q0 + lane) : s + q0 + lane;
-                const int kq = a.ai[p];
-                aq = a.av[p];
-                if (a.s) aq = __dmul_rn(aq, a.s[kq]);
-                bs = a.bp[kq];
-                be = a.bp[kq + 1];
-            }
-            const int cnt = min(32, len - q0);
-            int cj = -1;
-            double cb = 0.0;
-            {
-                const int rs = __shfl_sync(0xffffffffu, bs, 0), re = __shfl_sync(0xffffffffu, be, 0);
-                if (rs + lane < re) { cj = a.bi[rs + lane]; cb = a.bv[rs + lane]; }
-            }
-            for (int qq = 0; qq < cnt; ++qq) {
-                const double av = __shfl_sync(0xffffffffu, aq, qq);
-                const int rs = __shfl_sync(0xffffffffu, bs, qq), re = __shfl_sync(0xffffffffu, be, qq);
-                const int ns = __shfl_sync(0xffffffffu, bs, (qq + 1) & 31), ne = __shfl_sync(0xffffffffu, be, (qq + 1) & 31);
-                int nj = -1;
-                double nbv = 0.0;
-                if (qq + 1 < cnt && ns + lane < ne) { nj = a.bi[ns + lane]; nbv = a.bv[ns + lane]; }
-                if (av != 0.0) {   // zero products never change a sum (scipy drops them)
-                    auto acc = [&](int j, double bv) {
-                        if (bv == 0.0) return;
-                        const double pr = __dmul_rn(av, bv);
-                        const int sl = tab_slot(t, j);
-                        if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
-                        else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
-                    };
-                    if (cj >= 0) acc(cj, cb);
-                    for (int r = rs + 32 + lane; r < re; r += 32) acc(a.bi[r], a.bv[r]);
-                    __syncwarp();
-                }
-                cj = nj;
-                cb = nbv;
-            }
-        }
-        // survivors (slot order), then rank sort by column
+        accumulate_row(a, row, lane, [&](int j, double pr) {
+            const int sl = tab_slot(t, j);
+            if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
+            else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
+        });
+        // survivors (slot order) ...
         int nsurv = 0;
         for (int h0 = 0; h0 < t.cap; h0 += 32) {
             const int h = h0 + lane;
@@ -162,41 +285,58 @@ __global__ void __launch_bounds__(32 * W) k_spgemm(Args a, int cls) {
             if (h < t.cap && t.key[h] >= 0) {
                 const unsigned char f = t.has[h];
                 j = t.key[h];
-                if (!a.dp) v = t.x[h];                                   // C = A B
+                if (!a.dp) v = t.x[h];                                              // C = A B
                 else if (f & 1) v = (f & 2) ? __dsub_rn(t.d[h], t.x[h]) : -t.x[h];   // D - X
                 else v = t.d[h];
                 keep = a.keep_zeros || v != 0.0;
             }
-            unsigned m = __ballot_sync(0xffffffffu, keep);
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
-                int pos = nsurv + __popc(m & ((1u << lane) - 1));
+                const int pos = nsurv + __popc(m & ((1u << lane) - 1));
                 t.lk[pos] = j;
                 t.lv[pos] = v;
             }
             nsurv += __popc(m);
         }
         __syncwarp();
-        if (!FILL) {
-            if (lane == 0) a.cnt[row] = nsurv;
+        // ... ranked by column into the scratch
+        const int64_t o = a.toff[row];
+        if (K > 0) {
+            int mk[K > 0 ? K : 1], rk[K > 0 ? K : 1];
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                const int q = u * 32 + lane;
+                mk[u] = q < nsurv ? t.lk[q] : 0x7fffffff;
+                rk[u] = 0;
+            }
+            for (int v = 0; v < nsurv; ++v) {
+                const int kv = t.lk[v];
+#pragma unroll
+                for (int u = 0; u < K; ++u) rk[u] += kv < mk[u];
+            }
+#pragma unroll
+            for (int u = 0; u < K; ++u) {
+                const int q = u * 32 + lane;
+                if (q < nsurv) { a.ti[o + rk[u]] = mk[u]; a.tv[o + rk[u]] = t.lv[q]; }
+            }
         } else {
-            const int o = a.optr[row];
-            for (int u = lane; u < nsurv; u += 32) {
-                const int j = t.lk[u];
+            for (int q = lane; q < nsurv; q += 32) {
+                const int j = t.lk[q];
                 int rank = 0;
                 for (int v = 0; v < nsurv; ++v) rank += t.lk[v] < j;
-                a.oi[o + rank] = j;
-                a.ov[o + rank] = t.lv[u];
+                a.ti[o + rank] = j;
+                a.tv[o + rank] = t.lv[q];
             }
         }
+        if (lane == 0) a.cnt[row] = nsurv;
         __syncwarp();
     }
 }
 
 // Dense-accumulator variant for products with a small column space (coarse AMG
-// levels): each warp owns acc[ncols] + presence flags in shared memory, the
-// k-ordered accumulation is the same as the hashed kernel, and survivors come
-// out in column order (no sort).
-template <bool FILL>
+// levels): each warp owns acc[ncols] + presence flags in shared memory; the
+// survivors come out in column order (no sort), written to the scratch at
+// toff[row] (= row * ncols).
 __global__ void k_spgemm_dense(Args a, int ncols, int W) {
     extern __shared__ unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -214,35 +354,12 @@ __global__ void k_spgemm_dense(Args a, int ncols, int W) {
             }
             __syncwarp();
         }
-        const int s = a.ap[row], e = a.ap[row + 1], len = e - s;
-        for (int q0 = 0; q0 < len; q0 += 32) {
-            int bs = 0, be = 0;
-            double aq = 0.0;
-            if (q0 + lane < len) {
-                const int p = a.reverse ? e - 1 - (q0 + lane) : s + q0 + lane;
-                const int kq = a.ai[p];
-                aq = a.av[p];
-                if (a.s) aq = __dmul_rn(aq, a.s[kq]);
-                bs = a.bp[kq];
-                be = a.bp[kq + 1];
-            }
-            const int cnt = min(32, len - q0);
-            for (int qq = 0; qq < cnt; ++qq) {
-                const double av = __shfl_sync(0xffffffffu, aq, qq);
-                const int rs = __shfl_sync(0xffffffffu, bs, qq), re = __shfl_sync(0xffffffffu, be, qq);
-                if (av == 0.0) continue;
-                for (int r = rs + lane; r < re; r += 32) {
-                    const double bv = a.bv[r];
-                    if (bv == 0.0) continue;
-                    const int j = a.bi[r];
-                    const double pr = __dmul_rn(av, bv);
-                    if (has[j] & 1) acc[j] = __dadd_rn(acc[j], pr);
-                    else { acc[j] = __dadd_rn(0.0, pr); has[j] |= 1; }
-                }
-                __syncwarp();
-            }
-        }
-        int w0 = FILL ? a.optr[row] : 0, nsurv = 0;
+        accumulate_row(a, row, lane, [&](int j, double pr) {
+            if (has[j] & 1) acc[j] = __dadd_rn(acc[j], pr);
+            else { acc[j] = __dadd_rn(0.0, pr); has[j] |= 1; }
+        });
+        const int64_t o = a.toff[row];
+        int nsurv = 0;
         for (int j0 = 0; j0 < ncols; j0 += 32) {
             const int j = j0 + lane;
             bool keep = false;
@@ -255,75 +372,54 @@ __global__ void k_spgemm_dense(Args a, int ncols, int W) {
                 keep = a.keep_zeros || v != 0.0;
             }
             const unsigned m = __ballot_sync(0xffffffffu, keep);
-            if (FILL && keep) {
-                const int pos = w0 + nsurv + __popc(m & ((1u << lane) - 1));
-                a.oi[pos] = j;
-                a.ov[pos] = v;
+            if (keep) {
+                const int64_t pos = o + nsurv + __popc(m & ((1u << lane) - 1));
+                a.ti[pos] = j;
+                a.tv[pos] = v;
             }
             nsurv += __popc(m);
         }
-        if (!FILL && lane == 0) a.cnt[row] = nsurv;
+        if (lane == 0) a.cnt[row] = nsurv;
         __syncwarp();
     }
 }
 
-// upper bound of distinct columns per row -> table placement
-__global__ void k_bound(int rows, const int *ap, const int *ai, const int *bp, const int *dp,
-                        int bcols, int64_t *need) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
-        int64_t ub = dp ? dp[r + 1] - dp[r] : 0;
-        for (int p = ap[r]; p < ap[r + 1]; ++p) ub += bp[ai[p] + 1] - bp[ai[p]];
-        if (ub > bcols) ub = bcols;
-        need[r] = ub;
-    }
+__global__ void k_toff_dense(int rows, int ncols, int64_t *toff) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+        toff[r] = (int64_t)r * ncols;
 }
 
-constexpr int UCAP = 8192;   // key-only slots per warp for the symbolic pass
-constexpr int UWPB = 1;
-
-__global__ void __launch_bounds__(32 * UWPB) k_unique(int rows, const int *ap, const int *ai,
-                                                      const int *bp, const int *bi, const int *dp,
-                                                      const int *di, const int64_t *goff,
-                                                      const int *gcap, int *gkey, int *uniq) {
-    __shared__ int sk[UWPB][UCAP];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int64_t row = (int64_t)blockIdx.x * UWPB + w; row < rows; row += (int64_t)gridDim.x * UWPB) {
-        int *key;
-        int cap;
-        if (goff[row] < 0) { key = sk[w]; cap = UCAP; }
-        else { key = gkey + goff[row]; cap = gcap[row]; }
-        for (int h = lane; h < cap; h += 32) key[h] = -1;
-        __syncwarp();
-        int n = 0;
-        auto ins = [&](int j) {
-            unsigned h = hsh(j) & (cap - 1);
-            while (true) {
-                int old = atomicCAS(&key[h], -1, j);
-                if (old == -1) { ++n; return; }
-                if (old == j) return;
-                h = (h + 1) & (cap - 1);
-            }
-        };
-        if (dp)
-            for (int p = dp[row] + lane; p < dp[row + 1]; p += 32) ins(di[p]);
-        const int s = ap[row], len = ap[row + 1] - s;
-        for (int q0 = 0; q0 < len; q0 += 32) {
-            int bs = 0, be = 0;
-            if (q0 + lane < len) {
-                const int kq = ai[s + q0 + lane];
-                bs = bp[kq];
-                be = bp[kq + 1];
-            }
-            const int cnt = min(32, len - q0);
-            for (int qq = 0; qq < cnt; ++qq) {
-                const int rs = __shfl_sync(0xffffffffu, bs, qq), re = __shfl_sync(0xffffffffu, be, qq);
-                for (int r = rs + lane; r < re; r += 32) ins(bi[r]);
-            }
+// scratch (row segments at toff, cnt entries) -> canonical CSR (warp per row)
+__global__ void k_compact(int rows, const int64_t *toff, const int *ptr, const int *ti, const double *tv, int *oi,
+                          double *ov) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t s = toff[r];
+        const int o = ptr[r], n = ptr[r + 1] - o;
+        for (int q = lane; q < n; q += 32) {
+            oi[o + q] = ti[s + q];
+            ov[o + q] = tv[s + q];
         }
-        for (int o = 16; o > 0; o >>= 1) n += __shfl_down_sync(0xffffffffu, n, o);
-        if (lane == 0) uniq[row] = n;
-        __syncwarp();
     }
+}
+
+template <int CAP, int W, int K>
+void launch_num(Ctx *c, Args a, const std::vector<int> &rows_h) {
+    if (rows_h.empty()) return;
+    DBuf<int> rl(rows_h.size(), c->s);
+    rl.upload(rows_h.data(), rows_h.size());
+    a.rl = rl.p;
+    a.nrl = (int)rows_h.size();
+    const size_t smem = (size_t)CAP * SLOT_BYTES * W;
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_spgemm_num<CAP, W, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int grid = std::max(1, std::min<int>((a.nrl + W - 1) / W, c->sms * 16));
+    k_spgemm_num<CAP, W, K><<<grid, 32 * W, smem, c->s>>>(a);
+    launched(c);
 }
 
 }  // namespace
@@ -342,99 +438,6 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         return C;
     }
     DPP_TRACE_SCOPE(c, "spgemm");
-    // small column space and dense-ish rows: dense accumulator, no hashing / sorting
-    {
-        const int ncols = B.cols;
-        const size_t per = (size_t)ncols * 16 + (size_t)((ncols + 15) & ~15);
-        const double avg_out = rows ? (double)std::min<int64_t>((int64_t)ncols, (int64_t)((double)A.nnz / rows * ((double)B.nnz / std::max(1, B.rows)))) : 0.0;
-        if (ncols <= 4096 && avg_out * 8 >= ncols && per <= 200 * 1024) {
-            const int W = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per));
-            const size_t smem_d = per * W;
-            static bool dattr = false;
-            if (!dattr) {
-                CK(cudaFuncSetAttribute(k_spgemm_dense<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                CK(cudaFuncSetAttribute(k_spgemm_dense<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-                dattr = true;
-            }
-            Args a{};
-            a.rows = rows;
-            a.ap = A.ptr.p; a.ai = A.idx.p; a.av = A.val.p;
-            a.bp = B.ptr.p; a.bi = B.idx.p; a.bv = B.val.p;
-            a.s = s_dev;
-            if (D) { a.dp = D->ptr.p; a.di = D->idx.p; a.dv = D->val.p; }
-            a.reverse = reverse;
-            a.keep_zeros = keep_zeros;
-            DBuf<int> cnt(rows, c->s);
-            a.cnt = cnt.p;
-            const int grid = std::max(1, std::min<int>((rows + W - 1) / W, c->sms * 4));
-            k_spgemm_dense<false><<<grid, 32 * W, smem_d, c->s>>>(a, ncols, W);
-            launched(c);
-            C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
-            C.idx.alloc(C.nnz, c->s);
-            C.val.alloc(C.nnz, c->s);
-            a.optr = C.ptr.p;
-            a.oi = C.idx.p;
-            a.ov = C.val.p;
-            k_spgemm_dense<true><<<grid, 32 * W, smem_d, c->s>>>(a, ncols, W);
-            launched(c);
-            CK(cudaStreamSynchronize(c->s));
-            return C;
-        }
-    }
-    // 1) bound of distinct columns per row; 2) exact distinct count; 3) table placement
-    DBuf<int64_t> need(rows, c->s);
-    k_bound<<<grid_for(rows, 256, c->sms), 256, 0, c->s>>>(rows, A.ptr.p, A.idx.p, B.ptr.p,
-                                                          D ? D->ptr.p : nullptr, B.cols, need.p);
-    launched(c);
-    std::vector<int64_t> h = need.to_host();
-    DPP_TRACE_SCOPE(c, "spgemm.after_bound");
-    std::vector<int64_t> uoff(rows, -1);
-    std::vector<int> ucap(rows, 0);
-    int64_t utot = 0;
-    for (int r = 0; r < rows; ++r) {
-        if (h[r] < UCAP - 1) continue;
-        int cap = 64;
-        while (cap < 2 * h[r] + 2) cap <<= 1;
-        uoff[r] = utot;
-        ucap[r] = cap;
-        utot += cap;
-    }
-    std::vector<int> u(rows);
-    {
-        DPP_TRACE_SCOPE(c, "spgemm.unique");
-        DBuf<int64_t> duoff(rows, c->s);
-        DBuf<int> ducap(rows, c->s), dkey(utot, c->s), duniq(rows, c->s);
-        duoff.upload(uoff.data(), rows);
-        ducap.upload(ucap.data(), rows);
-        k_unique<<<grid_for((int64_t)rows * 32, 32 * UWPB, c->sms, 12), 32 * UWPB, 0, c->s>>>(
-            rows, A.ptr.p, A.idx.p, B.ptr.p, B.idx.p, D ? D->ptr.p : nullptr,
-            D ? D->idx.p : nullptr, duoff.p, ducap.p, dkey.p, duniq.p);
-        launched(c);
-        duniq.download(u.data(), rows);
-        CK(cudaStreamSynchronize(c->s));
-    }
-    std::vector<int64_t> goff(rows, -1);
-    std::vector<int> gcap(rows, 0);
-    int64_t gtot = 0;
-    int nlarge = 0;
-    for (int r = 0; r < rows; ++r) {
-        if (2 * (int64_t)u[r] + 2 <= SM_CAP) continue;
-        if (2 * (int64_t)u[r] + 2 <= SM_CAP_L) { goff[r] = -2; ++nlarge; continue; }
-        int cap = 64;
-        while (cap < 2 * (int64_t)u[r] + 2) cap <<= 1;
-        goff[r] = gtot;
-        gcap[r] = cap;
-        gtot += cap;
-    }
-    DBuf<int64_t> dgoff(rows, c->s);
-    DBuf<int> dgcap(rows, c->s);
-    dgoff.upload(goff.data(), rows);
-    dgcap.upload(gcap.data(), rows);
-    DBuf<int> gk(gtot, c->s), glk(gtot, c->s);
-    DBuf<unsigned char> ghas(gtot, c->s);
-    DBuf<double> gx(gtot, c->s), gd(gtot, c->s), glv(gtot, c->s);
-    DBuf<int> cnt(rows, c->s);
-
     Args a{};
     a.rows = rows;
     a.ap = A.ptr.p; a.ai = A.idx.p; a.av = A.val.p;
@@ -443,49 +446,141 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
     if (D) { a.dp = D->ptr.p; a.di = D->idx.p; a.dv = D->val.p; }
     a.reverse = reverse;
     a.keep_zeros = keep_zeros;
-    a.goff = dgoff.p; a.gcap = dgcap.p;
-    a.g_key = gk.p; a.g_has = ghas.p; a.g_x = gx.p; a.g_d = gd.p; a.g_lk = glk.p; a.g_lv = glv.p;
+    DBuf<int> cnt(rows, c->s);
     a.cnt = cnt.p;
-    const size_t smem = (size_t)WPB * SM_CAP * (4 + 1 + 8 + 8 + 4 + 8);
-    const size_t smem_l = (size_t)SM_CAP_L * (4 + 1 + 8 + 8 + 4 + 8);
-    static bool attr = false;
-    if (!attr) {
-        CK(cudaFuncSetAttribute(k_spgemm<false, SM_CAP, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute(k_spgemm<true, SM_CAP, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        CK(cudaFuncSetAttribute(k_spgemm<false, SM_CAP_L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l));
-        CK(cudaFuncSetAttribute(k_spgemm<true, SM_CAP_L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l));
-        attr = true;
-    }
-    const int grid = grid_for((int64_t)rows * 32 * WPB / WPB, 32 * WPB, c->sms, 12);
-    const int grid_l = std::max(1, std::min(nlarge, c->sms));
-    if (TraceScope::on()) {
-        int nglob = 0;
-        for (int r = 0; r < rows; ++r) nglob += goff[r] >= 0;
-        std::fprintf(stderr, "[dpp-trace]   spgemm %d x %d (A nnz %lld, B nnz %lld): %d large, %d global, gtot %lld\n",
-                     rows, B.cols, (long long)A.nnz, (long long)B.nnz, nlarge, nglob, (long long)gtot);
-    }
-    TraceScope ts_count(c, "spgemm.count");
-    k_spgemm<false, SM_CAP, WPB><<<grid, 32 * WPB, smem, c->s>>>(a, -1);
-    launched(c);
-    if (nlarge) {
-        k_spgemm<false, SM_CAP_L, 1><<<grid_l, 32, smem_l, c->s>>>(a, -2);
+    DBuf<int64_t> toff(rows, c->s);
+    DBuf<int> ti;
+    DBuf<double> tv;
+
+    // small column space and dense-ish rows: dense accumulator, no hashing / sorting
+    const int ncols = B.cols;
+    const size_t per = (size_t)ncols * 16 + (size_t)((ncols + 15) & ~15);
+    const double avg_out = std::min<double>(ncols, (double)A.nnz / rows * ((double)B.nnz / std::max(1, B.rows)));
+    if (ncols <= 4096 && avg_out * 8 >= ncols && per <= 200 * 1024 && (int64_t)rows * ncols <= (int64_t)1 << 24) {
+        const int W = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per));
+        static bool dattr = false;
+        if (!dattr) {
+            CK(cudaFuncSetAttribute(k_spgemm_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            dattr = true;
+        }
+        ti.alloc((size_t)rows * ncols, c->s);
+        tv.alloc((size_t)rows * ncols, c->s);
+        a.ti = ti.p;
+        a.tv = tv.p;
+        k_toff_dense<<<grid_for(rows, 256, c->sms), 256, 0, c->s>>>(rows, ncols, toff.p);
         launched(c);
+        a.toff = toff.p;
+        const int grid = std::max(1, std::min<int>((rows + W - 1) / W, c->sms * 4));
+        k_spgemm_dense<<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
+        launched(c);
+    } else {
+        // 1. symbolic: distinct columns per row
+        std::vector<int> u(rows);
+        {
+            DPP_TRACE_SCOPE(c, "spgemm.unique");
+            DBuf<int> duniq(rows, c->s);
+            k_unique_s<<<std::max(1, std::min<int>((rows + US_W - 1) / US_W, c->sms * 7)), 32 * US_W, 0, c->s>>>(
+                rows, A.ptr.p, A.idx.p, B.ptr.p, B.idx.p, D ? D->ptr.p : nullptr, D ? D->idx.p : nullptr, duniq.p);
+            launched(c);
+            duniq.download(u.data(), rows);
+            CK(cudaStreamSynchronize(c->s));
+            std::vector<int> over;
+            for (int r = 0; r < rows; ++r)
+                if (u[r] < 0) over.push_back(r);
+            if (!over.empty()) {
+                const int no = (int)over.size();
+                DBuf<int> drl(no, c->s);
+                drl.upload(over.data(), no);
+                DBuf<int64_t> need(no, c->s);
+                k_bound_list<<<grid_for(no, 256, c->sms), 256, 0, c->s>>>(drl.p, no, A.ptr.p, A.idx.p, B.ptr.p,
+                                                                          D ? D->ptr.p : nullptr, B.cols, need.p);
+                launched(c);
+                std::vector<int64_t> h = need.to_host();
+                std::vector<int64_t> uoff(no, -1);
+                std::vector<int> ucap(no, 0);
+                int64_t utot = 0;
+                for (int i = 0; i < no; ++i) {
+                    if (h[i] < UCAP - 1) continue;
+                    int cap = 64;
+                    while (cap < 2 * h[i] + 2) cap <<= 1;
+                    uoff[i] = utot;
+                    ucap[i] = cap;
+                    utot += cap;
+                }
+                DBuf<int64_t> duoff(no, c->s);
+                DBuf<int> ducap(no, c->s), dkey(std::max<int64_t>(utot, 1), c->s);
+                duoff.upload(uoff.data(), no);
+                ducap.upload(ucap.data(), no);
+                k_unique_l<<<std::min(no, c->sms * 6), 32, 0, c->s>>>(drl.p, no, A.ptr.p, A.idx.p, B.ptr.p, B.idx.p,
+                                                                    D ? D->ptr.p : nullptr, D ? D->idx.p : nullptr,
+                                                                    duoff.p, ducap.p, dkey.p, duniq.p);
+                launched(c);
+                duniq.download(u.data(), rows);
+                CK(cudaStreamSynchronize(c->s));
+            }
+        }
+        // 2. scratch offsets and size classes
+        std::vector<int64_t> to(rows);
+        int64_t ttot = 0;
+        std::vector<int> rs_s, rs_m, rs_l, rs_g;
+        std::vector<int64_t> goff;
+        std::vector<int> gcap;
+        int64_t gtot = 0;
+        for (int r = 0; r < rows; ++r) {
+            to[r] = ttot;
+            ttot += u[r];
+            const int64_t need = 2 * (int64_t)u[r] + 2;
+            if (need <= 256) rs_s.push_back(r);
+            else if (need <= 1024) rs_m.push_back(r);
+            else if (need <= 4096) rs_l.push_back(r);
+            else {
+                int cap = 64;
+                while (cap < need) cap <<= 1;
+                rs_g.push_back(r);
+                goff.push_back(gtot);
+                gcap.push_back(cap);
+                gtot += cap;
+            }
+        }
+        toff.upload(to.data(), rows);
+        a.toff = toff.p;
+        ti.alloc(std::max<int64_t>(ttot, 1), c->s);
+        tv.alloc(std::max<int64_t>(ttot, 1), c->s);
+        a.ti = ti.p;
+        a.tv = tv.p;
+        if (TraceScope::on())
+            std::fprintf(stderr, "[dpp-trace]   spgemm %d x %d (A nnz %lld, B nnz %lld): rows S %zu M %zu L %zu G %zu\n",
+                         rows, B.cols, (long long)A.nnz, (long long)B.nnz, rs_s.size(), rs_m.size(), rs_l.size(),
+                         rs_g.size());
+        // 3. numeric, one pass per class
+        DPP_TRACE_SCOPE(c, "spgemm.numeric");
+        launch_num<256, 8, 4>(c, a, rs_s);
+        launch_num<1024, 2, 16>(c, a, rs_m);
+        launch_num<4096, 1, 0>(c, a, rs_l);
+        if (!rs_g.empty()) {
+            const int ng = (int)rs_g.size();
+            DBuf<int64_t> dgoff(ng, c->s);
+            DBuf<int> dgcap(ng, c->s);
+            dgoff.upload(goff.data(), ng);
+            dgcap.upload(gcap.data(), ng);
+            DBuf<int> gk(gtot, c->s), glk(gtot, c->s);
+            DBuf<unsigned char> ghas(gtot, c->s);
+            DBuf<double> gx(gtot, c->s), gd(gtot, c->s), glv(gtot, c->s);
+            Args g = a;
+            g.goff = dgoff.p; g.gcap = dgcap.p;
+            g.g_key = gk.p; g.g_has = ghas.p; g.g_x = gx.p; g.g_d = gd.p; g.g_lk = glk.p; g.g_lv = glv.p;
+            launch_num<0, 1, 0>(c, g, rs_g);
+            CK(cudaStreamSynchronize(c->s));   // global tables go out of scope
+        }
     }
-    ts_count.~TraceScope();
-    new (&ts_count) TraceScope(c, "spgemm.fill");
+    // 4. compaction into canonical CSR
     C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
-    C.idx.alloc(C.nnz, c->s);
-    C.val.alloc(C.nnz, c->s);
-    a.optr = C.ptr.p;
-    a.oi = C.idx.p;
-    a.ov = C.val.p;
-    k_spgemm<true, SM_CAP, WPB><<<grid, 32 * WPB, smem, c->s>>>(a, -1);
+    C.idx.alloc(std::max<int64_t>(C.nnz, 1), c->s);
+    C.val.alloc(std::max<int64_t>(C.nnz, 1), c->s);
+    k_compact<<<grid_for((int64_t)rows * 32, 256, c->sms, 8), 256, 0, c->s>>>(rows, toff.p, C.ptr.p, ti.p, tv.p,
+                                                                            C.idx.p, C.val.p);
     launched(c);
-    if (nlarge) {
-        k_spgemm<true, SM_CAP_L, 1><<<grid_l, 32, smem_l, c->s>>>(a, -2);
-        launched(c);
-    }
-    CK(cudaStreamSynchronize(c->s));   // host vectors above go out of scope
+    CK(cudaStreamSynchronize(c->s));   // host vectors / scratch go out of scope
     return C;
 }
 

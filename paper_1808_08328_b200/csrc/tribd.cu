@@ -79,7 +79,7 @@ __global__ void k_bd_seg_size(int n, int B, int C, int nb, int backward, const i
     const int seg = blockIdx.x * blockDim.x + threadIdx.x;
     if (seg >= nb * C) return;
     const int blk = seg / C, k = seg % C, s = blk * B, m = min(B, n - s);
-    int nr = 0;
+    int nr = 0, mb = 0;
     long long nd = 0, ne = 0;
     for (int a = k; a < m; a += C) {
         ++nr;
@@ -89,9 +89,10 @@ __global__ void k_bd_seg_size(int n, int B, int C, int nb, int backward, const i
             const int bc = idx[p] / B;
             if (bc == blk) continue;
             ++ne;
-            atomicMax(maxback, backward ? bc - blk : blk - bc);
+            mb = max(mb, backward ? bc - blk : blk - bc);
         }
     }
+    if (mb) atomicMax(maxback, mb);
     bytes[seg] = seg_bytes(nr, nd, ne);
 }
 

@@ -44,6 +44,15 @@ __device__ __forceinline__ int ld_acquire(const int *p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// level values are the only data exchanged by the level analysis: relaxed (L2) accesses suffice
+__device__ __forceinline__ int ld_relaxed_i(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_i(int *p, int v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release(int *p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -68,18 +77,18 @@ __global__ void __launch_bounds__(256) k_levels(int n, int backward, const int *
             const int cnt = min(8, ptr[row + 1] - p0);
             int lj[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) lj[u] = u < cnt ? ld_acquire(level + idx[p0 + u]) : 0;
+            for (int u = 0; u < 8; ++u) lj[u] = u < cnt ? ld_relaxed_i(level + idx[p0 + u]) : 0;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 long long spins = 0;
                 while (lj[u] < 0) {
-                    lj[u] = ld_acquire(level + idx[p0 + u]);
+                    lj[u] = ld_relaxed_i(level + idx[p0 + u]);
                     if (++spins > SPIN_LIMIT) __trap();
                 }
                 lv = max(lv, lj[u] + 1);
             }
         }
-        st_release(level + row, lv);
+        st_relaxed_i(level + row, lv);
     }
 }
 
@@ -93,16 +102,16 @@ __global__ void __launch_bounds__(256) k_levels_warp(int n, int backward, const 
         int lv = 0;
         for (int p = ptr[row] + lane; p < ptr[row + 1]; p += 32) {
             const int j = idx[p];
-            int lj = ld_acquire(level + j);
+            int lj = ld_relaxed_i(level + j);
             long long spins = 0;
             while (lj < 0) {
-                lj = ld_acquire(level + j);
+                lj = ld_relaxed_i(level + j);
                 if (++spins > SPIN_LIMIT) __trap();
             }
             lv = max(lv, lj + 1);
         }
         for (int o = 16; o > 0; o >>= 1) lv = max(lv, __shfl_xor_sync(0xffffffffu, lv, o));
-        if (lane == 0) st_release(level + row, lv);
+        if (lane == 0) st_relaxed_i(level + row, lv);
     }
 }
 
@@ -305,7 +314,8 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
     launched(c);
 }
 
-Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense) {
+Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf<int> *pre_order,
+             DBuf<int> *pre_lev, int pre_nlev) {
     Tri T;
     T.n = A.rows;
     T.backward = !lower;
@@ -342,7 +352,13 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense) {
         return T;
     }
     DBuf<int> lev;
-    T.nlev = tri_levels(c, T.strict, T.backward, T.order, nullptr, &lev);
+    if (pre_lev) {   // the caller's analysis covers every dependency of this triangle
+        T.order = std::move(*pre_order);
+        lev = std::move(*pre_lev);
+        T.nlev = pre_nlev;
+    } else {
+        T.nlev = tri_levels(c, T.strict, T.backward, T.order, nullptr, &lev);
+    }
     // narrow, deep levels (coarse AMG): block-sequential sweep with dense block inverses
     static const bool no_block = [] { const char *e = std::getenv("DPP_NO_BLOCK"); return e && *e == '1'; }();
     if (TraceScope::on())
@@ -451,10 +467,11 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
     CK(cudaMemcpyAsync(&hm, missing, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
     if (hm) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "missing diagonal entry in sparsity pattern");
-    DBuf<int> order;
+    DBuf<int> order, lev;
+    int nlev = 0;
     {
         Csr lower = csr_part(c, A, -1, false);   // stored pattern: every row the IKJ loop may read
-        tri_levels(c, lower, false, order);
+        nlev = tri_levels(c, lower, false, order, nullptr, &lev);
     }
     DPP_TRACE_SCOPE(c, "ilu0.factor_kernel");
     if (n) {
@@ -467,7 +484,9 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
     CK(cudaMemcpyAsync(&he, err, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
     if (he != 0x7f7f7f7f) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(he));
-    f->L = make_tri(c, f->LU, true, true);
+    // L's zero-free strict pattern is a subset of the stored lower pattern: its levels
+    // are a valid schedule (each row's summation order does not depend on it)
+    f->L = make_tri(c, f->LU, true, true, false, &order, &lev, nlev);
     f->U = make_tri(c, f->LU, false, false);
     f->y.alloc(n, c->s);
     f->tmp.alloc(n, c->s);
