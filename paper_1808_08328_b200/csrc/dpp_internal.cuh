@@ -222,6 +222,7 @@ int tri_levels(Ctx *c, const Csr &strict, bool backward, DBuf<int> &order, DBuf<
 bool cluster_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L);
 bool block_plan(Ctx *c, Tri &T);
 bool bd_plan(Ctx *c, Tri &T, int B);
+void tri_dense_inverse(Ctx *c, Tri &T);
 void trsv_bd(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
              cudaStream_t st);
 void trsv_block(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,

@@ -74,14 +74,16 @@ __host__ __device__ inline long long seg_bytes(int nr, long long nd, long long n
 }
 __device__ __forceinline__ int row_len(int a, int m, int backward) { return backward ? m - a : a + 1; }
 
+// warp per segment: lanes take the segment's rows
 __global__ void k_bd_seg_size(int n, int B, int C, int nb, int backward, const int *__restrict__ ptr,
                               const int *__restrict__ idx, long long *bytes, int *maxback) {
-    const int seg = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int seg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (seg >= nb * C) return;
     const int blk = seg / C, k = seg % C, s = blk * B, m = min(B, n - s);
-    int nr = 0, mb = 0;
-    long long nd = 0, ne = 0;
-    for (int a = k; a < m; a += C) {
+    long long nr = 0, nd = 0, ne = 0;
+    int mb = 0;
+    for (int a = k + C * lane; a < m; a += 32 * C) {
         ++nr;
         nd += row_len(a, m, backward);
         const int r = s + a;
@@ -92,60 +94,75 @@ __global__ void k_bd_seg_size(int n, int B, int C, int nb, int backward, const i
             mb = max(mb, backward ? bc - blk : blk - bc);
         }
     }
-    if (mb) atomicMax(maxback, mb);
-    bytes[seg] = seg_bytes(nr, nd, ne);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        nr += __shfl_xor_sync(0xffffffffu, nr, o);
+        nd += __shfl_xor_sync(0xffffffffu, nd, o);
+        ne += __shfl_xor_sync(0xffffffffu, ne, o);
+        mb = max(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    }
+    if (lane == 0) {
+        if (mb) atomicMax(maxback, mb);
+        bytes[seg] = seg_bytes((int)nr, nd, ne);
+    }
 }
 
 // one CTA per segment: dense block inverse rows + off-block CSR rows -> segment
+// (row offsets from per-row counts; off-block entries keep their CSR order)
+constexpr int BD_SEG_ROWS = 1024;
 __global__ void k_bd_seg_fill(int n, int B, int C, int W, int backward, const int *__restrict__ ptr,
                               const int *__restrict__ idx, const double *__restrict__ val,
                               const double *__restrict__ dense, const long long *__restrict__ soff,
                               unsigned char *segs) {
+    __shared__ int roff_d[BD_SEG_ROWS + 1], roff_e[BD_SEG_ROWS + 1];
     const int seg = blockIdx.x, blk = seg / C, k = seg % C, s = blk * B, m = min(B, n - s);
     unsigned char *S = segs + soff[seg];
     const int nr = m > k ? (m - k + C - 1) / C : 0;
-    __shared__ int ne_s, nd_s;
-    int *dofs = reinterpret_cast<int *>(S + 16);
-    int *optr = dofs + nr + 1;
-    if (threadIdx.x == 0) {
-        int d = 0, e = 0;
-        for (int i = 0; i < nr; ++i) {
-            const int a = k + C * i, r = s + a;
-            dofs[i] = d;
-            optr[i] = e;
-            d += row_len(a, m, backward);
-            for (int p = ptr[r]; p < ptr[r + 1]; ++p) e += (idx[p] / B) != blk;
-        }
-        dofs[nr] = d;
-        optr[nr] = e;
-        reinterpret_cast<int *>(S)[0] = nr;
-        reinterpret_cast<int *>(S)[1] = e;
-        reinterpret_cast<int *>(S)[2] = 0;
-        reinterpret_cast<int *>(S)[3] = 0;
-        ne_s = e;
-        nd_s = d;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    // per-row lengths
+    for (int i = w; i < nr; i += nw) {
+        const int a = k + C * i, r = s + a;
+        int e = 0;
+        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32) e += (idx[p] / B) != blk;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (lane == 0) { roff_d[i + 1] = row_len(a, m, backward); roff_e[i + 1] = e; }
     }
     __syncthreads();
-    const int ne = ne_s, nd = nd_s;
+    if (threadIdx.x == 0) {
+        roff_d[0] = roff_e[0] = 0;
+        for (int i = 0; i < nr; ++i) { roff_d[i + 1] += roff_d[i]; roff_e[i + 1] += roff_e[i]; }
+    }
+    __syncthreads();
+    const int ne = roff_e[nr], nd = roff_d[nr];
+    int *hdr = reinterpret_cast<int *>(S);
+    int *dofs = hdr + 4;
+    int *optr = dofs + nr + 1;
     int *oidx = optr + nr + 1;
     double *dv = reinterpret_cast<double *>(S + bd_pad16(16 + 4LL * (nr + 1) * 2 + 4LL * ne));
     double *ov = dv + nd;
+    if (threadIdx.x == 0) { hdr[0] = nr; hdr[1] = ne; hdr[2] = 0; hdr[3] = 0; }
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) { dofs[i] = roff_d[i]; optr[i] = roff_e[i]; }
     const double *Db = dense + (size_t)blk * B * B;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int i = w; i < nr; i += nw) {
         const int a = k + C * i, r = s + a;
         const int j0 = backward ? a : 0, len = row_len(a, m, backward);
-        for (int q = lane; q < len; q += 32) dv[dofs[i] + q] = Db[(size_t)a * B + j0 + q];
-        if (lane == 0) {
-            int e = optr[i];
-            for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
-                const int bc = idx[p] / B;
-                if (bc == blk) continue;
+        for (int q = lane; q < len; q += 32) dv[roff_d[i] + q] = Db[(size_t)a * B + j0 + q];
+        int o = roff_e[i];
+        for (int p0 = ptr[r]; p0 < ptr[r + 1]; p0 += 32) {
+            const int p = p0 + lane;
+            const bool in = p < ptr[r + 1];
+            const int j = in ? idx[p] : 0;
+            const int bc = j / B;
+            const bool keep = in && bc != blk;
+            const unsigned msk = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int q = o + __popc(msk & ((1u << lane) - 1));
                 // every off-block column lies in the x window (W >= the largest block distance)
-                oidx[e] = (bc % W) * B + (idx[p] - bc * B);
-                ov[e] = val[p];
-                ++e;
+                oidx[q] = (bc % W) * B + (j - bc * B);
+                ov[q] = val[p];
             }
+            o += __popc(msk);
         }
     }
 }
@@ -164,21 +181,57 @@ __global__ void __launch_bounds__(32 * BD_INV_WPB)
     if (c >= m) return;
     for (int i = lane; i < m; i += 32) xc[i] = 0.0;
     __syncwarp();
-    // forward: rows c, c+1, ..., m-1 ; backward: rows c, c-1, ..., 0
-    for (int a = c; backward ? a >= 0 : a < m; a += backward ? -1 : 1) {
-        const int r = s + a;
+    // forward: rows c, c+1, ..., m-1 ; backward: rows c, c-1, ..., 0.  Software
+    // pipelined: row bounds two rows ahead, the first 32 entries and the diagonal
+    // of the next row one row ahead, so a row costs shared-memory latency only.
+    const int step = backward ? -1 : 1;
+    auto valid = [&](int aa) { return backward ? aa >= 0 : aa < m; };
+    int a = c;
+    int pa0 = ptr[s + a], pa1 = ptr[s + a + 1];
+    int pb0 = 0, pb1 = 0;
+    if (valid(a + step)) { pb0 = ptr[s + a + step]; pb1 = ptr[s + a + step + 1]; }
+    constexpr int IPF = 3;   // entries per lane held for the current / next row
+    int jc[IPF];
+    double vc[IPF], dc = diag ? diag[s + a] : 1.0;
+#pragma unroll
+    for (int u = 0; u < IPF; ++u) {
+        const int p = pa0 + 32 * u + lane;
+        jc[u] = p < pa1 ? idx[p] - s : -1;
+        vc[u] = p < pa1 ? val[p] : 0.0;
+    }
+    while (true) {
+        const int an = a + step;
+        int jn[IPF], pc0 = 0, pc1 = 0;
+        double vn[IPF], dn = 1.0;
+        const bool nv = valid(an);
+#pragma unroll
+        for (int u = 0; u < IPF; ++u) {
+            const int p = pb0 + 32 * u + lane;
+            jn[u] = nv && p < pb1 ? idx[p] - s : -1;
+            vn[u] = nv && p < pb1 ? val[p] : 0.0;
+        }
+        if (nv) {
+            if (diag) dn = diag[s + an];
+            if (valid(an + step)) { pc0 = ptr[s + an + step]; pc1 = ptr[s + an + step + 1]; }
+        }
         double acc = 0.0;
-        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
+#pragma unroll
+        for (int u = 0; u < IPF; ++u)
+            if (jc[u] >= 0 && jc[u] < m) acc += vc[u] * xc[jc[u]];
+        for (int p = pa0 + 32 * IPF + lane; p < pa1; p += 32) {
             const int j = idx[p] - s;
             if (j >= 0 && j < m) acc += val[p] * xc[j];
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) {
-            const double d = diag ? diag[r] : 1.0;
-            xc[a] = ((a == c ? 1.0 : 0.0) - acc) / d;
-        }
+        if (lane == 0) xc[a] = ((a == c ? 1.0 : 0.0) - acc) / dc;
         __syncwarp();
+        if (!nv) break;
+        a = an;
+        pa0 = pb0; pa1 = pb1; pb0 = pc0; pb1 = pc1;
+#pragma unroll
+        for (int u = 0; u < IPF; ++u) { jc[u] = jn[u]; vc[u] = vn[u]; }
+        dc = dn;
     }
     double *D = dense + (size_t)blk * B * B;
     for (int i = lane; i < m; i += 32) D[(size_t)i * B + c] = xc[i];
@@ -349,6 +402,24 @@ static int bd_cluster_size() {
     return C;
 }
 
+// dense inverse of a whole (small) triangle: T.dense = T^{-1}, n x n row-major
+void tri_dense_inverse(Ctx *c, Tri &T) {
+    const int n = T.n;
+    T.dense.alloc((size_t)n * n, c->s);
+    CK(cudaMemsetAsync(T.dense.p, 0, sizeof(double) * (size_t)n * n, c->s));
+    const size_t sm = (size_t)BD_INV_WPB * n * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CK(cudaFuncSetAttribute(k_bd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(BD_INV_WPB * 1024 * sizeof(double))));
+        attr = true;
+    }
+    dim3 grid((n + BD_INV_WPB - 1) / BD_INV_WPB, 1);
+    k_bd_inverse<<<grid, 32 * BD_INV_WPB, sm, c->s>>>(n, n, T.backward, T.strict.ptr.p, T.strict.idx.p,
+                                                       T.strict.val.p, T.diag.n ? T.diag.p : nullptr, T.dense.p);
+    launched(c);
+}
+
 bool bd_plan(Ctx *c, Tri &T, int B) {
     const int n = T.n;
     if (n == 0 || B <= 0) return false;
@@ -361,7 +432,7 @@ bool bd_plan(Ctx *c, Tri &T, int B) {
     DBuf<long long> sz(nseg, c->s);
     DBuf<int> mb(1, c->s);
     CK(cudaMemsetAsync(mb.p, 0, sizeof(int), c->s));
-    k_bd_seg_size<<<(nseg + 127) / 128, 128, 0, c->s>>>(n, B, C, P->nb, T.backward, T.strict.ptr.p,
+    k_bd_seg_size<<<(nseg * 32 + 127) / 128, 128, 0, c->s>>>(n, B, C, P->nb, T.backward, T.strict.ptr.p,
                                                          T.strict.idx.p, sz.p, mb.p);
     launched(c);
     P->W = std::max(1, mb.to_host()[0] + 1);   // window slots: blocks back 1..maxback, plus the current

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(256) k_levels(int n, int backward, const int *
             for (int u = 0; u < 8; ++u) {
                 long long spins = 0;
                 while (lj[u] < 0) {
+                    __nanosleep(32);
                     lj[u] = ld_relaxed_i(level + idx[p0 + u]);
                     if (++spins > SPIN_LIMIT) __trap();
                 }
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(256) k_levels_warp(int n, int backward, const 
             int lj = ld_relaxed_i(level + j);
             long long spins = 0;
             while (lj < 0) {
+                __nanosleep(32);
                 lj = ld_relaxed_i(level + j);
                 if (++spins > SPIN_LIMIT) __trap();
             }
@@ -327,16 +329,7 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf
     if (allow_dense && T.n <= DENSE_TRI_MAX) {
         // exact-arithmetic rewrite for small, deep coarse levels: x = T^-1 b as a GEMV
         const int n = T.n;
-        DBuf<double> D((size_t)n * n, c->s);
-        CK(cudaMemsetAsync(D.p, 0, sizeof(double) * n * n, c->s));
-        T.dense.alloc((size_t)n * n, c->s);
-        k_tri_dense<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, T.strict.ptr.p, T.strict.idx.p, T.strict.val.p,
-                                                              T.diag.n ? T.diag.p : nullptr, D.p);
-        launched(c);
-        const size_t sm = (size_t)INV_WPB * n * sizeof(double);
-        CK(cudaFuncSetAttribute(k_tri_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        k_tri_inverse<<<(n + INV_WPB - 1) / INV_WPB, 32 * INV_WPB, sm, c->s>>>(n, T.backward, D.p, T.dense.p);
-        launched(c);
+        tri_dense_inverse(c, T);
         CK(cudaStreamSynchronize(c->s));
         T.nlev = n;
         return T;
@@ -467,11 +460,10 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
     CK(cudaMemcpyAsync(&hm, missing, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
     if (hm) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "missing diagonal entry in sparsity pattern");
-    DBuf<int> order, lev;
-    int nlev = 0;
+    DBuf<int> order;
     {
         Csr lower = csr_part(c, A, -1, false);   // stored pattern: every row the IKJ loop may read
-        nlev = tri_levels(c, lower, false, order, nullptr, &lev);
+        tri_levels(c, lower, false, order);
     }
     DPP_TRACE_SCOPE(c, "ilu0.factor_kernel");
     if (n) {
@@ -484,9 +476,9 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
     CK(cudaMemcpyAsync(&he, err, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
     if (he != 0x7f7f7f7f) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(he));
-    // L's zero-free strict pattern is a subset of the stored lower pattern: its levels
-    // are a valid schedule (each row's summation order does not depend on it)
-    f->L = make_tri(c, f->LU, true, true, false, &order, &lev, nlev);
+    // (the factorization's levels follow the STORED pattern, explicit zeros included:
+    // 363 levels on C2 against 121 for L's zero-free pattern, so L gets its own analysis)
+    f->L = make_tri(c, f->LU, true, true);
     f->U = make_tri(c, f->LU, false, false);
     f->y.alloc(n, c->s);
     f->tmp.alloc(n, c->s);
