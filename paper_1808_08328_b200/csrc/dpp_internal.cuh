@@ -194,6 +194,12 @@ struct ClusterPlan {      // level-ordered per-CTA blocks for the cluster sweep 
     DBuf<unsigned char> blocks;
     DBuf<long long> boff;
 };
+struct PushPlan {         // cluster sweep with st.async point-to-point x exchange (tripush.cu)
+    int C = 0, chunk = 0, L = 0, G = 32, stage = 0, nst = 0, threads = 1024, hmax = 0;
+    DBuf<unsigned char> blocks;
+    DBuf<long long> boff;
+    DBuf<int> tx;         // bytes each CTA receives per level
+};
 struct BlockPlan {        // block-sequential sweep with dense diagonal-block inverses (triblock.cu)
     int nblk = 0, stage = 0, nst = 0;
     DBuf<unsigned char> blocks;
@@ -210,6 +216,7 @@ struct Tri {              // one sweep: strict part (zero-free) + optional diago
     DBuf<int> order;      // rows in (dependency level, row) order: the sweep's ticket order
     DBuf<int> levptr;     // level l = order[levptr[l] .. levptr[l+1])
     std::unique_ptr<ClusterPlan> cl;   // cluster-resident sweep when x fits in one cluster
+    std::unique_ptr<PushPlan> pu;      // cluster-resident sweep, push exchange (preferred)
     std::unique_ptr<BlockPlan> bl;     // block-sequential sweep (small n, narrow levels)
     std::unique_ptr<BdPlan> bd;        // block-dense sweep (AMG smoother factors)
     DBuf<double> dense;   // optional dense inverse (small coarse levels): sweep = triangular GEMV
@@ -220,6 +227,9 @@ struct Tri {              // one sweep: strict part (zero-free) + optional diago
 int tri_levels(Ctx *c, const Csr &strict, bool backward, DBuf<int> &order, DBuf<int> *levptr = nullptr,
                DBuf<int> *lev_out = nullptr);
 bool cluster_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L);
+bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L);
+void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+               cudaStream_t st);
 bool block_plan(Ctx *c, Tri &T);
 bool bd_plan(Ctx *c, Tri &T, int B);
 void tri_dense_inverse(Ctx *c, Tri &T);

@@ -1,0 +1,499 @@
+// Level-scheduled sparse triangular sweep on one thread-block cluster, with
+// point-to-point x exchange (push) instead of a cluster barrier per level.
+//
+// Same problem and arithmetic as tricluster.cu (reference linalg.py:225-227 ILU(0)
+// apply, :383-385 Gauss-Seidel sweeps): each CTA owns a contiguous slice of rows
+// (x seeded with b in shared memory), rows are processed level by level, and
+// every (CTA, level) block is streamed into a shared-memory ring by TMA.  The
+// difference is how a level's results reach the CTAs that need them:
+//
+//   * at setup, every cross-CTA dependency (consumer CTA d reads row j owned by
+//     another CTA) gets a slot in d's halo buffer; a row's block entry carries
+//     its push list (destination CTA, halo slot), and column codes address
+//     either the own slice or the halo;
+//   * when a row is solved, its value is written with st.async straight into
+//     every consumer's halo, counting 8 bytes on the consumer's mbarrier of
+//     the producing level (one single-use mbarrier per level, armed at launch
+//     with the exact byte count the CTA will receive for that level);
+//   * before level l a CTA waits only on its level l-1 mbarrier (all values
+//     it will ever read from level l-1) and on a CTA barrier for its own rows.
+//
+// So a level costs one push latency on the critical path instead of a
+// release/acquire cluster barrier (MEMBAR.GPU + ERRBAR + barrier round trip).
+#include <cooperative_groups.h>
+#include <cub/cub.cuh>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "dpp_internal.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace dpp {
+
+namespace {
+
+constexpr int PU_THREADS = 1024;
+constexpr int PU_MAX = 16;
+constexpr int PU_NST_MAX = 16;
+constexpr int PU_LMAX = 2048;              // one mbarrier per level in shared memory
+constexpr size_t PU_SMEM_LIMIT = 227 * 1024;
+
+__host__ __device__ __forceinline__ long long p16(long long b) { return (b + 15) & ~15LL; }
+__device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned mapa_u32(unsigned a, int rank) {
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+// bounded wait: a miscounted exchange traps (~2 s) instead of hanging the device
+__device__ __forceinline__ void mwait(unsigned a, unsigned parity) {
+    unsigned ok = 0;
+    const long long t0 = clock64();
+    while (true) {
+        asm volatile(
+            "{\n .reg .pred p;\n"
+            " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+        if (ok) return;
+        if (clock64() - t0 > (4ll << 30)) __trap();
+    }
+}
+
+// shared memory: ring mbarriers | level mbarriers [L] | xs [chunk] | halo [hmax] | boff [L+1] | ring
+__host__ __device__ inline size_t pu_fixed(int chunk, int L, int hmax) {
+    return 8 * PU_NST_MAX + p16(8LL * L) + p16(8LL * chunk) + p16(8LL * hmax) + p16(8LL * (L + 1));
+}
+
+// block layout (16-byte aligned):
+//   int nr, ne, np, 0 | lrow[nr] | rend[nr] | double dg[nr] | code[ne] | double val[ne] | ppt[nr+1] | push[np]
+__host__ __device__ inline long long pu_block_bytes(long long nr, long long ne, long long np) {
+    return p16(16 + p16(4 * nr) * 2 + 8 * nr + p16(4 * ne) + 8 * ne + p16(4 * (nr + 1)) + p16(4 * np));
+}
+
+template <int G>
+__global__ void __launch_bounds__(PU_THREADS, 1)
+    k_trsv_push(int n, int chunk, int L, int hmax, int stage, int nst, const unsigned char *__restrict__ blocks,
+                const long long *__restrict__ boff, const int *__restrict__ tx, const double *__restrict__ b,
+                double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long *mring = reinterpret_cast<unsigned long long *>(smem);
+    unsigned long long *mlev = mring + PU_NST_MAX;
+    double *xs = reinterpret_cast<double *>(smem + 8 * PU_NST_MAX + p16(8LL * L));
+    double *halo = xs + p16(8LL * chunk) / 8;
+    long long *boff_s = reinterpret_cast<long long *>(halo + p16(8LL * hmax) / 8);
+    unsigned char *ring = smem + pu_fixed(chunk, L, hmax);
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
+    const int gl = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngrp = blockDim.x / G;
+    const int lane = threadIdx.x & 31;
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1) << (lane & ~(G - 1)));
+    const int base = k * chunk, mine = min(chunk, n - base);
+    const int b0 = k * L;
+    if (threadIdx.x < nst)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mring[threadIdx.x])) : "memory");
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mlev[l])) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mlev[l])), "r"(tx[b0 + l])
+                     : "memory");
+    }
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) xs[i] = b[base + i];
+    for (int i = threadIdx.x; i <= L; i += blockDim.x) boff_s[i] = boff[b0 + i];
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    auto issue = [&](int l, int s) {
+        const unsigned bytes = (unsigned)(boff_s[l + 1] - boff_s[l]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mring[s])), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su32(ring + (size_t)s * stage)), "l"(blocks + boff_s[l]), "r"(bytes), "r"(su32(&mring[s]))
+                     : "memory");
+    };
+    if (threadIdx.x == 0)
+        for (int l = 0; l < min(nst - 1, L); ++l) issue(l, l);
+    // every CTA's level mbarriers are armed before the first push
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    const unsigned halo_a = su32(halo), mlev_a = su32(mlev);
+    int slot = 0, islot = nst - 1;
+    unsigned phase = 0;
+    for (int l = 0; l < L; ++l) {
+        if (threadIdx.x == 0) {
+            mwait(su32(&mring[slot]), phase);
+            if (l > 0) mwait(su32(&mlev[l - 1]), 0);   // every value this CTA reads from level l-1 landed
+        }
+        __syncthreads();   // ... and its own rows of level l-1 are written
+        if (threadIdx.x == 0 && l + nst - 1 < L) issue(l + nst - 1, islot);   // the slot of level l-1 is free
+        const unsigned char *blk = ring + (size_t)slot * stage;
+        if (++slot == nst) { slot = 0; phase ^= 1u; }
+        if (++islot == nst) islot = 0;
+        const int *hd = reinterpret_cast<const int *>(blk);
+        const int nr = hd[0], ne = hd[1];
+        const int *lrow = hd + 4;
+        const int *rend = reinterpret_cast<const int *>(blk + 16 + p16(4LL * nr));
+        const double *dg = reinterpret_cast<const double *>(blk + 16 + 2 * p16(4LL * nr));
+        const int *code = reinterpret_cast<const int *>(blk + 16 + 2 * p16(4LL * nr) + 8LL * nr);
+        const double *val = reinterpret_cast<const double *>(blk + 16 + 2 * p16(4LL * nr) + 8LL * nr + p16(4LL * ne));
+        const int *ppt = reinterpret_cast<const int *>(reinterpret_cast<const unsigned char *>(val) + 8LL * ne);
+        const int *pl = reinterpret_cast<const int *>(reinterpret_cast<const unsigned char *>(ppt) + p16(4LL * (nr + 1)));
+        const unsigned mlev_l = mlev_a + 8u * l;
+        for (int q = grp; q < nr; q += ngrp) {
+            const int r = lrow[q];
+            const int e0 = q ? rend[q - 1] : 0, e1 = rend[q];
+            double sum = 0.0;
+            for (int e = e0 + gl; e < e1; e += G) {
+                const int cd = code[e];
+                sum += val[e] * (cd >= 0 ? xs[cd] : halo[cd & 0x7fffffff]);
+            }
+#pragma unroll
+            for (int s = G / 2; s > 0; s >>= 1) sum += __shfl_xor_sync(gmask, sum, s, G);
+            const double xr = (xs[r] - sum) * dg[q];   // dg = 1/t_ii (as SuperLU's pre-scaled solve)
+            __syncwarp(gmask);
+            if (gl == 0) xs[r] = xr;
+            for (int u = ppt[q] + gl; u < ppt[q + 1]; u += G) {
+                const int pe = pl[u];
+                const int dst = (int)((unsigned)pe >> 28);
+                const unsigned sl = (unsigned)pe & 0x0fffffffu;
+                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                             ::"r"(mapa_u32(halo_a + 8u * sl, dst)), "l"(__double_as_longlong(xr)),
+                             "r"(mapa_u32(mlev_l, dst))
+                             : "memory");
+            }
+        }
+    }
+    __syncthreads();
+    (void)C;
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) {
+        x[base + i] = xs[i];
+        if (xout) xout[base + i] = xadd[base + i] + xs[i];
+    }
+}
+
+// ----------------------------------------------------------------- setup
+__global__ void k_pu_keys(int n, int chunk, int L, const int *lev, int *key, int *rows) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        key[r] = (r / chunk) * L + lev[r];
+        rows[r] = r;
+    }
+}
+__global__ void k_pu_key_ptr(int n, const int *skey, int nkeys, int *lp) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x) {
+        const int v = i < n ? skey[i] : nkeys;
+        const int prev = i ? skey[i - 1] : -1;
+        for (int k = prev + 1; k <= v && k <= nkeys; ++k) lp[k] = i;
+    }
+}
+__global__ void k_pu_cross_count(int n, int chunk, const int *ptr, const int *idx, int *cnt) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        int c = 0;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) c += (idx[p] / chunk) != (r / chunk);
+        cnt[r] = c;
+    }
+}
+__global__ void k_pu_cross_fill(int n, int chunk, const int *ptr, const int *idx, const int *xptr,
+                                unsigned long long *keys) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        int w = xptr[r];
+        const unsigned long long d = (unsigned long long)(r / chunk);
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p)
+            if ((idx[p] / chunk) != (r / chunk)) keys[w++] = (d << 32) | (unsigned)idx[p];
+    }
+}
+// hstart[d] = first halo pair of consumer d (pairs sorted by (d, j))
+__global__ void k_pu_hstart(int nh, const unsigned long long *h, int C, int *hstart) {
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    if (d > C) return;
+    const unsigned long long key = (unsigned long long)d << 32;
+    int lo = 0, hi = nh;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (h[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    hstart[d] = lo;
+}
+// push pairs keyed by source row: (j << 4 | d) -> slot; byte counts per (consumer, level of j)
+__global__ void k_pu_push_keys(int nh, const unsigned long long *h, const int *hstart, int L, const int *lev,
+                               unsigned long long *k2, int *slot, int *tx) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+        const int d = (int)(h[i] >> 32), j = (int)(h[i] & 0xffffffffu);
+        k2[i] = ((unsigned long long)j << 4) | (unsigned)d;
+        slot[i] = i - hstart[d];
+        atomicAdd(&tx[d * L + lev[j]], 8);
+    }
+}
+// pptr[j] = first push pair of source row j
+__global__ void k_pu_pptr(int nh, const unsigned long long *k2s, int n, int *pptr) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= nh; i += gridDim.x * blockDim.x) {
+        const int v = i < nh ? (int)(k2s[i] >> 4) : n;
+        const int prev = i ? (int)(k2s[i - 1] >> 4) : -1;
+        for (int j = prev + 1; j <= v && j <= n; ++j) pptr[j] = i;
+    }
+}
+__global__ void k_pu_lens(int n, const int *perm, const int *ptr, const int *pptr, int *len, int *plen) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int r = perm[q];
+        len[q] = ptr[r + 1] - ptr[r];
+        plen[q] = pptr[r + 1] - pptr[r];
+    }
+}
+__global__ void k_pu_bytes(int nblk, const int *lp, const int *rptr, const int *rpp, long long *bytes) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nblk; i += gridDim.x * blockDim.x) {
+        const int nr = lp[i + 1] - lp[i];
+        const int ne = rptr[lp[i + 1]] - rptr[lp[i]];
+        const int np = rpp[lp[i + 1]] - rpp[lp[i]];
+        bytes[i] = pu_block_bytes(nr, ne, np);
+    }
+}
+__global__ void k_pu_headers(int nblk, const int *lp, const int *rptr, const int *rpp, unsigned char *blocks,
+                             const long long *boff) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nblk; i += gridDim.x * blockDim.x) {
+        int *h = reinterpret_cast<int *>(blocks + boff[i]);
+        const int nr = lp[i + 1] - lp[i];
+        h[0] = nr;
+        h[1] = rptr[lp[i + 1]] - rptr[lp[i]];
+        h[2] = rpp[lp[i + 1]] - rpp[lp[i]];
+        h[3] = 0;
+        if (nr == 0) {   // empty block: ppt[0] = 0
+            *reinterpret_cast<int *>(blocks + boff[i] + 16) = 0;
+        }
+    }
+}
+__global__ void k_pu_fill(int n, int chunk, const int *skey, const int *perm, const int *lp, const int *rptr,
+                          const int *rpp, const long long *boff, const int *ptr, const int *idx, const double *val,
+                          const double *diag, const unsigned long long *h, const int *hstart, const int *pptr,
+                          const unsigned long long *k2s, const int *slots, unsigned char *blocks) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int blk = skey[q];
+        const int q0 = lp[blk], nr = lp[blk + 1] - q0, i = q - q0;
+        const int ne = rptr[lp[blk + 1]] - rptr[q0];
+        unsigned char *B = blocks + boff[blk];
+        const int r = perm[q];
+        const int owner = r / chunk;
+        int *lrow = reinterpret_cast<int *>(B + 16);
+        int *rend = reinterpret_cast<int *>(B + 16 + p16(4LL * nr));
+        double *dg = reinterpret_cast<double *>(B + 16 + 2 * p16(4LL * nr));
+        int *code = reinterpret_cast<int *>(B + 16 + 2 * p16(4LL * nr) + 8LL * nr);
+        double *vv = reinterpret_cast<double *>(B + 16 + 2 * p16(4LL * nr) + 8LL * nr + p16(4LL * ne));
+        int *ppt = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(vv) + 8LL * ne);
+        int *pl = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(ppt) + p16(4LL * (nr + 1)));
+        lrow[i] = r - owner * chunk;
+        rend[i] = rptr[q + 1] - rptr[q0];
+        dg[i] = diag ? 1.0 / diag[r] : 1.0;
+        int w = rptr[q] - rptr[q0];
+        const int hs = hstart[owner], he = hstart[owner + 1];
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p, ++w) {
+            const int j = idx[p];
+            const int o = j / chunk;
+            if (o == owner) {
+                code[w] = j - o * chunk;
+            } else {
+                const unsigned long long key = ((unsigned long long)owner << 32) | (unsigned)j;
+                int lo = hs, hi = he;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (h[mid] < key) lo = mid + 1; else hi = mid;
+                }
+                code[w] = (int)(0x80000000u | (unsigned)(lo - hs));
+            }
+            vv[w] = val[p];
+        }
+        if (i == 0) ppt[0] = 0;
+        ppt[i + 1] = rpp[q + 1] - rpp[q0];
+        int u = rpp[q] - rpp[q0];
+        for (int t = pptr[r]; t < pptr[r + 1]; ++t, ++u)
+            pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28) | (unsigned)slots[t]);
+    }
+}
+
+template <typename T>
+void cub_sort_keys(Ctx *c, T *in, T *out, int n, int end_bit) {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortKeys(nullptr, tb, in, out, n, 0, end_bit, c->s));
+    DBuf<char> t(tb, c->s);
+    CK(cub::DeviceRadixSort::SortKeys(t.p, tb, in, out, n, 0, end_bit, c->s));
+    launched(c);
+}
+
+bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
+    const int n = T.n;
+    const int chunk = (n + C - 1) / C;
+    const int nblk = C * L;
+    const Csr &S = T.strict;
+    // rows grouped by (owner CTA, level)
+    DBuf<int> key(n, c->s), skey(n, c->s), rows(n, c->s), perm(n, c->s), lp((size_t)nblk + 1, c->s);
+    k_pu_keys<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, L, lev.p, key.p, rows.p);
+    launched(c);
+    {
+        int bits = 1;
+        while (bits < 31 && (1 << bits) <= nblk) ++bits;
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, key.p, skey.p, rows.p, perm.p, n, 0, bits, c->s));
+        DBuf<char> t(tb, c->s);
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, key.p, skey.p, rows.p, perm.p, n, 0, bits, c->s));
+        launched(c);
+    }
+    k_pu_key_ptr<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(n, skey.p, nblk, lp.p);
+    launched(c);
+    // unique cross-CTA (consumer, source row) pairs -> halo slots
+    DBuf<int> xcnt(n, c->s), xptr;
+    k_pu_cross_count<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, S.ptr.p, S.idx.p, xcnt.p);
+    launched(c);
+    const int64_t X = counts_to_ptr(c, xcnt.p, n, xptr);
+    int nh = 0;
+    DBuf<unsigned long long> H;
+    if (X > 0) {
+        DBuf<unsigned long long> keys(X, c->s), skeys(X, c->s);
+        k_pu_cross_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, S.ptr.p, S.idx.p, xptr.p, keys.p);
+        launched(c);
+        int cb = 1;
+        while ((1 << cb) <= C) ++cb;
+        cub_sort_keys(c, keys.p, skeys.p, (int)X, 32 + cb);
+        H.alloc(X, c->s);
+        DBuf<int> nsel(1, c->s);
+        size_t tb = 0;
+        CK(cub::DeviceSelect::Unique(nullptr, tb, skeys.p, H.p, nsel.p, (int)X, c->s));
+        DBuf<char> t(tb, c->s);
+        CK(cub::DeviceSelect::Unique(t.p, tb, skeys.p, H.p, nsel.p, (int)X, c->s));
+        launched(c);
+        nh = nsel.to_host()[0];
+    }
+    DBuf<int> hstart(C + 1, c->s);
+    k_pu_hstart<<<1, 32, 0, c->s>>>(nh, H.p, C, hstart.p);
+    launched(c);
+    std::vector<int> hh = hstart.to_host();
+    int hmax = 0;
+    for (int d = 0; d < C; ++d) hmax = std::max(hmax, hh[d + 1] - hh[d]);
+    if (hmax >= (1 << 28)) return false;
+    // push lists by source row, byte counts per (consumer, level)
+    DBuf<unsigned long long> k2(std::max(nh, 1), c->s), k2s(std::max(nh, 1), c->s);
+    DBuf<int> slot(std::max(nh, 1), c->s), slots(std::max(nh, 1), c->s), pptr(n + 1, c->s);
+    auto P = std::make_unique<PushPlan>();
+    P->tx.alloc((size_t)C * L, c->s);
+    CK(cudaMemsetAsync(P->tx.p, 0, sizeof(int) * (size_t)C * L, c->s));
+    if (nh > 0) {
+        k_pu_push_keys<<<grid_for(nh, 256, c->sms), 256, 0, c->s>>>(nh, H.p, hstart.p, L, lev.p, k2.p, slot.p,
+                                                                    P->tx.p);
+        launched(c);
+        int nb = 1;
+        while (nb < 31 && (1LL << nb) <= n) ++nb;
+        size_t tb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k2.p, k2s.p, slot.p, slots.p, nh, 0, 4 + nb, c->s));
+        DBuf<char> t(tb, c->s);
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, k2.p, k2s.p, slot.p, slots.p, nh, 0, 4 + nb, c->s));
+        launched(c);
+    }
+    k_pu_pptr<<<grid_for(nh + 1, 256, c->sms), 256, 0, c->s>>>(nh, k2s.p, n, pptr.p);
+    launched(c);
+    // block sizes
+    DBuf<int> len(n, c->s), plen(n, c->s), rptr, rpp;
+    k_pu_lens<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, perm.p, S.ptr.p, pptr.p, len.p, plen.p);
+    launched(c);
+    counts_to_ptr(c, len.p, n, rptr);
+    counts_to_ptr(c, plen.p, n, rpp);
+    DBuf<long long> bytes((size_t)nblk + 1, c->s), boff((size_t)nblk + 1, c->s);
+    CK(cudaMemsetAsync(bytes.p + nblk, 0, sizeof(long long), c->s));
+    k_pu_bytes<<<grid_for(nblk, 256, c->sms), 256, 0, c->s>>>(nblk, lp.p, rptr.p, rpp.p, bytes.p);
+    launched(c);
+    {
+        size_t tb = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, bytes.p, boff.p, nblk + 1, c->s));
+        DBuf<char> t(tb, c->s);
+        CK(cub::DeviceScan::ExclusiveSum(t.p, tb, bytes.p, boff.p, nblk + 1, c->s));
+        launched(c);
+    }
+    std::vector<long long> hb = bytes.to_host();
+    long long mx = 16;
+    for (int i = 0; i < nblk; ++i) mx = std::max(mx, hb[i]);
+    std::vector<int> hlp = lp.to_host();
+    int widest = 1;
+    for (int i = 0; i < nblk; ++i) widest = std::max(widest, hlp[i + 1] - hlp[i]);
+    const size_t fixed = pu_fixed(chunk, L, hmax);
+    if (fixed >= PU_SMEM_LIMIT) return false;
+    const long long stage = (mx + 127) & ~127LL;
+    const int nst = (int)std::min<long long>(PU_NST_MAX, (long long)(PU_SMEM_LIMIT - fixed) / stage);
+    if (nst < 2) return false;
+    long long total = 0;
+    CK(cudaMemcpyAsync(&total, boff.p + nblk, sizeof(long long), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    P->C = C;
+    P->chunk = chunk;
+    P->L = L;
+    P->hmax = hmax;
+    P->stage = (int)stage;
+    P->nst = nst;
+    const double avg = (double)S.nnz / n;
+    P->G = 2;
+    while (P->G < 32 && P->G * 4 < avg) P->G *= 2;
+    int threads = 64;
+    while (threads < PU_THREADS && (threads / P->G) < widest) threads *= 2;
+    P->threads = threads;
+    P->blocks.alloc((size_t)total, c->s);
+    P->boff = std::move(boff);
+    k_pu_headers<<<grid_for(nblk, 256, c->sms), 256, 0, c->s>>>(nblk, lp.p, rptr.p, rpp.p, P->blocks.p, P->boff.p);
+    launched(c);
+    k_pu_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, skey.p, perm.p, lp.p, rptr.p, rpp.p, P->boff.p,
+                                                          S.ptr.p, S.idx.p, S.val.p, T.diag.n ? T.diag.p : nullptr,
+                                                          H.p, hstart.p, pptr.p, k2s.p, slots.p, P->blocks.p);
+    launched(c);
+    CK(cudaStreamSynchronize(c->s));
+    if (TraceScope::on())
+        std::fprintf(stderr, "[dpp-trace]   push_plan n=%d C=%d L=%d G=%d thr=%d halo max %d (pairs %d) stage=%lld nst=%d\n",
+                     n, C, L, P->G, threads, hmax, nh, stage, nst);
+    T.pu = std::move(P);
+    return true;
+}
+
+}  // namespace
+
+bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
+    const int n = T.n;
+    if (n == 0 || L < 1 || L > PU_LMAX) return false;
+    static bool attr = false;
+    if (!attr) {
+        auto setk = [](const void *f) {
+            CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PU_SMEM_LIMIT));
+            CK(cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        };
+        setk((const void *)k_trsv_push<2>);
+        setk((const void *)k_trsv_push<4>);
+        setk((const void *)k_trsv_push<8>);
+        setk((const void *)k_trsv_push<16>);
+        setk((const void *)k_trsv_push<32>);
+        attr = true;
+    }
+    // as many CTAs as useful: each keeps >= ~2k rows of x
+    const int C0 = std::max(2, std::min(PU_MAX, (n + 2047) / 2048));
+    for (int C = C0; C <= PU_MAX; ++C)
+        if (try_push(c, T, lev, L, C)) return true;
+    return false;
+}
+
+void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+               cudaStream_t st) {
+    const PushPlan &P = *T.pu;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.C, 1, 1);
+    cfg.blockDim = dim3(P.threads, 1, 1);
+    cfg.dynamicSmemBytes = pu_fixed(P.chunk, P.L, P.hmax) + (size_t)P.nst * P.stage;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = P.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const unsigned char *B = P.blocks.p;
+    const long long *O = P.boff.p;
+    cudaError_t e;
+    switch (P.G) {
+        case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_push<2>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_push<4>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
+        case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_push<8>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
+        case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_push<16>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_trsv_push<32>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
+    }
+    CK(e);
+    launched(c);
+}
+
+}  // namespace dpp

@@ -303,6 +303,10 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
         trsv_block(c, T, b, x, xadd, xout, st);
         return;
     }
+    if (T.pu) {
+        trsv_push(c, T, b, x, xadd, xout, st);
+        return;
+    }
     if (T.cl) {
         trsv_cluster(c, T, b, x, xadd, xout, st);
         return;
@@ -359,7 +363,8 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf
                      (long long)T.strict.nnz, T.nlev, (int)T.backward);
     if (!no_block && T.n <= 8192 && (int64_t)T.nlev * 64 > T.n && block_plan(c, T)) return T;
     static const bool no_cluster = [] { const char *e = std::getenv("DPP_NO_CLUSTER"); return e && *e == '1'; }();
-    if (!no_cluster) cluster_plan(c, T, lev, T.nlev);
+    static const bool no_push = [] { const char *e = std::getenv("DPP_NO_PUSH"); return e && *e == '1'; }();
+    if (!no_cluster && !(!no_push && push_plan(c, T, lev, T.nlev))) cluster_plan(c, T, lev, T.nlev);
     return T;
 }
 
