@@ -187,10 +187,19 @@ def sync():
     call("dpp_ctx_sync", ctx())
 
 
-# power-iteration start vector of the reference (linalg.py:330)
+# power-iteration start vector of the reference (linalg.py:330): a fresh
+# default_rng(12345) per call, so the vector depends on n only -- cached per n
+_RANDN_CACHE = {}
+
+
 def _randn(n, out, _user):
-    v = np.random.default_rng(12345).standard_normal(int(n))
-    C.memmove(out, v.ctypes.data, 8 * int(n))
+    n = int(n)
+    v = _RANDN_CACHE.get(n)
+    if v is None:
+        v = np.random.default_rng(12345).standard_normal(n)
+        if len(_RANDN_CACHE) < 64:
+            _RANDN_CACHE[n] = v
+    C.memmove(out, v.ctypes.data, 8 * n)
 
 
 RANDN = RANDN_FN(_randn)

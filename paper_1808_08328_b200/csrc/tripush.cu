@@ -38,7 +38,7 @@ constexpr int PU_THREADS = 1024;
 constexpr int PU_MAX = 16;
 constexpr int PU_NST_MAX = 16;
 constexpr int PU_LMAX = 2048;              // one mbarrier per level in shared memory
-constexpr size_t PU_SMEM_LIMIT = 227 * 1024;
+constexpr size_t PU_SMEM_LIMIT = 226 * 1024;   // dynamic; leaves room for static shared memory
 
 __host__ __device__ __forceinline__ long long p16(long long b) { return (b + 15) & ~15LL; }
 __device__ __forceinline__ unsigned su32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -76,8 +76,11 @@ template <int G>
 __global__ void __launch_bounds__(PU_THREADS, 1)
     k_trsv_push(int n, int chunk, int L, int hmax, int stage, int nst, const unsigned char *__restrict__ blocks,
                 const long long *__restrict__ boff, const int *__restrict__ tx, const double *__restrict__ b,
-                double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout) {
+                double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout, int l2pf,
+                unsigned long long *dbg) {
     extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ unsigned long long t_last, t_pre, t_w[32], t_wp[32];
+    unsigned long long acc_ring = 0, acc_lev = 0, acc_sync = 0, acc_comp = 0, acc_pre = 0, tA = 0, tB = 0, tC = 0, tD = 0;
     unsigned long long *mring = reinterpret_cast<unsigned long long *>(smem);
     unsigned long long *mlev = mring + PU_NST_MAX;
     double *xs = reinterpret_cast<double *>(smem + 8 * PU_NST_MAX + p16(8LL * L));
@@ -100,6 +103,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     }
     for (int i = threadIdx.x; i < mine; i += blockDim.x) xs[i] = b[base + i];
     for (int i = threadIdx.x; i <= L; i += blockDim.x) boff_s[i] = boff[b0 + i];
+    if (dbg && threadIdx.x < 32) { t_w[threadIdx.x] = 0; t_wp[threadIdx.x] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     auto issue = [&](int l, int s) {
@@ -109,20 +113,46 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                      ::"r"(su32(ring + (size_t)s * stage)), "l"(blocks + boff_s[l]), "r"(bytes), "r"(su32(&mring[s]))
                      : "memory");
     };
-    if (threadIdx.x == 0)
+    // blocks further ahead than the ring are pulled into L2, so the ring's
+    // copies come from L2 rather than HBM
+    auto prefetch = [&](int l) {
+        const unsigned bytes = (unsigned)(boff_s[l + 1] - boff_s[l]);
+        if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[l]), "r"(bytes) : "memory");
+    };
+    if (threadIdx.x == 0) {
         for (int l = 0; l < min(nst - 1, L); ++l) issue(l, l);
+        for (int l = nst - 1; l < min(nst - 1 + l2pf, L); ++l) prefetch(l);
+    }
     // every CTA's level mbarriers are armed before the first push
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     const unsigned halo_a = su32(halo), mlev_a = su32(mlev);
     int slot = 0, islot = nst - 1;
     unsigned phase = 0;
     for (int l = 0; l < L; ++l) {
+        if (dbg && threadIdx.x == 0) {
+            tA = clock64();
+            if (l > 0) {
+                unsigned long long m1 = 0, m2 = 0;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { m1 = max(m1, t_w[w]); m2 = max(m2, t_wp[w]); }
+                if (m1 > tD) acc_comp += m1 - tD;   // level l-1: sync exit -> last warp pushed
+                if (m2 > tD) acc_pre += m2 - tD;    // level l-1: sync exit -> last warp computed
+            }
+        }
         if (threadIdx.x == 0) {
             mwait(su32(&mring[slot]), phase);
+            if (dbg) tB = clock64();
             if (l > 0) mwait(su32(&mlev[l - 1]), 0);   // every value this CTA reads from level l-1 landed
+            if (dbg) tC = clock64();
         }
         __syncthreads();   // ... and its own rows of level l-1 are written
-        if (threadIdx.x == 0 && l + nst - 1 < L) issue(l + nst - 1, islot);   // the slot of level l-1 is free
+        if (dbg && threadIdx.x == 0) {
+            tD = clock64();
+            acc_ring += tB - tA; acc_lev += tC - tB; acc_sync += tD - tC;
+        }
+        if (threadIdx.x == 0) {
+            if (l + nst - 1 < L) issue(l + nst - 1, islot);   // the slot of level l-1 is free
+            if (l + nst - 1 + l2pf < L) prefetch(l + nst - 1 + l2pf);
+        }
         const unsigned char *blk = ring + (size_t)slot * stage;
         if (++slot == nst) { slot = 0; phase ^= 1u; }
         if (++islot == nst) islot = 0;
@@ -149,6 +179,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
             const double xr = (xs[r] - sum) * dg[q];   // dg = 1/t_ii (as SuperLU's pre-scaled solve)
             __syncwarp(gmask);
             if (gl == 0) xs[r] = xr;
+            if (dbg && lane == 0) t_wp[threadIdx.x >> 5] = clock64();
             for (int u = ppt[q] + gl; u < ppt[q + 1]; u += G) {
                 const int pe = pl[u];
                 const int dst = (int)((unsigned)pe >> 28);
@@ -159,8 +190,13 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                              : "memory");
             }
         }
+        if (dbg) { __syncwarp(); if (lane == 0) t_w[threadIdx.x >> 5] = clock64(); }
     }
     __syncthreads();
+    if (dbg && threadIdx.x == 0) {
+        const int k0 = (int)cl.block_rank();
+        dbg[k0 * 4 + 0] = acc_ring; dbg[k0 * 4 + 1] = acc_pre; dbg[k0 * 4 + 2] = acc_sync; dbg[k0 * 4 + 3] = acc_comp;
+    }
     (void)C;
     for (int i = threadIdx.x; i < mine; i += blockDim.x) {
         x[base + i] = xs[i];
@@ -484,16 +520,32 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     cfg.numAttrs = 1;
     const unsigned char *B = P.blocks.p;
     const long long *O = P.boff.p;
+    static const int l2pf = [] { const char *e = std::getenv("DPP_PU_NOPF"); return e && *e == '1' ? 0 : 4; }();
+    static const bool dbg_on = [] { const char *e = std::getenv("DPP_PU_DEBUG"); return e && *e == '1'; }();
+    unsigned long long *dbg = nullptr;
+    if (dbg_on && !c->capturing) {
+        CK(cudaMallocAsync((void **)&dbg, sizeof(unsigned long long) * 4 * P.C, st));
+        CK(cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 4 * P.C, st));
+    }
     cudaError_t e;
     switch (P.G) {
-        case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_push<2>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
-        case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_push<4>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
-        case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_push<8>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
-        case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_push<16>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
-        default: e = cudaLaunchKernelEx(&cfg, k_trsv_push<32>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout); break;
+        case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_push<2>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_push<4>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
+        case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_push<8>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
+        case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_push<16>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_trsv_push<32>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
     }
     CK(e);
     launched(c);
+    if (dbg) {
+        std::vector<unsigned long long> h(4 * P.C);
+        CK(cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFreeAsync(dbg, st);
+        std::fprintf(stderr, "[dpp-push] n=%d L=%d G=%d cycles/level CTA0: ring %.0f computed %.0f sync %.0f pushed %.0f | CTA8: ring %.0f computed %.0f sync %.0f pushed %.0f\n",
+                     T.n, P.L, P.G, (double)h[0] / P.L, (double)h[1] / P.L, (double)h[2] / P.L, (double)h[3] / P.L,
+                     (double)h[32] / P.L, (double)h[33] / P.L, (double)h[34] / P.L, (double)h[35] / P.L);
+    }
 }
 
 }  // namespace dpp
