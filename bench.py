@@ -40,6 +40,17 @@ CONFIG = dict(workload="C2: 3D TET 40^3 CG-VMS P1, k2=0.01, scale split, GMRES(3
               formulation="cgvms", dim=3, kind="tet", n=40, k2=0.01, method="scale", rtol=1e-8)
 
 
+def measured_traffic():
+    """DRAM bytes (read + write) of one Arnoldi step from the newest committed ncu
+    capture (profiles/r*_traffic.json, written by tools/summarize_profiles.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None, None
+    d = json.load(open(files[-1]))
+    return d.get("arnoldi_step_dram_bytes"), d.get("source")
+
+
 def measured_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -281,6 +292,7 @@ def main():
     if rank != 0:
         return
     peak, peak_kind = measured_peak()
+    traffic, traffic_src = measured_traffic()
     prof = r["prof"]
     step_bytes = prof.spmv_bytes + prof.pc_bytes
     step_ms = prof.spmv_ms + prof.pc_ms
@@ -297,7 +309,8 @@ def main():
         "gpu_launches": int(r["launches"] / max(args.steps, 1)),
         "clocks": r["clocks"],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind,
                      "kernel": "Arnoldi step: CSR SpMV(K) + preconditioner apply (graph)",
                      "bytes_per_step": step_bytes, "spmv_ms": prof.spmv_ms, "pc_ms": prof.pc_ms,
                      "spmv_gbs": prof.spmv_bytes / (prof.spmv_ms * 1e-3) / 1e9,

@@ -276,7 +276,7 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
         if (worker.joinable()) worker.join();
         if (werr) std::rethrow_exception(werr);
     };
-    static const bool serial = [] { const char *e = std::getenv("DPP_SERIAL_SETUP"); return e && *e == '1'; }();
+    const bool serial = !(fork_mask() & FORK_AMG_SMOOTHER);
     struct Joiner {
         std::thread &t;
         ~Joiner() { if (t.joinable()) t.join(); }

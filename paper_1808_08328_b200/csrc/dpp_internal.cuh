@@ -137,8 +137,11 @@ struct SideStream {
     ~SideStream();
 };
 // run side(view) on a host thread with the side stream while main_fn() runs here
+// kind: FORK_ADDITIVE / FORK_SCHUR (DPP_FORK_MASK bits; DPP_SERIAL_SETUP=1 clears all)
+constexpr int FORK_ADDITIVE = 1, FORK_SCHUR = 2, FORK_AMG_SMOOTHER = 4;
+int fork_mask();
 void fork_join(Ctx *c, SideStream &owner, const std::function<void(Ctx *)> &side,
-               const std::function<void()> &main_fn);
+               const std::function<void()> &main_fn, int kind);
 
 int64_t counts_to_ptr(Ctx *c, const int *counts, int n, DBuf<int> &ptr);
 

@@ -165,7 +165,7 @@ struct Builder {
                           bb.c = sc;
                           N->b = bb.leaf(nd.child_type[1], nd.child_node[1], D, gB);
                       },
-                      [&] { N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA); });
+                      [&] { N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA); }, FORK_ADDITIVE);
             CK(cudaEventCreateWithFlags(&N->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&N->ev_join, cudaEventDisableTiming));
             N->desc = "additive(" + N->a.desc + ", " + N->b.desc + ")";
@@ -196,7 +196,7 @@ struct Builder {
                           S = spgemm(c, C, B, dinv.p, true, &D);
                       }
                       N->b = leaf(nd.child_type[1], nd.child_node[1], S, gB);
-                  });
+                  }, FORK_SCHUR);
         N->Bc = csr_drop_zeros(c, B);
         N->Cc = csr_drop_zeros(c, C);
         N->desc = "schur-full(" + N->a.desc + ", selfp->" + N->b.desc + ")";

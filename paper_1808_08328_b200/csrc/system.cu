@@ -27,8 +27,10 @@ TraceScope::~TraceScope() {
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
         cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
     }
-    std::fprintf(stderr, "[dpp-trace] %-28s %9.3f ms   pool reserved %7.1f MB used %7.1f MB\n", name,
-                 now() - t0, res / 1048576.0, used / 1048576.0);
+    static const double origin = now();
+    const size_t tid = std::hash<std::thread::id>{}(std::this_thread::get_id()) % 1000;
+    std::fprintf(stderr, "[dpp-trace] %-28s %9.3f ms   pool reserved %7.1f MB used %7.1f MB  @%10.3f t%03zu\n", name,
+                 now() - t0, res / 1048576.0, used / 1048576.0, t0 - origin, tid);
 }
 
 void SideStream::ensure(Ctx *parent) {
@@ -48,12 +50,21 @@ SideStream::~SideStream() {
     cudaStreamDestroy(s);
 }
 
+int fork_mask() {
+    static const int m = [] {
+        const char *s = std::getenv("DPP_SERIAL_SETUP");
+        if (s && *s == '1') return 0;
+        const char *e = std::getenv("DPP_FORK_MASK");
+        return e ? std::atoi(e) : 7;
+    }();
+    return m;
+}
+
 void fork_join(Ctx *c, SideStream &owner, const std::function<void(Ctx *)> &side,
-               const std::function<void()> &main_fn) {
+               const std::function<void()> &main_fn, int kind) {
     owner.ensure(c);
     CK(cudaStreamSynchronize(c->s));   // inputs produced on the parent stream are ready
-    static const bool serial = [] { const char *e = std::getenv("DPP_SERIAL_SETUP"); return e && *e == '1'; }();
-    if (serial) {
+    if (!(fork_mask() & kind)) {
         side(&owner.ctx);
         CK(cudaStreamSynchronize(owner.s));
         main_fn();

@@ -150,6 +150,11 @@ int tri_levels(Ctx *c, const Csr &S, bool backward, DBuf<int> &order, DBuf<int> 
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_levels, block, 0));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_w, k_levels_warp, block, 0));
     if (per_sm < 1 || per_sm_w < 1) DPP_FAIL(DPP_ERR_CUDA, "level analysis kernels cannot be resident");
+    // the spinning analysis kernels take at most half of every SM, so setup work of
+    // other fork_join branches (SpGEMM, other analyses) keeps running beside them
+    static const int share = [] { const char *e = std::getenv("DPP_LEVELS_SHARE"); return e ? std::atoi(e) : 2; }();
+    per_sm = std::max(1, per_sm / std::max(1, share));
+    per_sm_w = std::max(1, per_sm_w / std::max(1, share));
     const int64_t warps_res = (int64_t)c->sms * per_sm_w * (block / 32);
     const double avg = n ? (double)S.nnz / n : 0.0;
     if (n <= warps_res && avg > 8.0) {
@@ -472,7 +477,7 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
     }
     DPP_TRACE_SCOPE(c, "ilu0.factor_kernel");
     if (n) {
-        const int warps = std::min<int64_t>(n, (int64_t)c->sms * 16);
+        const int warps = std::min<int64_t>(n, (int64_t)c->sms * 8);
         k_ilu0<<<(warps + ILU_WPB - 1) / ILU_WPB, 32 * ILU_WPB, 0, c->s>>>(
             n, f->LU.ptr.p, f->LU.idx.p, f->LU.val.p, dpos.p, flags.p, ticket, err, order.p);
         launched(c);
