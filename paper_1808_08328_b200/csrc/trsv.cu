@@ -71,19 +71,26 @@ __global__ void __launch_bounds__(256) k_levels(int n, int backward, const int *
         const int64_t t = base + lane * W + w;
         if (t >= n) continue;
         const int row = backward ? n - 1 - (int)t : (int)t;
-        // dependencies in batches of 8 loads in flight; spin only on the ones not ready
+        // dependencies in batches of 8 loads in flight; spin only on the ones not ready.
+        // Far dependencies first (CSR columns ascend: the nearest row is last for a
+        // lower triangle, first for an upper one): while the nearest -- normally the
+        // last to finish -- is pending, the others are already loaded.
         int lv = 0;
-        for (int p0 = ptr[row]; p0 < ptr[row + 1]; p0 += 8) {
-            const int cnt = min(8, ptr[row + 1] - p0);
-            int lj[8];
+        const int rs = ptr[row], re = ptr[row + 1];
+        for (int k0 = 0; k0 < re - rs; k0 += 8) {
+            const int cnt = min(8, re - rs - k0);
+            int lj[8], pj[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) lj[u] = u < cnt ? ld_relaxed_i(level + idx[p0 + u]) : 0;
+            for (int u = 0; u < 8; ++u) {
+                pj[u] = backward ? re - 1 - (k0 + u) : rs + k0 + u;
+                lj[u] = u < cnt ? ld_relaxed_i(level + idx[pj[u]]) : 0;
+            }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 long long spins = 0;
                 while (lj[u] < 0) {
                     __nanosleep(32);
-                    lj[u] = ld_relaxed_i(level + idx[p0 + u]);
+                    lj[u] = ld_relaxed_i(level + idx[pj[u]]);
                     if (++spins > SPIN_LIMIT) __trap();
                 }
                 lv = max(lv, lj[u] + 1);
@@ -101,8 +108,9 @@ __global__ void __launch_bounds__(256) k_levels_warp(int n, int backward, const 
     for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += W) {
         const int row = backward ? n - 1 - (int)t : (int)t;
         int lv = 0;
-        for (int p = ptr[row] + lane; p < ptr[row + 1]; p += 32) {
-            const int j = idx[p];
+        const int rs = ptr[row], re = ptr[row + 1];
+        for (int k = lane; k < re - rs; k += 32) {   // far dependencies first (see k_levels)
+            const int j = idx[backward ? re - 1 - k : rs + k];
             int lj = ld_relaxed_i(level + j);
             long long spins = 0;
             while (lj < 0) {
