@@ -49,8 +49,7 @@ struct Args {
     const int *gcap;
     int *g_key;
     unsigned char *g_has;
-    double *g_x, *g_d, *g_lv;
-    int *g_lk;
+    double *g_x, *g_d;
     // output: sorted survivors at toff[row] in the scratch, count in cnt[row]
     const int64_t *toff;
     int *ti;
@@ -218,8 +217,6 @@ struct Table {
     int *key;
     unsigned char *has;   // bit0: x present, bit1: d present
     double *x, *d;
-    int *lk;
-    double *lv;
     int cap;
 };
 __device__ __forceinline__ int tab_slot(Table &t, int j) {
@@ -230,26 +227,26 @@ __device__ __forceinline__ int tab_slot(Table &t, int j) {
         h = (h + 1) & (t.cap - 1);
     }
 }
-constexpr int SLOT_BYTES = 4 + 1 + 8 + 8 + 4 + 8;
+// shared table per warp: x[CAP] | d[CAP] (only with a D operand) | key[CAP] | has[CAP];
+// survivors are compacted in place (key -> column, x -> value)
+__host__ __device__ constexpr int slot_bytes(bool has_d) { return 8 + (has_d ? 8 : 0) + 4 + 1; }
 
 // CAP: shared table slots per warp (0 => global tables); K: survivor keys per
 // lane held in registers for ranking (0 => rank loop over shared memory)
-template <int CAP, int W, int K>
+template <int CAP, int W, int K, bool HD>
 __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
-    extern __shared__ unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char *base = smem + (size_t)CAP * SLOT_BYTES * w;
+    unsigned char *base = smem + (size_t)CAP * slot_bytes(HD) * w;
     for (int li = blockIdx.x * W + w; li < a.nrl; li += gridDim.x * W) {
         const int row = a.rl[li];
         Table t;
         if (CAP > 0) {
             t.cap = CAP;
             t.x = (double *)base;
-            t.d = t.x + CAP;
-            t.lv = t.d + CAP;
-            t.key = (int *)(t.lv + CAP);
-            t.lk = t.key + CAP;
-            t.has = (unsigned char *)(t.lk + CAP);
+            t.d = HD ? t.x + CAP : t.x;
+            t.key = (int *)(t.x + (HD ? 2 : 1) * CAP);
+            t.has = (unsigned char *)(t.key + CAP);
         } else {
             const int64_t go = a.goff[li];
             t.cap = a.gcap[li];
@@ -257,12 +254,10 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             t.has = a.g_has + go;
             t.x = a.g_x + go;
             t.d = a.g_d + go;
-            t.lk = a.g_lk + go;
-            t.lv = a.g_lv + go;
         }
         for (int h = lane; h < t.cap; h += 32) { t.key[h] = -1; t.has[h] = 0; }
         __syncwarp();
-        if (a.dp) {
+        if (HD) {
             for (int p = a.dp[row] + lane; p < a.dp[row + 1]; p += 32) {
                 const int sl = tab_slot(t, a.di[p]);
                 t.d[sl] = a.dv[p];
@@ -275,7 +270,8 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
             else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
         });
-        // survivors (slot order) ...
+        // survivors compacted in place, in slot order (a survivor's position never
+        // exceeds its slot, so no unread slot is overwritten) ...
         int nsurv = 0;
         for (int h0 = 0; h0 < t.cap; h0 += 32) {
             const int h = h0 + lane;
@@ -285,7 +281,7 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             if (h < t.cap && t.key[h] >= 0) {
                 const unsigned char f = t.has[h];
                 j = t.key[h];
-                if (!a.dp) v = t.x[h];                                              // C = A B
+                if (!HD) v = t.x[h];                                                 // C = A B
                 else if (f & 1) v = (f & 2) ? __dsub_rn(t.d[h], t.x[h]) : -t.x[h];   // D - X
                 else v = t.d[h];
                 keep = a.keep_zeros || v != 0.0;
@@ -293,12 +289,12 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             const unsigned m = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int pos = nsurv + __popc(m & ((1u << lane) - 1));
-                t.lk[pos] = j;
-                t.lv[pos] = v;
+                t.key[pos] = j;
+                t.x[pos] = v;
             }
             nsurv += __popc(m);
+            __syncwarp();
         }
-        __syncwarp();
         // ... ranked by column into the scratch
         const int64_t o = a.toff[row];
         if (K > 0) {
@@ -306,26 +302,26 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
 #pragma unroll
             for (int u = 0; u < K; ++u) {
                 const int q = u * 32 + lane;
-                mk[u] = q < nsurv ? t.lk[q] : 0x7fffffff;
+                mk[u] = q < nsurv ? t.key[q] : 0x7fffffff;
                 rk[u] = 0;
             }
             for (int v = 0; v < nsurv; ++v) {
-                const int kv = t.lk[v];
+                const int kv = t.key[v];
 #pragma unroll
                 for (int u = 0; u < K; ++u) rk[u] += kv < mk[u];
             }
 #pragma unroll
             for (int u = 0; u < K; ++u) {
                 const int q = u * 32 + lane;
-                if (q < nsurv) { a.ti[o + rk[u]] = mk[u]; a.tv[o + rk[u]] = t.lv[q]; }
+                if (q < nsurv) { a.ti[o + rk[u]] = mk[u]; a.tv[o + rk[u]] = t.x[q]; }
             }
         } else {
             for (int q = lane; q < nsurv; q += 32) {
-                const int j = t.lk[q];
+                const int j = t.key[q];
                 int rank = 0;
-                for (int v = 0; v < nsurv; ++v) rank += t.lk[v] < j;
+                for (int v = 0; v < nsurv; ++v) rank += t.key[v] < j;
                 a.ti[o + rank] = j;
-                a.tv[o + rank] = t.lv[q];
+                a.tv[o + rank] = t.x[q];
             }
         }
         if (lane == 0) a.cnt[row] = nsurv;
@@ -404,6 +400,18 @@ __global__ void k_compact(int rows, const int64_t *toff, const int *ptr, const i
     }
 }
 
+template <int CAP, int W, int K, bool HD>
+void launch_num_t(Ctx *c, const Args &a, int nrl) {
+    const size_t smem = (size_t)CAP * slot_bytes(HD) * W;
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_spgemm_num<CAP, W, K, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int grid = std::max(1, std::min<int>((nrl + W - 1) / W, c->sms * 32));
+    k_spgemm_num<CAP, W, K, HD><<<grid, 32 * W, smem, c->s>>>(a);
+    launched(c);
+}
 template <int CAP, int W, int K>
 void launch_num(Ctx *c, Args a, const std::vector<int> &rows_h) {
     if (rows_h.empty()) return;
@@ -411,15 +419,8 @@ void launch_num(Ctx *c, Args a, const std::vector<int> &rows_h) {
     rl.upload(rows_h.data(), rows_h.size());
     a.rl = rl.p;
     a.nrl = (int)rows_h.size();
-    const size_t smem = (size_t)CAP * SLOT_BYTES * W;
-    static bool attr = false;
-    if (!attr && smem > 48 * 1024) {
-        CK(cudaFuncSetAttribute(k_spgemm_num<CAP, W, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    const int grid = std::max(1, std::min<int>((a.nrl + W - 1) / W, c->sms * 16));
-    k_spgemm_num<CAP, W, K><<<grid, 32 * W, smem, c->s>>>(a);
-    launched(c);
+    if (a.dp) launch_num_t<CAP, W, K, true>(c, a, a.nrl);
+    else launch_num_t<CAP, W, K, false>(c, a, a.nrl);
 }
 
 }  // namespace
@@ -555,20 +556,20 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         // 3. numeric, one pass per class
         DPP_TRACE_SCOPE(c, "spgemm.numeric");
         launch_num<256, 8, 4>(c, a, rs_s);
-        launch_num<1024, 2, 16>(c, a, rs_m);
-        launch_num<4096, 1, 0>(c, a, rs_l);
+        launch_num<1024, 4, 16>(c, a, rs_m);
+        launch_num<4096, 2, 0>(c, a, rs_l);
         if (!rs_g.empty()) {
             const int ng = (int)rs_g.size();
             DBuf<int64_t> dgoff(ng, c->s);
             DBuf<int> dgcap(ng, c->s);
             dgoff.upload(goff.data(), ng);
             dgcap.upload(gcap.data(), ng);
-            DBuf<int> gk(gtot, c->s), glk(gtot, c->s);
+            DBuf<int> gk(gtot, c->s);
             DBuf<unsigned char> ghas(gtot, c->s);
-            DBuf<double> gx(gtot, c->s), gd(gtot, c->s), glv(gtot, c->s);
+            DBuf<double> gx(gtot, c->s), gd(gtot, c->s);
             Args g = a;
             g.goff = dgoff.p; g.gcap = dgcap.p;
-            g.g_key = gk.p; g.g_has = ghas.p; g.g_x = gx.p; g.g_d = gd.p; g.g_lk = glk.p; g.g_lv = glv.p;
+            g.g_key = gk.p; g.g_has = ghas.p; g.g_x = gx.p; g.g_d = gd.p;
             launch_num<0, 1, 0>(c, g, rs_g);
             CK(cudaStreamSynchronize(c->s));   // global tables go out of scope
         }

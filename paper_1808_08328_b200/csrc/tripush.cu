@@ -37,7 +37,7 @@ namespace {
 constexpr int PU_THREADS = 1024;
 constexpr int PU_MAX = 16;
 constexpr int PU_NST_MAX = 16;
-constexpr int PU_LMAX = 2048;              // one mbarrier per level in shared memory
+constexpr int PU_LMAX = 4096;              // one mbarrier per level in shared memory (32 KB)
 constexpr size_t PU_SMEM_LIMIT = 226 * 1024;   // dynamic; leaves room for static shared memory
 
 __host__ __device__ __forceinline__ long long p16(long long b) { return (b + 15) & ~15LL; }
