@@ -61,15 +61,20 @@ __device__ __forceinline__ void mwait(unsigned a, unsigned parity) {
     }
 }
 
-// shared memory: ring mbarriers | level mbarriers [L] | xs [chunk] | halo [hmax] | boff [L+1] | ring
+// shared memory: ring mbarriers | level mbarriers [L] | xh = [x slice (chunk, padded) | halo (hmax)] |
+//                boff [L+1] | peer addresses | ring
+__host__ __device__ inline int pu_chunkp(int chunk) { return (int)(p16(8LL * chunk) / 8); }
 __host__ __device__ inline size_t pu_fixed(int chunk, int L, int hmax) {
-    return 8 * PU_NST_MAX + p16(8LL * L) + p16(8LL * chunk) + p16(8LL * hmax) + p16(8LL * (L + 1));
+    return 8 * PU_NST_MAX + p16(8LL * L) + p16(8LL * chunk) + p16(8LL * hmax) + p16(8LL * (L + 1)) + 8 * PU_MAX;
 }
 
 // block layout (16-byte aligned):
-//   int nr, ne, np, 0 | lrow[nr] | rend[nr] | double dg[nr] | code[ne] | double val[ne] | ppt[nr+1] | push[np]
+//   int4 {nr, ne, np, 0} | int4 row[nr] = {local row, e0, e1, p0 << 4 | npush} | double dg[nr] |
+//   int code[ne] (index into xh) | (16) double val[ne] | int push[np] (dest << 28 | halo slot)
+__host__ __device__ inline long long pu_off_code(long long nr) { return 16 + 24 * nr; }
+__host__ __device__ inline long long pu_off_val(long long nr, long long ne) { return p16(pu_off_code(nr) + 4 * ne); }
 __host__ __device__ inline long long pu_block_bytes(long long nr, long long ne, long long np) {
-    return p16(16 + p16(4 * nr) * 2 + 8 * nr + p16(4 * ne) + 8 * ne + p16(4 * (nr + 1)) + p16(4 * np));
+    return p16(pu_off_val(nr, ne) + 8 * ne + 4 * np);
 }
 
 template <int G>
@@ -79,13 +84,13 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout, int l2pf,
                 unsigned long long *dbg) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned long long t_last, t_pre, t_w[32], t_wp[32];
+    __shared__ unsigned long long t_w[32], t_wp[32];
     unsigned long long acc_ring = 0, acc_lev = 0, acc_sync = 0, acc_comp = 0, acc_pre = 0, tA = 0, tB = 0, tC = 0, tD = 0;
     unsigned long long *mring = reinterpret_cast<unsigned long long *>(smem);
     unsigned long long *mlev = mring + PU_NST_MAX;
-    double *xs = reinterpret_cast<double *>(smem + 8 * PU_NST_MAX + p16(8LL * L));
-    double *halo = xs + p16(8LL * chunk) / 8;
-    long long *boff_s = reinterpret_cast<long long *>(halo + p16(8LL * hmax) / 8);
+    double *xh = reinterpret_cast<double *>(smem + 8 * PU_NST_MAX + p16(8LL * L));
+    long long *boff_s = reinterpret_cast<long long *>(xh + pu_chunkp(chunk) + p16(8LL * hmax) / 8);
+    unsigned *peer = reinterpret_cast<unsigned *>(boff_s + p16(8LL * (L + 1)) / 8);   // [0,16): halo, [16,32): mlev
     unsigned char *ring = smem + pu_fixed(chunk, L, hmax);
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
@@ -101,7 +106,11 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mlev[l])), "r"(tx[b0 + l])
                      : "memory");
     }
-    for (int i = threadIdx.x; i < mine; i += blockDim.x) xs[i] = b[base + i];
+    if (threadIdx.x < C) {   // every peer's halo / level-mbarrier base in the cluster window
+        peer[threadIdx.x] = mapa_u32(su32(xh + pu_chunkp(chunk)), threadIdx.x);
+        peer[16 + threadIdx.x] = mapa_u32(su32(mlev), threadIdx.x);
+    }
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[base + i];
     for (int i = threadIdx.x; i <= L; i += blockDim.x) boff_s[i] = boff[b0 + i];
     if (dbg && threadIdx.x < 32) { t_w[threadIdx.x] = 0; t_wp[threadIdx.x] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -125,7 +134,6 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     }
     // every CTA's level mbarriers are armed before the first push
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    const unsigned halo_a = su32(halo), mlev_a = su32(mlev);
     int slot = 0, islot = nst - 1;
     unsigned phase = 0;
     for (int l = 0; l < L; ++l) {
@@ -156,37 +164,31 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         const unsigned char *blk = ring + (size_t)slot * stage;
         if (++slot == nst) { slot = 0; phase ^= 1u; }
         if (++islot == nst) islot = 0;
-        const int *hd = reinterpret_cast<const int *>(blk);
-        const int nr = hd[0], ne = hd[1];
-        const int *lrow = hd + 4;
-        const int *rend = reinterpret_cast<const int *>(blk + 16 + p16(4LL * nr));
-        const double *dg = reinterpret_cast<const double *>(blk + 16 + 2 * p16(4LL * nr));
-        const int *code = reinterpret_cast<const int *>(blk + 16 + 2 * p16(4LL * nr) + 8LL * nr);
-        const double *val = reinterpret_cast<const double *>(blk + 16 + 2 * p16(4LL * nr) + 8LL * nr + p16(4LL * ne));
-        const int *ppt = reinterpret_cast<const int *>(reinterpret_cast<const unsigned char *>(val) + 8LL * ne);
-        const int *pl = reinterpret_cast<const int *>(reinterpret_cast<const unsigned char *>(ppt) + p16(4LL * (nr + 1)));
-        const unsigned mlev_l = mlev_a + 8u * l;
+        const int4 hd = *reinterpret_cast<const int4 *>(blk);
+        const int nr = hd.x, ne = hd.y;
+        const int4 *rows = reinterpret_cast<const int4 *>(blk + 16);
+        const double *dg = reinterpret_cast<const double *>(blk + 16 + 16LL * nr);
+        const int *code = reinterpret_cast<const int *>(blk + pu_off_code(nr));
+        const double *val = reinterpret_cast<const double *>(blk + pu_off_val(nr, ne));
+        const int *pl = reinterpret_cast<const int *>(val + ne);
         for (int q = grp; q < nr; q += ngrp) {
-            const int r = lrow[q];
-            const int e0 = q ? rend[q - 1] : 0, e1 = rend[q];
+            const int4 R = rows[q];
+            const double dq = dg[q];
             double sum = 0.0;
-            for (int e = e0 + gl; e < e1; e += G) {
-                const int cd = code[e];
-                sum += val[e] * (cd >= 0 ? xs[cd] : halo[cd & 0x7fffffff]);
-            }
+            for (int e = R.y + gl; e < R.z; e += G) sum += val[e] * xh[code[e]];
 #pragma unroll
             for (int s = G / 2; s > 0; s >>= 1) sum += __shfl_xor_sync(gmask, sum, s, G);
-            const double xr = (xs[r] - sum) * dg[q];   // dg = 1/t_ii (as SuperLU's pre-scaled solve)
+            const double xr = (xh[R.x] - sum) * dq;   // dq = 1/t_ii (as SuperLU's pre-scaled solve)
             __syncwarp(gmask);
-            if (gl == 0) xs[r] = xr;
+            if (gl == 0) xh[R.x] = xr;
             if (dbg && lane == 0) t_wp[threadIdx.x >> 5] = clock64();
-            for (int u = ppt[q] + gl; u < ppt[q + 1]; u += G) {
-                const int pe = pl[u];
+            const int p0 = R.w >> 4, pc = R.w & 15;
+            for (int u = gl; u < pc; u += G) {
+                const int pe = pl[p0 + u];
                 const int dst = (int)((unsigned)pe >> 28);
                 const unsigned sl = (unsigned)pe & 0x0fffffffu;
                 asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
-                             ::"r"(mapa_u32(halo_a + 8u * sl, dst)), "l"(__double_as_longlong(xr)),
-                             "r"(mapa_u32(mlev_l, dst))
+                             ::"r"(peer[dst] + 8u * sl), "l"(__double_as_longlong(xr)), "r"(peer[16 + dst] + 8u * l)
                              : "memory");
             }
         }
@@ -194,13 +196,11 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     }
     __syncthreads();
     if (dbg && threadIdx.x == 0) {
-        const int k0 = (int)cl.block_rank();
-        dbg[k0 * 4 + 0] = acc_ring; dbg[k0 * 4 + 1] = acc_pre; dbg[k0 * 4 + 2] = acc_sync; dbg[k0 * 4 + 3] = acc_comp;
+        dbg[k * 4 + 0] = acc_ring; dbg[k * 4 + 1] = acc_pre; dbg[k * 4 + 2] = acc_sync; dbg[k * 4 + 3] = acc_comp;
     }
-    (void)C;
     for (int i = threadIdx.x; i < mine; i += blockDim.x) {
-        x[base + i] = xs[i];
-        if (xout) xout[base + i] = xadd[base + i] + xs[i];
+        x[base + i] = xh[i];
+        if (xout) xout[base + i] = xadd[base + i] + xh[i];
     }
 }
 
@@ -283,20 +283,16 @@ __global__ void k_pu_headers(int nblk, const int *lp, const int *rptr, const int
                              const long long *boff) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nblk; i += gridDim.x * blockDim.x) {
         int *h = reinterpret_cast<int *>(blocks + boff[i]);
-        const int nr = lp[i + 1] - lp[i];
-        h[0] = nr;
+        h[0] = lp[i + 1] - lp[i];
         h[1] = rptr[lp[i + 1]] - rptr[lp[i]];
         h[2] = rpp[lp[i + 1]] - rpp[lp[i]];
         h[3] = 0;
-        if (nr == 0) {   // empty block: ppt[0] = 0
-            *reinterpret_cast<int *>(blocks + boff[i] + 16) = 0;
-        }
     }
 }
-__global__ void k_pu_fill(int n, int chunk, const int *skey, const int *perm, const int *lp, const int *rptr,
-                          const int *rpp, const long long *boff, const int *ptr, const int *idx, const double *val,
-                          const double *diag, const unsigned long long *h, const int *hstart, const int *pptr,
-                          const unsigned long long *k2s, const int *slots, unsigned char *blocks) {
+__global__ void k_pu_fill(int n, int chunk, int chunkp, const int *skey, const int *perm, const int *lp,
+                          const int *rptr, const int *rpp, const long long *boff, const int *ptr, const int *idx,
+                          const double *val, const double *diag, const unsigned long long *h, const int *hstart,
+                          const int *pptr, const unsigned long long *k2s, const int *slots, unsigned char *blocks) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int blk = skey[q];
         const int q0 = lp[blk], nr = lp[blk + 1] - q0, i = q - q0;
@@ -304,17 +300,16 @@ __global__ void k_pu_fill(int n, int chunk, const int *skey, const int *perm, co
         unsigned char *B = blocks + boff[blk];
         const int r = perm[q];
         const int owner = r / chunk;
-        int *lrow = reinterpret_cast<int *>(B + 16);
-        int *rend = reinterpret_cast<int *>(B + 16 + p16(4LL * nr));
-        double *dg = reinterpret_cast<double *>(B + 16 + 2 * p16(4LL * nr));
-        int *code = reinterpret_cast<int *>(B + 16 + 2 * p16(4LL * nr) + 8LL * nr);
-        double *vv = reinterpret_cast<double *>(B + 16 + 2 * p16(4LL * nr) + 8LL * nr + p16(4LL * ne));
-        int *ppt = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(vv) + 8LL * ne);
-        int *pl = reinterpret_cast<int *>(reinterpret_cast<unsigned char *>(ppt) + p16(4LL * (nr + 1)));
-        lrow[i] = r - owner * chunk;
-        rend[i] = rptr[q + 1] - rptr[q0];
+        int4 *rows = reinterpret_cast<int4 *>(B + 16);
+        double *dg = reinterpret_cast<double *>(B + 16 + 16LL * nr);
+        int *code = reinterpret_cast<int *>(B + pu_off_code(nr));
+        double *vv = reinterpret_cast<double *>(B + pu_off_val(nr, ne));
+        int *pl = reinterpret_cast<int *>(vv + ne);
+        const int e0 = rptr[q] - rptr[q0], e1 = rptr[q + 1] - rptr[q0];
+        const int p0 = rpp[q] - rpp[q0], pc = rpp[q + 1] - rpp[q];
+        rows[i] = make_int4(r - owner * chunk, e0, e1, (p0 << 4) | pc);
         dg[i] = diag ? 1.0 / diag[r] : 1.0;
-        int w = rptr[q] - rptr[q0];
+        int w = e0;
         const int hs = hstart[owner], he = hstart[owner + 1];
         for (int p = ptr[r]; p < ptr[r + 1]; ++p, ++w) {
             const int j = idx[p];
@@ -328,13 +323,11 @@ __global__ void k_pu_fill(int n, int chunk, const int *skey, const int *perm, co
                     const int mid = (lo + hi) >> 1;
                     if (h[mid] < key) lo = mid + 1; else hi = mid;
                 }
-                code[w] = (int)(0x80000000u | (unsigned)(lo - hs));
+                code[w] = chunkp + (lo - hs);
             }
             vv[w] = val[p];
         }
-        if (i == 0) ppt[0] = 0;
-        ppt[i + 1] = rpp[q + 1] - rpp[q0];
-        int u = rpp[q] - rpp[q0];
+        int u = p0;
         for (int t = pptr[r]; t < pptr[r + 1]; ++t, ++u)
             pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28) | (unsigned)slots[t]);
     }
@@ -459,14 +452,18 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     const double avg = (double)S.nnz / n;
     P->G = 2;
     while (P->G < 32 && P->G * 4 < avg) P->G *= 2;
+    static const int force_g = [] { const char *e = std::getenv("DPP_PU_G"); return e ? std::atoi(e) : 0; }();
+    if (force_g && P->G < force_g) P->G = force_g;   // experiment: wider lane groups for thin rows
     int threads = 64;
     while (threads < PU_THREADS && (threads / P->G) < widest) threads *= 2;
+    static const int force_thr = [] { const char *e = std::getenv("DPP_PU_THREADS"); return e ? std::atoi(e) : 0; }();
+    if (force_thr) threads = std::min(threads, force_thr);
     P->threads = threads;
     P->blocks.alloc((size_t)total, c->s);
     P->boff = std::move(boff);
     k_pu_headers<<<grid_for(nblk, 256, c->sms), 256, 0, c->s>>>(nblk, lp.p, rptr.p, rpp.p, P->blocks.p, P->boff.p);
     launched(c);
-    k_pu_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, skey.p, perm.p, lp.p, rptr.p, rpp.p, P->boff.p,
+    k_pu_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, pu_chunkp(chunk), skey.p, perm.p, lp.p, rptr.p, rpp.p, P->boff.p,
                                                           S.ptr.p, S.idx.p, S.val.p, T.diag.n ? T.diag.p : nullptr,
                                                           H.p, hstart.p, pptr.p, k2s.p, slots.p, P->blocks.p);
     launched(c);

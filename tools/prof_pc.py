@@ -1,4 +1,6 @@
-"""Build the C2 system + scale-split PC and run a few PC applies (profiling target)."""
+"""Build a system + PC and run a few PC applies (profiling target).
+
+PROF_CFG = C2 (default, CG-VMS TET 40 scale) | C3 (CG-VMS HEX 64 field) | C4 (DG-VMS TET 32 scale)."""
 import ctypes as C
 import os
 import sys
@@ -7,11 +9,16 @@ import numpy as np
 import paper_1808_08328_b200 as dpp
 from paper_1808_08328_b200 import _native as N
 
-n = int(os.environ.get("PROF_N", "40"))
-meth = os.environ.get("PROF_METHOD", "scale")
-p = dpp.DppParameters(k2=0.01, gamma_b=(0.0, 0.0, 0.0))
-m = dpp.generate_unit_mesh(3, "tet", n)
-bs = dpp.assemble(m, "cgvms", p, dpp.boundary_data(dpp.mms_3d(p), m))
+cfg = os.environ.get("PROF_CFG", "C2")
+form, kind, n, meth, p = {
+    "C2": ("cgvms", "tet", 40, "scale", dpp.DppParameters(k2=0.01, gamma_b=(0.0, 0.0, 0.0))),
+    "C3": ("cgvms", "hex", 64, "field", dpp.DppParameters(k2=0.01, gamma_b=(0.0, 0.0, 0.0))),
+    "C4": ("dgvms", "tet", 32, "scale", dpp.paper_3d_parameters()),
+}[cfg]
+n = int(os.environ.get("PROF_N", n))
+meth = os.environ.get("PROF_METHOD", meth)
+m = dpp.generate_unit_mesh(3, kind, n)
+bs = dpp.assemble(m, form, p, dpp.boundary_data(dpp.mms_3d(p), m))
 pc = dpp.build_preconditioner(bs, dpp.method_config(meth))
 prof = N.StepProfile()
 N.call("dpp_profile_step", N.ctx(), bs.device().h, pc.handle(), int(os.environ.get("PROF_REPS", "3")), 0, C.byref(prof))
