@@ -118,6 +118,12 @@ int dpp_system_from_blocks(dpp_ctx *ctx, const dpp_csr *const blocks[10],
                            const double *const rhs_host[4], const int64_t sizes[4],
                            dpp_system **out);
 int dpp_system_sizes(const dpp_system *s, int64_t sizes[4]);
+/* assembly._eliminate (assembly.py:200-226): symmetric strong elimination of dofs idx
+ * (sorted, host) of field 0..3 = (u1, p1, u2, p2) with the given values; used for
+ * CG-VMS pressure_dirichlet='strong' (assembly.py:410-415).  H(div) prescribed-flux
+ * facets are eliminated inside dpp_assemble from dpp_bc.vfacets / vdata. */
+int dpp_system_eliminate(dpp_system *s, int field, int64_t n, const int64_t *idx_host,
+                         const double *values_host);
 /* borrowed handle, valid while the system lives */
 int dpp_system_block(dpp_system *s, int block, dpp_csr **out);
 int dpp_system_rhs(const dpp_system *s, int field, double *out_host);

@@ -83,6 +83,7 @@ SIGNATURES = {
     "dpp_facet_rule_size": [I32, I32, I32, C.POINTER(I32)],
     "dpp_facet_points": [P, P, I32, I64, P, P, P],
     "dpp_assemble": [P, P, I32, C.POINTER(Params), C.POINTER(Bc), PP],
+    "dpp_system_eliminate": [P, I32, I64, P, P],
     "dpp_system_from_blocks": [P, C.POINTER(P), C.POINTER(P), C.POINTER(I64), PP],
     "dpp_system_sizes": [P, C.POINTER(I64)],
     "dpp_system_block": [P, I32, PP],

@@ -149,6 +149,39 @@ def _pressure_data(mesh: Mesh, bcs: BoundarySpec, net: int):
     return pf, p0
 
 
+def _facet_points(mesh: Mesh, facets: np.ndarray, degree: int):
+    """(X, W) of the facet rule on `facets` (reference assembly.py:173-181), from the device."""
+    fids = N.i64(facets)
+    nq = C.c_int()
+    N.call("dpp_facet_rule_size", mesh.dim, N.KINDS[mesh.cell_kind.value], degree, C.byref(nq))
+    X = np.empty((len(fids), nq.value, mesh.dim))
+    W = np.empty((len(fids), nq.value))
+    if len(fids):
+        N.call("dpp_facet_points", N.ctx(), mesh._h, degree, len(fids), N.ptr(fids), N.ptr(X), N.ptr(W))
+    return X, W
+
+
+def _velocity_flux_data(mesh: Mesh, bcs: BoundarySpec, net: int):
+    """Prescribed flux integrals g_f = sum_q W_fq (u.n)(X_fq) on the velocity facets of one
+    network (reference assembly.py:301-309, one callable evaluation per facet)."""
+    vel = np.array(sorted(bcs.velocity_facets[net - 1]), dtype=np.int64)
+    X, W = _facet_points(mesh, vel, DATA_QUAD_DEGREE)
+    g = np.empty(len(vel))
+    for i, f in enumerate(vel):
+        un = bcs.un_data[net - 1](X[i], mesh.facet_normals[f])
+        g[i] = W[i] @ un
+    return vel, g
+
+
+def _pressure_dirichlet_vertices(mesh: Mesh, bcs: BoundarySpec, net: int) -> np.ndarray:
+    """Vertices of the pressure facets (reference assembly.py:192-197), sorted."""
+    bf = mesh.boundary_facets
+    vel = bcs.velocity_facets[net - 1]
+    if vel:
+        bf = bf[~np.isin(bf, np.fromiter(vel, dtype=np.int64))]
+    return np.unique(mesh.facet_vertex_ids[bf].ravel()).astype(np.int64)
+
+
 def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec | None,
              workers: int = 1, pressure_dirichlet: str = "weak") -> BlockSystem:
     """Device assembly (reference assembly.py:564-566).  `workers` is accepted
@@ -160,15 +193,15 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
         raise ValueError("gamma_b dimension does not match the mesh")
     if pressure_dirichlet not in ("weak", "strong"):
         raise ValueError("pressure_dirichlet must be 'weak' or 'strong'")
-    if pressure_dirichlet == "strong":
-        raise NotImplementedError("strong pressure elimination is not implemented on the device yet")
+    if pressure_dirichlet == "strong" and form != Formulation.CG_VMS:
+        raise ValueError("pressure_dirichlet='strong' is a CG-VMS option (reference assemble_cgvms)")
     p = N.Params(params.mu, params.beta, params.k1, params.k2, params.eta_u, params.eta_p,
                  (C.c_double * 3)(*(list(gb) + [0.0] * (3 - len(gb)))))
     keep = []
     bcp = None
     if bcs is not None:
-        if any(len(v) for v in bcs.velocity_facets):
-            raise NotImplementedError("prescribed-velocity boundary facets are not implemented on the device yet")
+        if form == Formulation.DG_VMS and any(len(v) for v in bcs.velocity_facets):
+            raise NotImplementedError("prescribed-velocity facets of the DG-VMS form are not implemented on the device yet")
         bc = N.Bc()
         for net in (1, 2):
             pf, p0 = _pressure_data(mesh, bcs, net)
@@ -176,10 +209,22 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
             bc.n_pfacets[net - 1] = len(pf)
             bc.pfacets[net - 1] = pf.ctypes.data
             bc.p0[net - 1] = p0.ctypes.data
+            if form == Formulation.HDIV and bcs.velocity_facets[net - 1]:
+                vel, gflux = _velocity_flux_data(mesh, bcs, net)
+                keep += [vel, gflux]
+                bc.n_vfacets[net - 1] = len(vel)
+                bc.vfacets[net - 1] = vel.ctypes.data
+                bc.vdata[net - 1] = gflux.ctypes.data
         bcp = C.byref(bc)
     h = C.c_void_p()
     N.call("dpp_assemble", N.ctx(), mesh._h, N.FORMS[form.value], C.byref(p), bcp, C.byref(h))
     dev = DeviceSystem(h)
+    if bcs is not None and pressure_dirichlet == "strong":
+        # strong boundary pressure: eliminate p1 then p2 (reference assembly.py:410-415)
+        for net in (1, 2):
+            verts = _pressure_dirichlet_vertices(mesh, bcs, net)
+            vals = N.f64(np.asarray(bcs.p_data[net - 1](mesh.vertices[verts]), dtype=float))
+            N.call("dpp_system_eliminate", h, 1 if net == 1 else 3, len(verts), N.ptr(verts), N.ptr(vals))
     bs = BlockSystem(formulation=form, mesh=mesh, params=params)
     object.__setattr__(bs, "_dev", dev)
     wall = time.perf_counter() - t0

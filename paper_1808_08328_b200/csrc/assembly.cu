@@ -797,6 +797,119 @@ static void add_at(Ctx *c, int64_t n, DBuf<int64_t> &dof, DBuf<double> &val, dou
     CK(cudaStreamSynchronize(c->s));
 }
 
+// ------------------------------------------------------------------ body force (gamma_b)
+// VMS (assembly.py:352-356): fu[c,a,i] = 0.5 det intN_a g_i ; fp[c,a] = 0.5 k/mu det sum_q w_q (Gp_qa . g)
+__global__ void k_body_vms(int64_t C, Elem E, const double *det, const double *Jinv, const int *cells, int dg,
+                           double g0, double g1, double g2, double kmu, int64_t *du, double *vu, int64_t *dp,
+                           double *vp) {
+    const int dim = E.dim, nn = E.nn;
+    const double gb[3] = {g0, g1, g2};
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+        const double d = det[c];
+        const double *Ji = Jinv + c * dim * dim;
+        for (int a = 0; a < nn; ++a) {
+            const int64_t node = dg ? c * nn + a : cells[c * nn + a];
+            double intN = 0.0;
+            for (int q = 0; q < E.nq; ++q) intN += E.w[q] * E.N[q][a];
+            for (int i = 0; i < dim; ++i) {
+                const int64_t k = (c * nn + a) * dim + i;
+                du[k] = node * dim + i;
+                vu[k] = 0.5 * d * intN * gb[i];
+            }
+            double s = 0.0;
+            for (int q = 0; q < E.nq; ++q) {
+                double ga[3];
+                grad_phys(E, Ji, q, a, ga);
+                double t = 0.0;
+                for (int i = 0; i < dim; ++i) t += ga[i] * gb[i];
+                s += E.w[q] * t;
+            }
+            dp[c * nn + a] = node;
+            vp[c * nn + a] = kmu * d * s;
+        }
+    }
+}
+// H(div) (assembly.py:274-276): fu[c,f] = (sum_q w_q Vphys_qf . g) det s_cf
+struct HdivBody {
+    int dim, nf, nq, nn, kind;
+    double w[8];
+    double Vref[8][6][3];
+};
+__global__ void k_body_hdiv(int64_t C, HdivBody B, const double *V, const double *det, const int *cells,
+                            const int *cf, const signed char *cs, double g0, double g1, double g2, int64_t *du,
+                            double *vu) {
+    const int dim = B.dim;
+    const double gb[3] = {g0, g1, g2};
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
+        double J[9];
+        const int *cv = cells + c * B.nn;
+        if (B.kind == DPP_TRI || B.kind == DPP_TET) {
+            for (int k = 0; k < dim; ++k)
+                for (int d = 0; d < dim; ++d) J[d * dim + k] = V[(int64_t)cv[k + 1] * dim + d] - V[(int64_t)cv[0] * dim + d];
+        } else {
+            for (int k = 0; k < dim * dim; ++k) J[k] = 0.0;
+            for (int d = 0; d < dim; ++d) J[d * dim + d] = V[(int64_t)cv[B.nn - 1] * dim + d] - V[(int64_t)cv[0] * dim + d];
+        }
+        const double dt = det[c];
+        for (int f = 0; f < B.nf; ++f) {
+            double s = 0.0;
+            for (int q = 0; q < B.nq; ++q) {
+                double t = 0.0;
+                for (int i = 0; i < dim; ++i) {
+                    double v = 0.0;
+                    for (int j = 0; j < dim; ++j) v += J[i * dim + j] * B.Vref[q][f][j];
+                    t += (v / dt) * gb[i];
+                }
+                s += B.w[q] * t;
+            }
+            du[c * B.nf + f] = cf[c * B.nf + f];
+            vu[c * B.nf + f] = s * dt * cs[c * B.nf + f];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ strong elimination
+// assembly._eliminate (assembly.py:200-226) on one block: B @ D_keep (columns of the
+// pinned dofs and every exact zero dropped, as scipy's csr_matmat does), D_keep @ B
+// (pinned rows dropped), and for the (field, field) block + D_pin (unit diagonal).
+__global__ void k_elim_count(int rows, const int *ptr, const int *idx, const double *val, const unsigned char *pin,
+                             int rowpin, int colpin, int diag, int *cnt) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        if (rowpin && pin[r]) { cnt[r] = diag ? 1 : 0; continue; }
+        int k = 0;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) k += val[p] != 0.0 && !(colpin && pin[idx[p]]);
+        cnt[r] = k;
+    }
+}
+__global__ void k_elim_fill(int rows, const int *ptr, const int *idx, const double *val, const unsigned char *pin,
+                            int rowpin, int colpin, int diag, const int *optr, int *oidx, double *oval) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        int w = optr[r];
+        if (rowpin && pin[r]) {
+            if (diag) { oidx[w] = r; oval[w] = 1.0; }
+            continue;
+        }
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p)
+            if (val[p] != 0.0 && !(colpin && pin[idx[p]])) { oidx[w] = idx[p]; oval[w] = val[p]; ++w; }
+    }
+}
+// rhs[r] -= B @ lift with scipy's csr_matvec order (sequential per row, no FMA), then
+// numpy's elementwise subtraction: bitwise what the reference computes
+__global__ void k_sub_matvec_seq(int rows, const int *ptr, const int *idx, const double *val, const double *x,
+                                 double *rhs) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) s = __dadd_rn(s, __dmul_rn(val[p], x[idx[p]]));
+        rhs[r] = __dsub_rn(rhs[r], s);
+    }
+}
+__global__ void k_scatter_vals(int64_t n, const int64_t *idx, const double *v, double *dst, unsigned char *pin) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (dst) dst[idx[i]] = v[i];
+        if (pin) pin[idx[i]] = 1;
+    }
+}
+
 // ------------------------------------------------------------------ drivers
 static void alloc_blk(Ctx *c, Csr &B, int rows, int cols, int64_t nnz) { B.alloc(rows, cols, nnz, c->s); }
 
@@ -907,6 +1020,20 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
         launched(c);
     }
     c21 = csr_copy(c, c12);
+    if (p.gamma_b[0] != 0.0 || p.gamma_b[1] != 0.0 || (dim == 3 && p.gamma_b[2] != 0.0)) {
+        // body force, np.add.at in cell order (assembly.py:395-399)
+        const int64_t nu_c = C * nn * dim, np_c = C * nn;
+        for (int n = 0; n < 2; ++n) {
+            DBuf<int64_t> du(nu_c, c->s), dpi(np_c, c->s);
+            DBuf<double> vu(nu_c, c->s), vp(np_c, c->s);
+            k_body_vms<<<grid_for(C, 128, c->sms), 128, 0, c->s>>>(C, E, m.det.p, m.Jinv.p, m.cells.p, dg,
+                                                                 p.gamma_b[0], p.gamma_b[1], p.gamma_b[2],
+                                                                 0.5 * ks[n] / p.mu, du.p, vu.p, dpi.p, vp.p);
+            launched(c);
+            add_at(c, nu_c, du, vu, S.rhs[n == 0 ? 0 : 2].p);
+            add_at(c, np_c, dpi, vp, S.rhs[n == 0 ? 1 : 3].p);
+        }
+    }
     CK(cudaStreamSynchronize(c->s));
 }
 
@@ -1001,8 +1128,73 @@ static void assemble_hdiv(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p,
     S.blk[DPP_K2_PU] = csr_copy(c, pu1);
     S.blk[DPP_K2_PP] = csr_copy(c, pp1);
     S.blk[DPP_K21_PP] = csr_copy(c, c12);
+    if (p.gamma_b[0] != 0.0 || p.gamma_b[1] != 0.0 || (dim == 3 && p.gamma_b[2] != 0.0)) {
+        // body force, np.add.at in cell order (assembly.py:274-277); same for both networks
+        HdivBody B{};
+        B.dim = dim; B.nf = nf; B.nq = A.nq; B.nn = m.nn; B.kind = m.kind;
+        for (int q = 0; q < A.nq; ++q) {
+            B.w[q] = A.w[q];
+            for (int f = 0; f < nf; ++f)
+                for (int j = 0; j < dim; ++j) B.Vref[q][f][j] = A.Vref[q][f][j];
+        }
+        for (int n = 0; n < 2; ++n) {
+            DBuf<int64_t> du(C * nf, c->s);
+            DBuf<double> vu(C * nf, c->s);
+            k_body_hdiv<<<grid_for(C, 128, c->sms), 128, 0, c->s>>>(C, B, m.verts.p, m.det.p, m.cells.p, m.cf.p,
+                                                                  m.cs.p, p.gamma_b[0], p.gamma_b[1], p.gamma_b[2],
+                                                                  du.p, vu.p);
+            launched(c);
+            add_at(c, C * nf, du, vu, S.rhs[n == 0 ? 0 : 2].p);
+        }
+    }
     CK(cudaStreamSynchronize(c->s));
     (void)hm;
+}
+
+// field: 0 u1, 1 p1, 2 u2, 3 p2; idx/values host arrays (sorted dofs, as the reference's)
+static const int BLK_RC[10][2] = {{0, 0}, {0, 1}, {1, 0}, {1, 1}, {2, 2}, {2, 3}, {3, 2}, {3, 3}, {1, 3}, {3, 1}};
+void eliminate(Ctx *c, dpp_system &S, int field, int64_t n, const int64_t *idx_h, const double *vals_h) {
+    if (n <= 0) return;
+    const int64_t nf = S.sizes[field];
+    DBuf<int64_t> idx(n, c->s);
+    DBuf<double> vals(n, c->s), lift(nf, c->s);
+    DBuf<unsigned char> pin(nf, c->s);
+    idx.upload(idx_h, n);
+    vals.upload(vals_h, n);
+    CK(cudaMemsetAsync(lift.p, 0, sizeof(double) * nf, c->s));
+    CK(cudaMemsetAsync(pin.p, 0, nf, c->s));
+    k_scatter_vals<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, idx.p, vals.p, lift.p, pin.p);
+    launched(c);
+    for (int b = 0; b < 10; ++b) {
+        const int r = BLK_RC[b][0], cc = BLK_RC[b][1];
+        if (r != field && cc != field) continue;
+        Csr &B = S.blk[b];
+        if (cc == field && B.rows) {   // rhs[r] -= B @ lift
+            k_sub_matvec_seq<<<grid_for(B.rows, 256, c->sms), 256, 0, c->s>>>(B.rows, B.ptr.p, B.idx.p, B.val.p,
+                                                                           lift.p, S.rhs[r].p);
+            launched(c);
+        }
+        Csr O;
+        O.rows = B.rows;
+        O.cols = B.cols;
+        DBuf<int> cnt(std::max(B.rows, 1), c->s);
+        const int diag = r == field && cc == field;
+        k_elim_count<<<grid_for(B.rows, 256, c->sms), 256, 0, c->s>>>(B.rows, B.ptr.p, B.idx.p, B.val.p, pin.p,
+                                                                    r == field, cc == field, diag, cnt.p);
+        launched(c);
+        O.nnz = counts_to_ptr(c, cnt.p, B.rows, O.ptr);
+        O.idx.alloc(std::max<int64_t>(O.nnz, 1), c->s);
+        O.val.alloc(std::max<int64_t>(O.nnz, 1), c->s);
+        k_elim_fill<<<grid_for(B.rows, 256, c->sms), 256, 0, c->s>>>(B.rows, B.ptr.p, B.idx.p, B.val.p, pin.p,
+                                                                   r == field, cc == field, diag, O.ptr.p, O.idx.p,
+                                                                   O.val.p);
+        launched(c);
+        B = std::move(O);
+    }
+    k_scatter_vals<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, idx.p, vals.p, S.rhs[field].p, nullptr);
+    launched(c);
+    S.hasK = false;   // the monolithic view is rebuilt from the new blocks
+    CK(cudaStreamSynchronize(c->s));
 }
 
 static void boundary_rhs(Ctx *c, DevMesh &m, int formulation, const dpp_bc *bc, dpp_system &S) {
@@ -1145,6 +1337,15 @@ int dpp_facet_points(dpp_ctx *ctx, dpp_mesh *mm, int degree, int64_t nf, const i
     });
 }
 
+int dpp_system_eliminate(dpp_system *s, int field, int64_t n, const int64_t *idx, const double *values) {
+    return guard([&] {
+        if (field < 0 || field > 3) DPP_FAIL(DPP_ERR_VALUE, "field must be 0..3 (u1, p1, u2, p2)");
+        for (int64_t i = 0; i < n; ++i)
+            if (idx[i] < 0 || idx[i] >= s->sizes[field]) DPP_FAIL(DPP_ERR_VALUE, "eliminated dof out of range");
+        eliminate(s->ctx, *s, field, n, idx, values);
+    });
+}
+
 int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *p, const dpp_bc *bc,
                  dpp_system **out) {
     return guard([&] {
@@ -1152,13 +1353,10 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
         Ctx *c = &ctx->c;
         HostMesh &hm = mm->m;
         if (p->mu <= 0 || p->k1 <= 0 || p->k2 <= 0) DPP_FAIL(DPP_ERR_VALUE, "mu, k1, k2 must be positive");
-        for (int d = 0; d < hm.dim; ++d)
-            if (p->gamma_b[d] != 0.0)
-                DPP_FAIL(DPP_ERR_VALUE, "nonzero body force gamma_b is not supported by the device assembler yet");
-        if (bc)
+        if (bc && formulation == DPP_DGVMS)
             for (int n = 0; n < 2; ++n)
                 if (bc->n_vfacets[n] > 0)
-                    DPP_FAIL(DPP_ERR_VALUE, "prescribed-velocity boundary facets are not supported by the device assembler yet");
+                    DPP_FAIL(DPP_ERR_VALUE, "prescribed-velocity facets of the DG-VMS form are not supported by the device assembler yet");
         DPP_TRACE_SCOPE(c, "assemble.total");
         DevMesh *mp;
         {
@@ -1192,6 +1390,12 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
         {
             DPP_TRACE_SCOPE(c, "assemble.rhs");
             boundary_rhs(c, m, formulation, bc, *S);
+            // H(div) prescribed flux: strong elimination of the facet dofs (assembly.py:301-309);
+            // CG-VMS velocity facets only drop the pressure functional (the caller's pfacets)
+            if (bc && formulation == DPP_HDIV)
+                for (int n = 0; n < 2; ++n)
+                    if (bc->n_vfacets[n] > 0)
+                        eliminate(c, *S, n == 0 ? 0 : 2, bc->n_vfacets[n], bc->vfacets[n], bc->vdata[n]);
         }
         CK(cudaStreamSynchronize(c->s));
         S->assembly_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
