@@ -94,8 +94,10 @@ typedef struct {
 
 /* boundary data, per network (index 0 = network 1).  p0 / un are the user's
  * boundary functions evaluated at the points returned by dpp_facet_points
- * (degree 4 facet rule, assembly.py:173-181, DATA_QUAD_DEGREE).  hdiv:
- * vdata = one prescribed flux integral per velocity facet (assembly.py:303-309). */
+ * (degree 4 facet rule, assembly.py:173-181, DATA_QUAD_DEGREE).  vfacets sorted; hdiv:
+ * vdata = one prescribed flux integral per velocity facet (assembly.py:303-309);
+ * dgvms: vdata = u.n at the degree-4 facet points, (n_vfacets, nq) (assembly.py:532-535);
+ * cgvms: velocity facets only leave the pressure functional (pfacets exclude them). */
 typedef struct {
     int64_t n_pfacets[2];
     const int64_t *pfacets[2];

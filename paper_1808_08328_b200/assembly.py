@@ -200,8 +200,6 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
     keep = []
     bcp = None
     if bcs is not None:
-        if form == Formulation.DG_VMS and any(len(v) for v in bcs.velocity_facets):
-            raise NotImplementedError("prescribed-velocity facets of the DG-VMS form are not implemented on the device yet")
         bc = N.Bc()
         for net in (1, 2):
             pf, p0 = _pressure_data(mesh, bcs, net)
@@ -215,6 +213,16 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
                 bc.n_vfacets[net - 1] = len(vel)
                 bc.vfacets[net - 1] = vel.ctypes.data
                 bc.vdata[net - 1] = gflux.ctypes.data
+            elif form == Formulation.DG_VMS and bcs.velocity_facets[net - 1]:
+                # (u.n) at the degree-4 points, one callable evaluation per facet (assembly.py:532-534)
+                vel = np.array(sorted(bcs.velocity_facets[net - 1]), dtype=np.int64)
+                X, _ = _facet_points(mesh, vel, DATA_QUAD_DEGREE)
+                un = N.f64(np.stack([np.asarray(bcs.un_data[net - 1](X[i], mesh.facet_normals[f]), dtype=float)
+                                     for i, f in enumerate(vel)]) if len(vel) else np.empty((0, 1)))
+                keep += [vel, un]
+                bc.n_vfacets[net - 1] = len(vel)
+                bc.vfacets[net - 1] = vel.ctypes.data
+                bc.vdata[net - 1] = un.ctypes.data
         bcp = C.byref(bc)
     h = C.c_void_p()
     N.call("dpp_assemble", N.ctx(), mesh._h, N.FORMS[form.value], C.byref(p), bcp, C.byref(h))

@@ -464,6 +464,10 @@ struct VmsArgs {
     const int *interior;
     const double *fW, *fNp, *fNm, *fn;  // (Fi,nq), (Fi,nq,nn) x2, normals of all facets
     int fnq;
+    // DG prescribed-flux facets: network 1's nv1 facets then network 2's
+    int64_t nvt, nv1;
+    const int *vfac;
+    const double *vW, *vN;              // (nvt,nq), (nvt,nq,nn)
     // outputs (CSR idx/val) ; ptr arrays computed separately
     int *uu_i[2], *up_i[2], *pu_i[2], *pp_i[2], *cr_i;
     double *uu_v[2], *up_v[2], *pu_v[2], *pp_v[2], *cr_v;
@@ -482,7 +486,7 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
     const Elem &E = A.E;
     const int dim = E.dim, nn = E.nn;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < A.nnz; e += (int64_t)gridDim.x * blockDim.x) {
-        double uu[2][3][3] = {}, up[3] = {}, pu[3] = {}, pp[2] = {}, cr = 0.0;
+        double uu[2][3][3] = {}, up[2][3] = {}, pu[2][3] = {}, pp[2] = {}, cr = 0.0;
         for (int64_t t = A.seg[e]; t < A.seg[e + 1]; ++t) {
             const int64_t p = A.pay[t];
             const int64_t per = (int64_t)nn * nn;
@@ -511,10 +515,24 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                     pp[n] += A.s_pp_gg[n] * gg + A.s_pp_m * mass;
                 }
                 for (int i = 0; i < dim; ++i) {
-                    up[i] += -(gnab[i] + 0.5 * gnba[i]);
-                    pu[i] += gnba[i] + 0.5 * gnab[i];
+                    const double vu = -(gnab[i] + 0.5 * gnba[i]), vp = gnba[i] + 0.5 * gnab[i];
+                    up[0][i] += vu; up[1][i] += vu;
+                    pu[0][i] += vp; pu[1][i] += vp;
                 }
                 cr += A.s_cross * mass;
+            } else if (p >= A.C * per + 4 * A.Fi * per) {   // DG prescribed-flux facet (assembly.py:521-531)
+                const int64_t idx = p - A.C * per - 4 * A.Fi * per;
+                const int64_t vi = idx / per;
+                const int a = (int)((idx / nn) % nn), b = (int)(idx % nn);
+                const int net = vi < A.nv1 ? 0 : 1;
+                double F = 0.0;
+                for (int q = 0; q < A.fnq; ++q)
+                    F += A.vW[vi * A.fnq + q] * A.vN[(vi * A.fnq + q) * nn + a] * A.vN[(vi * A.fnq + q) * nn + b];
+                const double *n = A.fn + (int64_t)A.vfac[vi] * dim;
+                for (int i = 0; i < dim; ++i) {
+                    up[net][i] += F * n[i];
+                    pu[net][i] += -(F * n[i]);
+                }
             } else {                   // DG interior facet side pair (assembly.py:497-517)
                 const int64_t idx = p - A.C * per;
                 const int64_t q2 = idx / per;
@@ -534,8 +552,9 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                     pp[k] += A.c_pp[k] * ss * tt * F;
                 }
                 for (int i = 0; i < dim; ++i) {
-                    up[i] += 0.5 * ss * (F * n[i]);
-                    pu[i] += -0.5 * tt * (F * n[i]);
+                    const double vu = 0.5 * ss * (F * n[i]), vp = -0.5 * tt * (F * n[i]);
+                    up[0][i] += vu; up[1][i] += vu;
+                    pu[0][i] += vp; pu[1][i] += vp;
                 }
             }
         }
@@ -552,12 +571,12 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                 }
                 const int64_t ps = (int64_t)dim * g0 + (int64_t)i * len + o;
                 A.up_i[n][ps] = v2;
-                A.up_v[n][ps] = up[i];
+                A.up_v[n][ps] = up[n][i];
             }
             for (int j = 0; j < dim; ++j) {
                 const int64_t pos = (int64_t)dim * g0 + o * dim + j;
                 A.pu_i[n][pos] = v2 * dim + j;
-                A.pu_v[n][pos] = pu[j];
+                A.pu_v[n][pos] = pu[n][j];
             }
             A.pp_i[n][e] = v2;
             A.pp_v[n][e] = pp[n];
@@ -617,7 +636,42 @@ __global__ void k_dg_facet_tables(int64_t Fi, FRule R, int kind, int dim, int nn
         facet_point(R, dim, nvf, fv, V, f, q, X);
         W[t] = R.w[q] * (fm[f] / R.rm);
         trace(kind, dim, nn, V, cells, Jinv, fplus[f], X, Np + t * nn);
-        trace(kind, dim, nn, V, cells, Jinv, fminus[f], X, Nm + t * nn);
+        if (Nm) trace(kind, dim, nn, V, cells, Jinv, fminus[f], X, Nm + t * nn);
+    }
+}
+// DG-VMS prescribed-flux facets (assembly.py:521-531): plus-cell pairs of every velocity
+// facet, both networks' lists back to back (payloads after the interior-facet ones)
+__global__ void k_emit_dg_vel(int64_t nvt, int nn, int64_t base, const int *vfac, const int *fplus, int64_t nodes,
+                              uint64_t *keys, int *pay) {
+    const int64_t per = (int64_t)nn * nn;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nvt * per; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t vi = t / per;
+        const int a = (int)((t / nn) % nn), b = (int)(t % nn);
+        const int64_t c = fplus[vfac[vi]];
+        keys[t] = (uint64_t)(c * nn + a) * (uint64_t)nodes + (uint64_t)(c * nn + b);
+        pay[t] = (int)(base + t);
+    }
+}
+// f_p -= sum_q W_q (u.n)_q N_a on the velocity facets (assembly.py:532-535)
+__global__ void k_rhs_dg_vel(int64_t nv, const int64_t *fids, FRule R, int kind, int dim, int nn, int nvf,
+                             const int *fv, const int *fplus, const double *fm, const double *V, const int *cells,
+                             const double *Jinv, const double *un, int64_t *dof, double *val) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = fids[i];
+        const int64_t c = fplus[f];
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int q = 0; q < R.nq; ++q) {
+            double X[3], N[8];
+            facet_point(R, dim, nvf, fv, V, f, q, X);
+            trace(kind, dim, nn, V, cells, Jinv, c, X, N);
+            const double W = R.w[q] * (fm[f] / R.rm);
+            const double wu = W * un[i * R.nq + q];
+            for (int a = 0; a < nn; ++a) acc[a] += wu * N[a];
+        }
+        for (int a = 0; a < nn; ++a) {
+            dof[i * nn + a] = c * nn + a;
+            val[i * nn + a] = -acc[a];
+        }
     }
 }
 
@@ -914,7 +968,7 @@ __global__ void k_scatter_vals(int64_t n, const int64_t *idx, const double *v, d
 static void alloc_blk(Ctx *c, Csr &B, int rows, int cols, int64_t nnz) { B.alloc(rows, cols, nnz, c->s); }
 
 static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, bool dg,
-                         dpp_system &S) {
+                         const dpp_bc *bc, dpp_system &S) {
     const Elem E = make_elem(m.kind);
     const int dim = m.dim, nn = m.nn;
     const int64_t C = m.C;
@@ -925,7 +979,18 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
         for (int64_t f = 0; f < hm.n_facets; ++f)
             if (hm.facet_minus[f] >= 0) inter.push_back(f);
     const int64_t Fi = (int64_t)inter.size();
-    const int64_t ncell = C * nn * nn, nfac = dg ? 4 * Fi * nn * nn : 0, ntot = ncell + nfac;
+    // DG prescribed-flux facets of both networks (assembly.py:519-535)
+    std::vector<int> vfh;
+    int64_t nv1 = 0;
+    if (dg && bc) {
+        for (int n = 0; n < 2; ++n) {
+            for (int64_t i = 0; i < bc->n_vfacets[n]; ++i) vfh.push_back((int)bc->vfacets[n][i]);
+            if (n == 0) nv1 = (int64_t)vfh.size();
+        }
+    }
+    const int64_t nvt = (int64_t)vfh.size();
+    const int64_t ncell = C * nn * nn, nfac = dg ? 4 * Fi * nn * nn : 0, nvel = nvt * nn * nn;
+    const int64_t ntot = ncell + nfac + nvel;
     if (ntot > INT32_MAX) DPP_FAIL(DPP_ERR_VALUE, "mesh too large for 32-bit contribution ids");
     DBuf<uint64_t> keys(ntot, c->s);
     DBuf<int> pay(ntot, c->s);
@@ -950,6 +1015,20 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
             m.cells.p, m.Jinv.p, m.fm.p, fW.p, fNp.p, fNm.p);
         launched(c);
         CK(cudaStreamSynchronize(c->s));
+    }
+    DBuf<int> dvfac(nvt, c->s);
+    DBuf<double> vW, vN;
+    if (nvt) {
+        dvfac.upload(vfh.data(), nvt);
+        k_emit_dg_vel<<<grid_for(nvel, 256, c->sms), 256, 0, c->s>>>(nvt, nn, ncell + nfac, dvfac.p, m.fplus.p, nodes,
+                                                                   keys.p + ncell + nfac, pay.p + ncell + nfac);
+        launched(c);
+        vW.alloc(nvt * R2.nq, c->s);
+        vN.alloc(nvt * R2.nq * nn, c->s);
+        k_dg_facet_tables<<<grid_for(nvt * R2.nq, 128, c->sms), 128, 0, c->s>>>(
+            nvt, R2, m.kind, dim, nn, m.nvf, dvfac.p, m.fv.p, m.fplus.p, m.fminus.p, m.verts.p, m.cells.p,
+            m.Jinv.p, m.fm.p, vW.p, vN.p, nullptr);
+        launched(c);
     }
     Graph G;
     {
@@ -1004,6 +1083,11 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
     A.fNm = fNm.p;
     A.fn = m.fn.p;
     A.fnq = R2.nq;
+    A.nvt = nvt;
+    A.nv1 = nv1;
+    A.vfac = dvfac.p;
+    A.vW = vW.p;
+    A.vN = vN.p;
     Csr &c12 = S.blk[DPP_K12_PP], &c21 = S.blk[DPP_K21_PP];
     if (!dg) {
         alloc_blk(c, c12, np_, np_, g);
@@ -1032,6 +1116,22 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
             launched(c);
             add_at(c, nu_c, du, vu, S.rhs[n == 0 ? 0 : 2].p);
             add_at(c, np_c, dpi, vp, S.rhs[n == 0 ? 1 : 3].p);
+        }
+    }
+    if (nvt) {   // f_p -= (u.n, q) on the prescribed-flux facets, after the body force (assembly.py:532-535)
+        FRule R4 = frule(m.kind, 4);
+        for (int n = 0; n < 2; ++n) {
+            const int64_t nv = bc->n_vfacets[n];
+            if (nv <= 0) continue;
+            DBuf<int64_t> fids(nv, c->s), dof(nv * nn, c->s);
+            DBuf<double> un(nv * R4.nq, c->s), val(nv * nn, c->s);
+            fids.upload(bc->vfacets[n], nv);
+            un.upload(bc->vdata[n], nv * R4.nq);
+            k_rhs_dg_vel<<<grid_for(nv, 128, c->sms), 128, 0, c->s>>>(nv, fids.p, R4, m.kind, dim, nn, m.nvf, m.fv.p,
+                                                                     m.fplus.p, m.fm.p, m.verts.p, m.cells.p, m.Jinv.p,
+                                                                     un.p, dof.p, val.p);
+            launched(c);
+            add_at(c, nv * nn, dof, val, S.rhs[n == 0 ? 1 : 3].p);
         }
     }
     CK(cudaStreamSynchronize(c->s));
@@ -1353,10 +1453,6 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
         Ctx *c = &ctx->c;
         HostMesh &hm = mm->m;
         if (p->mu <= 0 || p->k1 <= 0 || p->k2 <= 0) DPP_FAIL(DPP_ERR_VALUE, "mu, k1, k2 must be positive");
-        if (bc && formulation == DPP_DGVMS)
-            for (int n = 0; n < 2; ++n)
-                if (bc->n_vfacets[n] > 0)
-                    DPP_FAIL(DPP_ERR_VALUE, "prescribed-velocity facets of the DG-VMS form are not supported by the device assembler yet");
         DPP_TRACE_SCOPE(c, "assemble.total");
         DevMesh *mp;
         {
@@ -1385,7 +1481,7 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
         {
             DPP_TRACE_SCOPE(c, "assemble.blocks");
             if (formulation == DPP_HDIV) assemble_hdiv(c, hm, m, *p, *S);
-            else assemble_vms(c, hm, m, *p, formulation == DPP_DGVMS, *S);
+            else assemble_vms(c, hm, m, *p, formulation == DPP_DGVMS, bc, *S);
         }
         {
             DPP_TRACE_SCOPE(c, "assemble.rhs");

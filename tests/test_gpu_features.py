@@ -95,7 +95,8 @@ def test_body_force(form, dim, kind, n):
     check_solve(bs, obs)
 
 
-@pytest.mark.parametrize("form,dim,kind,n", [("hdiv", 2, "tri", 8), ("cgvms", 2, "quad", 6)])
+@pytest.mark.parametrize("form,dim,kind,n", [("hdiv", 2, "tri", 8), ("cgvms", 2, "quad", 6), ("dgvms", 2, "tri", 4),
+                                             ("dgvms", 3, "tet", 2)])
 def test_velocity_facets(form, dim, kind, n):
     bs, obs = pair(form, dim, kind, n, vel_side=True)
     check_system(bs, obs)
@@ -120,16 +121,6 @@ def test_strong_pressure(dim, kind, n):
 def test_strong_pressure_with_velocity_facets():
     bs, obs = pair("cgvms", 2, "tri", 6, vel_side=True, strong=True)
     check_system(bs, obs, exact_pattern=False)
-
-
-def test_dg_velocity_facets_rejected():
-    m = dpp.generate_unit_mesh(2, "tri", 3)
-    p = dpp.DppParameters(gamma_b=(0.0, 0.0))
-    bf = m.boundary_facets
-    bcs = dpp.boundary_data(dpp.manufactured_solution(2, p), m,
-                            velocity_facets=(frozenset({int(bf[0])}), frozenset()))
-    with pytest.raises(NotImplementedError):
-        dpp.assemble(m, "dgvms", p, bcs)
 
 
 def test_strong_is_cgvms_only():
