@@ -242,7 +242,7 @@ void trsv_block(Ctx *c, const Tri &T, const double *b, double *x, const double *
                 cudaStream_t st);
 void trsv_cluster(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
                   cudaStream_t st);
-constexpr int DENSE_TRI_MAX = 1024;
+constexpr int DENSE_TRI_MAX = 4096;   // dense inverse up to 134 MB per factor: a sweep is one GEMV
 // pre_order / pre_lev: a level analysis of a superset pattern of this triangle
 // (e.g. ILU(0)'s stored lower pattern for its L factor), reused as the schedule
 Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense = false,

@@ -172,17 +172,22 @@ struct Builder {
             return N;
         }
         if (nd.split_type != DPP_SPLIT_SCHUR_FULL_SELFP) DPP_FAIL(DPP_ERR_VALUE, "unknown split type");
-        Csr B = csr_submatrix(c, M, N->segA, N->segB);
-        Csr C = csr_submatrix(c, M, N->segB, N->segA);
+        Csr B, C;
+        {
+            DPP_TRACE_SCOPE(c, "pc.schur_BC");
+            B = csr_submatrix(c, M, N->segA, N->segB);
+            C = csr_submatrix(c, M, N->segB, N->segA);
+        }
         // diag_lump(A) (linalg.py:234-241) and selfp (linalg.py:244-254)
         DBuf<double> d(N->nA, c->s), dinv(N->nA, c->s);
-        csr_diag(c, A, d.p, nullptr);
         {
+            DPP_TRACE_SCOPE(c, "pc.schur_diag");
+            csr_diag(c, A, d.p, nullptr);
             std::vector<double> hd = d.to_host();
             for (double v : hd)
                 if (v == 0.0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero diagonal entry in diag_lump");
+            reciprocal(c, N->nA, d.p, dinv.p);
         }
-        reciprocal(c, N->nA, d.p, dinv.p);
         Csr S;
         fork_join(c, N->side_owner,
                   [&](Ctx *sc) {   // the A-block leaf (ILU(0)) does not need S_p

@@ -411,7 +411,7 @@ void tri_dense_inverse(Ctx *c, Tri &T) {
     static bool attr = false;
     if (!attr) {
         CK(cudaFuncSetAttribute(k_bd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)(BD_INV_WPB * 1024 * sizeof(double))));
+                                (int)(BD_INV_WPB * 4096 * sizeof(double))));
         attr = true;
     }
     dim3 grid((n + BD_INV_WPB - 1) / BD_INV_WPB, 1);
@@ -458,7 +458,7 @@ bool bd_plan(Ctx *c, Tri &T, int B) {
         static bool attr = false;
         if (!attr) {
             CK(cudaFuncSetAttribute(k_bd_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)(BD_INV_WPB * 1024 * sizeof(double))));
+                                    (int)(BD_INV_WPB * 4096 * sizeof(double))));
             CK(cudaFuncSetAttribute(k_trsv_bd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD_SMEM_LIMIT));
             attr = true;
         }
