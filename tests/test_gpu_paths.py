@@ -1,0 +1,70 @@
+"""Every triangular-sweep strategy stays correct (the default path picks one per
+triangle; these force the others).  Each variant runs in a fresh process (the
+switches are read once per process) and must match the CPU oracle to the usual
+bars: solution within 1e-9 relative, iterations within +-2.
+
+  default                     push-exchange cluster sweeps + block-dense / dense smoothers
+  DPP_PU_MODE=push            (same; explicit)
+  DPP_NO_PUSH=1               barrier-per-level cluster sweeps (tricluster.cu)
+  DPP_BD_MAX=0                no block-dense smoothers (level sweeps on every AMG level)
+  DPP_BD_MAX=0 DPP_NO_PUSH=1 DPP_NO_CLUSTER=1
+                              block-sequential (triblock.cu) / sync-free warp-per-row sweeps
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests.conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_1808_08328_b200 as dpp
+p = dpp.DppParameters(k2=0.01, gamma_b=(0.0, 0.0, 0.0))
+m = dpp.generate_unit_mesh(3, "tet", 16)
+bs = dpp.assemble(m, "cgvms", p, dpp.boundary_data(dpp.mms_3d(p), m))
+r = dpp.solve(bs, dpp.method_config("scale", rtol=1e-8))
+np.save({out!r}, r.solution_vector())
+print(json.dumps({{"its": r.stats.iterations, "converged": bool(r.stats.converged)}}))
+"""
+
+VARIANTS = {
+    "default": {},
+    "pull_cluster": {"DPP_NO_PUSH": "1"},
+    "no_block_dense": {"DPP_BD_MAX": "0"},
+    "sync_free_and_block": {"DPP_BD_MAX": "0", "DPP_NO_PUSH": "1", "DPP_NO_CLUSTER": "1"},
+}
+
+
+@pytest.fixture(scope="module")
+def oracle_ref():
+    import oracle
+    op = oracle.Params(k2=0.01, gamma_b=(0.0, 0.0, 0.0))
+    om = oracle.generate_unit_mesh(3, "tet", 16)
+    obs = oracle.assemble(om, "cgvms", op, oracle.boundary_data(oracle.mms(3, op), om))
+    rep = oracle.solve(obs, oracle.method_config("scale", rtol=1e-8))
+    return rep.x, rep.stats.iterations
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("name", list(VARIANTS))
+def test_sweep_strategy(name, oracle_ref, tmp_path):
+    out = str(tmp_path / "x.npy")
+    env = dict(os.environ, **VARIANTS[name])
+    res = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, out=out)], env=env,
+                         capture_output=True, text=True, timeout=500)
+    assert res.returncode == 0, res.stderr[-2000:]
+    info = json.loads(res.stdout.strip().splitlines()[-1])
+    x_ref, its_ref = oracle_ref
+    x = np.load(out)
+    rel = np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref)
+    assert info["converged"] and abs(info["its"] - its_ref) <= 2, (info, its_ref)
+    assert rel < 1e-9, rel
