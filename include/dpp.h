@@ -105,6 +105,13 @@ typedef struct {
     int64_t n_vfacets[2];
     const int64_t *vfacets[2];
     const double *vdata[2];
+    /* p0_kind[k] != 0: p0[k] is not read; the device evaluates the reference's
+     * manufactured pressure (problem.py:100-144) at the facet points itself:
+     * 1 = 2-D (Eq. 44), 2 = 3-D (Eq. 46); p0_coef = {mu/pi, c, e} with
+     * p = mu/pi * X * S + c * E (X = exp(pi x), S = sin(pi y) [+ sin(pi z)],
+     * E = exp(e y) [+ exp(e z)]; c = -mu/(beta k1) for network 1, +mu/(beta k) for 2) */
+    int32_t p0_kind[2];
+    double p0_coef[2][4];
 } dpp_bc;
 
 int dpp_facet_rule_size(int dim, int kind, int degree, int *nq);

@@ -34,7 +34,8 @@ class Params(C.Structure):
 
 class Bc(C.Structure):
     _fields_ = [("n_pfacets", C.c_int64 * 2), ("pfacets", C.c_void_p * 2), ("p0", C.c_void_p * 2),
-                ("n_vfacets", C.c_int64 * 2), ("vfacets", C.c_void_p * 2), ("vdata", C.c_void_p * 2)]
+                ("n_vfacets", C.c_int64 * 2), ("vfacets", C.c_void_p * 2), ("vdata", C.c_void_p * 2),
+                ("p0_kind", C.c_int32 * 2), ("p0_coef", (C.c_double * 4) * 2)]
 
 
 class SplitNode(C.Structure):
@@ -84,6 +85,7 @@ SIGNATURES = {
     "dpp_facet_points": [P, P, I32, I64, P, P, P],
     "dpp_assemble": [P, P, I32, C.POINTER(Params), C.POINTER(Bc), PP],
     "dpp_system_eliminate": [P, I32, I64, P, P],
+    "dpp_mesh_upload_bytes": [P, C.POINTER(I64)],
     "dpp_system_from_blocks": [P, C.POINTER(P), C.POINTER(P), C.POINTER(I64), PP],
     "dpp_system_sizes": [P, C.POINTER(I64)],
     "dpp_system_block": [P, I32, PP],

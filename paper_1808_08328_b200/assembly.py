@@ -131,12 +131,17 @@ def monolithic_view(block_system: BlockSystem):
 
 
 def _pressure_data(mesh: Mesh, bcs: BoundarySpec, net: int):
-    """Pressure facets of one network and p0 at their degree-4 quadrature points."""
+    """Pressure facets of one network and p0 at their degree-4 quadrature points.
+    Returns (pf, p0, device) with device = (kind, coef) when the pressure closure is a
+    package manufactured solution the device evaluates itself (p0 is then None)."""
     bf = mesh.boundary_facets
     vel = bcs.velocity_facets[net - 1]
     if vel:
         bf = bf[~np.isin(bf, np.fromiter(vel, dtype=np.int64))]
     pf = N.i64(bf)
+    dev = getattr(bcs.p_data[net - 1], "_dpp_device", None)
+    if dev is not None:
+        return pf, None, dev
     nq = C.c_int()
     N.call("dpp_facet_rule_size", mesh.dim, N.KINDS[mesh.cell_kind.value], DATA_QUAD_DEGREE,
            C.byref(nq))
@@ -146,7 +151,19 @@ def _pressure_data(mesh: Mesh, bcs: BoundarySpec, net: int):
                N.ptr(X), None)
     p0 = N.f64(np.asarray(bcs.p_data[net - 1](X.reshape(-1, mesh.dim)), dtype=float)
                .reshape(len(pf), nq.value))
-    return pf, p0
+    return pf, p0, None
+
+
+def fill_bc_pressure(bc, net: int, pf, p0, dev):
+    """Pressure-facet part of a dpp_bc (host p0 values or a device-evaluated MMS)."""
+    bc.n_pfacets[net - 1] = len(pf)
+    bc.pfacets[net - 1] = pf.ctypes.data
+    if dev is not None:
+        bc.p0_kind[net - 1] = dev[0]
+        for i, v in enumerate(dev[1]):
+            bc.p0_coef[net - 1][i] = v
+    else:
+        bc.p0[net - 1] = p0.ctypes.data
 
 
 def _facet_points(mesh: Mesh, facets: np.ndarray, degree: int):
@@ -202,11 +219,9 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
     if bcs is not None:
         bc = N.Bc()
         for net in (1, 2):
-            pf, p0 = _pressure_data(mesh, bcs, net)
+            pf, p0, dev = _pressure_data(mesh, bcs, net)
             keep += [pf, p0]
-            bc.n_pfacets[net - 1] = len(pf)
-            bc.pfacets[net - 1] = pf.ctypes.data
-            bc.p0[net - 1] = p0.ctypes.data
+            fill_bc_pressure(bc, net, pf, p0, dev)
             if form == Formulation.HDIV and bcs.velocity_facets[net - 1]:
                 vel, gflux = _velocity_flux_data(mesh, bcs, net)
                 keep += [vel, gflux]

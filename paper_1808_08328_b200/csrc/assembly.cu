@@ -18,6 +18,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <cstring>
 
 #include "abi_guard.cuh"
 #include "mesh.h"
@@ -256,27 +257,53 @@ static DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
     d->V = m.n_vertices;
     d->C = m.n_cells;
     d->F = m.n_facets;
-    auto up32 = [&](DBuf<int> &b, const std::vector<int64_t> &v) {
-        std::vector<int> t(v.begin(), v.end());
-        b.alloc(t.size(), c->s);
-        b.upload(t.data(), t.size());
-        CK(cudaStreamSynchronize(c->s));
+    // device-layout image (int32 ids) in pinned host memory, built once per mesh: every
+    // upload is then asynchronous copies at full PCIe / C2C bandwidth
+    struct Part { size_t off, bytes; };
+    auto pad = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t nV = m.vertices.size(), nD = m.det.size(), nC = m.cells.size(), nCF = m.cell_facets.size(),
+                 nFV = m.facet_vertex_ids.size(), nF = m.facet_plus.size(), nCS = m.cell_facet_signs.size(),
+                 nFN = m.facet_normals.size(), nFM = m.facet_measures.size();
+    Part pv{0, 8 * nV}, pd{0, 8 * nD}, pc{0, 4 * nC}, pcf{0, 4 * nCF}, pfv{0, 4 * nFV}, pfp{0, 4 * nF},
+        pfm{0, 4 * nF}, pcs{0, nCS}, pfn{0, 8 * nFN}, pfs{0, 8 * nFM};
+    size_t total = 0;
+    for (Part *q : {&pv, &pd, &pc, &pcf, &pfv, &pfp, &pfm, &pcs, &pfn, &pfs}) { q->off = total; total += pad(q->bytes); }
+    if (!m.pinned || m.pinned_bytes != total) {
+        void *h = nullptr;
+        CK(cudaMallocHost(&h, std::max<size_t>(total, 256)));
+        m.pinned = std::shared_ptr<void>(h, [](void *q) { cudaFreeHost(q); });
+        m.pinned_bytes = total;
+        unsigned char *B = static_cast<unsigned char *>(h);
+        std::memcpy(B + pv.off, m.vertices.data(), pv.bytes);
+        std::memcpy(B + pd.off, m.det.data(), pd.bytes);
+        auto narrow = [&](const Part &q, const std::vector<int64_t> &v) {
+            int *o = reinterpret_cast<int *>(B + q.off);
+            for (size_t i = 0; i < v.size(); ++i) o[i] = (int)v[i];
+        };
+        narrow(pc, m.cells);
+        narrow(pcf, m.cell_facets);
+        narrow(pfv, m.facet_vertex_ids);
+        narrow(pfp, m.facet_plus);
+        narrow(pfm, m.facet_minus);
+        std::memcpy(B + pcs.off, m.cell_facet_signs.data(), pcs.bytes);
+        std::memcpy(B + pfn.off, m.facet_normals.data(), pfn.bytes);
+        std::memcpy(B + pfs.off, m.facet_measures.data(), pfs.bytes);
+    }
+    const unsigned char *B = static_cast<const unsigned char *>(m.pinned.get());
+    auto up = [&](auto &buf, const Part &q, size_t count) {
+        buf.alloc(count, c->s);
+        if (count) CK(cudaMemcpyAsync(buf.p, B + q.off, q.bytes, cudaMemcpyHostToDevice, c->s));
     };
-    d->verts.alloc(m.vertices.size(), c->s);
-    d->verts.upload(m.vertices.data(), m.vertices.size());
-    d->det.alloc(m.det.size(), c->s);
-    d->det.upload(m.det.data(), m.det.size());
-    up32(d->cells, m.cells);
-    up32(d->cf, m.cell_facets);
-    up32(d->fv, m.facet_vertex_ids);
-    up32(d->fplus, m.facet_plus);
-    up32(d->fminus, m.facet_minus);
-    d->cs.alloc(m.cell_facet_signs.size(), c->s);
-    d->cs.upload((const signed char *)m.cell_facet_signs.data(), m.cell_facet_signs.size());
-    d->fn.alloc(m.facet_normals.size(), c->s);
-    d->fn.upload(m.facet_normals.data(), m.facet_normals.size());
-    d->fm.alloc(m.facet_measures.size(), c->s);
-    d->fm.upload(m.facet_measures.data(), m.facet_measures.size());
+    up(d->verts, pv, nV);
+    up(d->det, pd, nD);
+    up(d->cells, pc, nC);
+    up(d->cf, pcf, nCF);
+    up(d->fv, pfv, nFV);
+    up(d->fplus, pfp, nF);
+    up(d->fminus, pfm, nF);
+    up(d->cs, pcs, nCS);
+    up(d->fn, pfn, nFN);
+    up(d->fm, pfs, nFM);
     d->Jinv.alloc((size_t)d->C * d->dim * d->dim, c->s);
     if (d->C) {
         k_geom<<<grid_for(d->C, 128, c->sms), 128, 0, c->s>>>(d->C, d->dim, d->kind, d->nn, d->verts.p,
@@ -788,6 +815,25 @@ __global__ void k_hdiv_up(int64_t F, const int *fplus, const int *fminus, const 
 __global__ void k_hdiv_up_cnt(int64_t F, const int *fminus, int *cnt) {
     for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F; f += (int64_t)gridDim.x * blockDim.x)
         cnt[f] = fminus[f] >= 0 ? 2 : 1;
+}
+
+// ------------------------------------------------------------------ manufactured pressure on the device
+// problem.py:100-144 in numpy's operation order: mu/pi * X * (sy [+ sz]) + c * (Y [+ Z])
+__global__ void k_mms_p0(int64_t nf, const int64_t *fids, FRule R, int dim, int nvf, const int *fv, const double *V,
+                         int kind, double mupi, double cc, double e, double *p0) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nf * R.nq; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = t / R.nq;
+        const int q = (int)(t % R.nq);
+        double X[3];
+        facet_point(R, dim, nvf, fv, V, fids[i], q, X);
+        const double Xe = exp(M_PI * X[0]);
+        double s = sin(M_PI * X[1]), ee = exp(e * X[1]);
+        if (kind == 2) {
+            s = s + sin(M_PI * X[2]);
+            ee = ee + exp(e * X[2]);
+        }
+        p0[t] = mupi * Xe * s + cc * ee;
+    }
 }
 
 // ------------------------------------------------------------------ boundary RHS
@@ -1307,7 +1353,14 @@ static void boundary_rhs(Ctx *c, DevMesh &m, int formulation, const dpp_bc *bc, 
         DBuf<int64_t> fids(nfp, c->s);
         fids.upload(bc->pfacets[net], nfp);
         DBuf<double> p0(nfp * R4.nq, c->s);
-        p0.upload(bc->p0[net], nfp * R4.nq);
+        if (bc->p0_kind[net]) {
+            const double *cf = bc->p0_coef[net];
+            k_mms_p0<<<grid_for(nfp * R4.nq, 256, c->sms), 256, 0, c->s>>>(nfp, fids.p, R4, m.dim, m.nvf, m.fv.p, m.verts.p,
+                                                                        bc->p0_kind[net], cf[0], cf[1], cf[2], p0.p);
+            launched(c);
+        } else {
+            p0.upload(bc->p0[net], nfp * R4.nq);
+        }
         double *rhs = S.rhs[net == 0 ? 0 : 2].p;
         if (formulation == DPP_HDIV) {
             DBuf<int64_t> dof(nfp, c->s);
@@ -1405,6 +1458,16 @@ int dpp_mesh_export(const dpp_mesh *mm, double *vertices, int64_t *cells, int64_
 
 int dpp_mesh_destroy(dpp_mesh *m) {
     return guard([&] { delete m; });
+}
+
+int dpp_mesh_upload_bytes(dpp_mesh *m, int64_t *bytes) {
+    return guard([&] {
+        const HostMesh &h = m->m;
+        *bytes = (int64_t)(8 * (h.vertices.size() + h.det.size() + h.facet_normals.size() + h.facet_measures.size()) +
+                           4 * (h.cells.size() + h.cell_facets.size() + h.facet_vertex_ids.size() +
+                                2 * h.facet_plus.size()) +
+                           h.cell_facet_signs.size());
+    });
 }
 
 int dpp_mesh_release_device(dpp_mesh *m) {

@@ -21,6 +21,8 @@ struct HostMesh {
     std::vector<double> facet_normals, facet_measures;
     std::vector<double> J, det;               // (C, dim, dim), (C,)
     std::shared_ptr<DevMesh> dev;             // lazily uploaded
+    std::shared_ptr<void> pinned;             // device-layout image in pinned host memory (built once)
+    size_t pinned_bytes = 0;
     void build();
 };
 

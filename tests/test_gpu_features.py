@@ -129,3 +129,20 @@ def test_strong_is_cgvms_only():
     with pytest.raises(ValueError):
         dpp.assemble(m, "hdiv", p, dpp.boundary_data(dpp.manufactured_solution(2, p), m),
                      pressure_dirichlet="strong")
+
+
+@pytest.mark.parametrize("dim,kind,n,form", [(2, "tri", 8, "cgvms"), (3, "tet", 4, "cgvms"), (2, "quad", 6, "hdiv"),
+                                             (3, "hex", 3, "dgvms")])
+def test_device_mms_traces_match_host(dim, kind, n, form):
+    """The package's manufactured pressures are evaluated on the device (dpp_bc.p0_kind);
+    wrapping them in plain lambdas forces the host path: the RHS must agree."""
+    p = dpp.DppParameters(gamma_b=(0.0,) * dim)
+    m = dpp.generate_unit_mesh(dim, kind, n)
+    mms = dpp.manufactured_solution(dim, p)
+    assert hasattr(mms.p1, "_dpp_device") and hasattr(mms.p2, "_dpp_device")
+    from paper_1808_08328_b200.problem import ManufacturedSolution
+    host = ManufacturedSolution(dim, mms.u1, lambda x: mms.p1(x), mms.u2, lambda x: mms.p2(x))
+    a = dpp.assemble(m, form, p, dpp.boundary_data(mms, m))
+    b = dpp.assemble(m, form, p, dpp.boundary_data(host, m))
+    for name in ("f1_u", "f1_p", "f2_u", "f2_p"):
+        assert rel_close(getattr(a, name), getattr(b, name), 1e-13), name

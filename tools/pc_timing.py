@@ -16,8 +16,9 @@ config = dpp.method_config(cfg["method"], rtol=cfg["rtol"])
 ctx = N.ctx()
 pdata = [_pressure_data(mesh, bcs, net) for net in (1, 2)]
 bc = N.Bc()
-for k, (pf, p0) in enumerate(pdata):
-    bc.n_pfacets[k], bc.pfacets[k], bc.p0[k] = len(pf), pf.ctypes.data, p0.ctypes.data
+from paper_1808_08328_b200.assembly import fill_bc_pressure
+for k, (pf, p0, dev) in enumerate(pdata):
+    fill_bc_pressure(bc, k + 1, pf, p0, dev)
 prm = N.Params(p.mu, p.beta, p.k1, p.k2, p.eta_u, p.eta_p, (C.c_double * 3)(0, 0, 0))
 arr, nn = flatten(config.split)
 hist = np.empty(config.max_iter)
