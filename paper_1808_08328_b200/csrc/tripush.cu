@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         const unsigned bytes = (unsigned)(boff_s[l + 1] - boff_s[l]);
         if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[l]), "r"(bytes) : "memory");
     };
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == blockDim.x - 32) {
         for (int l = 0; l < min(nst - 1, L); ++l) issue(l, l);
         for (int l = nst - 1; l < min(nst - 1 + l2pf, L); ++l) prefetch(l);
     }
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     int slot = 0, islot = nst - 1;
     unsigned phase = 0;
     for (int l = 0; l < L; ++l) {
-        if (dbg && threadIdx.x == 0) {
+        if (dbg && threadIdx.x == blockDim.x - 32) {
             tA = clock64();
             if (l > 0) {
                 unsigned long long m1 = 0, m2 = 0;
@@ -146,18 +146,22 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 if (m2 > tD) acc_pre += m2 - tD;    // level l-1: sync exit -> last warp computed
             }
         }
-        if (threadIdx.x == 0) {
+        // the producer is lane 0 of the LAST warp: rows are dealt to lane groups from
+        // group 0 up, so warp 0 (which holds every level's first rows) starts its rows
+        // right after the barrier instead of first issuing the next TMA copy
+        const bool producer = threadIdx.x == blockDim.x - 32;
+        if (producer) {
             mwait(su32(&mring[slot]), phase);
             if (dbg) tB = clock64();
             if (l > 0) mwait(su32(&mlev[l - 1]), 0);   // every value this CTA reads from level l-1 landed
             if (dbg) tC = clock64();
         }
         __syncthreads();   // ... and its own rows of level l-1 are written
-        if (dbg && threadIdx.x == 0) {
+        if (dbg && producer) {
             tD = clock64();
             acc_ring += tB - tA; acc_lev += tC - tB; acc_sync += tD - tC;
         }
-        if (threadIdx.x == 0) {
+        if (producer) {
             if (l + nst - 1 < L) issue(l + nst - 1, islot);   // the slot of level l-1 is free
             if (l + nst - 1 + l2pf < L) prefetch(l + nst - 1 + l2pf);
         }
@@ -195,7 +199,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         if (dbg) { __syncwarp(); if (lane == 0) t_w[threadIdx.x >> 5] = clock64(); }
     }
     __syncthreads();
-    if (dbg && threadIdx.x == 0) {
+    if (dbg && threadIdx.x == blockDim.x - 32) {
         dbg[k * 4 + 0] = acc_ring; dbg[k * 4 + 1] = acc_pre; dbg[k * 4 + 2] = acc_sync; dbg[k * 4 + 3] = acc_comp;
     }
     for (int i = threadIdx.x; i < mine; i += blockDim.x) {
