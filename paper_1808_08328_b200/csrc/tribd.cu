@@ -306,7 +306,10 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    if (threadIdx.x == 0) {
+    // producer: lane 0 of the last warp (the TMA issue / mbarrier bookkeeping stays off
+    // warp 0, whose row is the first of every block)
+    const bool producer = threadIdx.x == blockDim.x - 32;
+    if (producer) {
         for (int t = 0; t < min(nst - 1, nb); ++t) issue(t);
         bd_arm(&mby[0], 8u * rows_of(0));
         bd_arm(&mbx[0], 8u * rows_of(0));
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
         const int s = blk * B, m = min(B, n - s);
         const unsigned par = (unsigned)((t >> 1) & 1);
         if (dbg) tc = clock64();
-        if (threadIdx.x == 0) {
+        if (producer) {
             if (t + nst - 1 < nb) issue(t + nst - 1);   // slot of step t-1 is free
             if (t + 1 < nb) bd_arm(&mby[(t + 1) & 1], 8u * rows_of(t + 1));   // its previous phase (t-1) completed
         }
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
         // x of the previous block has landed in the window
         if (t > 0) bd_mbar_wait(&mbx[(t - 1) & 1], (unsigned)(((t - 1) >> 1) & 1));
         // mbx[(t+1) & 1] is re-armed only after its previous phase (block t-1) completed
-        if (threadIdx.x == 0 && t + 1 < nb) bd_arm(&mbx[(t + 1) & 1], 8u * rows_of(t + 1));
+        if (producer && t + 1 < nb) bd_arm(&mbx[(t + 1) & 1], 8u * rows_of(t + 1));
         if (dbg) { const unsigned long long u = clock64(); ph[0] += u - tc; tc = u; }
         // 1. y = b - T_off x over this CTA's rows (warp per row), pushed to every CTA
         for (int i = warp; i < nr; i += nw) {
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
         }
         if (dbg) { const unsigned long long u = clock64(); ph[3] += u - tc; tc = u; }
         // next step's segment landed; this step's ring slot and yf buffer are free
-        if (threadIdx.x == 0 && t + 1 < nb) bd_mbar_wait(&mbar[(t + 1) % nst], (unsigned)(((t + 1) / nst) & 1));
+        if (producer && t + 1 < nb) bd_mbar_wait(&mbar[(t + 1) % nst], (unsigned)(((t + 1) / nst) & 1));
         if (dbg) { const unsigned long long u = clock64(); ph[4] += u - tc; tc = u; }
         __syncthreads();
     }
