@@ -97,11 +97,37 @@ struct Builder {
     Ctx *c;
     const dpp_split_node *nodes;
     int n_nodes;
-    const int64_t *fsz;    // global field sizes
+    dpp_system *sys;       // field blocks (u1, p1, u2, p2)
     dpp_randn_fn randn;
     void *user;
 
-    PcLeaf leaf(int type, int nested, const Csr &M, const std::vector<int> &fids) {
+    // The submatrix of the monolithic K on field lists (rows fr, cols fc): the reference
+    // extracts it from K by index sets (blocksolve.py:227-228, order-preserving, stored
+    // zeros kept), which is exactly the system's field block (borrowed, no copy), an
+    // empty block for fields that do not couple, or sp.bmat of field blocks.
+    const Csr &fmat(const std::vector<int> &fr, const std::vector<int> &fc, Csr &store) {
+        static const int RC[10][2] = {{0, 0}, {0, 1}, {1, 0}, {1, 1}, {2, 2}, {2, 3}, {3, 2}, {3, 3}, {1, 3}, {3, 1}};
+        auto block = [&](int r, int cc) -> const Csr * {
+            for (int b = 0; b < 10; ++b)
+                if (RC[b][0] == r && RC[b][1] == cc) return &sys->blk[b];
+            return nullptr;
+        };
+        if (fr.size() == 1 && fc.size() == 1) {
+            if (const Csr *B = block(fr[0], fc[0])) return *B;
+            store = csr_empty(c, (int)sys->sizes[fr[0]], (int)sys->sizes[fc[0]]);
+            return store;
+        }
+        std::vector<const Csr *> grid;
+        std::vector<int> rsz, csz;
+        for (int r : fr) rsz.push_back((int)sys->sizes[r]);
+        for (int cc : fc) csz.push_back((int)sys->sizes[cc]);
+        for (int r : fr)
+            for (int cc : fc) grid.push_back(block(r, cc));
+        store = csr_bmat(c, grid, (int)fr.size(), (int)fc.size(), rsz, csz);
+        return store;
+    }
+
+    PcLeaf leaf_on(int type, const Csr &M) {
         PcLeaf L;
         L.type = type;
         if (type == DPP_LEAF_BJACOBI_ILU0) {
@@ -110,24 +136,23 @@ struct Builder {
         } else if (type == DPP_LEAF_AMG) {
             L.amg = amg_setup(c, M, 0.5, 2.0 / 3.0, 64, 25, randn, user);
             L.desc = "amg[" + std::to_string(L.amg->lv.size()) + "]";
-        } else if (type == DPP_LEAF_NESTED) {
-            if (nested < 0 || nested >= n_nodes) DPP_FAIL(DPP_ERR_VALUE, "bad nested split index");
-            L.node = node(nested, M, fids);
-            L.desc = L.node->desc;
         } else {
             DPP_FAIL(DPP_ERR_VALUE, "unknown leaf type");
         }
         return L;
     }
 
-    std::unique_ptr<PcNode> node(int id, const Csr &M, const std::vector<int> &fids) {
+    // Node on fields `fids`: M == nullptr -> the system's field blocks (fmat); otherwise M is
+    // the node's explicit matrix (e.g. the Schur complement) and blocks are extracted from it
+    // by index sets, as the reference does (blocksolve.py:241-256).
+    std::unique_ptr<PcNode> node(int id, const std::vector<int> &fids, const Csr *M = nullptr) {
         const dpp_split_node &nd = nodes[id];
         auto N = std::make_unique<PcNode>();
         N->split = nd.split_type;
         std::vector<int> off(fids.size() + 1, 0);
-        for (size_t i = 0; i < fids.size(); ++i) off[i + 1] = off[i] + (int)fsz[fids[i]];
+        for (size_t i = 0; i < fids.size(); ++i) off[i + 1] = off[i] + (int)sys->sizes[fids[i]];
         N->n = off.back();
-        if (N->n != M.rows) DPP_FAIL(DPP_ERR_VALUE, "split node: matrix does not match field sizes");
+        if (M && N->n != M->rows) DPP_FAIL(DPP_ERR_VALUE, "split node: matrix does not match field sizes");
         std::vector<int> gA(nd.groups[0], nd.groups[0] + nd.ngroup[0]);
         std::vector<int> gB(nd.groups[1], nd.groups[1] + nd.ngroup[1]);
         auto segs = [&](const std::vector<int> &g) {
@@ -145,14 +170,32 @@ struct Builder {
         N->segB = segs(gB);
         for (auto &s : N->segA) N->nA += s.second;
         for (auto &s : N->segB) N->nB += s.second;
-        Csr A, D;
-        {
-            DPP_TRACE_SCOPE(c, "pc.submatrix");
-            A = csr_submatrix(c, M, N->segA, N->segA);
-            D = csr_submatrix(c, M, N->segB, N->segB);
-        }
         for (DBuf<double> *b : {&N->rA, &N->zA, &N->zA2, &N->w}) b->alloc(N->nA, c->s);
         for (DBuf<double> *b : {&N->rB, &N->zB, &N->t}) b->alloc(N->nB, c->s);
+        // sub-block (rows g1, cols g2) of this node's matrix
+        auto sub = [&](Builder &bb, const std::vector<int> &g1, const std::vector<std::pair<int, int>> &s1,
+                       const std::vector<int> &g2, const std::vector<std::pair<int, int>> &s2,
+                       Csr &store) -> const Csr & {
+            if (!M) return bb.fmat(g1, g2, store);
+            DPP_TRACE_SCOPE(bb.c, "pc.submatrix");
+            store = csr_submatrix(bb.c, *M, s1, s2);
+            return store;
+        };
+        // a child on group g of this node
+        auto child = [&](Builder &bb, int type, int nested, const std::vector<int> &g,
+                         const std::vector<std::pair<int, int>> &s) {
+            Csr store;
+            if (type == DPP_LEAF_NESTED) {
+                if (nested < 0 || nested >= n_nodes) DPP_FAIL(DPP_ERR_VALUE, "bad nested split index");
+                PcLeaf L;
+                L.type = type;
+                if (M) store = csr_submatrix(bb.c, *M, s, s);
+                L.node = bb.node(nested, g, M ? &store : nullptr);
+                L.desc = L.node->desc;
+                return L;
+            }
+            return bb.leaf_on(type, sub(bb, g, s, g, s, store));
+        };
         if (nd.split_type == DPP_SPLIT_ADDITIVE) {
             // the two children are independent: build B on the side stream from a
             // second host thread while A is built here (both pore networks of the
@@ -163,21 +206,20 @@ struct Builder {
                       [&](Ctx *sc) {
                           Builder bb = *this;
                           bb.c = sc;
-                          N->b = bb.leaf(nd.child_type[1], nd.child_node[1], D, gB);
+                          N->b = child(bb, nd.child_type[1], nd.child_node[1], gB, N->segB);
                       },
-                      [&] { N->a = leaf(nd.child_type[0], nd.child_node[0], A, gA); }, FORK_ADDITIVE);
+                      [&] { N->a = child(*this, nd.child_type[0], nd.child_node[0], gA, N->segA); }, FORK_ADDITIVE);
             CK(cudaEventCreateWithFlags(&N->ev_fork, cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&N->ev_join, cudaEventDisableTiming));
             N->desc = "additive(" + N->a.desc + ", " + N->b.desc + ")";
             return N;
         }
         if (nd.split_type != DPP_SPLIT_SCHUR_FULL_SELFP) DPP_FAIL(DPP_ERR_VALUE, "unknown split type");
-        Csr B, C;
-        {
-            DPP_TRACE_SCOPE(c, "pc.schur_BC");
-            B = csr_submatrix(c, M, N->segA, N->segB);
-            C = csr_submatrix(c, M, N->segB, N->segA);
-        }
+        Csr sA, sD, sB, sC;
+        const Csr &A = sub(*this, gA, N->segA, gA, N->segA, sA);
+        const Csr &D = sub(*this, gB, N->segB, gB, N->segB, sD);
+        const Csr &B = sub(*this, gA, N->segA, gB, N->segB, sB);
+        const Csr &C = sub(*this, gB, N->segB, gA, N->segA, sC);
         // diag_lump(A) (linalg.py:234-241) and selfp (linalg.py:244-254)
         DBuf<double> d(N->nA, c->s), dinv(N->nA, c->s);
         {
@@ -193,14 +235,30 @@ struct Builder {
                   [&](Ctx *sc) {   // the A-block leaf (ILU(0)) does not need S_p
                       Builder bb = *this;
                       bb.c = sc;
-                      N->a = bb.leaf(nd.child_type[0], nd.child_node[0], A, gA);
+                      if (nd.child_type[0] == DPP_LEAF_NESTED) {
+                          if (nd.child_node[0] < 0 || nd.child_node[0] >= n_nodes)
+                              DPP_FAIL(DPP_ERR_VALUE, "bad nested split index");
+                          N->a.type = DPP_LEAF_NESTED;
+                          N->a.node = bb.node(nd.child_node[0], gA, &A);
+                          N->a.desc = N->a.node->desc;
+                      } else {
+                          N->a = bb.leaf_on(nd.child_type[0], A);
+                      }
                   },
                   [&] {
                       {
                           DPP_TRACE_SCOPE(c, "pc.selfp_spgemm");
                           S = spgemm(c, C, B, dinv.p, true, &D);
                       }
-                      N->b = leaf(nd.child_type[1], nd.child_node[1], S, gB);
+                      if (nd.child_type[1] == DPP_LEAF_NESTED) {
+                          if (nd.child_node[1] < 0 || nd.child_node[1] >= n_nodes)
+                              DPP_FAIL(DPP_ERR_VALUE, "bad nested split index");
+                          N->b.type = DPP_LEAF_NESTED;
+                          N->b.node = node(nd.child_node[1], gB, &S);
+                          N->b.desc = N->b.node->desc;
+                      } else {
+                          N->b = leaf_on(nd.child_type[1], S);
+                      }
                   }, FORK_SCHUR);
         N->Bc = csr_drop_zeros(c, B);
         N->Cc = csr_drop_zeros(c, C);
@@ -241,15 +299,9 @@ dpp_pc *pc_create(Ctx *c, dpp_system *s, const dpp_split_node *nodes, int n_node
     auto pc = std::make_unique<dpp_pc>();
     pc->ctx = c;
     DPP_TRACE_SCOPE(c, "pc.total");
-    const Csr *Kp;
-    {
-        DPP_TRACE_SCOPE(c, "pc.monolithic");
-        Kp = &system_K(c, s);
-    }
-    const Csr &K = *Kp;
-    Builder b{c, nodes, n_nodes, s->sizes, randn, user};
-    pc->root = b.node(0, K, {0, 1, 2, 3});
-    pc->n = K.rows;
+    Builder b{c, nodes, n_nodes, s, randn, user};
+    pc->root = b.node(0, {0, 1, 2, 3});
+    pc->n = (int)(s->sizes[0] + s->sizes[1] + s->sizes[2] + s->sizes[3]);
     pc->r.alloc(pc->n, c->s);
     pc->z.alloc(pc->n, c->s);
     CK(cudaEventRecord(e1, c->s));
