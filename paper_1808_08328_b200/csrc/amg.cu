@@ -83,7 +83,13 @@ static int64_t aggregate(Ctx *c, const Csr &A, double theta, std::vector<int64_t
     DBuf<int> sidx(snnz, c->s);
     k_strength<<<grid, 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, theta, sptr.p, nullptr, sidx.p);
     launched(c);
-    std::vector<int> hp = sptr.to_host(), hi = sidx.to_host();
+    std::vector<int> hp, hi;
+    {
+        DPP_TRACE_SCOPE(c, "amg.strength_d2h");
+        hp = sptr.to_host();
+        hi = sidx.to_host();
+    }
+    DPP_TRACE_SCOPE(c, "amg.greedy_host");
     return greedy(n, hp, hi, agg);
 }
 
@@ -260,16 +266,24 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
     auto h = std::make_unique<Amg>();
     h->ctx = c;
     {
+        DPP_TRACE_SCOPE(c, "amg.diag_check");
         DBuf<double> d(A0.rows, c->s);
         csr_diag(c, A0, d.p, nullptr);
         std::vector<double> hd = d.to_host();
         for (double v : hd)
             if (v == 0.0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "structurally singular input: zero diagonal entry");
     }
-    Csr cur = csr_copy(c, A0);
+    Csr cur;
+    {
+        DPP_TRACE_SCOPE(c, "amg.copy");
+        cur = csr_copy(c, A0);
+    }
     // smoother setup (level analysis + sweep plans) of level l runs on a worker
     // thread / side stream while this thread builds level l+1
-    h->side.ensure(c);
+    {
+        DPP_TRACE_SCOPE(c, "amg.side_ensure");
+        h->side.ensure(c);
+    }
     std::thread worker;
     std::exception_ptr werr;
     auto join_worker = [&] {
