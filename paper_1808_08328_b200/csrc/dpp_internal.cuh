@@ -68,6 +68,15 @@ inline void launched(Ctx *c) {
 }
 
 // Stream-ordered device buffer.
+// process-wide pool of pinned host staging buffers (never freed; first fit)
+struct PinnedBuf {
+    void *p = nullptr;
+    size_t cap = 0;
+};
+constexpr size_t PINNED_MIN = 64 * 1024;
+PinnedBuf pinned_acquire(size_t bytes);
+void pinned_release(PinnedBuf b);
+
 template <typename T>
 struct DBuf {
     T *p = nullptr;
@@ -98,11 +107,33 @@ struct DBuf {
         p = nullptr;
         n = 0;
     }
+    // transfers >= PINNED_MIN bytes go through pinned staging buffers (pinned_acquire):
+    // pageable copies are staged by the driver and serialise across the setup threads
     void upload(const T *h, size_t count) {
-        if (count) CK(cudaMemcpyAsync(p, h, sizeof(T) * count, cudaMemcpyHostToDevice, s));
+        if (!count) return;
+        const size_t bytes = sizeof(T) * count;
+        if (bytes < PINNED_MIN) {
+            CK(cudaMemcpyAsync(p, h, bytes, cudaMemcpyHostToDevice, s));
+            return;
+        }
+        PinnedBuf b = pinned_acquire(bytes);
+        std::memcpy(b.p, h, bytes);
+        CK(cudaMemcpyAsync(p, b.p, bytes, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));   // the staging buffer is reused after this
+        pinned_release(b);
     }
     void download(T *h, size_t count) const {
-        if (count) CK(cudaMemcpyAsync(h, p, sizeof(T) * count, cudaMemcpyDeviceToHost, s));
+        if (!count) return;
+        const size_t bytes = sizeof(T) * count;
+        if (bytes < PINNED_MIN) {
+            CK(cudaMemcpyAsync(h, p, bytes, cudaMemcpyDeviceToHost, s));
+            return;
+        }
+        PinnedBuf b = pinned_acquire(bytes);
+        CK(cudaMemcpyAsync(b.p, p, bytes, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        std::memcpy(h, b.p, bytes);
+        pinned_release(b);
     }
     std::vector<T> to_host() const {
         std::vector<T> v(n);

@@ -60,6 +60,31 @@ void pool_release(int device, cudaStream_t s) {
 }
 }  // namespace
 
+namespace {
+std::mutex g_pin_mu;
+std::vector<PinnedBuf> g_pin_free;
+}  // namespace
+PinnedBuf pinned_acquire(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> lk(g_pin_mu);
+        for (size_t i = 0; i < g_pin_free.size(); ++i)
+            if (g_pin_free[i].cap >= bytes) {
+                PinnedBuf b = g_pin_free[i];
+                g_pin_free.erase(g_pin_free.begin() + (long)i);
+                return b;
+            }
+    }
+    PinnedBuf b;
+    b.cap = 1 << 22;
+    while (b.cap < bytes) b.cap <<= 1;
+    CK(cudaMallocHost(&b.p, b.cap));
+    return b;
+}
+void pinned_release(PinnedBuf b) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(b);
+}
+
 void SideStream::ensure(Ctx *parent) {
     if (s) return;
     s = pool_acquire(parent->device);
