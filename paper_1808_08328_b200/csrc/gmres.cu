@@ -11,7 +11,11 @@
 #include <chrono>
 #include <cmath>
 
+#include <cooperative_groups.h>
+
 #include "system.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dpp {
 
@@ -40,6 +44,63 @@ __global__ void k_axpy_neg_dev(int64_t n, const double *h, const double *v, doub
     const double a = *h;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) w[i] -= a * v[i];
 }
+// One Arnoldi step's modified Gram-Schmidt in one cooperative kernel:
+//   for i = 0..j: h_i = <V_i, w> ; w -= h_i V_i      then h_{j+1} = ||w||
+// Bitwise the sequence k_dot_partial + k_sum + k_axpy_neg_dev (+ norm2_dev) computes:
+// the same NRM_BLOCKS x 256 grid-stride partials and block reductions, every block
+// forms the final 32-lane ordered sum itself, and each thread only touches its own
+// elements of w between two dots, so one grid barrier per basis vector suffices
+// (partials are double-buffered).
+__device__ __forceinline__ double mgs_block_partial(double s, double *sh) {
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) r += __shfl_down_sync(0xffffffffu, r, o);
+    }
+    __syncthreads();
+    return r;   // valid in thread 0
+}
+__device__ __forceinline__ double mgs_final_sum(const double *part, int np, double *sh) {
+    if (threadIdx.x < 32) {
+        double s = 0.0;
+        for (int i = threadIdx.x; i < np; i += 32) s += __ldcg(part + i);
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (threadIdx.x == 0) sh[0] = s;
+    }
+    __syncthreads();
+    const double s = sh[0];
+    __syncthreads();
+    return s;
+}
+__global__ void __launch_bounds__(256) k_mgs(int64_t n, int j, const double *V, double *w, double *hcol,
+                                            double *part0, double *part1) {
+    __shared__ double sh[32];
+    cg::grid_group grid = cg::this_grid();
+    const int64_t g0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    for (int i = 0; i <= j + 1; ++i) {
+        double *part = (i & 1) ? part1 : part0;
+        const double *Vi = V + (size_t)i * n;
+        double s = 0.0;
+        if (i <= j)
+            for (int64_t k = g0; k < n; k += gs) s += Vi[k] * w[k];
+        else
+            for (int64_t k = g0; k < n; k += gs) s += w[k] * w[k];
+        const double bp = mgs_block_partial(s, sh);
+        if (threadIdx.x == 0) part[blockIdx.x] = bp;
+        grid.sync();
+        const double h = mgs_final_sum(part, gridDim.x, sh);
+        if (i <= j) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) hcol[i] = h;
+            for (int64_t k = g0; k < n; k += gs) w[k] -= h * Vi[k];
+        } else if (blockIdx.x == 0 && threadIdx.x == 0) {
+            hcol[j + 1] = sqrt(h);
+        }
+    }
+}
+
 // x = x + V[:k]^T y
 __global__ void k_update_x(int64_t n, int k, const double *V, const double *y, double *x) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -56,7 +117,7 @@ struct Gm {
     const Operator &A;
     const PcOp &M;
     std::vector<double> hin, hout;
-    DBuf<double> part;
+    DBuf<double> part, part2;
     int mv = 0, pcs = 0;
 
     void host_apply(dpp_apply_fn cb, void *user, const double *in, double *out) {
@@ -100,6 +161,7 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
     const auto t0 = std::chrono::steady_clock::now();
     Gm g{c, n, A, M};
     g.part.alloc(NRM_BLOCKS, c->s);
+    g.part2.alloc(NRM_BLOCKS, c->s);
     *st = dpp_krylov_stats{};
     DBuf<double> sc(restart + 8, c->s), r(n, c->s), z(n, c->s), w(n, c->s), tmp(n, c->s);
     double *hcol = sc.p;                  // H[0..j+1, j]
@@ -161,13 +223,15 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
             g.pc(tmp.p, w.p);                      // w = M^-1 A V[j]
             }
             DPP_TRACE_SCOPE(c, "gmres.mgs_givens");
-            for (int i = 0; i <= j; ++i) {         // modified Gram-Schmidt
-                const double *Vi = V.p + (size_t)i * n;
-                g.dot_dev(Vi, w.p, hcol + i);
-                k_axpy_neg_dev<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, hcol + i, Vi, w.p);
+            {   // modified Gram-Schmidt + ||w||, one cooperative kernel
+                int64_t nn = n;
+                int jj = j;
+                const double *Vp = V.p;
+                double *wp = w.p, *hp = hcol, *p0 = g.part.p, *p1 = g.part2.p;
+                void *args[] = {&nn, &jj, &Vp, &wp, &hp, &p0, &p1};
+                CK(cudaLaunchCooperativeKernel((const void *)k_mgs, NRM_BLOCKS, 256, args, 0, c->s));
                 launched(c);
             }
-            norm2_dev(c, n, w.p, hcol + j + 1);
             std::vector<double> hc(j + 2);
             CK(cudaMemcpyAsync(hc.data(), hcol, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->s));
             CK(cudaStreamSynchronize(c->s));
