@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(256) k_spmv(int rows, const int *__restrict__ 
                                               const double *__restrict__ val,
                                               const double *__restrict__ x, double *__restrict__ y,
                                               const double *__restrict__ b, double alpha) {
+    pdl_wait();
     constexpr int RPW = 32 / G;
     const int lane = threadIdx.x & (G - 1);
     const int grp = (threadIdx.x & 31) / G;
@@ -66,6 +67,7 @@ __global__ void __launch_bounds__(256) k_spmv(int rows, const int *__restrict__ 
         for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
         if (r < rows && lane == 0) y[r] = b ? b[r] + alpha * sum : alpha * sum;
     }
+    pdl_trigger();
 }
 
 void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b, double alpha,
@@ -77,7 +79,8 @@ void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b, dou
     auto launch = [&](auto kern, int G) {
         int64_t warps = ((int64_t)A.rows * G + 31) / 32;
         int grid = grid_for(warps * 32, block, c->sms, 8);
-        kern<<<grid, block, 0, st>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, x, y, b, alpha);
+        CK(launch_pdl(kern, dim3(grid), dim3(block), 0, st, A.rows, (const int *)A.ptr.p, (const int *)A.idx.p,
+                      (const double *)A.val.p, x, y, b, alpha));
     };
     if (avg <= 6) launch(k_spmv<4>, 4);
     else if (avg <= 12) launch(k_spmv<8>, 8);
@@ -94,7 +97,9 @@ __global__ void k_axpy(int64_t n, double a, const double *x, double *y) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) y[i] += a * x[i];
 }
 __global__ void k_axpby_to(int64_t n, const double *x, double a, const double *y, double *o) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) o[i] = x[i] + a * y[i];
+    pdl_trigger();
 }
 __global__ void k_div_dev(int64_t n, const double *x, const double *num, double *o) {
     const double d = *num;
@@ -114,7 +119,7 @@ void axpy(Ctx *c, int64_t n, double a, const double *x, double *y, cudaStream_t 
 void axpby_to(Ctx *c, int64_t n, const double *x, double a, const double *y, double *o,
               cudaStream_t st) {
     if (!n) return;
-    k_axpby_to<<<grid_for(n, 256, c->sms), 256, 0, S(c, st)>>>(n, x, a, y, o);
+    CK(launch_pdl(k_axpby_to, dim3(grid_for(n, 256, c->sms)), dim3(256), 0, S(c, st), n, x, a, y, o));
     launched(c);
 }
 void scale_by_dev(Ctx *c, int64_t n, const double *x, const double *num, double *o,
@@ -165,9 +170,11 @@ double norm2(Ctx *c, int64_t n, const double *x) {
 
 struct Segs { int64_t d[4], s[4], l[4]; int n; };
 __global__ void k_copy_segs(double *dst, const double *src, Segs g) {
+    pdl_wait();
     for (int k = 0; k < g.n; ++k)
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.l[k]; i += (int64_t)gridDim.x * blockDim.x)
             dst[g.d[k] + i] = src[g.s[k] + i];
+    pdl_trigger();
 }
 void copy_segments(Ctx *c, double *dst, const double *src, int nseg, const int64_t *doff,
                    const int64_t *soff, const int64_t *len, cudaStream_t st) {
@@ -177,7 +184,7 @@ void copy_segments(Ctx *c, double *dst, const double *src, int nseg, const int64
     g.n = nseg;
     for (int k = 0; k < nseg; ++k) g.d[k] = doff[k], g.s[k] = soff[k], g.l[k] = len[k], tot = std::max(tot, len[k]);
     if (!tot) return;
-    k_copy_segs<<<grid_for(tot, 256, c->sms), 256, 0, S(c, st)>>>(dst, src, g);
+    CK(launch_pdl(k_copy_segs, dim3(grid_for(tot, 256, c->sms)), dim3(256), 0, S(c, st), dst, src, g));
     launched(c);
 }
 

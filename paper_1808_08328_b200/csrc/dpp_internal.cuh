@@ -60,6 +60,29 @@ struct TraceScope {
 #define DPP_CAT(a, b) DPP_CAT2(a, b)
 #define DPP_TRACE_SCOPE(c, name) ::dpp::TraceScope DPP_CAT(dpp_trace_scope_, __LINE__)((c), (name))
 
+// Programmatic dependent launch (PC-apply kernels): a kernel launched with
+// launch_pdl may start while its predecessor in the stream runs; it triggers its own
+// dependents at entry and waits (griddepcontrol.wait) before touching any data the
+// predecessor produces or reads.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_on();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_on() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // record one kernel launch (checks launch errors outside graph capture)
 inline void launched(Ctx *c) {
     c->launches++;

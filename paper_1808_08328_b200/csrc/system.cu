@@ -104,6 +104,11 @@ SideStream::~SideStream() {
     pool_release(ctx.device, s);
 }
 
+bool pdl_on() {
+    static const bool on = [] { const char *e = std::getenv("DPP_NO_PDL"); return !(e && *e == '1'); }();
+    return on;
+}
+
 int fork_mask() {
     static const int m = [] {
         const char *s = std::getenv("DPP_SERIAL_SETUP");

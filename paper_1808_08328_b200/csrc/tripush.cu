@@ -110,8 +110,9 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         peer[threadIdx.x] = mapa_u32(su32(xh + pu_chunkp(chunk)), threadIdx.x);
         peer[16 + threadIdx.x] = mapa_u32(su32(mlev), threadIdx.x);
     }
-    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[base + i];
     for (int i = threadIdx.x; i <= L; i += blockDim.x) boff_s[i] = boff[b0 + i];
+    pdl_wait();   // b is the previous kernel's output (the prologue above reads static plan data only)
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[base + i];
     if (dbg && threadIdx.x < 32) { t_w[threadIdx.x] = 0; t_wp[threadIdx.x] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         if (dbg) { __syncwarp(); if (lane == 0) t_w[threadIdx.x >> 5] = clock64(); }
     }
     __syncthreads();
+    pdl_trigger();   // the dependent kernel's launch overlaps the x write-out below
     if (dbg && threadIdx.x == blockDim.x - 32) {
         dbg[k * 4 + 0] = acc_ring; dbg[k * 4 + 1] = acc_pre; dbg[k * 4 + 2] = acc_sync; dbg[k * 4 + 3] = acc_comp;
     }
@@ -512,13 +514,15 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     cfg.blockDim = dim3(P.threads, 1, 1);
     cfg.dynamicSmemBytes = pu_fixed(P.chunk, P.L, P.hmax) + (size_t)P.nst * P.stage;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = P.C;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_on() ? 2 : 1;
     const unsigned char *B = P.blocks.p;
     const long long *O = P.boff.p;
     static const int l2pf = [] { const char *e = std::getenv("DPP_PU_NOPF"); return e && *e == '1' ? 0 : 4; }();

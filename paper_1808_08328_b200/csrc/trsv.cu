@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(32 * INV_WPB) k_tri_inverse(int n, int backwar
 // x = Ti b over the triangle's nonzero half; xout = xadd + x
 __global__ void k_tri_gemv(int n, int backward, const double *__restrict__ Ti, const double *__restrict__ b,
                            double *x, const double *__restrict__ xadd, double *xout) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -251,6 +252,7 @@ __global__ void k_tri_gemv(int n, int backward, const double *__restrict__ Ti, c
             if (xout) xout[r] = xadd[r] + s;
         }
     }
+    pdl_trigger();
 }
 
 __global__ void __launch_bounds__(128) k_trsv(int n, const int *__restrict__ order, const int *__restrict__ ptr,
@@ -303,8 +305,8 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
     st = st ? st : c->s;
     if (T.n == 0) return;
     if (T.dense.n) {
-        k_tri_gemv<<<grid_for((int64_t)T.n * 32, 256, c->sms, 8), 256, 0, st>>>(T.n, T.backward, T.dense.p, b,
-                                                                               x, xadd, xout);
+        CK(launch_pdl(k_tri_gemv, dim3(grid_for((int64_t)T.n * 32, 256, c->sms, 8)), dim3(256), 0, st, T.n,
+                      (int)T.backward, (const double *)T.dense.p, b, x, xadd, xout));
         launched(c);
         return;
     }
