@@ -349,6 +349,9 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
             next = spgemm(c, L->R, AP, nullptr, false, nullptr);
         }
         L->A = std::move(cur);
+        spmv_plan(c, L->A);
+        spmv_plan(c, L->P);
+        spmv_plan(c, L->R);
         for (DBuf<double> *b : {&L->b, &L->x, &L->r, &L->t, &L->y}) b->alloc(n, c->s);
         L->ticket.alloc(4, c->s);
         CK(cudaStreamSynchronize(c->s));

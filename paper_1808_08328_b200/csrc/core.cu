@@ -4,6 +4,8 @@
 #include <cub/cub.cuh>
 
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 
 #include "dpp_internal.cuh"
 
@@ -70,10 +72,230 @@ __global__ void __launch_bounds__(256) k_spmv(int rows, const int *__restrict__ 
     pdl_trigger();
 }
 
+// nnz-streaming SpMV (CSR-stream): one CTA per row block of <= SB_CAP entries.  All
+// lanes load SB_E consecutive-strided (val, col) pairs up front -- 2*SB_E independent
+// coalesced loads per thread keep enough bytes in flight to cover HBM latency, which
+// the row-per-warp kernel above cannot at ~40 entries per row -- then gather x, park
+// the products in shared memory and reduce each row with G lanes.
+constexpr int SB_THREADS = 256, SB_E = 8, SB_CAP = SB_THREADS * SB_E, SB_T = SB_CAP - 256;
+
+__global__ void k_spmv_plan(int rows, const int *__restrict__ ptr, int nb, int *rb) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= nb; k += gridDim.x * blockDim.x) {
+        if (k == nb) { rb[k] = rows; continue; }
+        // first row whose first entry is at or after k*T
+        const int64_t key = (int64_t)k * SB_T;
+        int lo = 0, hi = rows;
+        while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if ((int64_t)ptr[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        rb[k] = lo;
+    }
+}
+
+// SELL-32 (sliced ELLPACK, slice height 32, rows kept in order): lane l of a warp owns
+// row 32k + l and walks its entries in column order, so a warp's loads of one slice
+// column are 256 B / 128 B coalesced and -- on the structured meshes of the DPP
+// systems, where the t-th neighbour of consecutive nodes is a consecutive node --
+// its x gathers hit a handful of lines instead of one line per couple of entries
+// (the CSR kernels are L1-wavefront bound on those gathers).  Each row is summed
+// sequentially in column order with separate multiply and add roundings: y = K x
+// is bitwise scipy's csr_matvec (linalg.py:27-32) on the same entries; skipped
+// exact zeros and the zero padding leave the sums unchanged.
+__global__ void k_sell_width(int rows, const int *__restrict__ ptr, int nsl, int *wcnt) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nsl;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t r = k * 32 + lane;
+        int len = r < rows ? ptr[r + 1] - ptr[r] : 0;
+        for (int o = 16; o > 0; o >>= 1) len = max(len, __shfl_xor_sync(0xffffffffu, len, o));
+        if (lane == 0) wcnt[k] = len * 32;
+    }
+}
+__global__ void k_sell_fill(int rows, const int *__restrict__ ptr, const int *__restrict__ idx,
+                            const double *__restrict__ val, int nsl, const int *__restrict__ sp, int *sc,
+                            double *sv) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nsl;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t r = k * 32 + lane;
+        const int a = r < rows ? ptr[r] : 0, len = r < rows ? ptr[r + 1] - a : 0;
+        const int w = (sp[k + 1] - sp[k]) >> 5;
+        int last = r < rows ? (int)r : 0;   // padding column: any valid index
+        for (int t = 0; t < w; ++t) {
+            const int64_t o = sp[k] + (int64_t)t * 32 + lane;
+            if (t < len) { last = idx[a + t]; sc[o] = last; sv[o] = val[a + t]; }
+            else { sc[o] = last; sv[o] = 0.0; }
+        }
+    }
+}
+
+// SELL-32 is used when padding stays under this factor of the stored entries
+constexpr double SELL_MAX_FILL = 1.25;
+// DPP_SPMV=row|stream|sell (default sell): kernel selection for A/B measurements
+static int spmv_mode() {
+    static const int m = [] {
+        const char *e = std::getenv("DPP_SPMV");
+        if (!e || !*e) return 2;
+        return !strcmp(e, "row") ? 0 : !strcmp(e, "stream") ? 1 : 2;
+    }();
+    return m;
+}
+
+void spmv_plan(Ctx *c, Csr &A) {
+    if (A.rows == 0 || A.nnz == 0 || spmv_mode() == 0) return;
+    if (spmv_mode() == 2) {
+        const int nsl = (A.rows + 31) / 32;
+        DBuf<int> wcnt((size_t)nsl, c->s);
+        const int grid = grid_for((int64_t)nsl * 32, 256, c->sms, 8);
+        k_sell_width<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, nsl, wcnt.p);
+        launched(c);
+        DBuf<int> sp;
+        const int64_t tot = counts_to_ptr(c, wcnt.p, nsl, sp);
+        if ((double)tot <= SELL_MAX_FILL * (double)A.nnz) {
+            A.sp = std::move(sp);
+            A.sc.alloc((size_t)tot, c->s);
+            A.sv.alloc((size_t)tot, c->s);
+            k_sell_fill<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, nsl, A.sp.p, A.sc.p, A.sv.p);
+            launched(c);
+            A.nsl = nsl;
+            return;
+        }
+    }
+    const int nb = (int)((A.nnz + SB_T - 1) / SB_T);
+    A.rb.alloc((size_t)nb + 1, c->s);
+    k_spmv_plan<<<grid_for(nb + 1, 256, c->sms), 256, 0, c->s>>>(A.rows, A.ptr.p, nb, A.rb.p);
+    launched(c);
+    A.nrb = nb;
+}
+
+__global__ void __launch_bounds__(SB_THREADS) k_spmv_stream(const int *__restrict__ rb,
+                                                            const int *__restrict__ ptr,
+                                                            const int *__restrict__ idx,
+                                                            const double *__restrict__ val,
+                                                            const double *__restrict__ x,
+                                                            double *__restrict__ y,
+                                                            const double *__restrict__ b, double alpha) {
+    __shared__ double prod[SB_CAP];
+    const int tid = threadIdx.x;
+    pdl_wait();
+    const int r0 = __ldg(rb + blockIdx.x), r1 = __ldg(rb + blockIdx.x + 1);
+    if (r0 >= r1) { pdl_trigger(); return; }
+    const int s = __ldg(ptr + r0), e = __ldg(ptr + r1), n = e - s, nr = r1 - r0;
+    auto out = [&](int r, double sum) { y[r] = b ? b[r] + alpha * sum : alpha * sum; };
+    if (n <= SB_CAP) {
+        double v[SB_E];
+        int j[SB_E];
+#pragma unroll
+        for (int k = 0; k < SB_E; ++k) {
+            const int p = s + k * SB_THREADS + tid;
+            v[k] = p < e ? __ldg(val + p) : 0.0;
+            j[k] = p < e ? __ldg(idx + p) : -1;
+        }
+#pragma unroll
+        for (int k = 0; k < SB_E; ++k)
+            if (j[k] >= 0) prod[k * SB_THREADS + tid] = v[k] * __ldg(x + j[k]);
+        __syncthreads();
+        // G lanes per row, G ~ mean row length / 4 (power of two in [2, 32])
+        const int avg = n / nr;
+        const int G = avg <= 8 ? 2 : avg <= 16 ? 4 : avg <= 32 ? 8 : avg <= 64 ? 16 : 32;
+        const int lane = tid & (G - 1), rpp = SB_THREADS / G;
+        for (int base = 0; base < nr; base += rpp) {
+            const int rr = base + tid / G;
+            double sum = 0.0;
+            if (rr < nr) {
+                const int a = __ldg(ptr + r0 + rr) - s, z = __ldg(ptr + r0 + rr + 1) - s;
+                for (int q = a + lane; q < z; q += G) sum += prod[q];
+            }
+            for (int o = G >> 1; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o, G);
+            if (rr < nr && lane == 0) out(r0 + rr, sum);
+        }
+    } else {   // oversized block (rows longer than ~256 entries): warp per row
+        const int lane = tid & 31;
+        for (int r = r0 + (tid >> 5); r < r1; r += SB_THREADS / 32) {
+            double sum = 0.0;
+            for (int p = __ldg(ptr + r) + lane; p < __ldg(ptr + r + 1); p += 32)
+                sum += __ldg(val + p) * __ldg(x + __ldg(idx + p));
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+            if (lane == 0) out(r, sum);
+        }
+    }
+    pdl_trigger();
+}
+
+// T warps share a slice: warp q of the slice sums columns q, q+T, ... of its lane's row
+// sequentially; the T partial sums are added in q order (T = 1: one sequential sum
+// per row in column order).  Up to SELL_U columns of a lane are in flight at once.
+constexpr int SELL_U = 8;
+template <int T>
+__global__ void __launch_bounds__(256) k_spmv_sell(int rows, int nsl, const int *__restrict__ sp,
+                                                   const int *__restrict__ sc, const double *__restrict__ sv,
+                                                   const double *__restrict__ x, double *__restrict__ y,
+                                                   const double *__restrict__ b, double alpha) {
+    constexpr int SPB = 8 / T;   // slices per CTA
+    __shared__ double part[T > 1 ? 8 : 1][32];
+    pdl_wait();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = warp % T;
+    const int64_t k = (int64_t)blockIdx.x * SPB + warp / T;
+    double sum = 0.0;
+    if (k < nsl) {
+        const int o0 = __ldg(sp + k), w = (__ldg(sp + k + 1) - o0) >> 5;
+        const int *J = sc + o0 + lane;
+        const double *V = sv + o0 + lane;
+        for (int t = q; t < w; t += T * SELL_U) {
+            double v[SELL_U], xv[SELL_U];
+            int j[SELL_U];
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) {
+                const int tt = t + u * T;
+                v[u] = tt < w ? __ldg(V + tt * 32) : 0.0;
+                j[u] = tt < w ? __ldg(J + tt * 32) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u) xv[u] = j[u] >= 0 ? __ldg(x + j[u]) : 0.0;
+#pragma unroll
+            for (int u = 0; u < SELL_U; ++u)
+                if (j[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(v[u], xv[u]));
+        }
+    }
+    if (T > 1) {
+        part[warp][lane] = sum;
+        __syncthreads();
+        if (q != 0) { pdl_trigger(); return; }
+#pragma unroll
+        for (int qq = 1; qq < T; ++qq) sum = __dadd_rn(sum, part[warp + qq][lane]);
+    }
+    const int64_t r = k * 32 + lane;
+    if (k < nsl && r < rows) y[r] = b ? __dadd_rn(b[r], __dmul_rn(alpha, sum)) : __dmul_rn(alpha, sum);
+    pdl_trigger();
+}
+
 void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b, double alpha,
           cudaStream_t st) {
     st = S(c, st);
     if (A.rows == 0) return;
+    if (A.nsl > 0) {
+        // warps per slice: about SELL_U columns per lane (one round of loads per row)
+        static const int tenv = [] { const char *e = std::getenv("DPP_SELL_T"); return e && *e ? atoi(e) : 0; }();
+        const int wavg = (int)(A.sc.n / ((size_t)A.nsl * 32));
+        const int T = tenv ? tenv : wavg <= SELL_U ? 1 : wavg <= 2 * SELL_U ? 2 : wavg <= 4 * SELL_U ? 4 : 8;
+        auto go = [&](auto kern, int spb) {
+            CK(launch_pdl(kern, dim3((A.nsl + spb - 1) / spb), dim3(256), 0, st, A.rows, A.nsl, (const int *)A.sp.p,
+                          (const int *)A.sc.p, (const double *)A.sv.p, x, y, b, alpha));
+        };
+        if (T == 1) go(k_spmv_sell<1>, 8);
+        else if (T == 2) go(k_spmv_sell<2>, 4);
+        else if (T == 4) go(k_spmv_sell<4>, 2);
+        else go(k_spmv_sell<8>, 1);
+        launched(c);
+        return;
+    }
+    if (A.nrb > 0) {
+        CK(launch_pdl(k_spmv_stream, dim3(A.nrb), dim3(SB_THREADS), 0, st, (const int *)A.rb.p,
+                      (const int *)A.ptr.p, (const int *)A.idx.p, (const double *)A.val.p, x, y, b, alpha));
+        launched(c);
+        return;
+    }
     const double avg = A.rows ? (double)A.nnz / A.rows : 0.0;
     const int block = 256;
     auto launch = [&](auto kern, int G) {

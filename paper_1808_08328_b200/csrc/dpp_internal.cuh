@@ -172,7 +172,16 @@ struct Csr {
     int64_t nnz = 0;
     DBuf<int> ptr, idx;
     DBuf<double> val;
+    // optional SpMV plans (spmv_plan), preferred in this order:
+    DBuf<int> sp;         // SELL-32: slice k = rows [32k, 32k+32), entries sp[k] .. sp[k+1]
+    DBuf<int> sc;         //   column of (slice k, column t, lane l) at sp[k] + 32 t + l
+    DBuf<double> sv;      //   value (padding: 0.0 with a valid column)
+    int nsl = 0;
+    DBuf<int> rb;         // CSR-stream row blocks: block k = rows starting in [k*T, (k+1)*T)
+    int nrb = 0;
     void alloc(int r, int c, int64_t z, cudaStream_t s) {
+        rb.release(); nrb = 0;
+        sp.release(); sc.release(); sv.release(); nsl = 0;
         rows = r; cols = c; nnz = z;
         ptr.alloc((size_t)r + 1, s);
         idx.alloc((size_t)z, s);
@@ -210,6 +219,8 @@ inline int grid_for(int64_t work, int block, int sms, int per_sm = 16) {
 // ---- core sparse / vector ops (core.cu) -----------------------------------
 void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b = nullptr,
           double alpha = 1.0, cudaStream_t st = nullptr);   // y = b + alpha*A x (b may be null)
+// row-block partition for the nnz-streaming SpMV (operators applied many times)
+void spmv_plan(Ctx *c, Csr &A);
 void fill(Ctx *c, double *x, int64_t n, double v, cudaStream_t st = nullptr);
 void axpy(Ctx *c, int64_t n, double a, const double *x, double *y, cudaStream_t st = nullptr);
 void axpby_to(Ctx *c, int64_t n, const double *x, double a, const double *y, double *out,

@@ -262,6 +262,8 @@ struct Builder {
                   }, FORK_SCHUR);
         N->Bc = csr_drop_zeros(c, B);
         N->Cc = csr_drop_zeros(c, C);
+        spmv_plan(c, N->Bc);
+        spmv_plan(c, N->Cc);
         N->desc = "schur-full(" + N->a.desc + ", selfp->" + N->b.desc + ")";
         CK(cudaStreamSynchronize(c->s));
         return N;

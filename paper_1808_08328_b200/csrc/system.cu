@@ -180,6 +180,7 @@ static void build_K(Ctx *c, dpp_system *s) {
     std::vector<int> sz = {(int)s->sizes[0], (int)s->sizes[1], (int)s->sizes[2], (int)s->sizes[3]};
     s->K = csr_bmat(c, grid, 4, 4, sz, sz);
     s->Kc = csr_drop_zeros(c, s->K);
+    spmv_plan(c, s->Kc);
     int64_t tot = s->sizes[0] + s->sizes[1] + s->sizes[2] + s->sizes[3], off = 0;
     s->f.alloc(tot, c->s);
     for (int k = 0; k < 4; ++k) {

@@ -21,5 +21,7 @@ m = dpp.generate_unit_mesh(3, kind, n)
 bs = dpp.assemble(m, form, p, dpp.boundary_data(dpp.mms_3d(p), m))
 pc = dpp.build_preconditioner(bs, dpp.method_config(meth))
 prof = N.StepProfile()
-N.call("dpp_profile_step", N.ctx(), bs.device().h, pc.handle(), int(os.environ.get("PROF_REPS", "3")), 0, C.byref(prof))
+if os.environ.get("PROF_RANGE") == "1":   # ncu --profile-from-start off: only the profiled step
+    C.CDLL("libcudart.so.12").cudaProfilerStart()
+N.call("dpp_profile_step", N.ctx(), bs.device().h, pc.handle(), int(os.environ.get("PROF_REPS", "3")), int(os.environ.get("PROF_FLUSH", "0")), C.byref(prof))
 print("spmv_ms", prof.spmv_ms, "pc_ms", prof.pc_ms, "kernels/apply", prof.pc_launches)
