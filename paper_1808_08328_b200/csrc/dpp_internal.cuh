@@ -263,9 +263,10 @@ struct ClusterPlan {      // level-ordered per-CTA blocks for the cluster sweep 
     DBuf<long long> boff;
 };
 struct PushPlan {         // cluster sweep with st.async point-to-point x exchange (tripush.cu)
-    int C = 0, chunk = 0, L = 0, G = 32, stage = 0, nst = 0, threads = 1024, hmax = 0;
+    int C = 0, chunk = 0, L = 0, G = 32, stage = 0, nst = 0, threads = 1024, hmax = 0, smax = 0;
     DBuf<unsigned char> blocks;
-    DBuf<long long> boff;
+    DBuf<long long> boff; // per step (CTA-major)
+    DBuf<int> sstart;     // first step of each CTA
     DBuf<int> tx;         // bytes each CTA receives per level
 };
 struct BlockPlan {        // block-sequential sweep with dense diagonal-block inverses (triblock.cu)
@@ -288,6 +289,10 @@ struct Tri {              // one sweep: strict part (zero-free) + optional diago
     std::unique_ptr<BlockPlan> bl;     // block-sequential sweep (small n, narrow levels)
     std::unique_ptr<BdPlan> bd;        // block-dense sweep (AMG smoother factors)
     DBuf<double> dense;   // optional dense inverse (small coarse levels): sweep = triangular GEMV
+    int ncomp = 1;        // Kronecker form: the triangle is this one (x) I_ncomp, rows interleaved
+    Csr W;                // level-merged form (merge_levels): x = solve_unit(strict, W b)
+    DBuf<double> wb;      //   scratch for W b
+    int64_t nnz_alg = -1; // stored entries of the original strict triangle (algorithmic bytes)
     bool backward = false;
     int n = 0, nlev = 0;
 };

@@ -373,7 +373,10 @@ void pc_destroy(dpp_pc *pc) { delete pc; }
 // B_spmv = 12 nnz_eff + 4 (r+1) + 8 c + 8 r ; B_tri = 12 nnz_eff(incl diag) + 4 (r+1) + 16 r
 namespace dpp {
 static double b_spmv(const Csr &A) { return 12.0 * A.nnz + 4.0 * (A.rows + 1) + 8.0 * A.cols + 8.0 * A.rows; }
-static double b_tri(const Tri &T) { return 12.0 * (T.strict.nnz + T.n) + 4.0 * (T.n + 1) + 16.0 * T.n; }
+static double b_tri(const Tri &T) {   // of the reference triangle, not of a merged form
+    const double nz = T.nnz_alg >= 0 ? (double)T.nnz_alg : (double)T.strict.nnz;
+    return 12.0 * (nz + T.n) + 4.0 * (T.n + 1) + 16.0 * T.n;
+}
 static double leaf_bytes(const PcLeaf &L);
 static double node_bytes(const PcNode &N) {
     if (N.split == DPP_SPLIT_ADDITIVE) return leaf_bytes(N.a) + leaf_bytes(N.b);

@@ -62,14 +62,16 @@ __device__ __forceinline__ void mwait(unsigned a, unsigned parity) {
 }
 
 // shared memory: ring mbarriers | level mbarriers [L] | xh = [x slice (chunk, padded) | halo (hmax)] |
-//                boff [L+1] | peer addresses | ring
+//                boff [smax+1] | peer addresses | ring
+// A CTA walks its own list of steps: the non-empty (level, part) blocks of its rows in
+// level order (a level's block is cut into parts that fit one ring stage).
 __host__ __device__ inline int pu_chunkp(int chunk) { return (int)(p16(8LL * chunk) / 8); }
-__host__ __device__ inline size_t pu_fixed(int chunk, int L, int hmax) {
-    return 8 * PU_NST_MAX + p16(8LL * L) + p16(8LL * chunk) + p16(8LL * hmax) + p16(8LL * (L + 1)) + 8 * PU_MAX;
+__host__ __device__ inline size_t pu_fixed(int chunk, int L, int hmax, int smax) {
+    return 8 * PU_NST_MAX + p16(8LL * L) + p16(8LL * chunk) + p16(8LL * hmax) + p16(8LL * (smax + 1)) + 8 * PU_MAX;
 }
 
 // block layout (16-byte aligned):
-//   int4 {nr, ne, np, 0} | int4 row[nr] = {local row, e0, e1, p0 << 4 | npush} | double dg[nr] |
+//   int4 {nr, ne, np, level} | int4 row[nr] = {local row, e0, e1, p0 << 4 | npush} | double dg[nr] |
 //   int code[ne] (index into xh) | (16) double val[ne] | int push[np] (dest << 28 | halo slot)
 __host__ __device__ inline long long pu_off_code(long long nr) { return 16 + 24 * nr; }
 __host__ __device__ inline long long pu_off_val(long long nr, long long ne) { return p16(pu_off_code(nr) + 4 * ne); }
@@ -79,8 +81,10 @@ __host__ __device__ inline long long pu_block_bytes(long long nr, long long ne, 
 
 template <int G>
 __global__ void __launch_bounds__(PU_THREADS, 1)
-    k_trsv_push(int n, int chunk, int L, int hmax, int stage, int nst, const unsigned char *__restrict__ blocks,
-                const long long *__restrict__ boff, const int *__restrict__ tx, const double *__restrict__ b,
+    k_trsv_push(int n, int ncomp, int chunk, int L, int smax, int hmax, int stage, int nst,
+                const unsigned char *__restrict__ blocks, const long long *__restrict__ boff,
+                const int *__restrict__ sstart, const int *__restrict__ tx, const int *__restrict__ wptr,
+                const int *__restrict__ widx, const double *__restrict__ wval, const double *__restrict__ b,
                 double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout, int l2pf,
                 unsigned long long *dbg) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -90,10 +94,12 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     unsigned long long *mlev = mring + PU_NST_MAX;
     double *xh = reinterpret_cast<double *>(smem + 8 * PU_NST_MAX + p16(8LL * L));
     long long *boff_s = reinterpret_cast<long long *>(xh + pu_chunkp(chunk) + p16(8LL * hmax) / 8);
-    unsigned *peer = reinterpret_cast<unsigned *>(boff_s + p16(8LL * (L + 1)) / 8);   // [0,16): halo, [16,32): mlev
-    unsigned char *ring = smem + pu_fixed(chunk, L, hmax);
+    unsigned *peer = reinterpret_cast<unsigned *>(boff_s + p16(8LL * (smax + 1)) / 8);   // [0,16): halo, [16,32): mlev
+    unsigned char *ring = smem + pu_fixed(chunk, L, hmax, smax);
     cg::cluster_group cl = cg::this_cluster();
     const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
+    const int comp = blockIdx.x / C;   // one cluster per Kronecker component (x[r * ncomp + comp])
+    const int s0 = sstart[k], S = sstart[k + 1] - s0;
     const int gl = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngrp = blockDim.x / G;
     const int lane = threadIdx.x & 31;
     const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1) << (lane & ~(G - 1)));
@@ -110,9 +116,17 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         peer[threadIdx.x] = mapa_u32(su32(xh + pu_chunkp(chunk)), threadIdx.x);
         peer[16 + threadIdx.x] = mapa_u32(su32(mlev), threadIdx.x);
     }
-    for (int i = threadIdx.x; i <= L; i += blockDim.x) boff_s[i] = boff[b0 + i];
+    for (int i = threadIdx.x; i <= S; i += blockDim.x) boff_s[i] = boff[s0 + i];
     pdl_wait();   // b is the previous kernel's output (the prologue above reads static plan data only)
-    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[base + i];
+    if (wptr) {   // level-merged sweep: right-hand side W b
+        for (int i = threadIdx.x; i < mine; i += blockDim.x) {
+            double v = 0.0;
+            for (int p = wptr[base + i]; p < wptr[base + i + 1]; ++p) v += wval[p] * b[(size_t)widx[p] * ncomp + comp];
+            xh[i] = v;
+        }
+    } else {
+        for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[(size_t)(base + i) * ncomp + comp];
+    }
     if (dbg && threadIdx.x < 32) { t_w[threadIdx.x] = 0; t_wp[threadIdx.x] = 0; }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
@@ -130,14 +144,15 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[l]), "r"(bytes) : "memory");
     };
     if (threadIdx.x == blockDim.x - 32) {
-        for (int l = 0; l < min(nst - 1, L); ++l) issue(l, l);
-        for (int l = nst - 1; l < min(nst - 1 + l2pf, L); ++l) prefetch(l);
+        for (int l = 0; l < min(nst - 1, S); ++l) issue(l, l);
+        for (int l = nst - 1; l < min(nst - 1 + l2pf, S); ++l) prefetch(l);
     }
     // every CTA's level mbarriers are armed before the first push
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    int slot = 0, islot = nst - 1;
+    int slot = 0, islot = nst - 1, waited = 0;
     unsigned phase = 0;
-    for (int l = 0; l < L; ++l) {
+    for (int st = 0; st < S; ++st) {
+        const int l = st;   // step index (debug timers)
         if (dbg && threadIdx.x == blockDim.x - 32) {
             tA = clock64();
             if (l > 0) {
@@ -151,26 +166,28 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         // group 0 up, so warp 0 (which holds every level's first rows) starts its rows
         // right after the barrier instead of first issuing the next TMA copy
         const bool producer = threadIdx.x == blockDim.x - 32;
+        const unsigned char *blk = ring + (size_t)slot * stage;
         if (producer) {
             mwait(su32(&mring[slot]), phase);
             if (dbg) tB = clock64();
-            if (l > 0) mwait(su32(&mlev[l - 1]), 0);   // every value this CTA reads from level l-1 landed
+            // every value this CTA reads from levels below this step's level landed
+            const int lv = reinterpret_cast<const int4 *>(blk)->w;
+            while (waited < lv) mwait(su32(&mlev[waited++]), 0);
             if (dbg) tC = clock64();
         }
-        __syncthreads();   // ... and its own rows of level l-1 are written
+        __syncthreads();   // ... and its own rows of earlier steps are written
         if (dbg && producer) {
             tD = clock64();
             acc_ring += tB - tA; acc_lev += tC - tB; acc_sync += tD - tC;
         }
         if (producer) {
-            if (l + nst - 1 < L) issue(l + nst - 1, islot);   // the slot of level l-1 is free
-            if (l + nst - 1 + l2pf < L) prefetch(l + nst - 1 + l2pf);
+            if (st + nst - 1 < S) issue(st + nst - 1, islot);   // the slot of step st-1 is free
+            if (st + nst - 1 + l2pf < S) prefetch(st + nst - 1 + l2pf);
         }
-        const unsigned char *blk = ring + (size_t)slot * stage;
         if (++slot == nst) { slot = 0; phase ^= 1u; }
         if (++islot == nst) islot = 0;
         const int4 hd = *reinterpret_cast<const int4 *>(blk);
-        const int nr = hd.x, ne = hd.y;
+        const int nr = hd.x, ne = hd.y, lvl = hd.w;
         const int4 *rows = reinterpret_cast<const int4 *>(blk + 16);
         const double *dg = reinterpret_cast<const double *>(blk + 16 + 16LL * nr);
         const int *code = reinterpret_cast<const int *>(blk + pu_off_code(nr));
@@ -193,7 +210,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 const int dst = (int)((unsigned)pe >> 28);
                 const unsigned sl = (unsigned)pe & 0x0fffffffu;
                 asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
-                             ::"r"(peer[dst] + 8u * sl), "l"(__double_as_longlong(xr)), "r"(peer[16 + dst] + 8u * l)
+                             ::"r"(peer[dst] + 8u * sl), "l"(__double_as_longlong(xr)), "r"(peer[16 + dst] + 8u * lvl)
                              : "memory");
             }
         }
@@ -205,8 +222,9 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         dbg[k * 4 + 0] = acc_ring; dbg[k * 4 + 1] = acc_pre; dbg[k * 4 + 2] = acc_sync; dbg[k * 4 + 3] = acc_comp;
     }
     for (int i = threadIdx.x; i < mine; i += blockDim.x) {
-        x[base + i] = xh[i];
-        if (xout) xout[base + i] = xadd[base + i] + xh[i];
+        const size_t g = (size_t)(base + i) * ncomp + comp;
+        x[g] = xh[i];
+        if (xout) xout[g] = xadd[g] + xh[i];
     }
 }
 
@@ -277,32 +295,29 @@ __global__ void k_pu_lens(int n, const int *perm, const int *ptr, const int *ppt
         plen[q] = pptr[r + 1] - pptr[r];
     }
 }
-__global__ void k_pu_bytes(int nblk, const int *lp, const int *rptr, const int *rpp, long long *bytes) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nblk; i += gridDim.x * blockDim.x) {
-        const int nr = lp[i + 1] - lp[i];
-        const int ne = rptr[lp[i + 1]] - rptr[lp[i]];
-        const int np = rpp[lp[i + 1]] - rpp[lp[i]];
-        bytes[i] = pu_block_bytes(nr, ne, np);
-    }
-}
-__global__ void k_pu_headers(int nblk, const int *lp, const int *rptr, const int *rpp, unsigned char *blocks,
-                             const long long *boff) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nblk; i += gridDim.x * blockDim.x) {
+__global__ void k_pu_headers(int np_, const int *pstart, const int *plev, const int *rptr, const int *rpp,
+                             unsigned char *blocks, const long long *boff) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np_; i += gridDim.x * blockDim.x) {
         int *h = reinterpret_cast<int *>(blocks + boff[i]);
-        h[0] = lp[i + 1] - lp[i];
-        h[1] = rptr[lp[i + 1]] - rptr[lp[i]];
-        h[2] = rpp[lp[i + 1]] - rpp[lp[i]];
-        h[3] = 0;
+        h[0] = pstart[i + 1] - pstart[i];
+        h[1] = rptr[pstart[i + 1]] - rptr[pstart[i]];
+        h[2] = rpp[pstart[i + 1]] - rpp[pstart[i]];
+        h[3] = plev[i];
     }
 }
-__global__ void k_pu_fill(int n, int chunk, int chunkp, const int *skey, const int *perm, const int *lp,
+__global__ void k_pu_fill(int n, int chunk, int chunkp, int np_, const int *pstart, const int *perm,
                           const int *rptr, const int *rpp, const long long *boff, const int *ptr, const int *idx,
                           const double *val, const double *diag, const unsigned long long *h, const int *hstart,
                           const int *pptr, const unsigned long long *k2s, const int *slots, unsigned char *blocks) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
-        const int blk = skey[q];
-        const int q0 = lp[blk], nr = lp[blk + 1] - q0, i = q - q0;
-        const int ne = rptr[lp[blk + 1]] - rptr[q0];
+        int lo = 0, hi = np_;   // part holding sorted row q: last part with pstart <= q
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pstart[mid] <= q) lo = mid; else hi = mid;
+        }
+        const int blk = lo;
+        const int q0 = pstart[blk], nr = pstart[blk + 1] - q0, i = q - q0;
+        const int ne = rptr[pstart[blk + 1]] - rptr[q0];
         unsigned char *B = blocks + boff[blk];
         const int r = perm[q];
         const int owner = r / chunk;
@@ -424,34 +439,66 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     launched(c);
     counts_to_ptr(c, len.p, n, rptr);
     counts_to_ptr(c, plen.p, n, rpp);
-    DBuf<long long> bytes((size_t)nblk + 1, c->s), boff((size_t)nblk + 1, c->s);
-    CK(cudaMemsetAsync(bytes.p + nblk, 0, sizeof(long long), c->s));
-    k_pu_bytes<<<grid_for(nblk, 256, c->sms), 256, 0, c->s>>>(nblk, lp.p, rptr.p, rpp.p, bytes.p);
-    launched(c);
-    {
-        size_t tb = 0;
-        CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, bytes.p, boff.p, nblk + 1, c->s));
-        DBuf<char> t(tb, c->s);
-        CK(cub::DeviceScan::ExclusiveSum(t.p, tb, bytes.p, boff.p, nblk + 1, c->s));
-        launched(c);
-    }
-    std::vector<long long> hb = bytes.to_host();
+    // steps: the non-empty (CTA, level) blocks, each cut into parts of at most `cap` bytes
+    std::vector<int> hlp = lp.to_host(), hr = rptr.to_host(), hp = rpp.to_host();
+    auto part_bytes = [&](int q0, int q1) {
+        return pu_block_bytes(q1 - q0, (long long)hr[q1] - hr[q0], (long long)hp[q1] - hp[q0]);
+    };
+    std::vector<int> pstart, plev, sstart(C + 1, 0);
+    std::vector<long long> pboff;
+    int smax = 0, widest = 1;
     long long mx = 16;
-    for (int i = 0; i < nblk; ++i) mx = std::max(mx, hb[i]);
-    std::vector<int> hlp = lp.to_host();
-    int widest = 1;
-    for (int i = 0; i < nblk; ++i) widest = std::max(widest, hlp[i + 1] - hlp[i]);
-    const size_t fixed = pu_fixed(chunk, L, hmax);
-    if (fixed >= PU_SMEM_LIMIT) return false;
+    bool ok = false;
+    for (int tries = 0; tries < 4 && !ok; ++tries) {
+        const int smax_est = tries == 0 ? L : smax;
+        const size_t fixed = pu_fixed(chunk, L, hmax, smax_est);
+        if (fixed + 2 * 16384 >= PU_SMEM_LIMIT) return false;
+        long long cap = (long long)(PU_SMEM_LIMIT - fixed) / 3;
+        if (cap < 16384) cap = (long long)(PU_SMEM_LIMIT - fixed) / 2;
+        cap &= ~127LL;
+        pstart.clear(); plev.clear(); pboff.assign(1, 0);
+        smax = 0; mx = 16; widest = 1;
+        bool fit = true;
+        for (int d = 0; d < C && fit; ++d) {
+            sstart[d] = (int)plev.size();
+            for (int l = 0; l < L && fit; ++l) {
+                const int a0 = hlp[d * L + l], a1 = hlp[d * L + l + 1];
+                for (int q = a0; q < a1;) {
+                    int e = q + 1;
+                    if (part_bytes(q, e) > cap) { fit = false; break; }
+                    while (e < a1 && part_bytes(q, e + 1) <= cap) ++e;
+                    const long long by = part_bytes(q, e);
+                    pstart.push_back(q); plev.push_back(l); pboff.push_back(pboff.back() + by);
+                    mx = std::max(mx, by);
+                    widest = std::max(widest, e - q);
+                    q = e;
+                }
+            }
+            smax = std::max(smax, (int)plev.size() - sstart[d]);
+        }
+        if (!fit) return false;
+        sstart[C] = (int)plev.size();
+        ok = smax <= smax_est;
+    }
+    if (!ok) return false;
+    const int np_ = (int)plev.size();
+    pstart.push_back(n);
+    const size_t fixed = pu_fixed(chunk, L, hmax, smax);
     const long long stage = (mx + 127) & ~127LL;
     const int nst = (int)std::min<long long>(PU_NST_MAX, (long long)(PU_SMEM_LIMIT - fixed) / stage);
     if (nst < 2) return false;
-    long long total = 0;
-    CK(cudaMemcpyAsync(&total, boff.p + nblk, sizeof(long long), cudaMemcpyDeviceToHost, c->s));
-    CK(cudaStreamSynchronize(c->s));
+    const long long total = pboff.back();
+    DBuf<int> dpstart((size_t)np_ + 1, c->s), dplev((size_t)std::max(np_, 1), c->s);
+    dpstart.upload(pstart.data(), pstart.size());
+    dplev.upload(plev.data(), plev.size());
+    P->sstart.alloc(C + 1, c->s);
+    P->sstart.upload(sstart.data(), sstart.size());
+    P->boff.alloc((size_t)np_ + 1, c->s);
+    P->boff.upload(pboff.data(), pboff.size());
     P->C = C;
     P->chunk = chunk;
     P->L = L;
+    P->smax = smax;
     P->hmax = hmax;
     P->stage = (int)stage;
     P->nst = nst;
@@ -466,17 +513,20 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     if (force_thr) threads = std::min(threads, force_thr);
     P->threads = threads;
     P->blocks.alloc((size_t)total, c->s);
-    P->boff = std::move(boff);
-    k_pu_headers<<<grid_for(nblk, 256, c->sms), 256, 0, c->s>>>(nblk, lp.p, rptr.p, rpp.p, P->blocks.p, P->boff.p);
-    launched(c);
-    k_pu_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, pu_chunkp(chunk), skey.p, perm.p, lp.p, rptr.p, rpp.p, P->boff.p,
-                                                          S.ptr.p, S.idx.p, S.val.p, T.diag.n ? T.diag.p : nullptr,
-                                                          H.p, hstart.p, pptr.p, k2s.p, slots.p, P->blocks.p);
-    launched(c);
+    if (np_) {
+        k_pu_headers<<<grid_for(np_, 256, c->sms), 256, 0, c->s>>>(np_, dpstart.p, dplev.p, rptr.p, rpp.p,
+                                                                   P->blocks.p, P->boff.p);
+        launched(c);
+        k_pu_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, pu_chunkp(chunk), np_, dpstart.p, perm.p,
+                                                              rptr.p, rpp.p, P->boff.p, S.ptr.p, S.idx.p, S.val.p,
+                                                              T.diag.n ? T.diag.p : nullptr, H.p, hstart.p, pptr.p,
+                                                              k2s.p, slots.p, P->blocks.p);
+        launched(c);
+    }
     CK(cudaStreamSynchronize(c->s));
     if (TraceScope::on())
-        std::fprintf(stderr, "[dpp-trace]   push_plan n=%d C=%d L=%d G=%d thr=%d halo max %d (pairs %d) stage=%lld nst=%d\n",
-                     n, C, L, P->G, threads, hmax, nh, stage, nst);
+        std::fprintf(stderr, "[dpp-trace]   push_plan n=%d C=%d L=%d steps max %d G=%d thr=%d halo max %d (pairs %d) stage=%lld nst=%d\n",
+                     n, C, L, smax, P->G, threads, hmax, nh, stage, nst);
     T.pu = std::move(P);
     return true;
 }
@@ -510,9 +560,9 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
                cudaStream_t st) {
     const PushPlan &P = *T.pu;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(P.C, 1, 1);
+    cfg.gridDim = dim3(P.C * T.ncomp, 1, 1);
     cfg.blockDim = dim3(P.threads, 1, 1);
-    cfg.dynamicSmemBytes = pu_fixed(P.chunk, P.L, P.hmax) + (size_t)P.nst * P.stage;
+    cfg.dynamicSmemBytes = pu_fixed(P.chunk, P.L, P.hmax, P.smax) + (size_t)P.nst * P.stage;
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -532,13 +582,15 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
         CK(cudaMallocAsync((void **)&dbg, sizeof(unsigned long long) * 4 * P.C, st));
         CK(cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 4 * P.C, st));
     }
+    const int *wp = T.W.rows ? (const int *)T.W.ptr.p : nullptr, *wi = T.W.rows ? (const int *)T.W.idx.p : nullptr;
+    const double *wv = T.W.rows ? (const double *)T.W.val.p : nullptr;
     cudaError_t e;
     switch (P.G) {
-        case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_push<2>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
-        case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_push<4>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
-        case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_push<8>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
-        case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_push<16>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
-        default: e = cudaLaunchKernelEx(&cfg, k_trsv_push<32>, T.n, P.chunk, P.L, P.hmax, P.stage, P.nst, B, O, (const int *)P.tx.p, b, x, xadd, xout, l2pf, dbg); break;
+        case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_push<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, (const int *)P.tx.p, wp, wi, wv, b, x, xadd, xout, l2pf, dbg); break;
+        case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_push<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, (const int *)P.tx.p, wp, wi, wv, b, x, xadd, xout, l2pf, dbg); break;
+        case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_push<8>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, (const int *)P.tx.p, wp, wi, wv, b, x, xadd, xout, l2pf, dbg); break;
+        case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_push<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, (const int *)P.tx.p, wp, wi, wv, b, x, xadd, xout, l2pf, dbg); break;
+        default: e = cudaLaunchKernelEx(&cfg, k_trsv_push<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, (const int *)P.tx.p, wp, wi, wv, b, x, xadd, xout, l2pf, dbg); break;
     }
     CK(e);
     launched(c);

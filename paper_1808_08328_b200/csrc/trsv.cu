@@ -304,6 +304,10 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
           double *xout, cudaStream_t st) {
     st = st ? st : c->s;
     if (T.n == 0) return;
+    if (T.W.rows && !T.pu) {   // level-merged form: sweep on W b (the push sweep folds W in)
+        spmv(c, T.W, b, T.wb.p, nullptr, 1.0, st);
+        b = T.wb.p;
+    }
     if (T.dense.n) {
         CK(launch_pdl(k_tri_gemv, dim3(grid_for((int64_t)T.n * 32, 256, c->sms, 8)), dim3(256), 0, st, T.n,
                       (int)T.backward, (const double *)T.dense.p, b, x, xadd, xout));
@@ -335,6 +339,169 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
     launched(c);
 }
 
+// ------------------------------------------------------------------ level merging
+// Exact-arithmetic rewrite of a level-scheduled sweep: consecutive
+// dependency levels are grouped m at a time.  With T = D + L_in + L_out (L_in: entries
+// inside a group, L_out: entries on earlier groups) and N = D^-1 L_in (nilpotent,
+// N^m = 0 inside a group),
+//     x = T^-1 b  <=>  x = W b - Z x,   W = (I + N)^-1 D^-1,   Z = (I + N)^-1 D^-1 L_out,
+// with (I + N)^-1 = sum_{k<m} (-N)^k evaluated by Horner (Z <- Z0 - N Z).  Z only
+// references earlier groups, so the sweep has at most ceil(levels / m) dependent
+// steps at the price of a wider Z; W b is one parallel SpMV ahead of the sweep.
+// Results differ from the sequential substitution by rounding only.
+__global__ void k_group_count(int n, const int *__restrict__ ptr, const int *__restrict__ idx,
+                              const int *__restrict__ lev, int m, int same, int *cnt) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int g = lev[r] / m;
+        int k = 0;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) k += ((lev[idx[p]] / m) == g) == (same != 0);
+        cnt[r] = k;
+    }
+}
+__global__ void k_group_fill(int n, const int *__restrict__ ptr, const int *__restrict__ idx,
+                             const double *__restrict__ val, const int *__restrict__ lev, int m, int same,
+                             const double *__restrict__ dinv, const int *__restrict__ optr, int *oidx,
+                             double *oval) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int g = lev[r] / m;
+        const double s = dinv ? dinv[r] : 1.0;
+        int w = optr[r];
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p)
+            if (((lev[idx[p]] / m) == g) == (same != 0)) { oidx[w] = idx[p]; oval[w] = val[p] * s; ++w; }
+    }
+}
+__global__ void k_diag_csr(int n, const double *__restrict__ d, int *ptr, int *idx, double *val) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += gridDim.x * blockDim.x) {
+        ptr[r] = r;
+        if (r < n) { idx[r] = r; val[r] = d ? 1.0 / d[r] : 1.0; }
+    }
+}
+
+static Csr group_part(Ctx *c, const Csr &S, const int *lev, int m, bool same, const double *dinv) {
+    const int n = S.rows;
+    DBuf<int> cnt(n, c->s);
+    k_group_count<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, S.ptr.p, S.idx.p, lev, m, same, cnt.p);
+    launched(c);
+    Csr B;
+    B.rows = n;
+    B.cols = S.cols;
+    B.nnz = counts_to_ptr(c, cnt.p, n, B.ptr);
+    B.idx.alloc(B.nnz, c->s);
+    B.val.alloc(B.nnz, c->s);
+    k_group_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, S.ptr.p, S.idx.p, S.val.p, lev, m, same, dinv,
+                                                             B.ptr.p, B.idx.p, B.val.p);
+    launched(c);
+    return B;
+}
+
+__global__ void k_recip_tri(int n, const double *d, double *o) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) o[r] = 1.0 / d[r];
+}
+
+static int merge_levels(Ctx *c, Tri &T, DBuf<int> &lev, int m) {
+    const int n = T.n;
+    DBuf<double> dinv;
+    if (T.diag.n) {
+        dinv.alloc(n, c->s);
+        k_recip_tri<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, T.diag.p, dinv.p);
+        launched(c);
+    }
+    const double *di = T.diag.n ? dinv.p : nullptr;
+    Csr N = group_part(c, T.strict, lev.p, m, true, di);     // D^-1 L_in
+    Csr Z0 = group_part(c, T.strict, lev.p, m, false, di);   // D^-1 L_out
+    Csr W0;
+    W0.alloc(n, n, n, c->s);
+    k_diag_csr<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(n, T.diag.n ? T.diag.p : nullptr, W0.ptr.p, W0.idx.p,
+                                                               W0.val.p);
+    launched(c);
+    Csr Z = csr_copy(c, Z0), W = csr_copy(c, W0);
+    if (N.nnz)
+        for (int k = 1; k < m; ++k) {
+            Z = spgemm(c, N, Z, nullptr, false, &Z0);
+            W = spgemm(c, N, W, nullptr, false, &W0);
+        }
+    T.nnz_alg = T.strict.nnz;
+    T.strict = std::move(Z);
+    T.diag.release();
+    T.W = std::move(W);
+    spmv_plan(c, T.W);
+    T.wb.alloc(n, c->s);
+    return tri_levels(c, T.strict, T.backward, T.order, nullptr, &lev);
+}
+
+// ------------------------------------------------------------------ Kronecker triangles
+// The velocity blocks of the VMS formulations are c M (x) I_dim with interleaved
+// components (assembly.py:339); ILU(0) keeps the cross-component entries exactly zero,
+// so each factor (zero-free) is T_s (x) I_dim with the same values in every component.
+// Such a triangle is swept as dim independent copies of T_s -- one cluster each, one
+// schedule, identical arithmetic per component.
+__global__ void k_kron_check(int n, int d, const int *__restrict__ ptr, const int *__restrict__ idx,
+                             const double *__restrict__ val, const double *__restrict__ diag, int *bad) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int c = r % d, r0 = r - c;
+        bool ok = true;
+        if (c == 0) {
+            for (int p = ptr[r]; p < ptr[r + 1]; ++p) ok &= idx[p] % d == 0;
+        } else {
+            const int a = ptr[r], a0 = ptr[r0], len = ptr[r + 1] - a;
+            ok = len == ptr[r0 + 1] - a0;
+            for (int k = 0; ok && k < len; ++k)
+                ok = idx[a + k] == idx[a0 + k] + c && __double_as_longlong(val[a + k]) == __double_as_longlong(val[a0 + k]);
+            if (diag) ok &= __double_as_longlong(diag[r]) == __double_as_longlong(diag[r0]);
+        }
+        if (!ok) atomicAdd(bad, 1);
+    }
+}
+__global__ void k_kron_count(int ns, int d, const int *ptr, int *cnt) {
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < ns; a += gridDim.x * blockDim.x)
+        cnt[a] = ptr[a * d + 1] - ptr[a * d];
+}
+__global__ void k_kron_fill(int ns, int d, const int *ptr, const int *idx, const double *val, const double *diag,
+                            const int *optr, int *oidx, double *oval, double *odiag) {
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < ns; a += gridDim.x * blockDim.x) {
+        int w = optr[a];
+        for (int p = ptr[a * d]; p < ptr[a * d + 1]; ++p, ++w) { oidx[w] = idx[p] / d; oval[w] = val[p]; }
+        if (diag) odiag[a] = diag[a * d];
+    }
+}
+// largest d in {3, 2} with T = T_s (x) I_d, else 1
+static int kron_detect(Ctx *c, const Tri &T) {
+    for (int d = 3; d >= 2; --d) {
+        if (T.n % d) continue;
+        DBuf<int> bad(1, c->s);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), c->s));
+        k_kron_check<<<grid_for(T.n, 256, c->sms), 256, 0, c->s>>>(T.n, d, T.strict.ptr.p, T.strict.idx.p,
+                                                                  T.strict.val.p, T.diag.n ? T.diag.p : nullptr, bad.p);
+        launched(c);
+        if (bad.to_host()[0] == 0) return d;
+    }
+    return 1;
+}
+static Tri kron_scalar(Ctx *c, const Tri &T, int d) {
+    Tri S;
+    const int ns = T.n / d;
+    S.n = ns;
+    S.backward = T.backward;
+    DBuf<int> cnt(ns, c->s);
+    k_kron_count<<<grid_for(ns, 256, c->sms), 256, 0, c->s>>>(ns, d, T.strict.ptr.p, cnt.p);
+    launched(c);
+    S.strict.rows = S.strict.cols = ns;
+    S.strict.nnz = counts_to_ptr(c, cnt.p, ns, S.strict.ptr);
+    S.strict.idx.alloc(S.strict.nnz, c->s);
+    S.strict.val.alloc(S.strict.nnz, c->s);
+    if (T.diag.n) S.diag.alloc(ns, c->s);
+    k_kron_fill<<<grid_for(ns, 256, c->sms), 256, 0, c->s>>>(ns, d, T.strict.ptr.p, T.strict.idx.p, T.strict.val.p,
+                                                            T.diag.n ? T.diag.p : nullptr, S.strict.ptr.p,
+                                                            S.strict.idx.p, S.strict.val.p, S.diag.p);
+    launched(c);
+    return S;
+}
+
+static int merge_factor() {
+    static const int m = [] { const char *e = std::getenv("DPP_MERGE"); return e ? std::atoi(e) : 1; }();
+    return m;
+}
+
 Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf<int> *pre_order,
              DBuf<int> *pre_lev, int pre_nlev) {
     Tri T;
@@ -363,6 +530,27 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf
         T.nlev = T.bd->nb;
         return T;
     }
+    static const bool kron_on = [] { const char *e = std::getenv("DPP_KRON"); return !(e && *e == '0'); }();
+    if (kron_on && !pre_lev && T.n > 2 * 8192) {
+        const int d = kron_detect(c, T);
+        if (d > 1) {
+            Tri S = kron_scalar(c, T, d);
+            DBuf<int> slev;
+            S.nlev = tri_levels(c, S.strict, S.backward, S.order, nullptr, &slev);
+            const int before = S.nlev;
+            const int m = merge_factor();
+            if (m > 1 && S.nlev >= 4 * m) S.nlev = merge_levels(c, S, slev, m);
+            if (push_plan(c, S, slev, S.nlev)) {
+                if (TraceScope::on())
+                    std::fprintf(stderr, "[dpp-trace]   make_tri kron d=%d n=%d levels %d -> %d strict nnz %lld (x%d)\n", d,
+                                 S.n, before, S.nlev, (long long)S.strict.nnz, d);
+                S.ncomp = d;
+                S.n = T.n;
+                S.nnz_alg = T.strict.nnz;
+                return S;
+            }
+        }
+    }
     DBuf<int> lev;
     if (pre_lev) {   // the caller's analysis covers every dependency of this triangle
         T.order = std::move(*pre_order);
@@ -370,6 +558,15 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf
         T.nlev = pre_nlev;
     } else {
         T.nlev = tri_levels(c, T.strict, T.backward, T.order, nullptr, &lev);
+    }
+    // wide, deep triangles (ILU factors, AMG level 0): merge levels m at a time
+    const int merge = merge_factor();
+    if (merge > 1 && T.n > 8192 && T.nlev >= 4 * merge) {
+        const int before = T.nlev;
+        T.nlev = merge_levels(c, T, lev, merge);
+        if (TraceScope::on())
+            std::fprintf(stderr, "[dpp-trace]   merge_levels m=%d levels %d -> %d, strict nnz %lld -> %lld, W nnz %lld\n",
+                         merge, before, T.nlev, (long long)T.nnz_alg, (long long)T.strict.nnz, (long long)T.W.nnz);
     }
     // narrow, deep levels (coarse AMG): block-sequential sweep with dense block inverses
     static const bool no_block = [] { const char *e = std::getenv("DPP_NO_BLOCK"); return e && *e == '1'; }();
@@ -460,20 +657,15 @@ __global__ void __launch_bounds__(32 * ILU_WPB) k_ilu0(int n, const int *__restr
     }
 }
 
-std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
-    DPP_TRACE_SCOPE(c, "ilu0.total");
-    if (A.rows != A.cols) DPP_FAIL(DPP_ERR_VALUE, "ilu0 requires a square matrix");
-    auto f = std::make_unique<Ilu>();
-    f->ctx = c;
-    f->n = A.rows;
-    f->LU = csr_copy(c, A);
-    const int n = A.rows;
+// In-place ILU(0) of LU (IKJ order, linalg.py:178-222); returns the failing row or -1.
+static int ilu_factor(Ctx *c, Csr &LU) {
+    const int n = LU.rows;
     DBuf<int> dpos(n, c->s), flags((size_t)n + 3, c->s);
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int) * (n + 3), c->s));
     int *missing = flags.p + n, *ticket = flags.p + n + 1, *err = flags.p + n + 2;
     CK(cudaMemsetAsync(err, 0x7f, sizeof(int), c->s));
     if (n) {
-        k_diag_pos<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, dpos.p, missing);
+        k_diag_pos<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, LU.ptr.p, LU.idx.p, dpos.p, missing);
         launched(c);
     }
     int hm = 0;
@@ -482,20 +674,136 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
     if (hm) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "missing diagonal entry in sparsity pattern");
     DBuf<int> order;
     {
-        Csr lower = csr_part(c, A, -1, false);   // stored pattern: every row the IKJ loop may read
+        Csr lower = csr_part(c, LU, -1, false);   // stored pattern: every row the IKJ loop may read
         tri_levels(c, lower, false, order);
     }
     DPP_TRACE_SCOPE(c, "ilu0.factor_kernel");
     if (n) {
         const int warps = std::min<int64_t>(n, (int64_t)c->sms * 8);
         k_ilu0<<<(warps + ILU_WPB - 1) / ILU_WPB, 32 * ILU_WPB, 0, c->s>>>(
-            n, f->LU.ptr.p, f->LU.idx.p, f->LU.val.p, dpos.p, flags.p, ticket, err, order.p);
+            n, LU.ptr.p, LU.idx.p, LU.val.p, dpos.p, flags.p, ticket, err, order.p);
         launched(c);
     }
     int he = 0;
     CK(cudaMemcpyAsync(&he, err, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
-    if (he != 0x7f7f7f7f) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(he));
+    return he != 0x7f7f7f7f ? he : -1;
+}
+
+// Kronecker ILU(0): when A = M (x) I_d on the node-blocked pattern (every cross-component
+// entry stored as +0, assembly.py:339), the IKJ loop never updates across components
+// (l_ik = 0 is skipped, a_kj = 0 leaves a_ij unchanged and +0), so the factor is the
+// ILU(0) of M in every component and +0 on every cross entry: bitwise the full
+// factorization at 1/d the rows and 1/d^2 the entries.
+__device__ __forceinline__ int row_find(const int *idx, int a, int e, int j) {
+    while (a < e) {
+        const int m = (a + e) >> 1;
+        if (idx[m] < j) a = m + 1; else e = m;
+    }
+    return a;
+}
+__global__ void k_ilu_kron_check(int n, int d, const int *__restrict__ ptr, const int *__restrict__ idx,
+                                 const double *__restrict__ val, const int *__restrict__ mp, const int *__restrict__ mi,
+                                 const double *__restrict__ mv, int *bad) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int a = r / d, c = r % d, m0 = mp[a], m1 = mp[a + 1];
+        int same = 0;
+        bool ok = true;
+        for (int p = ptr[r]; ok && p < ptr[r + 1]; ++p) {
+            const int j = idx[p];
+            if (j % d == c) {
+                const int q = row_find(mi, m0, m1, j / d);
+                ok = q < m1 && mi[q] == j / d && __double_as_longlong(mv[q]) == __double_as_longlong(val[p]);
+                ++same;
+            } else {
+                ok = __double_as_longlong(val[p]) == 0;
+            }
+        }
+        if (!ok || same != m1 - m0) atomicAdd(bad, 1);
+    }
+}
+__global__ void k_ilu_kron_expand(int n, int d, const int *__restrict__ ptr, const int *__restrict__ idx,
+                                  const int *__restrict__ mp, const int *__restrict__ mi, const double *__restrict__ mv,
+                                  double *val) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+        const int a = r / d, c = r % d;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
+            const int j = idx[p];
+            val[p] = j % d == c ? mv[row_find(mi, mp[a], mp[a + 1], j / d)] : 0.0;
+        }
+    }
+}
+__global__ void k_comp0_count(int ns, int d, const int *ptr, const int *idx, int *cnt) {
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < ns; a += gridDim.x * blockDim.x) {
+        int k = 0;
+        for (int p = ptr[a * d]; p < ptr[a * d + 1]; ++p) k += idx[p] % d == 0;
+        cnt[a] = k;
+    }
+}
+__global__ void k_comp0_fill(int ns, int d, const int *ptr, const int *idx, const double *val, const int *optr,
+                             int *oidx, double *oval) {
+    for (int a = blockIdx.x * blockDim.x + threadIdx.x; a < ns; a += gridDim.x * blockDim.x) {
+        int w = optr[a];
+        for (int p = ptr[a * d]; p < ptr[a * d + 1]; ++p)
+            if (idx[p] % d == 0) { oidx[w] = idx[p] / d; oval[w] = val[p]; ++w; }
+    }
+}
+// M from the component-0 rows / columns of A, if A = M (x) I_d (else M.rows = 0)
+static Csr kron_block(Ctx *c, const Csr &A) {
+    Csr M;
+    static const bool on = [] { const char *e = std::getenv("DPP_KRON"); return !(e && *e == '0'); }();
+    if (!on || A.rows < 2 * 8192) return M;
+    for (int d = 3; d >= 2; --d) {
+        if (A.rows % d) continue;
+        const int ns = A.rows / d;
+        DBuf<int> cnt(ns, c->s);
+        k_comp0_count<<<grid_for(ns, 256, c->sms), 256, 0, c->s>>>(ns, d, A.ptr.p, A.idx.p, cnt.p);
+        launched(c);
+        Csr B;
+        B.rows = B.cols = ns;
+        B.nnz = counts_to_ptr(c, cnt.p, ns, B.ptr);
+        B.idx.alloc(B.nnz, c->s);
+        B.val.alloc(B.nnz, c->s);
+        k_comp0_fill<<<grid_for(ns, 256, c->sms), 256, 0, c->s>>>(ns, d, A.ptr.p, A.idx.p, A.val.p, B.ptr.p, B.idx.p,
+                                                                 B.val.p);
+        launched(c);
+        DBuf<int> bad(1, c->s);
+        CK(cudaMemsetAsync(bad.p, 0, sizeof(int), c->s));
+        k_ilu_kron_check<<<grid_for(A.rows, 256, c->sms), 256, 0, c->s>>>(A.rows, d, A.ptr.p, A.idx.p, A.val.p,
+                                                                          B.ptr.p, B.idx.p, B.val.p, bad.p);
+        launched(c);
+        if (bad.to_host()[0] == 0) return B;
+    }
+    return M;
+}
+
+std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
+    DPP_TRACE_SCOPE(c, "ilu0.total");
+    if (A.rows != A.cols) DPP_FAIL(DPP_ERR_VALUE, "ilu0 requires a square matrix");
+    auto f = std::make_unique<Ilu>();
+    f->ctx = c;
+    f->n = A.rows;
+    f->LU = csr_copy(c, A);
+    const int n = A.rows;
+    Csr M = kron_block(c, A);
+    if (M.rows) {
+        const int d = n / M.rows;
+        {   // a missing diagonal in any component is one in component 0 (same pattern)
+            DBuf<int> dpos(n, c->s), missing(1, c->s);
+            CK(cudaMemsetAsync(missing.p, 0, sizeof(int), c->s));
+            k_diag_pos<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, dpos.p, missing.p);
+            launched(c);
+            if (missing.to_host()[0]) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "missing diagonal entry in sparsity pattern");
+        }
+        const int bad = ilu_factor(c, M);
+        if (bad >= 0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(bad * d));
+        k_ilu_kron_expand<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d, A.ptr.p, A.idx.p, M.ptr.p, M.idx.p,
+                                                                      M.val.p, f->LU.val.p);
+        launched(c);
+    } else {
+        const int bad = ilu_factor(c, f->LU);
+        if (bad >= 0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(bad));
+    }
     // (the factorization's levels follow the STORED pattern, explicit zeros included:
     // 363 levels on C2 against 121 for L's zero-free pattern, so L gets its own analysis)
     f->L = make_tri(c, f->LU, true, true);

@@ -151,7 +151,11 @@ def test_ilu0_errors():
 
 @pytest.mark.parametrize("form,dim,kind,n", [("cgvms", 2, "tri", 6), ("hdiv", 2, "tri", 6),
                                              ("dgvms", 2, "tri", 3), ("cgvms", 3, "tet", 3),
-                                             ("cgvms", 3, "hex", 3), ("dgvms", 3, "tet", 2)])
+                                             ("cgvms", 3, "hex", 3), ("dgvms", 3, "tet", 2),
+                                             # >= 16384 velocity rows: Kronecker factorization
+                                             # and component-parallel sweeps (M (x) I_dim)
+                                             ("cgvms", 3, "tet", 18), ("cgvms", 2, "tri", 95),
+                                             ("dgvms", 3, "tet", 7)])
 def test_ilu0_factors_bitwise_and_apply(form, dim, kind, n, rng):
     bs, obs = systems(form, dim, kind, n)
     # same input -> bitwise factors (same IKJ order, separate mul/sub)
