@@ -133,15 +133,19 @@ __global__ void k_recip(int n, const double *d, double *o) {
 
 // M = diag(dinv) @ A  (row scaling, exact products)
 __global__ void k_rowscale(int rows, const int *ptr, const double *val, const double *dinv, double *o) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
-        for (int p = ptr[r]; p < ptr[r + 1]; ++p) o[p] = __dmul_rn(dinv[r], val[p]);
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const double d = dinv[r];
+        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32) o[p] = __dmul_rn(d, val[p]);
+    }
 }
 
 static double spectral_radius(Ctx *c, const Csr &A, const double *dinv, dpp_randn_fn randn,
                               void *user) {
     const int n = A.rows;
     Csr M = csr_copy(c, A);
-    k_rowscale<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, M.ptr.p, A.val.p, dinv, M.val.p);
+    k_rowscale<<<grid_for((int64_t)n * 32, 256, c->sms, 8), 256, 0, c->s>>>(n, M.ptr.p, A.val.p, dinv, M.val.p);
     launched(c);
     std::vector<double> x0(n);
     if (!randn) DPP_FAIL(DPP_ERR_VALUE, "amg_setup needs the power-iteration start vector callback");

@@ -517,21 +517,31 @@ int64_t csr_count_nonzero(Ctx *c, const Csr &A) {
     return B.nnz;
 }
 
+// rows are sorted and duplicate-free here (canonical CSR), so the diagonal is one
+// entry: a warp per row finds it with one ballot
 __global__ void k_diag(int rows, const int *ptr, const int *idx, const double *val, double *d,
                        int *missing) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
         double v = 0.0;
         bool found = false;
-        for (int p = ptr[r]; p < ptr[r + 1]; ++p)
+        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32)
             if (idx[p] == r) { v += val[p]; found = true; }
-        d[r] = v;
-        if (!found && missing) atomicAdd(missing, 1);
+        for (int o = 16; o > 0; o >>= 1) {
+            v += __shfl_xor_sync(0xffffffffu, v, o);
+            found |= __shfl_xor_sync(0xffffffffu, (int)found, o);
+        }
+        if (lane == 0) {
+            d[r] = v;
+            if (!found && missing) atomicAdd(missing, 1);
+        }
     }
 }
 void csr_diag(Ctx *c, const Csr &A, double *d, int *missing) {
     int n = std::min(A.rows, A.cols);
     if (!n) return;
-    k_diag<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, d, missing);
+    k_diag<<<grid_for((int64_t)n * 32, 256, c->sms, 8), 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, d, missing);
     launched(c);
 }
 

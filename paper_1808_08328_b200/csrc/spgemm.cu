@@ -61,8 +61,8 @@ struct Args {
 // is taken 32 entries at a time (k, scaled a_ik, B-row bounds in lane registers);
 // each k's B row is held in registers (up to PF x 32 entries) and the NEXT k's
 // row is loaded while the current one is accumulated.
-constexpr int PF = 4;
-template <typename Upd>
+constexpr int PF_HASH = 4;
+template <int PF, typename Upd>
 __device__ __forceinline__ void accumulate_row(const Args &a, int64_t row, int lane, Upd &&upd) {
     const int s = a.ap[row], e = a.ap[row + 1], len = e - s;
     for (int q0 = 0; q0 < len; q0 += 32) {
@@ -105,9 +105,20 @@ __device__ __forceinline__ void accumulate_row(const Args &a, int64_t row, int l
 #pragma unroll
                 for (int u = 0; u < PF; ++u)
                     if (cj[u] >= 0 && cb[u] != 0.0) upd(cj[u], __dmul_rn(av, cb[u]));
-                for (int r = rs + 32 * PF + lane; r < re; r += 32) {
-                    const double bv = a.bv[r];
-                    if (bv != 0.0) upd(a.bi[r], __dmul_rn(av, bv));
+                // long B rows (dense coarse products): 4 x 32 entries in flight per batch;
+                // every (k, j) pair is unique, so the per-j accumulation order stays k-ordered
+                for (int r0 = rs + 32 * PF; r0 < re; r0 += 32 * 4) {
+                    int bj[4];
+                    double bb[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int r = r0 + 32 * u + lane;
+                        bj[u] = r < re ? a.bi[r] : -1;
+                        bb[u] = r < re ? a.bv[r] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (bj[u] >= 0 && bb[u] != 0.0) upd(bj[u], __dmul_rn(av, bb[u]));
                 }
                 __syncwarp();
             }
@@ -265,7 +276,7 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             }
             __syncwarp();
         }
-        accumulate_row(a, row, lane, [&](int j, double pr) {
+        accumulate_row<PF_HASH>(a, row, lane, [&](int j, double pr) {
             const int sl = tab_slot(t, j);
             if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
             else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
@@ -333,6 +344,7 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
 // levels): each warp owns acc[ncols] + presence flags in shared memory; the
 // survivors come out in column order (no sort), written to the scratch at
 // toff[row] (= row * ncols).
+template <int PFD>
 __global__ void k_spgemm_dense(Args a, int ncols, int W) {
     extern __shared__ unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -350,7 +362,7 @@ __global__ void k_spgemm_dense(Args a, int ncols, int W) {
             }
             __syncwarp();
         }
-        accumulate_row(a, row, lane, [&](int j, double pr) {
+        accumulate_row<PFD>(a, row, lane, [&](int j, double pr) {
             if (has[j] & 1) acc[j] = __dadd_rn(acc[j], pr);
             else { acc[j] = __dadd_rn(0.0, pr); has[j] |= 1; }
         });
@@ -461,9 +473,15 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         const int W = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / per));
         static bool dattr = false;
         if (!dattr) {
-            CK(cudaFuncSetAttribute(k_spgemm_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            for (const void *f : {(const void *)k_spgemm_dense<4>, (const void *)k_spgemm_dense<8>,
+                                  (const void *)k_spgemm_dense<16>})
+                CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             dattr = true;
         }
+        // B rows held in registers (and prefetched one k ahead): sized to ~1.5x the mean
+        // B row so long coarse rows do not fall back to unprefetched batches
+        const double bavg = (double)B.nnz / std::max(1, B.rows);
+        const int pfd = bavg * 1.5 > 256 ? 16 : bavg * 1.5 > 128 ? 8 : 4;
         ti.alloc((size_t)rows * ncols, c->s);
         tv.alloc((size_t)rows * ncols, c->s);
         a.ti = ti.p;
@@ -472,7 +490,9 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         launched(c);
         a.toff = toff.p;
         const int grid = std::max(1, std::min<int>((rows + W - 1) / W, c->sms * 4));
-        k_spgemm_dense<<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
+        if (pfd == 16) k_spgemm_dense<16><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
+        else if (pfd == 8) k_spgemm_dense<8><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
+        else k_spgemm_dense<4><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
         launched(c);
     } else {
         // 1. symbolic: distinct columns per row

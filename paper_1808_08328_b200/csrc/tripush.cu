@@ -47,6 +47,11 @@ __device__ __forceinline__ unsigned mapa_u32(unsigned a, int rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     return r;
 }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 // bounded wait: a miscounted exchange traps (~2 s) instead of hanging the device
 __device__ __forceinline__ void mwait(unsigned a, unsigned parity) {
     unsigned ok = 0;
@@ -88,8 +93,10 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout, int l2pf,
                 unsigned long long *dbg) {
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ unsigned long long t_w[32], t_wp[32];
-    unsigned long long acc_ring = 0, acc_lev = 0, acc_sync = 0, acc_comp = 0, acc_pre = 0, tA = 0, tB = 0, tC = 0, tD = 0;
+    // debug timeline (DPP_PU_DEBUG): per step {level, rows, t ring landed, t levels landed,
+    // t barrier passed, t last row pushed} in %globaltimer ns, row [cta][step] of dbg
+    __shared__ unsigned long long t_done[2];
+    unsigned long long tB = 0, tC = 0;
     unsigned long long *mring = reinterpret_cast<unsigned long long *>(smem);
     unsigned long long *mlev = mring + PU_NST_MAX;
     double *xh = reinterpret_cast<double *>(smem + 8 * PU_NST_MAX + p16(8LL * L));
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     } else {
         for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[(size_t)(base + i) * ncomp + comp];
     }
-    if (dbg && threadIdx.x < 32) { t_w[threadIdx.x] = 0; t_wp[threadIdx.x] = 0; }
+    if (dbg && threadIdx.x < 2) t_done[threadIdx.x] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     auto issue = [&](int l, int s) {
@@ -152,16 +159,6 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     int slot = 0, islot = nst - 1, waited = 0;
     unsigned phase = 0;
     for (int st = 0; st < S; ++st) {
-        const int l = st;   // step index (debug timers)
-        if (dbg && threadIdx.x == blockDim.x - 32) {
-            tA = clock64();
-            if (l > 0) {
-                unsigned long long m1 = 0, m2 = 0;
-                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { m1 = max(m1, t_w[w]); m2 = max(m2, t_wp[w]); }
-                if (m1 > tD) acc_comp += m1 - tD;   // level l-1: sync exit -> last warp pushed
-                if (m2 > tD) acc_pre += m2 - tD;    // level l-1: sync exit -> last warp computed
-            }
-        }
         // the producer is lane 0 of the LAST warp: rows are dealt to lane groups from
         // group 0 up, so warp 0 (which holds every level's first rows) starts its rows
         // right after the barrier instead of first issuing the next TMA copy
@@ -169,16 +166,19 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         const unsigned char *blk = ring + (size_t)slot * stage;
         if (producer) {
             mwait(su32(&mring[slot]), phase);
-            if (dbg) tB = clock64();
+            if (dbg) tB = gtimer();
             // every value this CTA reads from levels below this step's level landed
             const int lv = reinterpret_cast<const int4 *>(blk)->w;
             while (waited < lv) mwait(su32(&mlev[waited++]), 0);
-            if (dbg) tC = clock64();
+            if (dbg) tC = gtimer();
         }
         __syncthreads();   // ... and its own rows of earlier steps are written
         if (dbg && producer) {
-            tD = clock64();
-            acc_ring += tB - tA; acc_lev += tC - tB; acc_sync += tD - tC;
+            unsigned long long *o = dbg + ((size_t)blockIdx.x * smax + st) * 6;
+            o[0] = reinterpret_cast<const int4 *>(blk)->w;
+            o[1] = reinterpret_cast<const int4 *>(blk)->x;
+            o[2] = tB; o[3] = tC; o[4] = gtimer();
+            if (st > 0) { dbg[((size_t)blockIdx.x * smax + st - 1) * 6 + 5] = t_done[(st - 1) & 1]; t_done[(st - 1) & 1] = 0; }
         }
         if (producer) {
             if (st + nst - 1 < S) issue(st + nst - 1, islot);   // the slot of step st-1 is free
@@ -203,7 +203,6 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
             const double xr = (xh[R.x] - sum) * dq;   // dq = 1/t_ii (as SuperLU's pre-scaled solve)
             __syncwarp(gmask);
             if (gl == 0) xh[R.x] = xr;
-            if (dbg && lane == 0) t_wp[threadIdx.x >> 5] = clock64();
             const int p0 = R.w >> 4, pc = R.w & 15;
             for (int u = gl; u < pc; u += G) {
                 const int pe = pl[p0 + u];
@@ -214,13 +213,11 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                              : "memory");
             }
         }
-        if (dbg) { __syncwarp(); if (lane == 0) t_w[threadIdx.x >> 5] = clock64(); }
+        if (dbg) { __syncwarp(); if (lane == 0) atomicMax(&t_done[st & 1], gtimer()); }
     }
     __syncthreads();
     pdl_trigger();   // the dependent kernel's launch overlaps the x write-out below
-    if (dbg && threadIdx.x == blockDim.x - 32) {
-        dbg[k * 4 + 0] = acc_ring; dbg[k * 4 + 1] = acc_pre; dbg[k * 4 + 2] = acc_sync; dbg[k * 4 + 3] = acc_comp;
-    }
+    if (dbg && threadIdx.x == blockDim.x - 32 && S > 0) dbg[((size_t)blockIdx.x * smax + S - 1) * 6 + 5] = t_done[(S - 1) & 1];
     for (int i = threadIdx.x; i < mine; i += blockDim.x) {
         const size_t g = (size_t)(base + i) * ncomp + comp;
         x[g] = xh[i];
@@ -576,11 +573,12 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     const unsigned char *B = P.blocks.p;
     const long long *O = P.boff.p;
     static const int l2pf = [] { const char *e = std::getenv("DPP_PU_NOPF"); return e && *e == '1' ? 0 : 4; }();
-    static const bool dbg_on = [] { const char *e = std::getenv("DPP_PU_DEBUG"); return e && *e == '1'; }();
+    static const char *dbg_path = std::getenv("DPP_PU_DEBUG");
+    const size_t nd = (size_t)P.C * T.ncomp * std::max(P.smax, 1) * 6;
     unsigned long long *dbg = nullptr;
-    if (dbg_on && !c->capturing) {
-        CK(cudaMallocAsync((void **)&dbg, sizeof(unsigned long long) * 4 * P.C, st));
-        CK(cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 4 * P.C, st));
+    if (dbg_path && *dbg_path && !c->capturing) {
+        CK(cudaMallocAsync((void **)&dbg, sizeof(unsigned long long) * nd, st));
+        CK(cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * nd, st));
     }
     const int *wp = T.W.rows ? (const int *)T.W.ptr.p : nullptr, *wi = T.W.rows ? (const int *)T.W.idx.p : nullptr;
     const double *wv = T.W.rows ? (const double *)T.W.val.p : nullptr;
@@ -594,14 +592,19 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     }
     CK(e);
     launched(c);
-    if (dbg) {
-        std::vector<unsigned long long> h(4 * P.C);
-        CK(cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    if (dbg) {   // append "n C ncomp smax" then one line per (cta, step)
+        std::vector<unsigned long long> h(nd);
+        CK(cudaMemcpyAsync(h.data(), dbg, nd * 8, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         cudaFreeAsync(dbg, st);
-        std::fprintf(stderr, "[dpp-push] n=%d L=%d G=%d cycles/level CTA0: ring %.0f computed %.0f sync %.0f pushed %.0f | CTA8: ring %.0f computed %.0f sync %.0f pushed %.0f\n",
-                     T.n, P.L, P.G, (double)h[0] / P.L, (double)h[1] / P.L, (double)h[2] / P.L, (double)h[3] / P.L,
-                     (double)h[32] / P.L, (double)h[33] / P.L, (double)h[34] / P.L, (double)h[35] / P.L);
+        if (FILE *f = std::fopen(dbg_path, "a")) {
+            std::fprintf(f, "# n=%d C=%d ncomp=%d smax=%d L=%d G=%d\n", T.n, P.C, T.ncomp, P.smax, P.L, P.G);
+            for (size_t i = 0; i < nd / 6; ++i) {
+                const unsigned long long *o = &h[i * 6];
+                if (o[4]) std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu\n", i / P.smax, i % P.smax, o[0], o[1], o[2], o[3], o[4], o[5]);
+            }
+            std::fclose(f);
+        }
     }
 }
 

@@ -23,7 +23,11 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "dpp_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace dpp {
 

@@ -1,4 +1,6 @@
-"""Per-level phase cycles of the push sweeps (DPP_PU_DEBUG=1): ILU apply + one V-cycle, outside capture."""
+"""Timeline of the push sweeps (DPP_PU_DEBUG=<file>): ILU apply + one V-cycle, outside capture.
+
+Analyse with tools/push_timeline.py <file>."""
 import os, sys
 sys.path.insert(0, os.environ.get("GRAFT_REPO_ROOT", "/root/repo"))
 import numpy as np
@@ -9,7 +11,7 @@ bs = dpp.assemble(m, "cgvms", p, dpp.boundary_data(dpp.mms_3d(p), m))
 S = dpp.schur_selfp(bs.k1_pp, bs.k1_pu, dpp.diag_lump(bs.k1_uu), bs.k1_up)
 f = dpp.ilu0(bs.k1_uu)
 h = dpp.amg_setup(S)
-os.environ["DPP_PU_DEBUG"] = "1"
+os.environ["DPP_PU_DEBUG"] = os.environ.get("PU_TIMELINE", "gpurun_out/pu_timeline.txt")
 for _ in range(2):
     z = dpp.apply_ilu0(f, np.ones(bs.k1_uu.shape[0]))
     z = dpp.amg_vcycle(h, np.ones(S.shape[0]))
