@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <exception>
+#include <functional>
 #include <thread>
 
 #include "dpp_internal.cuh"
@@ -287,38 +288,74 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
     {
         DPP_TRACE_SCOPE(c, "amg.side_ensure");
         h->side.ensure(c);
+        h->side_rho.ensure(c);
     }
-    std::thread worker;
-    std::exception_ptr werr;
+    // sweep setups of every level run on their own host threads / side streams and
+    // are joined once, after the last Galerkin product
+    std::vector<std::thread> workers;
+    std::vector<std::unique_ptr<std::exception_ptr>> werrs;
     auto join_worker = [&] {
-        if (worker.joinable()) worker.join();
-        if (werr) std::rethrow_exception(werr);
+        for (auto &t : workers)
+            if (t.joinable()) t.join();
+        for (auto &e : werrs)
+            if (*e) std::rethrow_exception(*e);
     };
     const bool serial = !(fork_mask() & FORK_AMG_SMOOTHER);
     struct Joiner {
-        std::thread &t;
-        ~Joiner() { if (t.joinable()) t.join(); }
-    } joiner{worker};
+        std::vector<std::thread> &t;
+        ~Joiner() {
+            for (auto &x : t)
+                if (x.joinable()) x.join();
+        }
+    } joiner{workers};
     while (cur.rows > max_coarse && (int)h->lv.size() < max_levels - 1) {
         auto L = std::make_unique<AmgLevel>();
         const int n = cur.rows;
-        int64_t nc;
-        {
-            DPP_TRACE_SCOPE(c, "amg.aggregate");
-            nc = aggregate(c, cur, theta, L->agg);
-        }
-        if (nc >= n) {
-            if (n > 5000) DPP_FAIL(DPP_ERR_RUNTIME, "aggregation stalled on a large operator");
-            break;
-        }
         DBuf<double> d(n, c->s), dinv(n, c->s);
         csr_diag(c, cur, d.p, nullptr);
         k_recip<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d.p, dinv.p);
         launched(c);
-        {
-            DPP_TRACE_SCOPE(c, "amg.rho");
-            L->rho = spectral_radius(c, cur, dinv.p, randn, user);
+        // rho(D^-1 A) does not depend on the aggregates: the power iteration runs on its
+        // own side stream / host thread while this thread aggregates
+        double rho = 0.0;
+        std::exception_ptr rerr;
+        std::thread rt;
+        Ctx *rc = &h->side_rho.ctx;
+        auto rho_fn = [&] {
+            DPP_TRACE_SCOPE(rc, "amg.rho");
+            rho = spectral_radius(rc, cur, dinv.p, randn, user);
+            CK(cudaStreamSynchronize(rc->s));
+        };
+        CK(cudaStreamSynchronize(c->s));   // dinv is read on the side stream
+        if (serial) {
+            rho_fn();
+        } else {
+            rt = std::thread([&] {
+                try {
+                    CK(cudaSetDevice(rc->device));
+                    rho_fn();
+                } catch (...) {
+                    rerr = std::current_exception();
+                }
+            });
         }
+        int64_t nc;
+        {
+            DPP_TRACE_SCOPE(c, "amg.aggregate");
+            try {
+                nc = aggregate(c, cur, theta, L->agg);
+            } catch (...) {
+                if (rt.joinable()) rt.join();
+                throw;
+            }
+        }
+        if (rt.joinable()) rt.join();
+        if (rerr) std::rethrow_exception(rerr);
+        if (nc >= n) {
+            if (n > 5000) DPP_FAIL(DPP_ERR_RUNTIME, "aggregation stalled on a large operator");
+            break;
+        }
+        L->rho = rho;
         const double damping = 2.0 * omega / L->rho;
         std::vector<int> agg32(L->agg.begin(), L->agg.end());
         DBuf<int> dagg(n, c->s);
@@ -353,40 +390,63 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
             next = spgemm(c, L->R, AP, nullptr, false, nullptr);
         }
         L->A = std::move(cur);
-        spmv_plan(c, L->A);
-        spmv_plan(c, L->P);
-        spmv_plan(c, L->R);
         for (DBuf<double> *b : {&L->b, &L->x, &L->r, &L->t, &L->y}) b->alloc(n, c->s);
         L->ticket.alloc(4, c->s);
         CK(cudaStreamSynchronize(c->s));
-        join_worker();
+        // level setup off the critical path, on two side streams / host threads: the
+        // (D+L) sweep plan + SpMV plans, and the (D+U) sweep plan
         AmgLevel *Lp = L.get();
-        Ctx *sc = &h->side.ctx;
-        auto smoother = [Lp, sc] {
+        for (int q = 0; q < 2; ++q) {
+            h->lvside.push_back(std::make_unique<SideStream>());
+            h->lvside.back()->ensure(c);
+        }
+        Ctx *sc = &h->lvside[h->lvside.size() - 2]->ctx, *su = &h->lvside.back()->ctx;
+        auto smoother_lo = [Lp, sc] {
             DPP_TRACE_SCOPE(sc, "amg.smoother_setup");
             Lp->lo = make_tri(sc, Lp->A, true, false, true);
-            Lp->up = make_tri(sc, Lp->A, false, false, true);
+            spmv_plan(sc, Lp->A);
+            spmv_plan(sc, Lp->P);
+            spmv_plan(sc, Lp->R);
             CK(cudaStreamSynchronize(sc->s));
         };
+        auto smoother_up = [Lp, su] {
+            DPP_TRACE_SCOPE(su, "amg.smoother_setup_up");
+            Lp->up = make_tri(su, Lp->A, false, false, true);
+            CK(cudaStreamSynchronize(su->s));
+        };
         if (serial) {
-            smoother();
+            smoother_lo();
+            smoother_up();
         } else {
-            worker = std::thread([smoother, sc, &werr] {
-                try {
-                    CK(cudaSetDevice(sc->device));
-                    smoother();
-                } catch (...) {
-                    werr = std::current_exception();
-                }
-            });
+            auto spawn = [&](std::function<void()> fn, Ctx *x) {
+                werrs.push_back(std::make_unique<std::exception_ptr>());
+                std::exception_ptr *err = werrs.back().get();
+                workers.emplace_back([fn, x, err] {
+                    try {
+                        CK(cudaSetDevice(x->device));
+                        fn();
+                    } catch (...) {
+                        *err = std::current_exception();
+                    }
+                });
+            };
+            spawn(smoother_lo, sc);
+            spawn(smoother_up, su);
         }
         h->lv.push_back(std::move(L));
         cur = std::move(next);
         CK(cudaStreamSynchronize(c->s));
     }
-    join_worker();
-    c->launches += h->side.ctx.launches;
-    h->side.ctx.launches = 0;
+    {
+        DPP_TRACE_SCOPE(c, "amg.join_smoothers");
+        join_worker();
+    }
+    std::vector<SideStream *> sides = {&h->side, &h->side_rho};
+    for (auto &ss : h->lvside) sides.push_back(ss.get());
+    for (SideStream *ss : sides) {
+        c->launches += ss->ctx.launches;
+        ss->ctx.launches = 0;
+    }
     auto last = std::make_unique<AmgLevel>();
     coarse_setup(c, *h, cur);
     const int n = cur.rows;

@@ -343,6 +343,8 @@ struct AmgLevel {
 };
 struct Amg {
     SideStream side;           // smoother setup of level l overlaps the Galerkin product of l+1
+    SideStream side_rho;       // rho(D^-1 A) of a level, concurrent with its aggregation
+    std::vector<std::unique_ptr<SideStream>> lvside;   // per level: (D+L) and (D+U) sweep setups
     Ctx *ctx = nullptr;
     std::vector<std::unique_ptr<AmgLevel>> lv;
     DBuf<double> coarse_inv;   // dense inverse of the coarsest operator (row-major)

@@ -63,9 +63,10 @@ struct Args {
 // row is loaded while the current one is accumulated.
 constexpr int PF_HASH = 4;
 template <int PF, typename Upd>
-__device__ __forceinline__ void accumulate_row(const Args &a, int64_t row, int lane, Upd &&upd) {
-    const int s = a.ap[row], e = a.ap[row + 1], len = e - s;
-    for (int q0 = 0; q0 < len; q0 += 32) {
+__device__ __forceinline__ void accumulate_row(const Args &a, int64_t row, int lane, Upd &&upd, int qb = 0,
+                                               int qe = 0x7fffffff) {
+    const int s = a.ap[row], e = a.ap[row + 1], len = min(e - s, qe);
+    for (int q0 = qb; q0 < len; q0 += 32) {
         int bs = 0, be = 0;
         double aq = 0.0;
         if (q0 + lane < len) {
@@ -392,6 +393,78 @@ __global__ void k_spgemm_dense(Args a, int ncols, int W) {
     }
 }
 
+// Split-k dense variant for few long output rows (the Galerkin product R (A P) of a
+// coarse level: ~600 rows of ~250 k-terms over ~500-entry B rows): one CTA per row,
+// warp w accumulates the k-range w of the row in its own dense accumulator (k order
+// inside the range), the 8 partials are added in warp order, survivors compacted in
+// column order.  Differs from the k-sequential sum by rounding only (coarse levels
+// are insensitive to it; the reference's association is (P^T A) P).
+constexpr int SK_W = 8;
+template <int PFD>
+__global__ void __launch_bounds__(32 * SK_W) k_spgemm_dense_splitk(Args a, int ncols) {
+    extern __shared__ unsigned char smem[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *accs = reinterpret_cast<double *>(smem);                       // [SK_W][ncols]
+    double *dv = accs + (size_t)SK_W * ncols;                              // [ncols]
+    unsigned char *has = reinterpret_cast<unsigned char *>(dv + ncols);    // [SK_W][ncols]
+    __shared__ int wsum[SK_W];
+    const int64_t row = blockIdx.x;
+    for (int j = threadIdx.x; j < SK_W * ncols; j += blockDim.x) has[j] = 0;
+    __syncthreads();
+    if (a.dp) {
+        for (int p = a.dp[row] + threadIdx.x; p < a.dp[row + 1]; p += blockDim.x) dv[a.di[p]] = a.dv[p];
+    }
+    const int len = a.ap[row + 1] - a.ap[row];
+    const int per = (len + SK_W - 1) / SK_W;
+    double *acc = accs + (size_t)w * ncols;
+    unsigned char *hw = has + (size_t)w * ncols;
+    accumulate_row<PFD>(a, row, lane, [&](int j, double pr) {
+        if (hw[j]) acc[j] = __dadd_rn(acc[j], pr);
+        else { acc[j] = __dadd_rn(0.0, pr); hw[j] = 1; }
+    }, w * per, min(len, (w + 1) * per));
+    __syncthreads();
+    const int64_t o = a.toff[row];
+    int base = 0;
+    for (int j0 = 0; j0 < ncols; j0 += blockDim.x) {
+        const int j = j0 + threadIdx.x;
+        bool keep = false, any = false;
+        double v = 0.0;
+        if (j < ncols) {
+            for (int q = 0; q < SK_W; ++q)
+                if (has[(size_t)q * ncols + j]) {
+                    v = any ? __dadd_rn(v, accs[(size_t)q * ncols + j]) : accs[(size_t)q * ncols + j];
+                    any = true;
+                }
+            bool hd = false;
+            if (a.dp) {   // D present at j?  (dv was only written where D has entries)
+                const int p0 = a.dp[row], p1 = a.dp[row + 1];
+                int lo = p0, hi = p1;
+                while (lo < hi) { const int m = (lo + hi) >> 1; if (a.di[m] < j) lo = m + 1; else hi = m; }
+                hd = lo < p1 && a.di[lo] == j;
+            }
+            if (any || hd) {
+                if (!a.dp) v = v;
+                else if (any) v = hd ? __dsub_rn(dv[j], v) : -v;
+                else v = dv[j];
+                keep = a.keep_zeros || v != 0.0;
+            }
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) wsum[w] = __popc(m);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int q = 0; q < SK_W; ++q) { before += q < w ? wsum[q] : 0; tot += wsum[q]; }
+        if (keep) {
+            const int64_t pos = o + base + before + __popc(m & ((1u << lane) - 1));
+            a.ti[pos] = j;
+            a.tv[pos] = v;
+        }
+        base += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.cnt[row] = base;
+}
+
 __global__ void k_toff_dense(int rows, int ncols, int64_t *toff) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
         toff[r] = (int64_t)r * ncols;
@@ -490,7 +563,21 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         launched(c);
         a.toff = toff.p;
         const int grid = std::max(1, std::min<int>((rows + W - 1) / W, c->sms * 4));
-        if (pfd == 16) k_spgemm_dense<16><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
+        const size_t sk_smem = (size_t)SK_W * ncols * 9 + (size_t)ncols * 8;
+        const double alen = (double)A.nnz / rows;
+        static const bool no_sk = [] { const char *e = std::getenv("DPP_NO_SPLITK"); return e && *e == '1'; }();
+        if (!no_sk && rows < c->sms * 8 && alen >= 64 && sk_smem <= 200 * 1024) {
+            static bool sattr = false;
+            if (!sattr) {
+                for (const void *f : {(const void *)k_spgemm_dense_splitk<4>, (const void *)k_spgemm_dense_splitk<8>,
+                                      (const void *)k_spgemm_dense_splitk<16>})
+                    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+                sattr = true;
+            }
+            if (pfd == 16) k_spgemm_dense_splitk<16><<<rows, 32 * SK_W, sk_smem, c->s>>>(a, ncols);
+            else if (pfd == 8) k_spgemm_dense_splitk<8><<<rows, 32 * SK_W, sk_smem, c->s>>>(a, ncols);
+            else k_spgemm_dense_splitk<4><<<rows, 32 * SK_W, sk_smem, c->s>>>(a, ncols);
+        } else if (pfd == 16) k_spgemm_dense<16><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
         else if (pfd == 8) k_spgemm_dense<8><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
         else k_spgemm_dense<4><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
         launched(c);

@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(32 * BD_INV_WPB)
     int pa0 = ptr[s + a], pa1 = ptr[s + a + 1];
     int pb0 = 0, pb1 = 0;
     if (valid(a + step)) { pb0 = ptr[s + a + step]; pb1 = ptr[s + a + step + 1]; }
-    constexpr int IPF = 3;   // entries per lane held for the current / next row
+    constexpr int IPF = 8;   // entries per lane held for the current / next row (whole coarse rows)
     int jc[IPF];
     double vc[IPF], dc = diag ? diag[s + a] : 1.0;
 #pragma unroll

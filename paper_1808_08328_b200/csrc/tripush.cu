@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     // debug timeline (DPP_PU_DEBUG): per step {level, rows, t ring landed, t levels landed,
     // t barrier passed, t last row pushed} in %globaltimer ns, row [cta][step] of dbg
-    __shared__ unsigned long long t_done[2];
+    __shared__ unsigned long long t_done[2][32];   // per warp (no atomics on the timed path)
     unsigned long long tB = 0, tC = 0;
     unsigned long long *mring = reinterpret_cast<unsigned long long *>(smem);
     unsigned long long *mlev = mring + PU_NST_MAX;
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     } else {
         for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[(size_t)(base + i) * ncomp + comp];
     }
-    if (dbg && threadIdx.x < 2) t_done[threadIdx.x] = 0;
+    if (dbg && threadIdx.x < 64) t_done[threadIdx.x >> 5][threadIdx.x & 31] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     auto issue = [&](int l, int s) {
@@ -178,7 +178,11 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
             o[0] = reinterpret_cast<const int4 *>(blk)->w;
             o[1] = reinterpret_cast<const int4 *>(blk)->x;
             o[2] = tB; o[3] = tC; o[4] = gtimer();
-            if (st > 0) { dbg[((size_t)blockIdx.x * smax + st - 1) * 6 + 5] = t_done[(st - 1) & 1]; t_done[(st - 1) & 1] = 0; }
+            if (st > 0) {
+                unsigned long long m = 0;
+                for (int w = 0; w < 32; ++w) { m = max(m, t_done[(st - 1) & 1][w]); t_done[(st - 1) & 1][w] = 0; }
+                dbg[((size_t)blockIdx.x * smax + st - 1) * 6 + 5] = m;
+            }
         }
         if (producer) {
             if (st + nst - 1 < S) issue(st + nst - 1, islot);   // the slot of step st-1 is free
@@ -213,11 +217,15 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                              : "memory");
             }
         }
-        if (dbg) { __syncwarp(); if (lane == 0) atomicMax(&t_done[st & 1], gtimer()); }
+        if (dbg) { __syncwarp(); if (lane == 0) t_done[st & 1][threadIdx.x >> 5] = gtimer(); }
     }
     __syncthreads();
     pdl_trigger();   // the dependent kernel's launch overlaps the x write-out below
-    if (dbg && threadIdx.x == blockDim.x - 32 && S > 0) dbg[((size_t)blockIdx.x * smax + S - 1) * 6 + 5] = t_done[(S - 1) & 1];
+    if (dbg && threadIdx.x == blockDim.x - 32 && S > 0) {
+        unsigned long long m = 0;
+        for (int w = 0; w < 32; ++w) m = max(m, t_done[(S - 1) & 1][w]);
+        dbg[((size_t)blockIdx.x * smax + S - 1) * 6 + 5] = m;
+    }
     for (int i = threadIdx.x; i < mine; i += blockDim.x) {
         const size_t g = (size_t)(base + i) * ncomp + comp;
         x[g] = xh[i];
