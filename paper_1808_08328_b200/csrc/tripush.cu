@@ -156,7 +156,6 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     }
     // every CTA's level mbarriers are armed before the first push
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    long long pr_n = 0, pr_hdr = 0, pr_sum = 0, pr_push = 0;   // debug: row 0 phases (thread 0)
     int slot = 0, islot = nst - 1, waited = 0;
     unsigned phase = 0;
     for (int st = 0; st < S; ++st) {
@@ -198,12 +197,9 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         const int *code = reinterpret_cast<const int *>(blk + pu_off_code(nr));
         const double *val = reinterpret_cast<const double *>(blk + pu_off_val(nr, ne));
         const int *pl = reinterpret_cast<const int *>(val + ne);
-        long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-        if (dbg) c0 = clock64();
         for (int q = grp; q < nr; q += ngrp) {
             const int4 R = rows[q];
             const double dq = dg[q];
-            if (dbg) c1 = clock64();
             double sum = 0.0;
             for (int e = R.y + gl; e < R.z; e += G) sum += val[e] * xh[code[e]];
 #pragma unroll
@@ -211,7 +207,6 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
             const double xr = (xh[R.x] - sum) * dq;   // dq = 1/t_ii (as SuperLU's pre-scaled solve)
             __syncwarp(gmask);
             if (gl == 0) xh[R.x] = xr;
-            if (dbg) c2 = clock64();
             const int p0 = R.w >> 4, pc = R.w & 15;
             for (int u = gl; u < pc; u += G) {
                 const int pe = pl[p0 + u];
@@ -221,18 +216,11 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                              ::"r"(peer[dst] + 8u * sl), "l"(__double_as_longlong(xr)), "r"(peer[16 + dst] + 8u * lvl)
                              : "memory");
             }
-            if (dbg) c3 = clock64();
-        }
-        if (dbg && threadIdx.x == 0 && nr > 0) {
-            pr_n++; pr_hdr += c1 - c0; pr_sum += c2 - c1; pr_push += c3 - c2;
         }
         if (dbg) { __syncwarp(); if (lane == 0) t_done[st & 1][threadIdx.x >> 5] = gtimer(); }
     }
     __syncthreads();
     pdl_trigger();   // the dependent kernel's launch overlaps the x write-out below
-    if (dbg && threadIdx.x == 0 && blockIdx.x == 0 && pr_n)
-        printf("[dpp-push] n=%d G=%d row phases (cycles, thread 0): header %lld, dot+shuffle+store %lld, pushes %lld over %lld steps\n",
-               n, G, pr_hdr / pr_n, pr_sum / pr_n, pr_push / pr_n, pr_n);
     if (dbg && threadIdx.x == blockDim.x - 32 && S > 0) {
         unsigned long long m = 0;
         for (int w = 0; w < 32; ++w) m = max(m, t_done[(S - 1) & 1][w]);

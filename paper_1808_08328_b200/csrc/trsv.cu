@@ -662,7 +662,8 @@ __global__ void __launch_bounds__(32 * ILU_WPB) k_ilu0(int n, const int *__restr
 }
 
 // In-place ILU(0) of LU (IKJ order, linalg.py:178-222); returns the failing row or -1.
-static int ilu_factor(Ctx *c, Csr &LU) {
+static int ilu_factor(Ctx *c, Csr &LU, DBuf<int> *order_out = nullptr, DBuf<int> *lev_out = nullptr,
+                      int *nlev_out = nullptr) {
     const int n = LU.rows;
     DBuf<int> dpos(n, c->s), flags((size_t)n + 3, c->s);
     CK(cudaMemsetAsync(flags.p, 0, sizeof(int) * (n + 3), c->s));
@@ -676,10 +677,11 @@ static int ilu_factor(Ctx *c, Csr &LU) {
     CK(cudaMemcpyAsync(&hm, missing, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
     if (hm) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "missing diagonal entry in sparsity pattern");
-    DBuf<int> order;
+    DBuf<int> order, lev;
+    int nlev;
     {
         Csr lower = csr_part(c, LU, -1, false);   // stored pattern: every row the IKJ loop may read
-        tri_levels(c, lower, false, order);
+        nlev = tri_levels(c, lower, false, order, nullptr, &lev);
     }
     DPP_TRACE_SCOPE(c, "ilu0.factor_kernel");
     if (n) {
@@ -691,7 +693,46 @@ static int ilu_factor(Ctx *c, Csr &LU) {
     int he = 0;
     CK(cudaMemcpyAsync(&he, err, sizeof(int), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
+    if (order_out) {   // the stored lower pattern's schedule covers the factor's L sweep
+        *order_out = std::move(order);
+        *lev_out = std::move(lev);
+        *nlev_out = nlev;
+    }
     return he != 0x7f7f7f7f ? he : -1;
+}
+
+// Sweep of the Kronecker triangle T_s (x) I_d built from the scalar factor directly
+// (ilu0's Kronecker path); ok = false when the push plan does not fit
+static Tri make_tri_kron(Ctx *c, const Csr &M, bool lower, bool unit, int d, DBuf<int> *pre_order,
+                         DBuf<int> *pre_lev, int pre_nlev, bool &ok) {
+    Tri S;
+    S.n = M.rows;
+    S.backward = !lower;
+    S.strict = csr_part(c, M, lower ? -1 : 1, true);
+    if (!unit) {
+        S.diag.alloc(M.rows, c->s);
+        csr_diag(c, M, S.diag.p, nullptr);
+    }
+    DBuf<int> lev;
+    if (pre_lev) {
+        S.order = std::move(*pre_order);
+        lev = std::move(*pre_lev);
+        S.nlev = pre_nlev;
+    } else {
+        S.nlev = tri_levels(c, S.strict, S.backward, S.order, nullptr, &lev);
+    }
+    const int64_t snnz = S.strict.nnz;
+    const int m = merge_factor();
+    if (m > 1 && S.nlev >= 4 * m) S.nlev = merge_levels(c, S, lev, m);
+    ok = push_plan(c, S, lev, S.nlev);
+    if (!ok) return Tri{};
+    S.ncomp = d;
+    S.n = M.rows * d;
+    S.nnz_alg = snnz * d;
+    if (TraceScope::on())
+        std::fprintf(stderr, "[dpp-trace]   make_tri_kron d=%d n=%d levels %d strict nnz %lld (x%d)\n", d, M.rows,
+                     S.nlev, (long long)S.strict.nnz, d);
+    return S;
 }
 
 // Kronecker ILU(0): when A = M (x) I_d on the node-blocked pattern (every cross-component
@@ -799,11 +840,22 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
             launched(c);
             if (missing.to_host()[0]) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "missing diagonal entry in sparsity pattern");
         }
-        const int bad = ilu_factor(c, M);
+        DBuf<int> order, lev;
+        int nlev = 0;
+        const int bad = ilu_factor(c, M, &order, &lev, &nlev);
         if (bad >= 0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(bad * d));
         k_ilu_kron_expand<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d, A.ptr.p, A.idx.p, M.ptr.p, M.idx.p,
                                                                       M.val.p, f->LU.val.p);
         launched(c);
+        bool okl = false, oku = false;
+        f->L = make_tri_kron(c, M, true, true, d, &order, &lev, nlev, okl);
+        if (okl) f->U = make_tri_kron(c, M, false, false, d, nullptr, nullptr, 0, oku);
+        if (okl && oku) {
+            f->y.alloc(n, c->s);
+            f->tmp.alloc(n, c->s);
+            f->ticket.alloc(2, c->s);
+            return f;
+        }
     } else {
         const int bad = ilu_factor(c, f->LU);
         if (bad >= 0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero pivot at row " + std::to_string(bad));
