@@ -401,7 +401,7 @@ int dpp_gmres(dpp_ctx *ctx, const dpp_csr *A, dpp_apply_fn A_cb, void *A_user, d
         if (x0) dx.upload(x0, n);
         else if (n) CK(cudaMemsetAsync(dx.p, 0, sizeof(double) * n, c->s));
         std::vector<double> hist;
-        gmres_dev(c, n, op, pm, db.p, dx.p, rtol, max_iter, restart, stats, &hist);
+        gmres_dev(c, n, op, pm, db.p, dx.p, rtol, max_iter, restart, stats, &hist, x0 == nullptr);
         dx.download(x, n);
         CK(cudaStreamSynchronize(c->s));
         for (int i = 0; i < (int)hist.size() && i < history_cap; ++i) history[i] = hist[i];
@@ -424,7 +424,7 @@ int dpp_solve(dpp_ctx *ctx, dpp_system *s, dpp_pc *pc, double rtol, int max_iter
         std::vector<double> hist;
         {
             DPP_TRACE_SCOPE(c, "solve.gmres");
-            gmres_dev(c, n, op, pm, f, dx.p, rtol, max_iter, restart, stats, &hist);
+            gmres_dev(c, n, op, pm, f, dx.p, rtol, max_iter, restart, stats, &hist, true);
         }
         if (x) dx.download(x, n);
         CK(cudaStreamSynchronize(c->s));

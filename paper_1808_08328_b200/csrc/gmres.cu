@@ -157,7 +157,7 @@ struct Gm {
 
 void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double *b, double *x,
                double rtol, int max_iter, int restart, dpp_krylov_stats *st,
-               std::vector<double> *history) {
+               std::vector<double> *history, bool x_zero) {
     const auto t0 = std::chrono::steady_clock::now();
     Gm g{c, n, A, M};
     g.part.alloc(NRM_BLOCKS, c->s);
@@ -194,16 +194,30 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
     int total = 0, reason = 1, cycles = 0;
     bool converged = false;
     double last = -1.0;
+    // x0 = 0 with the device CSR operator and a device (or identity) preconditioner:
+    // the first cycle's r = b - A 0 is b bit for bit, so ||r|| = ||b|| and M r = M b,
+    // which is already in z -- the same values the reference recomputes (linalg.py:94-108)
+    bool first_is_b = x_zero && A.A && !M.cb;
     while (total < max_iter) {
-        g.matvec(x, r.p, b);                       // r = b - A x
-        norm2_dev(c, n, r.p, dnorm);
-        const double rel = g.fetch(dnorm) / norm_b;
-        if (rel <= rtol) { converged = true; reason = 0; break; }
-        if (last >= 0.0 && rel >= last * 0.9999) { reason = 2; break; }
-        last = rel;
-        g.pc(r.p, z.p);
-        norm2_dev(c, n, z.p, dnorm);
-        const double beta = g.fetch(dnorm);
+        double rel, beta;
+        if (first_is_b) {
+            first_is_b = false;
+            rel = norm_b / norm_b;
+            if (rel <= rtol) { converged = true; reason = 0; break; }
+            last = rel;
+            beta = norm_mb;
+            CK(cudaMemcpyAsync(dnorm, &norm_mb, sizeof(double), cudaMemcpyHostToDevice, c->s));
+        } else {
+            g.matvec(x, r.p, b);                   // r = b - A x
+            norm2_dev(c, n, r.p, dnorm);
+            rel = g.fetch(dnorm) / norm_b;
+            if (rel <= rtol) { converged = true; reason = 0; break; }
+            if (last >= 0.0 && rel >= last * 0.9999) { reason = 2; break; }
+            last = rel;
+            g.pc(r.p, z.p);
+            norm2_dev(c, n, z.p, dnorm);
+            beta = g.fetch(dnorm);
+        }
         if (beta == 0.0) { converged = true; reason = 0; break; }
         ++cycles;
         const int m = std::min(restart, max_iter - total);

@@ -51,7 +51,7 @@ struct PcOp {
 };
 void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double *b_dev,
                double *x_dev, double rtol, int max_iter, int restart, dpp_krylov_stats *st,
-               std::vector<double> *history);
+               std::vector<double> *history, bool x_zero = false);
 
 }  // namespace dpp
 
