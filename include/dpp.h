@@ -69,6 +69,12 @@ int dpp_csr_download(const dpp_csr *A, int32_t *indptr_host, int32_t *indices_ho
 int dpp_csr_destroy(dpp_csr *A);
 /* linalg.spmv (linalg.py:27-32): y = A x */
 int dpp_spmv(dpp_ctx *ctx, const dpp_csr *A, const double *x_host, double *y_host);
+/* SpMV plan of a matrix applied repeatedly (the operators inside dpp_solve get one
+ * automatically): 0 none (warp-per-row CSR), 1 CSR-stream row blocks, 2 SELL-32,
+ * 3 automatic (SELL-32 when its zero padding stays under 25 %, else CSR-stream).
+ * Replaces nothing in the reference (scipy's csr_matvec has one format); exposed so the
+ * kernels can be checked against linalg.py:27-32 one by one. */
+int dpp_csr_plan(dpp_csr *A, int kind);
 
 /* ---- mesh (mesh.py:73-277): numbering is bit-exact with the reference ----- */
 int dpp_mesh_generate(int dim, int kind, int n_div, dpp_mesh **out);

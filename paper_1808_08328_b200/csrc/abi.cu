@@ -131,6 +131,14 @@ int dpp_csr_destroy(dpp_csr *A) {
         else delete A;
     });
 }
+int dpp_csr_plan(dpp_csr *A, int kind) {
+    return guard([&] {
+        if (!A || A->m.rows < 0) DPP_FAIL(DPP_ERR_VALUE, "dpp_csr_plan needs an owned matrix");
+        if (kind < 0 || kind > 3) DPP_FAIL(DPP_ERR_VALUE, "unknown SpMV plan kind");
+        spmv_plan(A->ctx, A->m, kind);
+        CK(cudaStreamSynchronize(A->ctx->s));
+    });
+}
 int dpp_spmv(dpp_ctx *ctx, const dpp_csr *A, const double *x, double *y) {
     return guard([&] {
         Ctx *c = &ctx->c;

@@ -142,9 +142,12 @@ static int spmv_mode() {
     return m;
 }
 
-void spmv_plan(Ctx *c, Csr &A) {
-    if (A.rows == 0 || A.nnz == 0 || spmv_mode() == 0) return;
-    if (spmv_mode() == 2) {
+void spmv_plan(Ctx *c, Csr &A, int kind) {
+    A.rb.release(); A.nrb = 0;
+    A.sp.release(); A.sc.release(); A.sv.release(); A.nsl = 0;
+    if (kind == 3) kind = spmv_mode() == 0 ? 0 : spmv_mode() == 1 ? 1 : 3;
+    if (A.rows == 0 || A.nnz == 0 || kind == 0) return;
+    if (kind >= 2) {
         const int nsl = (A.rows + 31) / 32;
         DBuf<int> wcnt((size_t)nsl, c->s);
         const int grid = grid_for((int64_t)nsl * 32, 256, c->sms, 8);
@@ -152,7 +155,7 @@ void spmv_plan(Ctx *c, Csr &A) {
         launched(c);
         DBuf<int> sp;
         const int64_t tot = counts_to_ptr(c, wcnt.p, nsl, sp);
-        if ((double)tot <= SELL_MAX_FILL * (double)A.nnz) {
+        if (kind == 2 || (double)tot <= SELL_MAX_FILL * (double)A.nnz) {
             A.sp = std::move(sp);
             A.sc.alloc((size_t)tot, c->s);
             A.sv.alloc((size_t)tot, c->s);

@@ -220,7 +220,9 @@ inline int grid_for(int64_t work, int block, int sms, int per_sm = 16) {
 void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b = nullptr,
           double alpha = 1.0, cudaStream_t st = nullptr);   // y = b + alpha*A x (b may be null)
 // row-block partition for the nnz-streaming SpMV (operators applied many times)
-void spmv_plan(Ctx *c, Csr &A);
+// kind: 0 none (row kernel), 1 CSR-stream, 2 SELL-32 (any fill), 3 auto (SELL when the
+// padding stays small, else CSR-stream; DPP_SPMV=row|stream overrides)
+void spmv_plan(Ctx *c, Csr &A, int kind = 3);
 void fill(Ctx *c, double *x, int64_t n, double v, cudaStream_t st = nullptr);
 void axpy(Ctx *c, int64_t n, double a, const double *x, double *y, cudaStream_t st = nullptr);
 void axpby_to(Ctx *c, int64_t n, const double *x, double a, const double *y, double *out,

@@ -73,6 +73,43 @@ def test_spmv_matches_scipy(rng):
         dpp.spmv(sp.identity(3, format="csr"), np.ones(4))
 
 
+def _spmv_cases(rng):
+    """Row-length mixes the SpMV plans must handle: short / long / empty rows, a
+    row longer than a CSR-stream block, rows not a multiple of the SELL slice."""
+    yield "narrow", sp.random(1003, 900, density=0.004, random_state=2, format="csr")
+    yield "wide", sp.random(517, 4000, density=0.03, random_state=3, format="csr")
+    lens = rng.integers(0, 60, 2049)
+    lens[::97] = 0
+    lens[1000] = 5000                      # one row longer than a stream block (2048 entries)
+    rows = np.repeat(np.arange(2049), lens)
+    cols = np.concatenate([rng.choice(6000, l, replace=False) for l in lens])
+    yield "ragged", sp.csr_matrix((rng.standard_normal(rows.size), (rows, cols)), shape=(2049, 6000))
+    # a CG-VMS K (explicit zeros, the structured gathers SELL-32 is built for)
+    bs, _ = systems("cgvms", 3, "tet", 3)
+    yield "K", dpp.monolithic_view(bs)[0]
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+def test_spmv_plans_match_scipy(kind, rng):
+    """Every SpMV kernel (row / CSR-stream / SELL-32 / auto) against scipy's csr_matvec
+    (linalg.py:27-32): 1e-14 relative per row; SELL-32 with one warp per slice sums each
+    row sequentially in column order and is bitwise equal."""
+    import ctypes as C
+    from paper_1808_08328_b200 import _native as N
+    from paper_1808_08328_b200.device import DeviceCsr
+    for name, A in _spmv_cases(rng):
+        A = sp.csr_matrix(A)
+        A.sort_indices()
+        D = DeviceCsr.from_scipy(A)
+        N.call("dpp_csr_plan", D.h, kind)
+        x = rng.standard_normal(A.shape[1])
+        y, ref = D @ x, A @ x
+        scale = np.maximum(np.abs(A).dot(np.abs(x)), 1e-300)
+        assert np.all(np.abs(y - ref) <= 1e-14 * scale), (name, kind)
+        if kind == 2 and A.nnz / A.shape[0] <= 8:
+            assert np.array_equal(y, ref), name
+
+
 # ----------------------------------------------------------------------------- assembly
 
 @pytest.mark.parametrize("form", ["hdiv", "cgvms", "dgvms"])
