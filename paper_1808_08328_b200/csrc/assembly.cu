@@ -508,10 +508,32 @@ __device__ inline void grad_phys(const Elem &E, const double *Ji, int q, int a, 
         g[i] = s;
     }
 }
+template <int DIM>
+__device__ inline void grad_phys(const Elem &E, const double *Ji, int q, int a, double *g) {
+#pragma unroll
+    for (int i = 0; i < DIM; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < DIM; ++j) s += E.G[q][a][j] * Ji[j * DIM + i];
+        g[i] = s;
+    }
+}
 
+// One thread per node-graph entry, its contributions in insertion order (deterministic
+// sums).  DIM is a template parameter so the per-entry block accumulators stay in
+// registers, and the element tables are read from shared memory (per-thread a, b, q
+// indices would serialise constant-bank reads).
+template <int DIM>
 __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
-    const Elem &E = A.E;
-    const int dim = E.dim, nn = E.nn;
+    __shared__ Elem E;
+    {
+        const double *src = reinterpret_cast<const double *>(&A.E);
+        double *dst = reinterpret_cast<double *>(&E);
+        for (int i = threadIdx.x; i < (int)(sizeof(Elem) / sizeof(double)); i += blockDim.x) dst[i] = src[i];
+        __syncthreads();
+    }
+    constexpr int dim = DIM;
+    const int nn = E.nn;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < A.nnz; e += (int64_t)gridDim.x * blockDim.x) {
         double uu[2][3][3] = {}, up[2][3] = {}, pu[2][3] = {}, pp[2] = {}, cr = 0.0;
         for (int64_t t = A.seg[e]; t < A.seg[e + 1]; ++t) {
@@ -526,8 +548,9 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                 double gg = 0.0, gnab[3] = {0, 0, 0}, gnba[3] = {0, 0, 0};
                 for (int q = 0; q < E.nq; ++q) {
                     double ga[3], gb[3];
-                    grad_phys(E, Ji, q, a, ga);
-                    grad_phys(E, Ji, q, b, gb);
+                    grad_phys<DIM>(E, Ji, q, a, ga);
+                    grad_phys<DIM>(E, Ji, q, b, gb);
+                    #pragma unroll
                     for (int i = 0; i < dim; ++i) {
                         gg += E.w[q] * ga[i] * gb[i];
                         gnab[i] += E.w[q] * ga[i] * E.N[q][b];
@@ -535,12 +558,16 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                     }
                 }
                 gg *= det;
+                #pragma unroll
                 for (int i = 0; i < dim; ++i) { gnab[i] *= det; gnba[i] *= det; }
+                #pragma unroll
                 for (int n = 0; n < 2; ++n) {
                     const double v = A.s_uu[n] * mass;
+                    #pragma unroll
                     for (int i = 0; i < dim; ++i) uu[n][i][i] += v;
                     pp[n] += A.s_pp_gg[n] * gg + A.s_pp_m * mass;
                 }
+                #pragma unroll
                 for (int i = 0; i < dim; ++i) {
                     const double vu = -(gnab[i] + 0.5 * gnba[i]), vp = gnba[i] + 0.5 * gnab[i];
                     up[0][i] += vu; up[1][i] += vu;
@@ -556,9 +583,10 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                 for (int q = 0; q < A.fnq; ++q)
                     F += A.vW[vi * A.fnq + q] * A.vN[(vi * A.fnq + q) * nn + a] * A.vN[(vi * A.fnq + q) * nn + b];
                 const double *n = A.fn + (int64_t)A.vfac[vi] * dim;
-                for (int i = 0; i < dim; ++i) {
-                    up[net][i] += F * n[i];
-                    pu[net][i] += -(F * n[i]);
+                #pragma unroll
+                for (int i = 0; i < dim; ++i) {   // (branches keep the accumulators in registers)
+                    if (net == 0) { up[0][i] += F * n[i]; pu[0][i] += -(F * n[i]); }
+                    else { up[1][i] += F * n[i]; pu[1][i] += -(F * n[i]); }
                 }
             } else {                   // DG interior facet side pair (assembly.py:497-517)
                 const int64_t idx = p - A.C * per;
@@ -572,12 +600,16 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                 double F = 0.0;
                 for (int q = 0; q < A.fnq; ++q) F += A.fW[fi * A.fnq + q] * Ns[q * nn + a] * Nt[q * nn + b];
                 const double *n = A.fn + (int64_t)A.interior[fi] * dim;
+                #pragma unroll
                 for (int k = 0; k < 2; ++k) {
                     const double cu = A.c_uu[k] * ss * tt;
+                    #pragma unroll
                     for (int i = 0; i < dim; ++i)
+                        #pragma unroll
                         for (int j = 0; j < dim; ++j) uu[k][i][j] += cu * (F * n[i] * n[j]);
                     pp[k] += A.c_pp[k] * ss * tt * F;
                 }
+                #pragma unroll
                 for (int i = 0; i < dim; ++i) {
                     const double vu = 0.5 * ss * (F * n[i]), vp = -0.5 * tt * (F * n[i]);
                     up[0][i] += vu; up[1][i] += vu;
@@ -588,9 +620,12 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
         // Kronecker placement of entry e (row v, col v2) into the expanded blocks
         const int v = A.grow[e], v2 = A.gcol[e];
         const int64_t g0 = A.gptr[v], len = A.gptr[v + 1] - g0, o = e - g0;
+        #pragma unroll
         for (int n = 0; n < 2; ++n) {
+            #pragma unroll
             for (int i = 0; i < dim; ++i) {
                 const int64_t rs = (int64_t)dim * dim * g0 + (int64_t)i * dim * len;
+                #pragma unroll
                 for (int j = 0; j < dim; ++j) {
                     const int64_t pos = rs + o * dim + j;
                     A.uu_i[n][pos] = v2 * dim + j;
@@ -600,6 +635,7 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                 A.up_i[n][ps] = v2;
                 A.up_v[n][ps] = up[n][i];
             }
+            #pragma unroll
             for (int j = 0; j < dim; ++j) {
                 const int64_t pos = (int64_t)dim * g0 + o * dim + j;
                 A.pu_i[n][pos] = v2 * dim + j;
@@ -1141,7 +1177,8 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
         A.cr_i = c12.idx.p;
         A.cr_v = c12.val.p;
     }
-    k_vms_values<<<grid_for(g, 128, c->sms, 32), 128, 0, c->s>>>(A);
+    if (E.dim == 2) k_vms_values<2><<<grid_for(g, 128, c->sms, 32), 128, 0, c->s>>>(A);
+    else k_vms_values<3><<<grid_for(g, 128, c->sms, 32), 128, 0, c->s>>>(A);
     launched(c);
     if (dg) {
         alloc_blk(c, c12, np_, np_, C * nn * nn);
