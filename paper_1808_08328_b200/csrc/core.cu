@@ -396,9 +396,12 @@ double norm2(Ctx *c, int64_t n, const double *x) {
 struct Segs { int64_t d[4], s[4], l[4]; int n; };
 __global__ void k_copy_segs(double *dst, const double *src, Segs g) {
     pdl_wait();
-    for (int k = 0; k < g.n; ++k)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {   // constant indices: the segment table stays in the parameter bank
+        if (k >= g.n) break;
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < g.l[k]; i += (int64_t)gridDim.x * blockDim.x)
             dst[g.d[k] + i] = src[g.s[k] + i];
+    }
     pdl_trigger();
 }
 void copy_segments(Ctx *c, double *dst, const double *src, int nseg, const int64_t *doff,
