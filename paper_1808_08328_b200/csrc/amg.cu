@@ -10,6 +10,7 @@
 //                    D+L / D+U sweeps for SGS, dense inverse of the coarsest operator.
 //  apply:            V(1,1) with SGS (forward then backward GS as x += T^-1 (b - A x)),
 //                    restriction P^T, prolongation P, coarse dense solve.
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <exception>
@@ -118,6 +119,85 @@ __global__ void k_build_p(int rows, const int *yp, const int *yi, const double *
         }
         if (!seen) emit(a, 1.0);
         if (cnt) cnt[r] = n;
+    }
+}
+
+// Same P straight from A and the aggregates, without forming A @ P0: (A P0)_ij is the
+// sum of a_ik over the row's entries with agg[k] == j, accumulated from 0 in storage
+// order (scipy csr_matmat with b_kj = 1.0, so a_ik * 1.0 is exact), columns ascending.
+// Warp per row; distinct aggregate ids are extracted in ascending order by warp
+// min-reductions, each key's sum by walking its ballot mask in lane (= storage) order.
+// Rows up to 32*RC entries keep (key, value) in registers, longer rows re-read them.
+template <int RC>
+__global__ void __launch_bounds__(256) k_p_direct(int rows, const int *__restrict__ ap, const int *__restrict__ ai,
+                                                  const double *__restrict__ av, const int *__restrict__ agg,
+                                                  const double *__restrict__ dinv, double damping,
+                                                  const int *__restrict__ optr, int *cnt, int *oi, double *ov) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int s = ap[r], e = ap[r + 1], a = agg[r];
+        const double di = dinv[r];
+        const bool regs = e - s <= 32 * RC;
+        int kk[RC];
+        double vv[RC];
+#pragma unroll
+        for (int q = 0; q < RC; ++q) {
+            const int p = s + q * 32 + lane;
+            kk[q] = -1;
+            vv[q] = 0.0;
+            if (regs && p < e) { kk[q] = agg[ai[p]]; vv[q] = av[p]; }
+        }
+        int w = optr ? optr[r] : 0, n = 0, last = -1;
+        for (;;) {
+            int mk = a > last ? a : INT_MAX;
+            if (regs) {
+#pragma unroll
+                for (int q = 0; q < RC; ++q)
+                    if (kk[q] > last && kk[q] < mk) mk = kk[q];
+            } else {
+                for (int p = s + lane; p < e; p += 32) {
+                    const int k = agg[ai[p]];
+                    if (k > last && k < mk) mk = k;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) mk = min(mk, __shfl_xor_sync(0xffffffffu, mk, o));
+            if (mk == INT_MAX) break;
+            double y = 0.0;
+            if (regs) {
+#pragma unroll
+                for (int q = 0; q < RC; ++q) {
+                    if (s + q * 32 >= e) break;
+                    unsigned m = __ballot_sync(0xffffffffu, kk[q] == mk);
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        y = __dadd_rn(y, __shfl_sync(0xffffffffu, vv[q], b));
+                        m &= m - 1;
+                    }
+                }
+            } else {
+                for (int base = s; base < e; base += 32) {
+                    const int p = base + lane;
+                    const bool hit = p < e && agg[ai[p]] == mk;
+                    const double v = hit ? av[p] : 0.0;
+                    unsigned m = __ballot_sync(0xffffffffu, hit);
+                    while (m) {
+                        const int b = __ffs(m) - 1;
+                        y = __dadd_rn(y, __shfl_sync(0xffffffffu, v, b));
+                        m &= m - 1;
+                    }
+                }
+            }
+            const double dw = __dmul_rn(damping, __dmul_rn(di, y));
+            const double v = mk == a ? __dsub_rn(1.0, dw) : -dw;
+            if (v != 0.0) {
+                if (oi && lane == 0) { oi[w] = mk; ov[w] = v; }
+                ++w;
+                ++n;
+            }
+            last = mk;
+        }
+        if (cnt && lane == 0) cnt[r] = n;
     }
 }
 
@@ -360,25 +440,38 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
         std::vector<int> agg32(L->agg.begin(), L->agg.end());
         DBuf<int> dagg(n, c->s);
         dagg.upload(agg32.data(), n);
-        Csr P0;
-        P0.alloc(n, (int)nc, n, c->s);
-        k_p0<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(n, dagg.p, P0.ptr.p, P0.idx.p, P0.val.p);
-        launched(c);
-        Csr Y = spgemm(c, cur, P0, nullptr, false, nullptr);
-        DBuf<int> cnt(n, c->s);
-        k_build_p<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, Y.ptr.p, Y.idx.p, Y.val.p, dagg.p,
-                                                             dinv.p, damping, nullptr, cnt.p, nullptr,
-                                                             nullptr);
-        launched(c);
+        static const bool p_generic = [] { const char *e = std::getenv("DPP_P_GENERIC"); return e && *e == '1'; }();
         L->P.rows = n;
         L->P.cols = (int)nc;
-        L->P.nnz = counts_to_ptr(c, cnt.p, n, L->P.ptr);
-        L->P.idx.alloc(L->P.nnz, c->s);
-        L->P.val.alloc(L->P.nnz, c->s);
-        k_build_p<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, Y.ptr.p, Y.idx.p, Y.val.p, dagg.p,
-                                                             dinv.p, damping, L->P.ptr.p, nullptr,
-                                                             L->P.idx.p, L->P.val.p);
-        launched(c);
+        DBuf<int> cnt(n, c->s);
+        if (p_generic) {
+            Csr P0;
+            P0.alloc(n, (int)nc, n, c->s);
+            k_p0<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(n, dagg.p, P0.ptr.p, P0.idx.p, P0.val.p);
+            launched(c);
+            Csr Y = spgemm(c, cur, P0, nullptr, false, nullptr);
+            k_build_p<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, Y.ptr.p, Y.idx.p, Y.val.p, dagg.p, dinv.p,
+                                                                 damping, nullptr, cnt.p, nullptr, nullptr);
+            launched(c);
+            L->P.nnz = counts_to_ptr(c, cnt.p, n, L->P.ptr);
+            L->P.idx.alloc(L->P.nnz, c->s);
+            L->P.val.alloc(L->P.nnz, c->s);
+            k_build_p<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, Y.ptr.p, Y.idx.p, Y.val.p, dagg.p, dinv.p,
+                                                                 damping, L->P.ptr.p, nullptr, L->P.idx.p,
+                                                                 L->P.val.p);
+            launched(c);
+        } else {
+            const int g = grid_for((int64_t)n * 32, 256, c->sms, 8);
+            k_p_direct<4><<<g, 256, 0, c->s>>>(n, cur.ptr.p, cur.idx.p, cur.val.p, dagg.p, dinv.p, damping,
+                                                nullptr, cnt.p, nullptr, nullptr);
+            launched(c);
+            L->P.nnz = counts_to_ptr(c, cnt.p, n, L->P.ptr);
+            L->P.idx.alloc(L->P.nnz, c->s);
+            L->P.val.alloc(L->P.nnz, c->s);
+            k_p_direct<4><<<g, 256, 0, c->s>>>(n, cur.ptr.p, cur.idx.p, cur.val.p, dagg.p, dinv.p, damping,
+                                                L->P.ptr.p, nullptr, L->P.idx.p, L->P.val.p);
+            launched(c);
+        }
         Csr next;
         {
             DPP_TRACE_SCOPE(c, "amg.rap");

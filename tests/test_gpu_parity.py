@@ -238,6 +238,24 @@ def test_selfp_and_amg_match_oracle(form, dim, kind, n, rng):
     assert rel_close(dpp.amg_vcycle(h, r), oracle.amg_vcycle(ho, r), 1e-10)
 
 
+@pytest.mark.parametrize("form,dim,kind,n", [("hdiv", 2, "tri", 16), ("cgvms", 3, "tet", 6), ("dgvms", 2, "tri", 6)])
+def test_amg_prolongator_bitwise(form, dim, kind, n):
+    """P = P0 - (2 w / rho) Dinv (A P0) (linalg.py:369-371) with scipy's own rounding, rebuilt
+    here from the device's operator, aggregates and rho: the device forms P without A @ P0
+    (warp-per-row key extraction) and must agree bit for bit, pattern and order included."""
+    bs, obs = systems(form, dim, kind, n)
+    S = dpp.schur_selfp(obs.k1_pp, obs.k1_pu, oracle.diag_lump(obs.k1_uu), obs.k1_up)
+    h = dpp.amg_setup(S)
+    for lv in h.levels[:-1]:
+        A = lv.A.tocsr()
+        nr, nc = A.shape[0], lv.P.shape[1]
+        P0 = sp.csr_matrix((np.ones(nr), (np.arange(nr), lv.aggregates)), shape=(nr, nc))
+        Dinv = sp.diags(1.0 / A.diagonal(), format="csr")
+        P = (P0 - (2.0 * (2.0 / 3.0) / lv.rho) * (Dinv @ (A @ P0))).tocsr()
+        P.sort_indices()
+        assert same_pattern(lv.P, P) and np.array_equal(lv.P.data, P.data)
+
+
 def test_amg_known_answers(rng):
     # reference tests/test_linalg.py:234-305
     A = poisson_1d(63)
