@@ -125,79 +125,153 @@ __global__ void k_build_p(int rows, const int *yp, const int *yi, const double *
 // Same P straight from A and the aggregates, without forming A @ P0: (A P0)_ij is the
 // sum of a_ik over the row's entries with agg[k] == j, accumulated from 0 in storage
 // order (scipy csr_matmat with b_kj = 1.0, so a_ik * 1.0 is exact), columns ascending.
-// Warp per row; distinct aggregate ids are extracted in ascending order by warp
-// min-reductions, each key's sum by walking its ballot mask in lane (= storage) order.
-// Rows up to 32*RC entries keep (key, value) in registers, longer rows re-read them.
-template <int RC>
-__global__ void __launch_bounds__(256) k_p_direct(int rows, const int *__restrict__ ap, const int *__restrict__ ai,
-                                                  const double *__restrict__ av, const int *__restrict__ agg,
-                                                  const double *__restrict__ dinv, double damping,
-                                                  const int *__restrict__ optr, int *cnt, int *oi, double *ov) {
-    const int lane = threadIdx.x & 31;
+// Warp per row, 32 entries at a time: __match_any groups a chunk's lanes by key, the
+// group leader finds (or appends) the key in the warp's shared list of distinct keys
+// and adds the group's values to that key's running sum one member at a time in lane
+// (= storage) order.  The diagonal aggregate seeds the list with sum +0.0, so it is
+// always present without changing any sum.  Output slots are ranks among the distinct
+// keys (exact-zero results squeezed out).  Rows with PD_CAP or more entries extract
+// keys one at a time.
+constexpr int PD_CAP = 512, PD_W = 8;
+constexpr size_t PD_SMEM = (size_t)PD_W * PD_CAP * 12;
+__global__ void __launch_bounds__(32 * PD_W) k_p_direct(int rows, const int *__restrict__ ap,
+                                                        const int *__restrict__ ai, const double *__restrict__ av,
+                                                        const int *__restrict__ agg, const double *__restrict__ dinv,
+                                                        double damping, int ncols, int *__restrict__ cnt, int *__restrict__ oi,
+                                                        double *__restrict__ ov) {
+    extern __shared__ __align__(16) unsigned char pd_smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double *dy = reinterpret_cast<double *>(pd_smem) + (size_t)wid * PD_CAP;
+    int *dk = reinterpret_cast<int *>(pd_smem + (size_t)PD_W * PD_CAP * 8) + (size_t)wid * PD_CAP;
+    const unsigned lt = (1u << lane) - 1;
     for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
          r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-        const int s = ap[r], e = ap[r + 1], a = agg[r];
+        const int s = ap[r], e = ap[r + 1], a = agg[r], len = e - s;
         const double di = dinv[r];
-        const bool regs = e - s <= 32 * RC;
-        int kk[RC];
-        double vv[RC];
+        const int w0 = s + (int)r;   // scratch slot: at most len + 1 outputs
+        if (len < PD_CAP || ncols <= PD_CAP) {   // distinct keys <= min(len + 1, ncols)
+            __syncwarp();
+            if (lane == 0) { dk[0] = a; dy[0] = 0.0; }
+            int nd = 1;
+            __syncwarp();
+            // keys / values of up to PD_PF chunks are loaded before any is processed
+            constexpr int PD_PF = 3;
+            for (int base0 = s; base0 < e; base0 += 32 * PD_PF) {
+                int kq[PD_PF];
+                double vq[PD_PF];
 #pragma unroll
-        for (int q = 0; q < RC; ++q) {
-            const int p = s + q * 32 + lane;
-            kk[q] = -1;
-            vv[q] = 0.0;
-            if (regs && p < e) { kk[q] = agg[ai[p]]; vv[q] = av[p]; }
+                for (int q = 0; q < PD_PF; ++q) {
+                    const int p = base0 + 32 * q + lane;
+                    kq[q] = p < e ? ai[p] : -1;
+                    vq[q] = p < e ? av[p] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < PD_PF; ++q)
+                    if (kq[q] >= 0) kq[q] = agg[kq[q]];
+#pragma unroll
+                for (int q = 0; q < PD_PF; ++q) {
+                    if (base0 + 32 * q >= e) break;
+                    const int k = kq[q];
+                    const double v = vq[q];
+                    const bool valid = k >= 0;
+                    const unsigned g = __match_any_sync(0xffffffffu, k);
+                    const bool lead = valid && (g & lt) == 0;
+                    int slot = -1;
+                    if (lead)
+                        for (int j = 0; j < nd; ++j)
+                            if (dk[j] == k) { slot = j; break; }
+                    const unsigned nm = __ballot_sync(0xffffffffu, lead && slot < 0);
+                    if (lead && slot < 0) {
+                        slot = nd + __popc(nm & lt);
+                        dk[slot] = k;
+                        dy[slot] = 0.0;
+                    }
+                    nd += __popc(nm);
+                    const int gs = lead ? __popc(g) : 0;
+                    const int rounds = __reduce_max_sync(0xffffffffu, gs);
+                    double y = lead ? dy[slot] : 0.0;
+                    unsigned rem = lead ? g : 0u;   // members not yet added, lowest lane first
+                    for (int t = 0; t < rounds; ++t) {
+                        const int src = rem ? __ffs(rem) - 1 : lane;
+                        const double vt = __shfl_sync(0xffffffffu, v, src);
+                        if (rem) y = __dadd_rn(y, vt);
+                        rem &= rem - 1;
+                    }
+                    if (lead) dy[slot] = y;
+                    __syncwarp();
+                }
+            }
+            // values, then ranks among the nonzero distinct keys
+            bool zero = false;
+            for (int j = lane; j < nd; j += 32) {
+                const double dw = __dmul_rn(damping, __dmul_rn(di, dy[j]));
+                const double v = dk[j] == a ? __dsub_rn(1.0, dw) : -dw;
+                dy[j] = v;
+                zero |= v == 0.0;
+            }
+            zero = __any_sync(0xffffffffu, zero);
+            __syncwarp();
+            int nz = 0;
+            for (int j = lane; j < nd; j += 32) {
+                const int k = dk[j];
+                const double v = dy[j];
+                int pos = 0;
+                for (int q = 0; q < nd; ++q) pos += dk[q] < k && (!zero || dy[q] != 0.0);
+                if (v != 0.0) {
+                    oi[w0 + pos] = k;
+                    ov[w0 + pos] = v;
+                    ++nz;
+                }
+            }
+            nz = __reduce_add_sync(0xffffffffu, nz);
+            if (lane == 0) cnt[r] = nz;
+            continue;
         }
-        int w = optr ? optr[r] : 0, n = 0, last = -1;
+        int w = w0, n = 0, last = -1;
         for (;;) {
             int mk = a > last ? a : INT_MAX;
-            if (regs) {
-#pragma unroll
-                for (int q = 0; q < RC; ++q)
-                    if (kk[q] > last && kk[q] < mk) mk = kk[q];
-            } else {
-                for (int p = s + lane; p < e; p += 32) {
-                    const int k = agg[ai[p]];
-                    if (k > last && k < mk) mk = k;
-                }
+            for (int p = s + lane; p < e; p += 32) {
+                const int k = agg[ai[p]];
+                if (k > last && k < mk) mk = k;
             }
             for (int o = 16; o > 0; o >>= 1) mk = min(mk, __shfl_xor_sync(0xffffffffu, mk, o));
             if (mk == INT_MAX) break;
             double y = 0.0;
-            if (regs) {
-#pragma unroll
-                for (int q = 0; q < RC; ++q) {
-                    if (s + q * 32 >= e) break;
-                    unsigned m = __ballot_sync(0xffffffffu, kk[q] == mk);
-                    while (m) {
-                        const int b = __ffs(m) - 1;
-                        y = __dadd_rn(y, __shfl_sync(0xffffffffu, vv[q], b));
-                        m &= m - 1;
-                    }
-                }
-            } else {
-                for (int base = s; base < e; base += 32) {
-                    const int p = base + lane;
-                    const bool hit = p < e && agg[ai[p]] == mk;
-                    const double v = hit ? av[p] : 0.0;
-                    unsigned m = __ballot_sync(0xffffffffu, hit);
-                    while (m) {
-                        const int b = __ffs(m) - 1;
-                        y = __dadd_rn(y, __shfl_sync(0xffffffffu, v, b));
-                        m &= m - 1;
-                    }
+            for (int base = s; base < e; base += 32) {
+                const int p = base + lane;
+                const bool hit = p < e && agg[ai[p]] == mk;
+                const double v = hit ? av[p] : 0.0;
+                unsigned m = __ballot_sync(0xffffffffu, hit);
+                while (m) {
+                    const int b = __ffs(m) - 1;
+                    y = __dadd_rn(y, __shfl_sync(0xffffffffu, v, b));
+                    m &= m - 1;
                 }
             }
             const double dw = __dmul_rn(damping, __dmul_rn(di, y));
             const double v = mk == a ? __dsub_rn(1.0, dw) : -dw;
             if (v != 0.0) {
-                if (oi && lane == 0) { oi[w] = mk; ov[w] = v; }
+                if (lane == 0) { oi[w] = mk; ov[w] = v; }
                 ++w;
                 ++n;
             }
             last = mk;
         }
-        if (cnt && lane == 0) cnt[r] = n;
+        if (lane == 0) cnt[r] = n;
+    }
+}
+
+__global__ void k_p_compact(int rows, const int *__restrict__ ap, const int *__restrict__ ptr,
+                            const int *__restrict__ ti, const double *__restrict__ tv, int *oi, double *ov) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t s = ap[r] + r;
+        const int o = ptr[r], n = ptr[r + 1] - o;
+        for (int q = lane; q < n; q += 32) {
+            oi[o + q] = ti[s + q];
+            ov[o + q] = tv[s + q];
+        }
     }
 }
 
@@ -461,15 +535,22 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
                                                                  L->P.val.p);
             launched(c);
         } else {
-            const int g = grid_for((int64_t)n * 32, 256, c->sms, 8);
-            k_p_direct<4><<<g, 256, 0, c->s>>>(n, cur.ptr.p, cur.idx.p, cur.val.p, dagg.p, dinv.p, damping,
-                                                nullptr, cnt.p, nullptr, nullptr);
+            static bool pattr = false;
+            if (!pattr) {
+                CK(cudaFuncSetAttribute(k_p_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PD_SMEM));
+                pattr = true;
+            }
+            const int g = grid_for((int64_t)n * 32, 32 * PD_W, c->sms, 4);
+            DBuf<int> ti(cur.nnz + n, c->s);
+            DBuf<double> tv(cur.nnz + n, c->s);
+            k_p_direct<<<g, 32 * PD_W, PD_SMEM, c->s>>>(n, cur.ptr.p, cur.idx.p, cur.val.p, dagg.p, dinv.p, damping,
+                                                       (int)nc, cnt.p, ti.p, tv.p);
             launched(c);
             L->P.nnz = counts_to_ptr(c, cnt.p, n, L->P.ptr);
             L->P.idx.alloc(L->P.nnz, c->s);
             L->P.val.alloc(L->P.nnz, c->s);
-            k_p_direct<4><<<g, 256, 0, c->s>>>(n, cur.ptr.p, cur.idx.p, cur.val.p, dagg.p, dinv.p, damping,
-                                                L->P.ptr.p, nullptr, L->P.idx.p, L->P.val.p);
+            k_p_compact<<<grid_for((int64_t)n * 32, 256, c->sms, 8), 256, 0, c->s>>>(n, cur.ptr.p, L->P.ptr.p, ti.p,
+                                                                                    tv.p, L->P.idx.p, L->P.val.p);
             launched(c);
         }
         Csr next;
