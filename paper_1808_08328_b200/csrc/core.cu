@@ -552,19 +552,25 @@ void csr_diag(Ctx *c, const Csr &A, double *d, int *missing) {
 }
 
 // transpose via stable radix sort of (col,row) keys: rows of A^T ascending in A's row
-__global__ void k_coo_keys(int rows, const int *ptr, const int *idx, uint64_t *key, int *pos) {
-    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
-        for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
-            key[p] = ((uint64_t)(uint32_t)idx[p] << 32) | (uint32_t)r;
+// Transpose = stable radix sort of the column ids (entries enter in row-major order,
+// so rows stay ascending inside every column): only ceil(log2(cols)) key bits.
+__global__ void k_coo_keys(int rows, const int *ptr, const int *idx, unsigned *key, int *pos, int *rowof) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5)
+        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
+            key[p] = (unsigned)idx[p];
             pos[p] = p;
+            rowof[p] = (int)r;
         }
 }
-__global__ void k_tr_fill(int64_t nnz, const uint64_t *key, const int *pos, const double *val,
+__global__ void k_tr_fill(int64_t nnz, const unsigned *key, const int *pos, const int *rowof, const double *val,
                           int *oidx, double *oval, int *cnt) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz; i += (int64_t)gridDim.x * blockDim.x) {
-        oidx[i] = (int)(key[i] & 0xffffffffu);
-        oval[i] = val[pos[i]];
-        atomicAdd(&cnt[key[i] >> 32], 1);
+        const int p = pos[i];
+        oidx[i] = rowof[p];
+        oval[i] = val[p];
+        atomicAdd(&cnt[key[i]], 1);
     }
 }
 Csr csr_transpose(Ctx *c, const Csr &A) {
@@ -577,16 +583,20 @@ Csr csr_transpose(Ctx *c, const Csr &A) {
     T.idx.alloc((size_t)A.nnz, c->s);
     T.val.alloc((size_t)A.nnz, c->s);
     if (A.nnz) {
-        DBuf<uint64_t> k0(A.nnz, c->s), k1(A.nnz, c->s);
-        DBuf<int> p0(A.nnz, c->s), p1(A.nnz, c->s);
-        k_coo_keys<<<grid_for(A.rows, 256, c->sms), 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, k0.p, p0.p);
+        DBuf<unsigned> k0(A.nnz, c->s), k1(A.nnz, c->s);
+        DBuf<int> p0(A.nnz, c->s), p1(A.nnz, c->s), rowof(A.nnz, c->s);
+        k_coo_keys<<<grid_for((int64_t)A.rows * 32, 256, c->sms, 8), 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, k0.p,
+                                                                                   p0.p, rowof.p);
         launched(c);
+        int bits = 1;
+        while (bits < 32 && ((int64_t)1 << bits) < (int64_t)A.cols) ++bits;
         size_t tb = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.p, k1.p, p0.p, p1.p, (int)A.nnz, 0, 64, c->s));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.p, k1.p, p0.p, p1.p, (int)A.nnz, 0, bits, c->s));
         DBuf<char> t(tb, c->s);
-        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, k0.p, k1.p, p0.p, p1.p, (int)A.nnz, 0, 64, c->s));
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, k0.p, k1.p, p0.p, p1.p, (int)A.nnz, 0, bits, c->s));
         launched(c);
-        k_tr_fill<<<grid_for(A.nnz, 256, c->sms), 256, 0, c->s>>>(A.nnz, k1.p, p1.p, A.val.p, T.idx.p, T.val.p, cnt.p);
+        k_tr_fill<<<grid_for(A.nnz, 256, c->sms), 256, 0, c->s>>>(A.nnz, k1.p, p1.p, rowof.p, A.val.p, T.idx.p,
+                                                                  T.val.p, cnt.p);
         launched(c);
     }
     counts_to_ptr(c, cnt.p, A.cols, T.ptr);

@@ -254,6 +254,13 @@ def test_amg_prolongator_bitwise(form, dim, kind, n):
         P = (P0 - (2.0 * (2.0 / 3.0) / lv.rho) * (Dinv @ (A @ P0))).tocsr()
         P.sort_indices()
         assert same_pattern(lv.P, P) and np.array_equal(lv.P.data, P.data)
+    # Galerkin products A_c = R (A P), R = P^T (the device transpose is a stable sort of
+    # column ids); coarse rows may be split-k summed, so entries agree to rounding
+    for lv, nx in zip(h.levels[:-1], h.levels[1:]):
+        A, P = lv.A.tocsr(), lv.P.tocsr()
+        Ac = (P.T.tocsr() @ (A @ P)).tocsr()
+        Ac.sort_indices()
+        assert abs(nx.A - Ac).max() <= 1e-14 * abs(Ac).max()
 
 
 def test_amg_known_answers(rng):
