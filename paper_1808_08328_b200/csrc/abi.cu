@@ -45,8 +45,8 @@ int dpp_ctx_create(int device, dpp_ctx **out) {
         auto *h = new dpp_ctx;
         h->c.device = device;
         CK(cudaDeviceGetAttribute(&h->c.sms, cudaDevAttrMultiProcessorCount, device));
-        CK(cudaStreamCreateWithFlags(&h->c.s, cudaStreamNonBlocking));
-        CK(cudaStreamCreateWithFlags(&h->c.s2, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithPriority(&h->c.s, cudaStreamNonBlocking, stream_priority(false)));
+        CK(cudaStreamCreateWithPriority(&h->c.s2, cudaStreamNonBlocking, stream_priority(false)));
         CK(cudaMalloc(&h->c.nrm_part, sizeof(double) * NRM_BLOCKS));
         CK(cudaMalloc(&h->c.nrm_part2, sizeof(double) * NRM_BLOCKS));
         cudaMemPool_t pool;

@@ -572,7 +572,7 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
         AmgLevel *Lp = L.get();
         for (int q = 0; q < 2; ++q) {
             h->lvside.push_back(std::make_unique<SideStream>());
-            h->lvside.back()->ensure(c);
+            h->lvside.back()->ensure(c, true);
         }
         Ctx *sc = &h->lvside[h->lvside.size() - 2]->ctx, *su = &h->lvside.back()->ctx;
         auto smoother_lo = [Lp, sc] {

@@ -193,10 +193,14 @@ struct Csr {
 // A side stream plus a context view bound to it.  Objects built through the
 // view allocate (and later free) on the side stream, so the owner of those
 // objects must also own the SideStream and destroy it last.
+// stream priorities: setup work off the critical path (smoother plans, the ILU branch)
+// runs on low-priority streams so the AMG level chain's small kernels are scheduled first
+int stream_priority(bool low);
 struct SideStream {
     cudaStream_t s = nullptr;
+    int low = 0;
     Ctx ctx;
-    void ensure(Ctx *parent);
+    void ensure(Ctx *parent, bool low_prio = false);
     ~SideStream();
 };
 // run side(view) on a host thread with the side stream while main_fn() runs here

@@ -39,24 +39,28 @@ TraceScope::~TraceScope() {
 // branches have work in flight was measured at ~6 ms (at the head of every AMG setup)
 namespace {
 std::mutex g_pool_mu;
-std::vector<std::pair<int, cudaStream_t>> g_pool;   // (device, idle stream)
-cudaStream_t pool_acquire(int device) {
+struct Pooled {
+    int device, low;
+    cudaStream_t s;
+};
+std::vector<Pooled> g_pool;   // idle streams
+cudaStream_t pool_acquire(int device, int low) {
     {
         std::lock_guard<std::mutex> lk(g_pool_mu);
         for (size_t i = 0; i < g_pool.size(); ++i)
-            if (g_pool[i].first == device) {
-                cudaStream_t s = g_pool[i].second;
+            if (g_pool[i].device == device && g_pool[i].low == low) {
+                cudaStream_t s = g_pool[i].s;
                 g_pool.erase(g_pool.begin() + (long)i);
                 return s;
             }
     }
     cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, stream_priority(low != 0)));
     return s;
 }
-void pool_release(int device, cudaStream_t s) {
+void pool_release(int device, int low, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    g_pool.push_back({device, s});
+    g_pool.push_back({device, low, s});
 }
 }  // namespace
 
@@ -85,9 +89,17 @@ void pinned_release(PinnedBuf b) {
     g_pin_free.push_back(b);
 }
 
-void SideStream::ensure(Ctx *parent) {
+int stream_priority(bool low) {
+    static const bool off = [] { const char *e = std::getenv("DPP_NO_PRIO"); return e && *e == '1'; }();
+    int least = 0, greatest = 0;
+    if (off || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) return 0;
+    return low ? least : greatest;
+}
+
+void SideStream::ensure(Ctx *parent, bool low_prio) {
     if (s) return;
-    s = pool_acquire(parent->device);
+    low = low_prio;
+    s = pool_acquire(parent->device, low);
     ctx = *parent;
     ctx.s = ctx.s2 = s;
     ctx.launches = 0;
@@ -101,7 +113,7 @@ SideStream::~SideStream() {
     if (!s) return;
     if (ctx.nrm_part) cudaFreeAsync(ctx.nrm_part, s);
     cudaStreamSynchronize(s);
-    pool_release(ctx.device, s);
+    pool_release(ctx.device, low, s);
 }
 
 bool pdl_on() {
@@ -121,7 +133,7 @@ int fork_mask() {
 
 void fork_join(Ctx *c, SideStream &owner, const std::function<void(Ctx *)> &side,
                const std::function<void()> &main_fn, int kind) {
-    owner.ensure(c);
+    owner.ensure(c, kind == FORK_SCHUR);   // the Schur fork's side branch (ILU setup) has slack
     CK(cudaStreamSynchronize(c->s));   // inputs produced on the parent stream are ready
     if (!(fork_mask() & kind)) {
         side(&owner.ctx);
