@@ -419,7 +419,7 @@ static void coarse_setup(Ctx *c, Amg &h, const Csr &A) {
 
 // ---------------------------------------------------------------- setup
 std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega, int max_coarse,
-                               int max_levels, dpp_randn_fn randn, void *user) {
+                               int max_levels, dpp_randn_fn randn, void *user, Csr *A0_steal) {
     DPP_TRACE_SCOPE(c, "amg.total");
     if (A0.rows != A0.cols) DPP_FAIL(DPP_ERR_VALUE, "amg_setup requires a square matrix");
     auto h = std::make_unique<Amg>();
@@ -428,12 +428,13 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
         DPP_TRACE_SCOPE(c, "amg.diag_check");
         DBuf<double> d(A0.rows, c->s);
         csr_diag(c, A0, d.p, nullptr);
-        std::vector<double> hd = d.to_host();
-        for (double v : hd)
-            if (v == 0.0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "structurally singular input: zero diagonal entry");
+        if (any_zero_dev(c, A0.rows, d.p))
+            DPP_FAIL(DPP_ERR_ZERO_PIVOT, "structurally singular input: zero diagonal entry");
     }
     Csr cur;
-    {
+    if (A0_steal && A0_steal == &A0) {
+        cur = std::move(*A0_steal);
+    } else {
         DPP_TRACE_SCOPE(c, "amg.copy");
         cur = csr_copy(c, A0);
     }

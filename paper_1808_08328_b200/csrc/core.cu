@@ -544,6 +544,24 @@ __global__ void k_diag(int rows, const int *ptr, const int *idx, const double *v
         }
     }
 }
+__global__ void k_count_zero(int64_t n, const double *d, int *cnt) {
+    int z = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        z += d[i] == 0.0;
+    z = __reduce_add_sync(0xffffffffu, z);
+    if ((threadIdx.x & 31) == 0 && z) atomicAdd(cnt, z);
+}
+bool any_zero_dev(Ctx *c, int64_t n, const double *d) {
+    if (n <= 0) return false;
+    DBuf<int> cnt(1, c->s);
+    CK(cudaMemsetAsync(cnt.p, 0, sizeof(int), c->s));
+    k_count_zero<<<grid_for(n, 256, c->sms, 4), 256, 0, c->s>>>(n, d, cnt.p);
+    launched(c);
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, cnt.p, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return h != 0;
+}
 void csr_diag(Ctx *c, const Csr &A, double *d, int *missing) {
     int n = std::min(A.rows, A.cols);
     if (!n) return;
@@ -551,7 +569,6 @@ void csr_diag(Ctx *c, const Csr &A, double *d, int *missing) {
     launched(c);
 }
 
-// transpose via stable radix sort of (col,row) keys: rows of A^T ascending in A's row
 // Transpose = stable radix sort of the column ids (entries enter in row-major order,
 // so rows stay ascending inside every column): only ceil(log2(cols)) key bits.
 __global__ void k_coo_keys(int rows, const int *ptr, const int *idx, unsigned *key, int *pos, int *rowof) {

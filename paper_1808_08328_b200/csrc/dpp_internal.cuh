@@ -245,6 +245,8 @@ Csr csr_drop_zeros(Ctx *c, const Csr &A);
 // part: -1 strict lower, 0 diag only, +1 strict upper, 2 lower incl diag, 3 upper incl diag
 Csr csr_part(Ctx *c, const Csr &A, int part, bool drop_zeros);
 void csr_diag(Ctx *c, const Csr &A, double *d_out, int *missing_dev);
+// any exact zero among d[0..n) (one 4-byte read back instead of the whole vector)
+bool any_zero_dev(Ctx *c, int64_t n, const double *d);
 Csr csr_transpose(Ctx *c, const Csr &A);
 // rows/cols selected by segment lists of the parent index space (order preserving)
 Csr csr_submatrix(Ctx *c, const Csr &M, const std::vector<std::pair<int, int>> &rowseg,
@@ -356,8 +358,9 @@ struct Amg {
     DBuf<double> coarse_inv;   // dense inverse of the coarsest operator (row-major)
     int nc = 0;
 };
+// A0_steal: optional; its storage becomes level 0 (no copy) when the caller is done with it
 std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A, double theta, double omega, int max_coarse,
-                               int max_levels, dpp_randn_fn randn, void *user);
+                               int max_levels, dpp_randn_fn randn, void *user, Csr *A0_steal = nullptr);
 void amg_vcycle(Ctx *c, Amg &h, const double *r, double *z, cudaStream_t st = nullptr);
 
 // ---- launch bookkeeping for graph capture ----------------------------------

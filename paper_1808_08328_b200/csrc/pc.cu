@@ -225,9 +225,7 @@ struct Builder {
         {
             DPP_TRACE_SCOPE(c, "pc.schur_diag");
             csr_diag(c, A, d.p, nullptr);
-            std::vector<double> hd = d.to_host();
-            for (double v : hd)
-                if (v == 0.0) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero diagonal entry in diag_lump");
+            if (any_zero_dev(c, N->nA, d.p)) DPP_FAIL(DPP_ERR_ZERO_PIVOT, "zero diagonal entry in diag_lump");
             reciprocal(c, N->nA, d.p, dinv.p);
         }
         Csr S;
@@ -244,6 +242,12 @@ struct Builder {
                       } else {
                           N->a = bb.leaf_on(nd.child_type[0], A);
                       }
+                      // the coupling operators of the apply (zero-free copies + SpMV plans)
+                      // are built here too, off the S_p -> AMG critical path
+                      N->Bc = csr_drop_zeros(sc, B);
+                      N->Cc = csr_drop_zeros(sc, C);
+                      spmv_plan(sc, N->Bc);
+                      spmv_plan(sc, N->Cc);
                   },
                   [&] {
                       {
@@ -256,14 +260,15 @@ struct Builder {
                           N->b.type = DPP_LEAF_NESTED;
                           N->b.node = node(nd.child_node[1], gB, &S);
                           N->b.desc = N->b.node->desc;
+                      } else if (nd.child_type[1] == DPP_LEAF_AMG) {
+                          // S_p is not needed after the hierarchy is built: it becomes level 0
+                          N->b.type = DPP_LEAF_AMG;
+                          N->b.amg = amg_setup(c, S, 0.5, 2.0 / 3.0, 64, 25, randn, user, &S);
+                          N->b.desc = "amg[" + std::to_string(N->b.amg->lv.size()) + "]";
                       } else {
                           N->b = leaf_on(nd.child_type[1], S);
                       }
                   }, FORK_SCHUR);
-        N->Bc = csr_drop_zeros(c, B);
-        N->Cc = csr_drop_zeros(c, C);
-        spmv_plan(c, N->Bc);
-        spmv_plan(c, N->Cc);
         N->desc = "schur-full(" + N->a.desc + ", selfp->" + N->b.desc + ")";
         CK(cudaStreamSynchronize(c->s));
         return N;

@@ -160,13 +160,24 @@ __global__ void __launch_bounds__(32 * US_W) k_unique_s(int rows, const int *ap,
         };
         if (dp)
             for (int p = dp[row] + lane; p < dp[row + 1]; p += 32) ins(di[p]);
-        // the symbolic pass needs no k order: each lane inserts its own k's B row
-        for (int p = ap[row] + lane; p < ap[row + 1]; p += 32) {
-            const int kq = ai[p];
-            const int rs = bp[kq], re = bp[kq + 1];
-            for (int r = rs; r < re; ++r) {
-                ins(bi[r]);
-                if (over) break;
+        // the symbolic pass needs no k order: each lane inserts its own k's B row, four
+        // column ids loaded ahead of the inserts (the CAS loop would serialise them)
+        for (int p0 = ap[row]; p0 < ap[row + 1]; p0 += 32) {
+            const int p = p0 + lane;
+            int rs = 0, re = 0;
+            if (p < ap[row + 1]) {
+                const int kq = ai[p];
+                rs = bp[kq];
+                re = bp[kq + 1];
+            }
+            const int mlen = __reduce_max_sync(0xffffffffu, re - rs);
+            for (int u = 0; u < mlen; u += 4) {
+                int j[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) j[q] = rs + u + q < re ? bi[rs + u + q] : -1;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (j[q] >= 0) ins(j[q]);
             }
         }
         over = __any_sync(0xffffffffu, over);
