@@ -22,7 +22,10 @@
 // Small column spaces (coarse levels) use a dense per-warp accumulator instead,
 // whose survivors come out in column order without sorting.
 #include <cstdio>
+#include <cstdlib>
 #include <new>
+
+#include <cub/cub.cuh>
 
 #include "dpp_internal.cuh"
 
@@ -509,6 +512,32 @@ void launch_num_t(Ctx *c, const Args &a, int nrl) {
     launched(c);
 }
 template <int CAP, int W, int K>
+void launch_num_dev(Ctx *c, Args a, const int *rl, int nrl) {
+    if (nrl <= 0) return;
+    a.rl = rl;
+    a.nrl = nrl;
+    if (a.dp) launch_num_t<CAP, W, K, true>(c, a, a.nrl);
+    else launch_num_t<CAP, W, K, false>(c, a, a.nrl);
+}
+
+// rows -> size-class lists (order inside a list is irrelevant: every row writes only
+// its own scratch range), class counts in meta[0..2], overflow rows counted in meta[3]
+__global__ void k_sp_classify(int rows, const int *u, int *lists, int *meta) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+        const int v = u[r];
+        if (v < 0) { atomicAdd(&meta[3], 1); continue; }
+        const int64_t need = 2 * (int64_t)v + 2;
+        const int cls = need <= 256 ? 0 : need <= 1024 ? 1 : need <= 4096 ? 2 : 3;
+        if (cls == 3) { atomicAdd(&meta[3], 1); continue; }
+        lists[(size_t)cls * rows + atomicAdd(&meta[cls], 1)] = r;
+    }
+}
+__global__ void k_sp_widen(const int *u, int64_t *o, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
+        o[i] = i < n ? max(u[i], 0) : 0;
+}
+
+template <int CAP, int W, int K>
 void launch_num(Ctx *c, Args a, const std::vector<int> &rows_h) {
     if (rows_h.empty()) return;
     DBuf<int> rl(rows_h.size(), c->s);
@@ -594,13 +623,64 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         launched(c);
     } else {
         // 1. symbolic: distinct columns per row
-        std::vector<int> u(rows);
+        std::vector<int> u;
+        DBuf<int> duniq(rows, c->s);
+        k_unique_s<<<std::max(1, std::min<int>((rows + US_W - 1) / US_W, c->sms * 7)), 32 * US_W, 0, c->s>>>(
+            rows, A.ptr.p, A.idx.p, B.ptr.p, B.idx.p, D ? D->ptr.p : nullptr, D ? D->idx.p : nullptr, duniq.p);
+        launched(c);
+        // common case (no row beyond the small symbolic table): scratch offsets and
+        // size-class row lists are built on the device, one small read back
+        DBuf<int> meta(4, c->s), lists((size_t)3 * rows, c->s);
+        DBuf<int64_t> toff64((size_t)rows + 1, c->s), uw((size_t)rows + 1, c->s);
+        int hm[4] = {0, 0, 0, 0};
+        int64_t ttot_d = 0;
+        {
+            DPP_TRACE_SCOPE(c, "spgemm.classify");
+            CK(cudaMemsetAsync(meta.p, 0, 4 * sizeof(int), c->s));
+            k_sp_classify<<<grid_for(rows, 256, c->sms, 4), 256, 0, c->s>>>(rows, duniq.p, lists.p, meta.p);
+            launched(c);
+            k_sp_widen<<<grid_for(rows + 1, 256, c->sms, 4), 256, 0, c->s>>>(duniq.p, uw.p, rows);
+            launched(c);
+            size_t tb = 0;
+            CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, uw.p, toff64.p, rows + 1, c->s));
+            DBuf<char> t(tb, c->s);
+            CK(cub::DeviceScan::ExclusiveSum(t.p, tb, uw.p, toff64.p, rows + 1, c->s));
+            launched(c);
+            CK(cudaMemcpyAsync(hm, meta.p, sizeof(hm), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaMemcpyAsync(&ttot_d, toff64.p + rows, sizeof(int64_t), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+        }
+        static const bool host_lists = [] { const char *e = std::getenv("DPP_SPGEMM_HOSTLIST"); return e && *e == '1'; }();
+        if (hm[3] == 0 && !host_lists) {
+            a.toff = toff64.p;
+            ti.alloc(std::max<int64_t>(ttot_d, 1), c->s);
+            tv.alloc(std::max<int64_t>(ttot_d, 1), c->s);
+            a.ti = ti.p;
+            a.tv = tv.p;
+            if (TraceScope::on())
+                std::fprintf(stderr, "[dpp-trace]   spgemm %d x %d (A nnz %lld, B nnz %lld): rows S %d M %d L %d (device lists)\n",
+                             rows, B.cols, (long long)A.nnz, (long long)B.nnz, hm[0], hm[1], hm[2]);
+            DPP_TRACE_SCOPE(c, "spgemm.numeric");
+            launch_num_dev<256, 8, 4>(c, a, lists.p, hm[0]);
+            launch_num_dev<1024, 4, 16>(c, a, lists.p + rows, hm[1]);
+            launch_num_dev<4096, 2, 0>(c, a, lists.p + 2 * (size_t)rows, hm[2]);
+            C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
+            if (C.nnz == ttot_d) {   // no exact-zero sums: the scratch is the result
+                C.idx = std::move(ti);
+                C.val = std::move(tv);
+            } else {
+                C.idx.alloc(std::max<int64_t>(C.nnz, 1), c->s);
+                C.val.alloc(std::max<int64_t>(C.nnz, 1), c->s);
+                k_compact<<<grid_for((int64_t)rows * 32, 256, c->sms, 8), 256, 0, c->s>>>(
+                    rows, toff64.p, C.ptr.p, ti.p, tv.p, C.idx.p, C.val.p);
+                launched(c);
+            }
+            CK(cudaStreamSynchronize(c->s));
+            return C;
+        }
+        u.resize(rows);
         {
             DPP_TRACE_SCOPE(c, "spgemm.unique");
-            DBuf<int> duniq(rows, c->s);
-            k_unique_s<<<std::max(1, std::min<int>((rows + US_W - 1) / US_W, c->sms * 7)), 32 * US_W, 0, c->s>>>(
-                rows, A.ptr.p, A.idx.p, B.ptr.p, B.idx.p, D ? D->ptr.p : nullptr, D ? D->idx.p : nullptr, duniq.p);
-            launched(c);
             duniq.download(u.data(), rows);
             CK(cudaStreamSynchronize(c->s));
             std::vector<int> over;

@@ -169,14 +169,21 @@ int tri_levels(Ctx *c, const Csr &S, bool backward, DBuf<int> &order, DBuf<int> 
     per_sm_w = std::max(1, per_sm_w / std::max(1, share));
     const int64_t warps_res = (int64_t)c->sms * per_sm_w * (block / 32);
     const double avg = n ? (double)S.nnz / n : 0.0;
+    // cooperative launches: the grid is co-resident by construction, even while other
+    // setup branches' kernels (or other spinning analyses) hold part of the device --
+    // a plain launch could leave blocks whose rows others wait on unscheduled
+    int nn = n, bw = backward ? 1 : 0;
+    const int *pp = S.ptr.p, *ii = S.idx.p;
+    int *lv = lev.p;
+    void *args[] = {&nn, &bw, &pp, &ii, &lv};
     if (n <= warps_res && avg > 8.0) {
         const int grid = (int)(((int64_t)n * 32 + block - 1) / block);
-        k_levels_warp<<<grid, block, 0, c->s>>>(n, backward, S.ptr.p, S.idx.p, lev.p);
+        CK(cudaLaunchCooperativeKernel((const void *)k_levels_warp, grid, block, args, 0, c->s));
     } else {
         const int64_t need = ((int64_t)n + 31) / 32 * 32;
         const int64_t cap = (int64_t)c->sms * per_sm * block;
         const int grid = (int)((std::min(need, cap) + block - 1) / block);
-        k_levels<<<grid, block, 0, c->s>>>(n, backward, S.ptr.p, S.idx.p, lev.p);
+        CK(cudaLaunchCooperativeKernel((const void *)k_levels, grid, block, args, 0, c->s));
     }
     launched(c);
     k_iota<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, rows.p);
