@@ -45,6 +45,7 @@ struct Args {
     const int *dp, *di;   // optional D
     const double *dv;
     int reverse, keep_zeros;
+    int bmax;             // longest B row (host-side choice of the register prefetch depth)
     // numeric pass: rows of this launch and their global tables (if any)
     const int *rl;
     int nrl;
@@ -259,7 +260,7 @@ __host__ __device__ constexpr int slot_bytes(bool has_d) { return 8 + (has_d ? 8
 
 // CAP: shared table slots per warp (0 => global tables); K: survivor keys per
 // lane held in registers for ranking (0 => rank loop over shared memory)
-template <int CAP, int W, int K, bool HD>
+template <int CAP, int W, int K, bool HD, int PF>
 __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             }
             __syncwarp();
         }
-        accumulate_row<PF_HASH>(a, row, lane, [&](int j, double pr) {
+        accumulate_row<PF>(a, row, lane, [&](int j, double pr) {
             const int sl = tab_slot(t, j);
             if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
             else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
@@ -499,17 +500,33 @@ __global__ void k_compact(int rows, const int64_t *toff, const int *ptr, const i
     }
 }
 
-template <int CAP, int W, int K, bool HD>
-void launch_num_t(Ctx *c, const Args &a, int nrl) {
+template <int CAP, int W, int K, bool HD, int PF>
+void launch_num_pf(Ctx *c, const Args &a, int nrl) {
     const size_t smem = (size_t)CAP * slot_bytes(HD) * W;
     static bool attr = false;
     if (!attr && smem > 48 * 1024) {
-        CK(cudaFuncSetAttribute(k_spgemm_num<CAP, W, K, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CK(cudaFuncSetAttribute(k_spgemm_num<CAP, W, K, HD, PF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem));
         attr = true;
     }
     const int grid = std::max(1, std::min<int>((nrl + W - 1) / W, c->sms * 32));
-    k_spgemm_num<CAP, W, K, HD><<<grid, 32 * W, smem, c->s>>>(a);
+    k_spgemm_num<CAP, W, K, HD, PF><<<grid, 32 * W, smem, c->s>>>(a);
     launched(c);
+}
+// B rows held in registers PF x 32 entries at a time: short B rows (the velocity /
+// pressure couplings, P) take one slot, so the per-k loop carries no idle slots
+template <int CAP, int W, int K, bool HD>
+void launch_num_t(Ctx *c, const Args &a, int nrl) {
+    if (a.bmax <= 32) launch_num_pf<CAP, W, K, HD, 1>(c, a, nrl);
+    else if (a.bmax <= 64) launch_num_pf<CAP, W, K, HD, 2>(c, a, nrl);
+    else launch_num_pf<CAP, W, K, HD, PF_HASH>(c, a, nrl);
+}
+__global__ void k_row_max(int rows, const int *ptr, int *out) {
+    int m = 0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+        m = max(m, ptr[r + 1] - ptr[r]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
 }
 template <int CAP, int W, int K>
 void launch_num_dev(Ctx *c, Args a, const int *rl, int nrl) {
@@ -630,14 +647,16 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         launched(c);
         // common case (no row beyond the small symbolic table): scratch offsets and
         // size-class row lists are built on the device, one small read back
-        DBuf<int> meta(4, c->s), lists((size_t)3 * rows, c->s);
+        DBuf<int> meta(5, c->s), lists((size_t)3 * rows, c->s);
         DBuf<int64_t> toff64((size_t)rows + 1, c->s), uw((size_t)rows + 1, c->s);
-        int hm[4] = {0, 0, 0, 0};
+        int hm[5] = {0, 0, 0, 0, 0};
         int64_t ttot_d = 0;
         {
             DPP_TRACE_SCOPE(c, "spgemm.classify");
-            CK(cudaMemsetAsync(meta.p, 0, 4 * sizeof(int), c->s));
+            CK(cudaMemsetAsync(meta.p, 0, 5 * sizeof(int), c->s));
             k_sp_classify<<<grid_for(rows, 256, c->sms, 4), 256, 0, c->s>>>(rows, duniq.p, lists.p, meta.p);
+            launched(c);
+            k_row_max<<<grid_for(B.rows, 256, c->sms, 4), 256, 0, c->s>>>(B.rows, B.ptr.p, meta.p + 4);
             launched(c);
             k_sp_widen<<<grid_for(rows + 1, 256, c->sms, 4), 256, 0, c->s>>>(duniq.p, uw.p, rows);
             launched(c);
@@ -651,6 +670,7 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
             CK(cudaStreamSynchronize(c->s));
         }
         static const bool host_lists = [] { const char *e = std::getenv("DPP_SPGEMM_HOSTLIST"); return e && *e == '1'; }();
+        a.bmax = hm[4];
         if (hm[3] == 0 && !host_lists) {
             a.toff = toff64.p;
             ti.alloc(std::max<int64_t>(ttot_d, 1), c->s);
