@@ -260,13 +260,18 @@ __host__ __device__ constexpr int slot_bytes(bool has_d) { return 8 + (has_d ? 8
 
 // CAP: shared table slots per warp (0 => global tables); K: survivor keys per
 // lane held in registers for ranking (0 => rank loop over shared memory)
-template <int CAP, int W, int K, bool HD, int PF>
+// TR (trial pass, no symbolic pass before it): every row, a budget of TR_LIM distinct
+// columns per row, survivors at row * TR_LIM in the scratch; a row over budget is
+// abandoned with cnt = -1 (the caller then runs the symbolic + sized passes instead)
+constexpr int TR_LIM = 128;
+template <int CAP, int W, int K, bool HD, int PF, bool TR = false>
 __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int tr_n[W];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned char *base = smem + (size_t)CAP * slot_bytes(HD) * w;
     for (int li = blockIdx.x * W + w; li < a.nrl; li += gridDim.x * W) {
-        const int row = a.rl[li];
+        const int row = TR ? li : a.rl[li];
         Table t;
         if (CAP > 0) {
             t.cap = CAP;
@@ -283,20 +288,48 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             t.d = a.g_d + go;
         }
         for (int h = lane; h < t.cap; h += 32) { t.key[h] = -1; t.has[h] = 0; }
+        if (TR && lane == 0) tr_n[w] = 0;
         __syncwarp();
+        // slot of column j; in a trial pass -1 once the row is over budget (inserts stop,
+        // so the table never fills: at most TR_LIM + 31 keys)
+        auto slot = [&](int j) -> int {
+            if (!TR) return tab_slot(t, j);
+            unsigned h = hsh(j) & (t.cap - 1);
+            while (true) {
+                const int cur = t.key[h];
+                if (cur == j) return (int)h;
+                if (cur == -1) {
+                    if (*(volatile int *)&tr_n[w] >= TR_LIM) return -1;
+                    const int old = atomicCAS(&t.key[h], -1, j);
+                    if (old == -1) { atomicAdd(&tr_n[w], 1); return (int)h; }
+                    if (old == j) return (int)h;
+                }
+                h = (h + 1) & (t.cap - 1);
+            }
+        };
         if (HD) {
             for (int p = a.dp[row] + lane; p < a.dp[row + 1]; p += 32) {
-                const int sl = tab_slot(t, a.di[p]);
+                const int sl = slot(a.di[p]);
+                if (TR && sl < 0) continue;
                 t.d[sl] = a.dv[p];
                 t.has[sl] |= 2;
             }
             __syncwarp();
         }
         accumulate_row<PF>(a, row, lane, [&](int j, double pr) {
-            const int sl = tab_slot(t, j);
+            const int sl = slot(j);
+            if (TR && sl < 0) return;
             if (t.has[sl] & 1) t.x[sl] = __dadd_rn(t.x[sl], pr);
             else { t.x[sl] = __dadd_rn(0.0, pr); t.has[sl] |= 1; }
         });
+        if (TR) {
+            __syncwarp();
+            if (*(volatile int *)&tr_n[w] >= TR_LIM) {
+                if (lane == 0) a.cnt[row] = -1;
+                __syncwarp();
+                continue;
+            }
+        }
         // survivors compacted in place, in slot order (a survivor's position never
         // exceeds its slot, so no unread slot is overwritten) ...
         int nsurv = 0;
@@ -323,7 +356,7 @@ __global__ void __launch_bounds__(32 * W) k_spgemm_num(Args a) {
             __syncwarp();
         }
         // ... ranked by column into the scratch
-        const int64_t o = a.toff[row];
+        const int64_t o = TR ? (int64_t)row * TR_LIM : a.toff[row];
         if (K > 0) {
             int mk[K > 0 ? K : 1], rk[K > 0 ? K : 1];
 #pragma unroll
@@ -521,6 +554,30 @@ void launch_num_t(Ctx *c, const Args &a, int nrl) {
     else if (a.bmax <= 64) launch_num_pf<CAP, W, K, HD, 2>(c, a, nrl);
     else launch_num_pf<CAP, W, K, HD, PF_HASH>(c, a, nrl);
 }
+__global__ void k_count_neg(int rows, const int *cnt, int *out) {
+    int z = 0;
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) z += cnt[r] < 0;
+    z = __reduce_add_sync(0xffffffffu, z);
+    if ((threadIdx.x & 31) == 0 && z) atomicAdd(out, z);
+}
+__global__ void k_stride_off(int rows, int stride, int64_t *toff) {
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
+        toff[r] = (int64_t)r * stride;
+}
+template <bool HD, int PF>
+void launch_trial_pf(Ctx *c, const Args &a) {
+    constexpr int CAP = 256, W = 8, K = 4;
+    const size_t smem = (size_t)CAP * slot_bytes(HD) * W;
+    const int grid = std::max(1, std::min<int>((a.nrl + W - 1) / W, c->sms * 32));
+    k_spgemm_num<CAP, W, K, HD, PF, true><<<grid, 32 * W, smem, c->s>>>(a);
+    launched(c);
+}
+template <bool HD>
+void launch_trial(Ctx *c, const Args &a) {
+    if (a.bmax <= 32) launch_trial_pf<HD, 1>(c, a);
+    else if (a.bmax <= 64) launch_trial_pf<HD, 2>(c, a);
+    else launch_trial_pf<HD, PF_HASH>(c, a);
+}
 __global__ void k_row_max(int rows, const int *ptr, int *out) {
     int m = 0;
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x)
@@ -639,6 +696,48 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         else k_spgemm_dense<4><<<grid, 32 * W, per * W, c->s>>>(a, ncols, W);
         launched(c);
     } else {
+        // 0. trial pass for products whose rows are expected to be narrow: one numeric
+        // pass without the symbolic pass; used only when no row went over budget
+        static const bool no_trial = [] { const char *e = std::getenv("DPP_SPGEMM_NO_TRIAL"); return e && *e == '1'; }();
+        const double prod = (double)A.nnz / rows * ((double)B.nnz / std::max(1, B.rows)) +
+                            (D ? (double)D->nnz / rows : 0.0);
+        if (!no_trial && rows >= 256 && prod <= 1024.0) {
+            DPP_TRACE_SCOPE(c, "spgemm.trial");
+            DBuf<int> meta(2, c->s);
+            CK(cudaMemsetAsync(meta.p, 0, 2 * sizeof(int), c->s));
+            k_row_max<<<grid_for(B.rows, 256, c->sms, 4), 256, 0, c->s>>>(B.rows, B.ptr.p, meta.p + 1);
+            launched(c);
+            int hb[2] = {0, 0};
+            CK(cudaMemcpyAsync(hb, meta.p, sizeof(hb), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            a.bmax = hb[1];
+            ti.alloc((size_t)rows * TR_LIM, c->s);
+            tv.alloc((size_t)rows * TR_LIM, c->s);
+            a.ti = ti.p;
+            a.tv = tv.p;
+            a.nrl = rows;
+            if (D) launch_trial<true>(c, a);
+            else launch_trial<false>(c, a);
+            k_count_neg<<<grid_for(rows, 256, c->sms, 4), 256, 0, c->s>>>(rows, cnt.p, meta.p);
+            launched(c);
+            int nover = 0;
+            CK(cudaMemcpyAsync(&nover, meta.p, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaStreamSynchronize(c->s));
+            if (nover == 0) {
+                C.nnz = counts_to_ptr(c, cnt.p, rows, C.ptr);
+                C.idx.alloc(std::max<int64_t>(C.nnz, 1), c->s);
+                C.val.alloc(std::max<int64_t>(C.nnz, 1), c->s);
+                k_stride_off<<<grid_for(rows, 256, c->sms, 4), 256, 0, c->s>>>(rows, TR_LIM, toff.p);
+                launched(c);
+                k_compact<<<grid_for((int64_t)rows * 32, 256, c->sms, 8), 256, 0, c->s>>>(rows, toff.p, C.ptr.p, ti.p,
+                                                                                        tv.p, C.idx.p, C.val.p);
+                launched(c);
+                CK(cudaStreamSynchronize(c->s));
+                return C;
+            }
+            ti.release();
+            tv.release();
+        }
         // 1. symbolic: distinct columns per row
         std::vector<int> u;
         DBuf<int> duniq(rows, c->s);
