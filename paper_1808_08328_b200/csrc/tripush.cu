@@ -233,6 +233,155 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     }
 }
 
+// ----------------------------------------------------------------- dataflow variant
+// Same plan, same arithmetic, no per-level synchronisation: x slots (own slice and
+// halo) start as a NaN sentinel, a solved row is stored into its own slot and pushed
+// with plain remote stores into its consumers' halo slots, and every entry a row reads
+// is polled until it is no longer the sentinel.  A lane group moves on to its next row
+// as soon as that row's inputs exist, so the critical path is the dependency chain
+// (mostly shared-memory hops inside a CTA) instead of levels x (slowest producer + push
+// + barrier).  The blocks are streamed by a dedicated producer warp through a ring of
+// full / empty mbarriers (consumer warps release a slot after its rows).
+constexpr unsigned long long PU_SENT = 0xFFFFFFFFFFFFFFFFull;
+__device__ __forceinline__ double ld_vol_shared(unsigned a) {
+    unsigned long long v;
+    asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+    return __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ void st_vol_shared(unsigned a, double v) {
+    asm volatile("st.volatile.shared.b64 [%0], %1;" ::"r"(a), "l"(__double_as_longlong(v)) : "memory");
+}
+__device__ __forceinline__ void st_remote(unsigned a, double v) {
+    asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(a), "l"(__double_as_longlong(v)) : "memory");
+}
+
+template <int G>
+__global__ void __launch_bounds__(PU_THREADS, 1)
+    k_trsv_flow(int n, int ncomp, int chunk, int L, int smax, int hmax, int stage, int nst,
+                const unsigned char *__restrict__ blocks, const long long *__restrict__ boff,
+                const int *__restrict__ sstart, const double *__restrict__ b, double *__restrict__ x,
+                const double *__restrict__ xadd, double *__restrict__ xout, int l2pf) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long *mfull = reinterpret_cast<unsigned long long *>(smem);
+    unsigned long long *mempty = mfull + PU_NST_MAX;   // the level-mbarrier area (L >= nst)
+    double *xh = reinterpret_cast<double *>(smem + 8 * PU_NST_MAX + p16(8LL * L));
+    long long *boff_s = reinterpret_cast<long long *>(xh + pu_chunkp(chunk) + p16(8LL * hmax) / 8);
+    unsigned *peer = reinterpret_cast<unsigned *>(boff_s + p16(8LL * (smax + 1)) / 8);
+    unsigned char *ring = smem + pu_fixed(chunk, L, hmax, smax);
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
+    const int comp = blockIdx.x / C;
+    const int s0 = sstart[k], S = sstart[k + 1] - s0;
+    const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int gl = threadIdx.x & (G - 1), grp = threadIdx.x / G, ngrp = (blockDim.x - 32) / G;
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1) << (lane & ~(G - 1)));
+    const int base = k * chunk, mine = min(chunk, n - base);
+    const int chunkp = pu_chunkp(chunk);
+    if (threadIdx.x < nst) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mfull[threadIdx.x])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mempty[threadIdx.x])), "r"(nw - 1) : "memory");
+    }
+    if (threadIdx.x < C) peer[threadIdx.x] = mapa_u32(su32(xh + chunkp), threadIdx.x);
+    for (int i = threadIdx.x; i <= S; i += blockDim.x) boff_s[i] = boff[s0 + i];
+    const double sent = __longlong_as_double((long long)PU_SENT);
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = sent;
+    for (int i = threadIdx.x; i < hmax; i += blockDim.x) xh[chunkp + i] = sent;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    pdl_wait();   // b is the previous kernel's output
+    // every CTA's slots hold the sentinel before anyone pushes
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (wid == nw - 1) {   // producer warp: TMA ring
+        if (lane == 0) {
+            for (int t = 0; t < S; ++t) {
+                const int sl = t % nst;
+                if (t >= nst) mwait(su32(&mempty[sl]), (unsigned)((t / nst - 1) & 1));
+                const unsigned bytes = (unsigned)(boff_s[t + 1] - boff_s[t]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mfull[sl])), "r"(bytes)
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(su32(ring + (size_t)sl * stage)), "l"(blocks + boff_s[t]), "r"(bytes),
+                             "r"(su32(&mfull[sl]))
+                             : "memory");
+                const int tp = t + nst + l2pf - 1;
+                if (l2pf && tp < S) {
+                    const unsigned pb = (unsigned)(boff_s[tp + 1] - boff_s[tp]);
+                    if (pb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[tp]), "r"(pb) : "memory");
+                }
+            }
+        }
+    } else {
+        const unsigned xh_s = su32(xh);
+        for (int t = 0; t < S; ++t) {
+            const int sl = t % nst;
+            mwait(su32(&mfull[sl]), (unsigned)((t / nst) & 1));
+            const unsigned char *blk = ring + (size_t)sl * stage;
+            const int4 hd = *reinterpret_cast<const int4 *>(blk);
+            const int nr = hd.x, ne = hd.y;
+            const int4 *rows = reinterpret_cast<const int4 *>(blk + 16);
+            const double *dg = reinterpret_cast<const double *>(blk + 16 + 16LL * nr);
+            const int *code = reinterpret_cast<const int *>(blk + pu_off_code(nr));
+            const double *val = reinterpret_cast<const double *>(blk + pu_off_val(nr, ne));
+            const int *pl = reinterpret_cast<const int *>(val + ne);
+            // warp-uniform row loop and polling (a spinning lane group must not hold back
+            // the other groups of its warp): the groups of a warp take consecutive rows
+            const int g0 = (wid * 32) / G;   // first group of this warp
+            for (int q0 = g0; q0 < nr; q0 += ngrp) {
+                const int q = q0 + (grp - g0);
+                const bool act = q < nr;
+                int4 R = make_int4(0, 0, 0, 0);
+                double dq = 0.0, bi = 0.0;
+                if (act) {
+                    R = rows[q];
+                    dq = dg[q];
+                    bi = b[(size_t)(base + R.x) * ncomp + comp];
+                }
+                int len = R.z - R.y;
+                len = __reduce_max_sync(0xffffffffu, len);
+                double sum = 0.0;
+                for (int e0 = 0; e0 < len; e0 += G) {
+                    const int e = R.y + e0 + gl;
+                    const bool has = act && e < R.z;
+                    unsigned xa = 0;
+                    double xv = 0.0, v = 0.0;
+                    if (has) {
+                        xa = xh_s + 8u * (unsigned)code[e];
+                        v = val[e];
+                        xv = ld_vol_shared(xa);
+                    }
+                    long long spins = 0;
+                    while (__any_sync(0xffffffffu, has && __double_as_longlong(xv) == (long long)PU_SENT)) {
+                        if (has && __double_as_longlong(xv) == (long long)PU_SENT) xv = ld_vol_shared(xa);
+                        if (++spins > (1ll << 28)) __trap();
+                    }
+                    if (has) sum += v * xv;
+                }
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o, G);
+                if (act) {
+                    double xr = (bi - sum) * dq;   // dq = 1/t_ii (as SuperLU's pre-scaled solve)
+                    if (__double_as_longlong(xr) == (long long)PU_SENT) xr = __longlong_as_double(0x7ff8000000000000ll);
+                    if (gl == 0) st_vol_shared(xh_s + 8u * (unsigned)R.x, xr);
+                    const int p0 = R.w >> 4, pc = R.w & 15;
+                    for (int u = gl; u < pc; u += G) {
+                        const int pe = pl[p0 + u];
+                        st_remote(peer[(unsigned)pe >> 28] + 8u * ((unsigned)pe & 0x0fffffffu), xr);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
+        }
+    }
+    __syncthreads();
+    pdl_trigger();
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) {
+        const size_t g = (size_t)(base + i) * ncomp + comp;
+        x[g] = xh[i];
+        if (xout) xout[g] = xadd[g] + xh[i];
+    }
+}
+
 // ----------------------------------------------------------------- setup
 __global__ void k_pu_keys(int n, int chunk, int L, const int *lev, int *key, int *rows) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
@@ -554,6 +703,11 @@ bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
         setk((const void *)k_trsv_push<8>);
         setk((const void *)k_trsv_push<16>);
         setk((const void *)k_trsv_push<32>);
+        setk((const void *)k_trsv_flow<2>);
+        setk((const void *)k_trsv_flow<4>);
+        setk((const void *)k_trsv_flow<8>);
+        setk((const void *)k_trsv_flow<16>);
+        setk((const void *)k_trsv_flow<32>);
         attr = true;
     }
     // as many CTAs as useful: each keeps >= ~2k rows of x
@@ -593,6 +747,20 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     const int *wp = T.W.rows ? (const int *)T.W.ptr.p : nullptr, *wi = T.W.rows ? (const int *)T.W.idx.p : nullptr;
     const double *wv = T.W.rows ? (const double *)T.W.val.p : nullptr;
     cudaError_t e;
+    static const bool flow = [] { const char *e = std::getenv("DPP_PU_FLOW"); return !(e && *e == '0'); }();
+    if (flow && !wp && !dbg && P.L >= P.nst) {
+        cfg.blockDim = dim3(std::min(PU_THREADS, P.threads + 32), 1, 1);
+        switch (P.G) {
+            case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
+            case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
+            case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<8>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
+            case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
+            default: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
+        }
+        CK(e);
+        launched(c);
+        return;
+    }
     switch (P.G) {
         case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_push<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, (const int *)P.tx.p, wp, wi, wv, b, x, xadd, xout, l2pf, dbg); break;
         case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_push<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, (const int *)P.tx.p, wp, wi, wv, b, x, xadd, xout, l2pf, dbg); break;
