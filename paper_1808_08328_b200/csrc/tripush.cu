@@ -251,6 +251,14 @@ __device__ __forceinline__ double ld_vol_shared(unsigned a) {
 __device__ __forceinline__ void st_vol_shared(unsigned a, double v) {
     asm volatile("st.volatile.shared.b64 [%0], %1;" ::"r"(a), "l"(__double_as_longlong(v)) : "memory");
 }
+__device__ __forceinline__ int ld_vol_u8(unsigned a) {
+    unsigned short v;
+    asm volatile("ld.volatile.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void st_vol_u8(unsigned a, int v) {
+    asm volatile("st.volatile.shared.u8 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
 __device__ __forceinline__ void st_remote(unsigned a, double v) {
     asm volatile("st.relaxed.cluster.shared::cluster.b64 [%0], %1;" ::"r"(a), "l"(__double_as_longlong(v)) : "memory");
 }
@@ -260,7 +268,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     k_trsv_flow(int n, int ncomp, int chunk, int L, int smax, int hmax, int stage, int nst,
                 const unsigned char *__restrict__ blocks, const long long *__restrict__ boff,
                 const int *__restrict__ sstart, const double *__restrict__ b, double *__restrict__ x,
-                const double *__restrict__ xadd, double *__restrict__ xout, int l2pf) {
+                const double *__restrict__ xadd, double *__restrict__ xout, int l2pf, unsigned long long *dbg) {
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned long long *mfull = reinterpret_cast<unsigned long long *>(smem);
     unsigned long long *mempty = mfull + PU_NST_MAX;   // the level-mbarrier area (L >= nst)
@@ -283,12 +291,18 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     }
     if (threadIdx.x < C) peer[threadIdx.x] = mapa_u32(su32(xh + chunkp), threadIdx.x);
     for (int i = threadIdx.x; i <= S; i += blockDim.x) boff_s[i] = boff[s0 + i];
+    // own rows: x slot seeded with b (as the level-synchronous kernel), readiness in a
+    // byte flag behind the ring; halo slots: the NaN sentinel until the push lands
+    pdl_wait();   // b is the previous kernel's output
+    double *bsl = reinterpret_cast<double *>(ring + (size_t)nst * stage);
     const double sent = __longlong_as_double((long long)PU_SENT);
-    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = sent;
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) {
+        bsl[i] = b[(size_t)(base + i) * ncomp + comp];
+        xh[i] = sent;
+    }
     for (int i = threadIdx.x; i < hmax; i += blockDim.x) xh[chunkp + i] = sent;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
-    pdl_wait();   // b is the previous kernel's output
     // every CTA's slots hold the sentinel before anyone pushes
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (wid == nw - 1) {   // producer warp: TMA ring
@@ -315,6 +329,8 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         for (int t = 0; t < S; ++t) {
             const int sl = t % nst;
             mwait(su32(&mfull[sl]), (unsigned)((t / nst) & 1));
+            unsigned long long t_land = 0;
+            if (dbg && lane == 0) t_land = gtimer();
             const unsigned char *blk = ring + (size_t)sl * stage;
             const int4 hd = *reinterpret_cast<const int4 *>(blk);
             const int nr = hd.x, ne = hd.y;
@@ -334,27 +350,43 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 if (act) {
                     R = rows[q];
                     dq = dg[q];
-                    bi = b[(size_t)(base + R.x) * ncomp + comp];
+                    bi = bsl[R.x];
                 }
                 int len = R.z - R.y;
                 len = __reduce_max_sync(0xffffffffu, len);
+                // RND entries per lane loaded before any is waited on (independent loads in
+                // flight); per lane the products are added in the same e order as before
+                constexpr int RND = 4;
                 double sum = 0.0;
-                for (int e0 = 0; e0 < len; e0 += G) {
-                    const int e = R.y + e0 + gl;
-                    const bool has = act && e < R.z;
-                    unsigned xa = 0;
-                    double xv = 0.0, v = 0.0;
-                    if (has) {
-                        xa = xh_s + 8u * (unsigned)code[e];
-                        v = val[e];
-                        xv = ld_vol_shared(xa);
+                for (int e0 = 0; e0 < len; e0 += G * RND) {
+                    unsigned xa[RND];
+                    double v[RND], xv[RND];
+                    bool has[RND];
+#pragma unroll
+                    for (int r = 0; r < RND; ++r) {
+                        const int e = R.y + e0 + r * G + gl;
+                        has[r] = act && e < R.z;
+                        xa[r] = has[r] ? xh_s + 8u * (unsigned)code[e] : 0u;
+                        v[r] = has[r] ? val[e] : 0.0;
                     }
+#pragma unroll
+                    for (int r = 0; r < RND; ++r) xv[r] = has[r] ? ld_vol_shared(xa[r]) : 0.0;
+                    auto pending = [&] {
+                        bool w = false;
+#pragma unroll
+                        for (int r = 0; r < RND; ++r) w |= has[r] && __double_as_longlong(xv[r]) == (long long)PU_SENT;
+                        return w;
+                    };
                     long long spins = 0;
-                    while (__any_sync(0xffffffffu, has && __double_as_longlong(xv) == (long long)PU_SENT)) {
-                        if (has && __double_as_longlong(xv) == (long long)PU_SENT) xv = ld_vol_shared(xa);
+                    while (__any_sync(0xffffffffu, pending())) {
+#pragma unroll
+                        for (int r = 0; r < RND; ++r)
+                            if (has[r] && __double_as_longlong(xv[r]) == (long long)PU_SENT) xv[r] = ld_vol_shared(xa[r]);
                         if (++spins > (1ll << 28)) __trap();
                     }
-                    if (has) sum += v * xv;
+#pragma unroll
+                    for (int r = 0; r < RND; ++r)
+                        if (has[r]) sum += v[r] * xv[r];
                 }
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o, G);
@@ -370,6 +402,13 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 }
             }
             __syncwarp();
+            if (dbg && lane == 0 && (wid * 32) / G < nr) {   // warps with rows: landed / done (ns)
+                unsigned long long *o = dbg + ((size_t)blockIdx.x * smax + t) * 4;
+                atomicMin(o + 0, t_land);
+                atomicMax(o + 1, gtimer());
+                o[2] = hd.w;
+                o[3] = nr;
+            }
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
         }
     }
@@ -748,17 +787,44 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     const double *wv = T.W.rows ? (const double *)T.W.val.p : nullptr;
     cudaError_t e;
     static const bool flow = [] { const char *e = std::getenv("DPP_PU_FLOW"); return !(e && *e == '0'); }();
-    if (flow && !wp && !dbg && P.L >= P.nst) {
+    const size_t fixed = pu_fixed(P.chunk, P.L, P.hmax, P.smax), flags = (size_t)p16(8LL * P.chunk);   // b slice
+    const int nst_f = (int)std::min<size_t>(P.nst, (PU_SMEM_LIMIT - fixed - flags) / P.stage);
+    static const char *fdbg_path = std::getenv("DPP_FLOW_DEBUG");
+    unsigned long long *fdbg = nullptr;
+    const size_t nfd = (size_t)P.C * T.ncomp * std::max(P.smax, 1) * 4;
+    if (fdbg_path && *fdbg_path && !c->capturing && flow) {
+        CK(cudaMallocAsync((void **)&fdbg, sizeof(unsigned long long) * nfd, st));
+        std::vector<unsigned long long> init(nfd, 0);
+        for (size_t i = 0; i < nfd; i += 4) init[i] = ~0ull;
+        CK(cudaMemcpyAsync(fdbg, init.data(), nfd * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    if (flow && !wp && !dbg && P.L >= nst_f && nst_f >= 2 && fixed + flags + (size_t)nst_f * P.stage <= PU_SMEM_LIMIT) {
         cfg.blockDim = dim3(std::min(PU_THREADS, P.threads + 32), 1, 1);
+        cfg.dynamicSmemBytes = fixed + (size_t)nst_f * P.stage + flags;
         switch (P.G) {
-            case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
-            case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
-            case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<8>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
-            case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
-            default: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf); break;
+            case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<8>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            default: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
         }
         CK(e);
         launched(c);
+        if (fdbg) {   // "# n C ncomp smax" then per (cta, step): cta step level rows t_land t_done
+            std::vector<unsigned long long> h(nfd);
+            CK(cudaMemcpyAsync(h.data(), fdbg, nfd * 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            cudaFreeAsync(fdbg, st);
+            if (FILE *f = std::fopen(fdbg_path, "a")) {
+                std::fprintf(f, "# n=%d C=%d ncomp=%d smax=%d L=%d G=%d\n", T.n, P.C, T.ncomp, P.smax, P.L, P.G);
+                for (size_t i = 0; i < nfd / 4; ++i) {
+                    const unsigned long long *o = &h[i * 4];
+                    if (o[1]) std::fprintf(f, "%zu %zu %llu %llu %llu %llu\n", i / P.smax, i % P.smax, o[2], o[3], o[0], o[1]);
+                }
+                std::fclose(f);
+            }
+        }
         return;
     }
     switch (P.G) {
