@@ -701,7 +701,8 @@ Csr spgemm(Ctx *c, const Csr &A, const Csr &B, const double *s_dev, bool reverse
         static const bool no_trial = [] { const char *e = std::getenv("DPP_SPGEMM_NO_TRIAL"); return e && *e == '1'; }();
         const double prod = (double)A.nnz / rows * ((double)B.nnz / std::max(1, B.rows)) +
                             (D ? (double)D->nnz / rows : 0.0);
-        if (!no_trial && rows >= 256 && prod <= 1024.0) {
+        static const double trial_max = [] { const char *e = std::getenv("DPP_SPGEMM_TRIAL_MAX"); return e ? std::atof(e) : 1024.0; }();
+        if (!no_trial && rows >= 256 && prod <= trial_max) {
             DPP_TRACE_SCOPE(c, "spgemm.trial");
             DBuf<int> meta(2, c->s);
             CK(cudaMemsetAsync(meta.p, 0, 2 * sizeof(int), c->s));
