@@ -305,33 +305,47 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
     __syncthreads();
     // every CTA's slots hold the sentinel before anyone pushes
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    // ring slots of `stage` bytes hold runs of consecutive (CTA, level) blocks (contiguous in
+    // the plan): one TMA copy, one full / empty mbarrier round per run instead of per level
+    auto run_end = [&](int a) {
+        int e = a + 1;
+        while (e < S && boff_s[e + 1] - boff_s[a] <= stage) ++e;
+        return e;
+    };
     if (wid == nw - 1) {   // producer warp: TMA ring
         if (lane == 0) {
-            for (int t = 0; t < S; ++t) {
-                const int sl = t % nst;
-                if (t >= nst) mwait(su32(&mempty[sl]), (unsigned)((t / nst - 1) & 1));
-                const unsigned bytes = (unsigned)(boff_s[t + 1] - boff_s[t]);
+            int pa = 0, pq = 0;   // L2 prefetch cursor (runs ahead of the copies)
+            for (int a = 0, j = 0; a < S; ++j) {
+                const int e = run_end(a), sl = j % nst;
+                if (j >= nst) mwait(su32(&mempty[sl]), (unsigned)((j / nst - 1) & 1));
+                const unsigned bytes = (unsigned)(boff_s[e] - boff_s[a]);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mfull[sl])), "r"(bytes)
                              : "memory");
                 asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             ::"r"(su32(ring + (size_t)sl * stage)), "l"(blocks + boff_s[t]), "r"(bytes),
+                             ::"r"(su32(ring + (size_t)sl * stage)), "l"(blocks + boff_s[a]), "r"(bytes),
                              "r"(su32(&mfull[sl]))
                              : "memory");
-                const int tp = t + nst + l2pf - 1;
-                if (l2pf && tp < S) {
-                    const unsigned pb = (unsigned)(boff_s[tp + 1] - boff_s[tp]);
-                    if (pb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[tp]), "r"(pb) : "memory");
+                while (l2pf && pa < S && pq < j + nst + l2pf) {
+                    const int pe = run_end(pa);
+                    if (pq >= j + nst) {
+                        const unsigned pb = (unsigned)(boff_s[pe] - boff_s[pa]);
+                        if (pb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[pa]), "r"(pb) : "memory");
+                    }
+                    pa = pe;
+                    ++pq;
                 }
+                a = e;
             }
         }
     } else {
         const unsigned xh_s = su32(xh);
-        for (int t = 0; t < S; ++t) {
-            const int sl = t % nst;
-            mwait(su32(&mfull[sl]), (unsigned)((t / nst) & 1));
-            unsigned long long t_land = 0;
-            if (dbg && lane == 0) t_land = gtimer();
-            const unsigned char *blk = ring + (size_t)sl * stage;
+        for (int a = 0, j = 0; a < S; ++j) {
+          const int e_run = run_end(a), sl = j % nst;
+          mwait(su32(&mfull[sl]), (unsigned)((j / nst) & 1));
+          unsigned long long t_land = 0;
+          if (dbg && lane == 0) t_land = gtimer();
+          for (int t = a; t < e_run; ++t) {
+            const unsigned char *blk = ring + (size_t)sl * stage + (boff_s[t] - boff_s[a]);
             const int4 hd = *reinterpret_cast<const int4 *>(blk);
             const int nr = hd.x, ne = hd.y;
             const int4 *rows = reinterpret_cast<const int4 *>(blk + 16);
@@ -409,7 +423,10 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 o[2] = hd.w;
                 o[3] = nr;
             }
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
+          }
+          __syncwarp();
+          if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
+          a = e_run;
         }
     }
     __syncthreads();
@@ -788,7 +805,12 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     cudaError_t e;
     static const bool flow = [] { const char *e = std::getenv("DPP_PU_FLOW"); return !(e && *e == '0'); }();
     const size_t fixed = pu_fixed(P.chunk, P.L, P.hmax, P.smax), flags = (size_t)p16(8LL * P.chunk);   // b slice
-    const int nst_f = (int)std::min<size_t>(P.nst, (PU_SMEM_LIMIT - fixed - flags) / P.stage);
+    const int nst_b = (int)std::min<size_t>(P.nst, (PU_SMEM_LIMIT - fixed - flags) / P.stage);
+    // the ring's bytes regrouped into 2 large slots (runs of blocks per slot; 2 slots measured
+    // best: 1.75 vs 1.82 / 1.84 / 1.89 ms per C2 PC apply for 3 / 4 / per-block slots)
+    static const int flow_slots = [] { const char *e = std::getenv("DPP_FLOW_SLOTS"); return e ? std::atoi(e) : 2; }();
+    const int nst_f = std::max(1, std::min(nst_b, flow_slots));
+    const long long stage_f = nst_b >= 2 ? ((long long)nst_b * P.stage / nst_f) & ~15LL : P.stage;
     static const char *fdbg_path = std::getenv("DPP_FLOW_DEBUG");
     unsigned long long *fdbg = nullptr;
     const size_t nfd = (size_t)P.C * T.ncomp * std::max(P.smax, 1) * 4;
@@ -801,15 +823,16 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     }
     // dataflow for thin rows (C2: G = 2 / 8); the level-synchronous kernel measured faster for
     // the 32-lane groups of the long-row triangles of configs 3/4 (34.0 vs 37.8 ms per PC apply at C3)
-    if (flow && P.G <= 16 && !wp && !dbg && P.L >= nst_f && nst_f >= 2 && fixed + flags + (size_t)nst_f * P.stage <= PU_SMEM_LIMIT) {
+    if (flow && P.G <= 16 && !wp && !dbg && P.L >= nst_f && nst_b >= 2 && nst_f >= 2 &&
+        fixed + flags + (size_t)nst_f * stage_f <= PU_SMEM_LIMIT) {
         cfg.blockDim = dim3(std::min(PU_THREADS, P.threads + 32), 1, 1);
-        cfg.dynamicSmemBytes = fixed + (size_t)nst_f * P.stage + flags;
+        cfg.dynamicSmemBytes = fixed + (size_t)nst_f * stage_f + flags;
         switch (P.G) {
-            case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
-            case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
-            case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<8>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
-            case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
-            default: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<8>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            default: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
         }
         CK(e);
         launched(c);
