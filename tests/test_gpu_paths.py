@@ -3,8 +3,8 @@ triangle; these force the others).  Each variant runs in a fresh process (the
 switches are read once per process) and must match the CPU oracle to the usual
 bars: solution within 1e-9 relative, iterations within +-2.
 
-  default                     push-exchange cluster sweeps + block-dense / dense smoothers
-  DPP_PU_MODE=push            (same; explicit)
+  default                     dataflow cluster sweeps (k_trsv_flow) + block-dense / dense smoothers
+  DPP_PU_FLOW=0               level-synchronous push-exchange cluster sweeps (k_trsv_push)
   DPP_NO_PUSH=1               barrier-per-level cluster sweeps (tricluster.cu)
   DPP_BD_MAX=0                no block-dense smoothers (level sweeps on every AMG level)
   DPP_BD_MAX=0 DPP_NO_PUSH=1 DPP_NO_CLUSTER=1
@@ -38,6 +38,7 @@ print(json.dumps({{"its": r.stats.iterations, "converged": bool(r.stats.converge
 
 VARIANTS = {
     "default": {},
+    "level_sync_push": {"DPP_PU_FLOW": "0"},
     "pull_cluster": {"DPP_NO_PUSH": "1"},
     "no_block_dense": {"DPP_BD_MAX": "0"},
     "sync_free_and_block": {"DPP_BD_MAX": "0", "DPP_NO_PUSH": "1", "DPP_NO_CLUSTER": "1"},
@@ -68,3 +69,18 @@ def test_sweep_strategy(name, oracle_ref, tmp_path):
     rel = np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref)
     assert info["converged"] and abs(info["its"] - its_ref) <= 2, (info, its_ref)
     assert rel < 1e-9, rel
+
+
+@pytest.mark.timeout(600)
+def test_dataflow_sweep_bitwise_level_sync(tmp_path):
+    """The dataflow sweep only changes when a row is computed, not how: per-lane products
+    in entry order, the same xor-shuffle reduction, (b - sum) * (1/t_ii) -- so the whole
+    solve is bit-for-bit the level-synchronous kernel's."""
+    xs = []
+    for k, extra in enumerate(({}, {"DPP_PU_FLOW": "0"})):
+        out = str(tmp_path / f"x{k}.npy")
+        res = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, out=out)],
+                             env=dict(os.environ, **extra), capture_output=True, text=True, timeout=500)
+        assert res.returncode == 0, res.stderr[-2000:]
+        xs.append(np.load(out))
+    assert np.array_equal(xs[0], xs[1])
