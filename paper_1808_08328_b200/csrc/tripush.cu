@@ -823,7 +823,8 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     }
     // dataflow for thin rows (C2: G = 2 / 8); the level-synchronous kernel measured faster for
     // the 32-lane groups of the long-row triangles of configs 3/4 (34.0 vs 37.8 ms per PC apply at C3)
-    if (flow && P.G <= 16 && !wp && !dbg && P.L >= nst_f && nst_b >= 2 && nst_f >= 2 &&
+    static const int flow_gmax = [] { const char *e = std::getenv("DPP_FLOW_GMAX"); return e ? std::atoi(e) : 16; }();
+    if (flow && P.G <= flow_gmax && !wp && !dbg && P.L >= nst_f && nst_b >= 2 && nst_f >= 2 &&
         fixed + flags + (size_t)nst_f * stage_f <= PU_SMEM_LIMIT) {
         cfg.blockDim = dim3(std::min(PU_THREADS, P.threads + 32), 1, 1);
         cfg.dynamicSmemBytes = fixed + (size_t)nst_f * stage_f + flags;
