@@ -196,6 +196,8 @@ struct DevMesh {
     DBuf<int> cells, cf, fv, fplus, fminus;
     DBuf<signed char> cs;
     DBuf<double> fn, fm;
+    bool facets = false;   // facet arrays uploaded (H(div), DG-VMS, facet queries); CG-VMS needs none
+    size_t foff[7] = {0}, fbytes[7] = {0};   // facet parts in the pinned image
 };
 
 // J (mesh.py:175-183) and J^-1 by LU with partial pivoting (numpy.linalg.inv)
@@ -297,13 +299,11 @@ static DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
     up(d->verts, pv, nV);
     up(d->det, pd, nD);
     up(d->cells, pc, nC);
-    up(d->cf, pcf, nCF);
-    up(d->fv, pfv, nFV);
-    up(d->fplus, pfp, nF);
-    up(d->fminus, pfm, nF);
-    up(d->cs, pcs, nCS);
-    up(d->fn, pfn, nFN);
-    up(d->fm, pfs, nFM);
+    m.dev_bytes = pv.bytes + pd.bytes + pc.bytes;
+    m.bc_bytes = 0;
+    // the facet arrays (80 % of the image for TET meshes) follow only when a formulation uses them
+    const Part fparts[7] = {pcf, pfv, pfp, pfm, pcs, pfn, pfs};
+    for (int q = 0; q < 7; ++q) { d->foff[q] = fparts[q].off; d->fbytes[q] = fparts[q].bytes; }
     d->Jinv.alloc((size_t)d->C * d->dim * d->dim, c->s);
     if (d->C) {
         k_geom<<<grid_for(d->C, 128, c->sms), 128, 0, c->s>>>(d->C, d->dim, d->kind, d->nn, d->verts.p,
@@ -313,6 +313,29 @@ static DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
     CK(cudaStreamSynchronize(c->s));
     m.dev = d;
     return *d;
+}
+
+static void ensure_facets(Ctx *c, HostMesh &hm, DevMesh &d) {
+    if (d.facets) return;
+    const unsigned char *B = static_cast<const unsigned char *>(hm.pinned.get());
+    auto up = [&](auto &buf, int q, size_t count) {
+        buf.alloc(count, c->s);
+        if (count) CK(cudaMemcpyAsync(buf.p, B + d.foff[q], d.fbytes[q], cudaMemcpyHostToDevice, c->s));
+        hm.dev_bytes += d.fbytes[q];
+    };
+    up(d.cf, 0, hm.cell_facets.size());
+    up(d.fv, 1, hm.facet_vertex_ids.size());
+    up(d.fplus, 2, hm.facet_plus.size());
+    up(d.fminus, 3, hm.facet_minus.size());
+    up(d.cs, 4, hm.cell_facet_signs.size());
+    up(d.fn, 5, hm.facet_normals.size());
+    up(d.fm, 6, hm.facet_measures.size());
+    CK(cudaStreamSynchronize(c->s));
+    d.facets = true;
+}
+
+__global__ void k_iota64(int64_t n, int64_t *o) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) o[i] = i;
 }
 
 // ------------------------------------------------------------------ facet points
@@ -1380,7 +1403,7 @@ void eliminate(Ctx *c, dpp_system &S, int field, int64_t n, const int64_t *idx_h
     CK(cudaStreamSynchronize(c->s));
 }
 
-static void boundary_rhs(Ctx *c, DevMesh &m, int formulation, const dpp_bc *bc, dpp_system &S) {
+static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, const dpp_bc *bc, dpp_system &S) {
     if (!bc) return;
     FRule R4 = frule(m.kind, 4);
     const bool dg = formulation == DPP_DGVMS;
@@ -1389,10 +1412,40 @@ static void boundary_rhs(Ctx *c, DevMesh &m, int formulation, const dpp_bc *bc, 
         if (nfp <= 0) continue;
         DBuf<int64_t> fids(nfp, c->s);
         fids.upload(bc->pfacets[net], nfp);
+        // without the mesh's facet arrays on the device (CG-VMS): the pressure facets' rows
+        // (vertex ids, plus cell, normal, measure) gathered on the host, addressed 0..nfp-1
+        const int *fv = m.fv.p, *fplus = m.fplus.p;
+        const double *fn = m.fn.p, *fm = m.fm.p;
+        const int64_t *ids = fids.p;
+        DBuf<int> cfv, cfp;
+        DBuf<double> cfn, cfm;
+        DBuf<int64_t> iota;
+        if (!m.facets) {
+            const int64_t *f = bc->pfacets[net];
+            std::vector<int> hv((size_t)nfp * m.nvf), hp(nfp);
+            std::vector<double> hn((size_t)nfp * m.dim), hmz(nfp);
+            for (int64_t i = 0; i < nfp; ++i) {
+                const int64_t g = f[i];
+                if (g < 0 || g >= m.F) DPP_FAIL(DPP_ERR_VALUE, "pressure facet id out of range");
+                for (int k = 0; k < m.nvf; ++k) hv[(size_t)i * m.nvf + k] = (int)hm.facet_vertex_ids[(size_t)g * m.nvf + k];
+                hp[i] = (int)hm.facet_plus[g];
+                for (int k = 0; k < m.dim; ++k) hn[(size_t)i * m.dim + k] = hm.facet_normals[(size_t)g * m.dim + k];
+                hmz[i] = hm.facet_measures[g];
+            }
+            cfv.alloc(hv.size(), c->s); cfv.upload(hv.data(), hv.size());
+            cfp.alloc(nfp, c->s); cfp.upload(hp.data(), nfp);
+            cfn.alloc(hn.size(), c->s); cfn.upload(hn.data(), hn.size());
+            cfm.alloc(nfp, c->s); cfm.upload(hmz.data(), nfp);
+            hm.bc_bytes += 4 * (hv.size() + hp.size()) + 8 * (hn.size() + hmz.size());
+            iota.alloc(nfp, c->s);
+            k_iota64<<<grid_for(nfp, 256, c->sms), 256, 0, c->s>>>(nfp, iota.p);
+            launched(c);
+            fv = cfv.p; fplus = cfp.p; fn = cfn.p; fm = cfm.p; ids = iota.p;
+        }
         DBuf<double> p0(nfp * R4.nq, c->s);
         if (bc->p0_kind[net]) {
             const double *cf = bc->p0_coef[net];
-            k_mms_p0<<<grid_for(nfp * R4.nq, 256, c->sms), 256, 0, c->s>>>(nfp, fids.p, R4, m.dim, m.nvf, m.fv.p, m.verts.p,
+            k_mms_p0<<<grid_for(nfp * R4.nq, 256, c->sms), 256, 0, c->s>>>(nfp, ids, R4, m.dim, m.nvf, fv, m.verts.p,
                                                                         bc->p0_kind[net], cf[0], cf[1], cf[2], p0.p);
             launched(c);
         } else {
@@ -1402,7 +1455,7 @@ static void boundary_rhs(Ctx *c, DevMesh &m, int formulation, const dpp_bc *bc, 
         if (formulation == DPP_HDIV) {
             DBuf<int64_t> dof(nfp, c->s);
             DBuf<double> val(nfp, c->s);
-            k_rhs_hdiv<<<grid_for(nfp, 256, c->sms), 256, 0, c->s>>>(nfp, fids.p, R4, m.fm.p, p0.p, dof.p, val.p);
+            k_rhs_hdiv<<<grid_for(nfp, 256, c->sms), 256, 0, c->s>>>(nfp, ids, R4, fm, p0.p, dof.p, val.p);
             launched(c);
             add_at(c, nfp, dof, val, rhs);
         } else {
@@ -1410,7 +1463,7 @@ static void boundary_rhs(Ctx *c, DevMesh &m, int formulation, const dpp_bc *bc, 
             DBuf<int64_t> dof(ne, c->s);
             DBuf<double> val(ne, c->s);
             k_rhs_nodal<<<grid_for(nfp, 128, c->sms), 128, 0, c->s>>>(
-                nfp, fids.p, R4, m.kind, m.dim, m.nn, m.nvf, dg, m.fv.p, m.fplus.p, m.fn.p, m.fm.p,
+                nfp, ids, R4, m.kind, m.dim, m.nn, m.nvf, dg, fv, fplus, fn, fm,
                 m.verts.p, m.cells.p, m.Jinv.p, p0.p, dof.p, val.p);
             launched(c);
             add_at(c, ne, dof, val, rhs);
@@ -1499,11 +1552,10 @@ int dpp_mesh_destroy(dpp_mesh *m) {
 
 int dpp_mesh_upload_bytes(dpp_mesh *m, int64_t *bytes) {
     return guard([&] {
+        // what the current device image actually copied (the facet arrays only when a
+        // formulation needed them) plus the last assembly's compact boundary-facet data
         const HostMesh &h = m->m;
-        *bytes = (int64_t)(8 * (h.vertices.size() + h.det.size() + h.facet_normals.size() + h.facet_measures.size()) +
-                           4 * (h.cells.size() + h.cell_facets.size() + h.facet_vertex_ids.size() +
-                                2 * h.facet_plus.size()) +
-                           h.cell_facet_signs.size());
+        *bytes = (int64_t)(h.dev_bytes + h.bc_bytes);
     });
 }
 
@@ -1523,6 +1575,7 @@ int dpp_facet_points(dpp_ctx *ctx, dpp_mesh *mm, int degree, int64_t nf, const i
     return guard([&] {
         Ctx *c = &ctx->c;
         DevMesh &m = dev_mesh(c, mm->m);
+        ensure_facets(c, mm->m, m);
         FRule R = frule(m.kind, degree);
         if (nf <= 0) return;
         DBuf<int64_t> f(nf, c->s);
@@ -1578,6 +1631,9 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
             S->rhs[k].alloc(S->sizes[k], c->s);
             if (S->sizes[k]) CK(cudaMemsetAsync(S->rhs[k].p, 0, sizeof(double) * S->sizes[k], c->s));
         }
+        hm.bc_bytes = 0;
+        if (formulation != DPP_CGVMS || (bc && (bc->n_vfacets[0] > 0 || bc->n_vfacets[1] > 0)))
+            ensure_facets(c, hm, m);
         {
             DPP_TRACE_SCOPE(c, "assemble.blocks");
             if (formulation == DPP_HDIV) assemble_hdiv(c, hm, m, *p, *S);
@@ -1585,7 +1641,7 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
         }
         {
             DPP_TRACE_SCOPE(c, "assemble.rhs");
-            boundary_rhs(c, m, formulation, bc, *S);
+            boundary_rhs(c, hm, m, formulation, bc, *S);
             // H(div) prescribed flux: strong elimination of the facet dofs (assembly.py:301-309);
             // CG-VMS velocity facets only drop the pressure functional (the caller's pfacets)
             if (bc && formulation == DPP_HDIV)

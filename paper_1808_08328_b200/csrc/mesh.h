@@ -23,6 +23,8 @@ struct HostMesh {
     std::shared_ptr<DevMesh> dev;             // lazily uploaded
     std::shared_ptr<void> pinned;             // device-layout image in pinned host memory (built once)
     size_t pinned_bytes = 0;
+    size_t dev_bytes = 0;                     // host->device bytes of the current device image
+    size_t bc_bytes = 0;                      //   + the last assembly's compact boundary-facet data
     void build();
 };
 
