@@ -1410,8 +1410,12 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
     for (int net = 0; net < 2; ++net) {
         const int64_t nfp = bc->n_pfacets[net];
         if (nfp <= 0) continue;
-        DBuf<int64_t> fids(nfp, c->s);
-        fids.upload(bc->pfacets[net], nfp);
+        DBuf<int64_t> fids;
+        if (m.facets) {
+            fids.alloc(nfp, c->s);
+            fids.upload(bc->pfacets[net], nfp);
+            hm.bc_bytes += 8 * (size_t)nfp;
+        }
         // without the mesh's facet arrays on the device (CG-VMS): the pressure facets' rows
         // (vertex ids, plus cell, normal, measure) gathered on the host, addressed 0..nfp-1
         const int *fv = m.fv.p, *fplus = m.fplus.p;
@@ -1422,8 +1426,22 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
         DBuf<int64_t> iota;
         if (!m.facets) {
             const int64_t *f = bc->pfacets[net];
-            std::vector<int> hv((size_t)nfp * m.nvf), hp(nfp);
-            std::vector<double> hn((size_t)nfp * m.dim), hmz(nfp);
+            const size_t bv = 4 * (size_t)nfp * m.nvf, bp = 4 * (size_t)nfp, bn = 8 * (size_t)nfp * m.dim, bm = 8 * (size_t)nfp;
+            const size_t o_v = 0, o_p = (bv + 15) & ~(size_t)15, o_n = (o_p + bp + 15) & ~(size_t)15,
+                         o_m = (o_n + bn + 15) & ~(size_t)15;
+            // staging halves sized for the larger network's facet count
+            const size_t nmax = (size_t)std::max<int64_t>(bc->n_pfacets[0], bc->n_pfacets[1]);
+            const size_t tot = (16 * 4 + 4 * nmax * m.nvf + 4 * nmax + 8 * nmax * m.dim + 8 * nmax + 15) & ~(size_t)15;
+            if (!hm.bc_pinned || hm.bc_pinned_bytes < 2 * tot + 64) {   // both networks' halves
+                CK(cudaStreamSynchronize(c->s));   // the old staging may still be read
+                void *h = nullptr;
+                CK(cudaMallocHost(&h, 2 * tot + 64));
+                hm.bc_pinned = std::shared_ptr<void>(h, [](void *q) { cudaFreeHost(q); });
+                hm.bc_pinned_bytes = 2 * tot + 64;
+            }
+            unsigned char *B = static_cast<unsigned char *>(hm.bc_pinned.get()) + (net ? hm.bc_pinned_bytes / 2 : 0);
+            int *hv = reinterpret_cast<int *>(B + o_v), *hp = reinterpret_cast<int *>(B + o_p);
+            double *hn = reinterpret_cast<double *>(B + o_n), *hmz = reinterpret_cast<double *>(B + o_m);
             for (int64_t i = 0; i < nfp; ++i) {
                 const int64_t g = f[i];
                 if (g < 0 || g >= m.F) DPP_FAIL(DPP_ERR_VALUE, "pressure facet id out of range");
@@ -1432,11 +1450,17 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
                 for (int k = 0; k < m.dim; ++k) hn[(size_t)i * m.dim + k] = hm.facet_normals[(size_t)g * m.dim + k];
                 hmz[i] = hm.facet_measures[g];
             }
-            cfv.alloc(hv.size(), c->s); cfv.upload(hv.data(), hv.size());
-            cfp.alloc(nfp, c->s); cfp.upload(hp.data(), nfp);
-            cfn.alloc(hn.size(), c->s); cfn.upload(hn.data(), hn.size());
-            cfm.alloc(nfp, c->s); cfm.upload(hmz.data(), nfp);
-            hm.bc_bytes += 4 * (hv.size() + hp.size()) + 8 * (hn.size() + hmz.size());
+            // asynchronous copies: the staging is reused only by the next assembly, which
+            // starts after this one's final stream synchronisation
+            cfv.alloc((size_t)nfp * m.nvf, c->s);
+            cfp.alloc(nfp, c->s);
+            cfn.alloc((size_t)nfp * m.dim, c->s);
+            cfm.alloc(nfp, c->s);
+            CK(cudaMemcpyAsync(cfv.p, hv, bv, cudaMemcpyHostToDevice, c->s));
+            CK(cudaMemcpyAsync(cfp.p, hp, bp, cudaMemcpyHostToDevice, c->s));
+            CK(cudaMemcpyAsync(cfn.p, hn, bn, cudaMemcpyHostToDevice, c->s));
+            CK(cudaMemcpyAsync(cfm.p, hmz, bm, cudaMemcpyHostToDevice, c->s));
+            hm.bc_bytes += bv + bp + bn + bm;
             iota.alloc(nfp, c->s);
             k_iota64<<<grid_for(nfp, 256, c->sms), 256, 0, c->s>>>(nfp, iota.p);
             launched(c);
@@ -1450,6 +1474,7 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
             launched(c);
         } else {
             p0.upload(bc->p0[net], nfp * R4.nq);
+            hm.bc_bytes += 8 * (size_t)nfp * R4.nq;
         }
         double *rhs = S.rhs[net == 0 ? 0 : 2].p;
         if (formulation == DPP_HDIV) {

@@ -25,6 +25,8 @@ struct HostMesh {
     size_t pinned_bytes = 0;
     size_t dev_bytes = 0;                     // host->device bytes of the current device image
     size_t bc_bytes = 0;                      //   + the last assembly's compact boundary-facet data
+    std::shared_ptr<void> bc_pinned;          // pinned staging of that data (reused; assembly syncs at its end)
+    size_t bc_pinned_bytes = 0;
     void build();
 };
 
