@@ -164,6 +164,16 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
     g.part2.alloc(NRM_BLOCKS, c->s);
     *st = dpp_krylov_stats{};
     DBuf<double> sc(restart + 8, c->s), r(n, c->s), z(n, c->s), w(n, c->s), tmp(n, c->s);
+    // H column read back through pinned memory + an event, so the host can wait for it alone
+    PinnedBuf hbuf = pinned_acquire(sizeof(double) * (restart + 8));
+    double *hpin = static_cast<double *>(hbuf.p);
+    cudaEvent_t hev;
+    CK(cudaEventCreateWithFlags(&hev, cudaEventDisableTiming));
+    struct HRelease {
+        PinnedBuf b;
+        cudaEvent_t e;
+        ~HRelease() { cudaEventDestroy(e); pinned_release(b); }
+    } hrel{hbuf, hev};
     double *hcol = sc.p;                  // H[0..j+1, j]
     double *dnorm = sc.p + restart + 2;   // scratch scalars
     auto finish = [&](int its, double rel, bool conv, int reason) {
@@ -228,14 +238,15 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
         gg[0] = beta;
         scale_by_dev(c, n, z.p, dnorm, V.p);       // V[0] = z / beta
         int k_used = 0;
-        bool happy = false;
+        bool happy = false, ahead = false;   // ahead: V[j] and M^-1 A V[j] already enqueued
         for (int j = 0; j < m; ++j) {
             double *Vj = V.p + (size_t)j * n;
-            {
+            if (!ahead) {
             DPP_TRACE_SCOPE(c, "gmres.matvec_pc");
             g.matvec(Vj, tmp.p);
             g.pc(tmp.p, w.p);                      // w = M^-1 A V[j]
             }
+            ahead = false;
             DPP_TRACE_SCOPE(c, "gmres.mgs_givens");
             {   // modified Gram-Schmidt + ||w||, one cooperative kernel
                 int64_t nn = n;
@@ -246,12 +257,28 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
                 CK(cudaLaunchCooperativeKernel((const void *)k_mgs, NRM_BLOCKS, 256, args, 0, c->s));
                 launched(c);
             }
-            std::vector<double> hc(j + 2);
-            CK(cudaMemcpyAsync(hc.data(), hcol, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->s));
-            CK(cudaStreamSynchronize(c->s));
+            double *hc = hpin;
+            CK(cudaMemcpyAsync(hc, hcol, sizeof(double) * (j + 2), cudaMemcpyDeviceToHost, c->s));
+            CK(cudaEventRecord(hev, c->s));
+            // while the host waits for H[:, j] and does the Givens algebra, the device already
+            // forms V[j+1] = w / h_{j+1,j} and M^-1 A V[j+1] -- only when this iteration cannot
+            // end the cycle (estimate far above the target, not the last column), so the
+            // speculative work is always the next iteration's (a breakdown leaves it unused)
+            static const bool spec_on = [] { const char *e = std::getenv("DPP_GMRES_AHEAD"); return !(e && *e == '0'); }();
+            if (spec_on && j + 1 < m && total + 1 < max_iter && std::fabs(gg[j]) > 1e3 * rtol * norm_mb) {
+                double *Vn = V.p + (size_t)(j + 1) * n;
+                scale_by_dev(c, n, w.p, hcol + j + 1, Vn);
+                g.matvec(Vn, tmp.p);
+                g.pc(tmp.p, w.p);
+                ahead = true;
+            }
+            CK(cudaEventSynchronize(hev));   // H[:, j] only (not the work enqueued after it)
             for (int i = 0; i <= j + 1; ++i) Hij(i, j) = hc[i];
-            if (Hij(j + 1, j) > 1e-14 * beta) scale_by_dev(c, n, w.p, hcol + j + 1, V.p + (size_t)(j + 1) * n);
-            else happy = true;
+            if (Hij(j + 1, j) > 1e-14 * beta) {
+                if (!ahead) scale_by_dev(c, n, w.p, hcol + j + 1, V.p + (size_t)(j + 1) * n);
+            } else {
+                happy = true;
+            }
             for (int i = 0; i < j; ++i) {
                 const double t = cs[i] * Hij(i, j) + sn[i] * Hij(i + 1, j);
                 Hij(i + 1, j) = -sn[i] * Hij(i, j) + cs[i] * Hij(i + 1, j);
