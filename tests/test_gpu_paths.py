@@ -84,3 +84,17 @@ def test_dataflow_sweep_bitwise_level_sync(tmp_path):
         assert res.returncode == 0, res.stderr[-2000:]
         xs.append(np.load(out))
     assert np.array_equal(xs[0], xs[1])
+
+
+@pytest.mark.timeout(600)
+def test_gmres_lookahead_bitwise(tmp_path):
+    """Enqueueing the next Arnoldi column's SpMV + PC apply while the host reads H[:, j]
+    (DPP_GMRES_AHEAD, default on) changes only when work is issued: same iterates bit for bit."""
+    xs = []
+    for k, extra in enumerate(({}, {"DPP_GMRES_AHEAD": "0"})):
+        out = str(tmp_path / f"x{k}.npy")
+        res = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, out=out)],
+                             env=dict(os.environ, **extra), capture_output=True, text=True, timeout=500)
+        assert res.returncode == 0, res.stderr[-2000:]
+        xs.append(np.load(out))
+    assert np.array_equal(xs[0], xs[1])
