@@ -276,6 +276,10 @@ struct PushPlan {         // cluster sweep with st.async point-to-point x exchan
     DBuf<long long> boff; // per step (CTA-major)
     DBuf<int> sstart;     // first step of each CTA
     DBuf<int> tx;         // bytes each CTA receives per level
+    DBuf<int> lrows;      // rows of each (CTA, level)
+    DBuf<int> slev;       // fmt 1: level of each step
+    int widest = 1;       // most rows (fmt 1: 32-row chunks) in one block (step)
+    int fmt = 0;          // block format: 0 row-major (k_trsv_flow / k_trsv_push), 1 SELL chunks (k_trsv_lvl)
 };
 struct BlockPlan {        // block-sequential sweep with dense diagonal-block inverses (triblock.cu)
     int nblk = 0, stage = 0, nst = 0;

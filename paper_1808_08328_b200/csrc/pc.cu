@@ -326,6 +326,15 @@ void pc_apply_dev(dpp_pc *pc, const double *r_dev, double *z_dev) {
     Ctx *c = pc->ctx;
     if (r_dev != pc->r.p)
         CK(cudaMemcpyAsync(pc->r.p, r_dev, sizeof(double) * pc->n, cudaMemcpyDeviceToDevice, c->s));
+    static const bool nograph = [] { const char *e = std::getenv("DPP_PC_NOGRAPH"); return e && *e == '1'; }();
+    if (nograph) {   // debugging / per-kernel instrumentation: plain stream launches
+        const int64_t before = c->launches;
+        pc->root->apply(c, pc->r.p, pc->z.p, c->s);
+        pc->kernels_per_apply = c->launches - before;
+        if (z_dev != pc->z.p)
+            CK(cudaMemcpyAsync(z_dev, pc->z.p, sizeof(double) * pc->n, cudaMemcpyDeviceToDevice, c->s));
+        return;
+    }
     if (!pc->exec) {
         DPP_TRACE_SCOPE(c, "pc.capture_instantiate");
         const int64_t before = c->launches;

@@ -25,6 +25,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "dpp_internal.cuh"
 
@@ -62,6 +63,9 @@ __device__ __forceinline__ void mwait(unsigned a, unsigned parity) {
             " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
             " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(a), "r"(parity) : "memory");
         if (ok) return;
+#ifdef LV_BACKOFF
+        __nanosleep(LV_BACKOFF);
+#endif
         if (clock64() - t0 > (4ll << 30)) __trap();
     }
 }
@@ -82,6 +86,23 @@ __host__ __device__ inline long long pu_off_code(long long nr) { return 16 + 24 
 __host__ __device__ inline long long pu_off_val(long long nr, long long ne) { return p16(pu_off_code(nr) + 4 * ne); }
 __host__ __device__ inline long long pu_block_bytes(long long nr, long long ne, long long np) {
     return p16(pu_off_val(nr, ne) + 8 * ne + 4 * np);
+}
+
+// block layout of the level-mbarrier sweep (16-byte aligned), rows in 32-row chunks whose
+// entries are stored column by column (SELL-32: entry k of the chunk's lane-l row at
+// ebase + 32 k + l, so a warp's 32 lanes read 32 consecutive words -- no bank conflicts):
+//   int4 {nr, nch, np, level} | int4 chunk[nch] {ebase, nE, nL, 0} | int2 row[nr] {local row,
+//   p0 << 4 | npush} | double dq[nr] | int code[NE] | double val[NE] | int push[np]
+// where a chunk holds nE early columns (sources of level <= l-2) then nL late ones (level
+// l-1), padded with (zero slot, 0.0) entries.
+__host__ __device__ inline long long lv_off_rw(long long nch) { return 16 + 16 * nch; }
+__host__ __device__ inline long long lv_off_dq(long long nch, long long nr) { return p16(lv_off_rw(nch) + 8 * nr); }
+__host__ __device__ inline long long lv_off_code(long long nch, long long nr) { return p16(lv_off_dq(nch, nr) + 8 * nr); }
+__host__ __device__ inline long long lv_off_val(long long nch, long long nr, long long ne) {
+    return p16(lv_off_code(nch, nr) + 2 * ne);
+}
+__host__ __device__ inline long long lv_block_bytes(long long nch, long long nr, long long ne, long long np) {
+    return p16(lv_off_val(nch, nr, ne) + 8 * ne + 4 * np);
 }
 
 template <int G>
@@ -204,9 +225,10 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
             for (int e = R.y + gl; e < R.z; e += G) sum += val[e] * xh[code[e]];
 #pragma unroll
             for (int s = G / 2; s > 0; s >>= 1) sum += __shfl_xor_sync(gmask, sum, s, G);
-            const double xr = (xh[R.x] - sum) * dq;   // dq = 1/t_ii (as SuperLU's pre-scaled solve)
+            const int rx = R.x & 0xffff;   // local row (upper bits: late-entry count, k_trsv_lvl)
+            const double xr = (xh[rx] - sum) * dq;   // dq = 1/t_ii (as SuperLU's pre-scaled solve)
             __syncwarp(gmask);
-            if (gl == 0) xh[R.x] = xr;
+            if (gl == 0) xh[rx] = xr;
             const int p0 = R.w >> 4, pc = R.w & 15;
             for (int u = gl; u < pc; u += G) {
                 const int pe = pl[p0 + u];
@@ -243,6 +265,20 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
 // + barrier).  The blocks are streamed by a dedicated producer warp through a ring of
 // full / empty mbarriers (consumer warps release a slot after its rows).
 constexpr unsigned long long PU_SENT = 0xFFFFFFFFFFFFFFFFull;
+#ifdef DPP_FLOW_PHASES
+// per (CTA, warp): cycles in {ring wait, row header, loads+poll, fma+reduce, store+push, idle},
+// row-group iterations, spin rounds (profiling build only: tools/flow_phases.sh)
+__device__ unsigned long long *g_flow_phase = nullptr;
+__device__ unsigned long long *g_flow_tl = nullptr;   // per (CTA, step): {level, min t late-wait done, max t arrive}
+__device__ int g_flow_smax = 0;
+__device__ int g_flow_nopush = 0;
+__device__ __forceinline__ long long clk() { long long t; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)); return t; }
+#define PH_T(v) const long long v = clk()
+#define PH_ADD(i, d) ph[i] += (d)
+#else
+#define PH_T(v)
+#define PH_ADD(i, d)
+#endif
 __device__ __forceinline__ double ld_vol_shared(unsigned a) {
     unsigned long long v;
     asm volatile("ld.volatile.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
@@ -339,9 +375,16 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
         }
     } else {
         const unsigned xh_s = su32(xh);
+#ifdef DPP_FLOW_PHASES
+        long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long t_last = clk();
+#endif
         for (int a = 0, j = 0; a < S; ++j) {
           const int e_run = run_end(a), sl = j % nst;
+          PH_T(tw0);
           mwait(su32(&mfull[sl]), (unsigned)((j / nst) & 1));
+          PH_T(tw1);
+          PH_ADD(0, tw1 - tw0);
           unsigned long long t_land = 0;
           if (dbg && lane == 0) t_land = gtimer();
           for (int t = a; t < e_run; ++t) {
@@ -357,6 +400,10 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
             // the other groups of its warp): the groups of a warp take consecutive rows
             const int g0 = (wid * 32) / G;   // first group of this warp
             for (int q0 = g0; q0 < nr; q0 += ngrp) {
+                PH_T(t0);
+#ifdef DPP_FLOW_PHASES
+                PH_ADD(5, t0 - t_last);
+#endif
                 const int q = q0 + (grp - g0);
                 const bool act = q < nr;
                 int4 R = make_int4(0, 0, 0, 0);
@@ -364,10 +411,12 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 if (act) {
                     R = rows[q];
                     dq = dg[q];
-                    bi = bsl[R.x];
+                    bi = bsl[R.x & 0xffff];
                 }
                 int len = R.z - R.y;
                 len = __reduce_max_sync(0xffffffffu, len);
+                PH_T(t1);
+                PH_ADD(1, t1 - t0);
                 // RND entries per lane loaded before any is waited on (independent loads in
                 // flight); per lane the products are added in the same e order as before
                 constexpr int RND = 4;
@@ -398,22 +447,37 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                             if (has[r] && __double_as_longlong(xv[r]) == (long long)PU_SENT) xv[r] = ld_vol_shared(xa[r]);
                         if (++spins > (1ll << 28)) __trap();
                     }
+                    PH_ADD(7, spins);
 #pragma unroll
                     for (int r = 0; r < RND; ++r)
                         if (has[r]) sum += v[r] * xv[r];
                 }
+                PH_T(t2);
+                PH_ADD(2, t2 - t1);
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o, G);
+#ifdef DPP_FLOW_PHASES
+                sum = __shfl_sync(0xffffffffu, sum, lane);   // materialise before the timestamp
+#endif
+                PH_T(t3);
+                PH_ADD(3, t3 - t2);
                 if (act) {
                     double xr = (bi - sum) * dq;   // dq = 1/t_ii (as SuperLU's pre-scaled solve)
                     if (__double_as_longlong(xr) == (long long)PU_SENT) xr = __longlong_as_double(0x7ff8000000000000ll);
-                    if (gl == 0) st_vol_shared(xh_s + 8u * (unsigned)R.x, xr);
+                    if (gl == 0) st_vol_shared(xh_s + 8u * (unsigned)(R.x & 0xffff), xr);
                     const int p0 = R.w >> 4, pc = R.w & 15;
                     for (int u = gl; u < pc; u += G) {
                         const int pe = pl[p0 + u];
                         st_remote(peer[(unsigned)pe >> 28] + 8u * ((unsigned)pe & 0x0fffffffu), xr);
                     }
                 }
+                __syncwarp();
+                PH_T(t4);
+                PH_ADD(4, t4 - t3);
+                PH_ADD(6, 1);
+#ifdef DPP_FLOW_PHASES
+                t_last = t4;
+#endif
             }
             __syncwarp();
             if (dbg && lane == 0 && (wid * 32) / G < nr) {   // warps with rows: landed / done (ns)
@@ -428,6 +492,324 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
           if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
           a = e_run;
         }
+#ifdef DPP_FLOW_PHASES
+        (void)t_last;
+        if (lane == 0 && g_flow_phase)
+            for (int i = 0; i < 8; ++i) g_flow_phase[((size_t)blockIdx.x * 32 + wid) * 8 + i] = ph[i];
+#endif
+    }
+    __syncthreads();
+    pdl_trigger();
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) {
+        const size_t g = (size_t)(base + i) * ncomp + comp;
+        x[g] = xh[i];
+        if (xout) xout[g] = xadd[g] + xh[i];
+    }
+}
+
+// ----------------------------------------------------------------- level-mbarrier variant
+// Same plan and arithmetic again (so bit-for-bit the other two kernels), but readiness is
+// tracked per level with one single-use mbarrier per (CTA, level), armed at launch with
+//   count = local rows of the level + 1   and   tx = bytes pushed into this CTA from the level.
+// A warp arrives once per step with the number of rows it solved (after its x stores: release),
+// remote producers push with st.async + complete_tx, so a completed level mbarrier means every
+// value of that level this CTA will read is in place.  Before its rows of level l a warp waits
+// (hardware-suspended try_wait, no polling of x slots) on the levels from the CTA's previous
+// step's level up to l-1; earlier levels are implied (the previous step's rows waited on them).
+// Warps without rows in a step do nothing for it, so no warp spins on shared memory and the
+// critical path per level is one wake-up + one row (measured phase breakdown: DESIGN.md §5).
+constexpr int LV_THREADS = 512;
+// Warp layout: warp w sits on SM sub-partition w % 4.  Warp 0 is the TMA producer and has
+// sub-partition 0 to itself (warps 4, 8, .. idle): a producer sharing a sub-partition with a team
+// slowed that team's levels 3-5x (bulk-copy issue).  Team t (= level % LV_TEAMS) = warps w with
+// w % 4 == t + 1, so each team owns one sub-partition.
+constexpr int LV_TEAMS = 3;   // level teams of k_trsv_lvl (and the plan's column classes)
+constexpr int LV_NS_MAX = 16;  // ring slots (one block each)
+// shared memory: ring mbarriers [2][LV_NS_MAX] | level mbarriers [L] | x slice | halo |
+//                step offsets [smax+1] | step levels [smax] | peer addresses [32] | ring [ns][stage]
+__host__ __device__ inline size_t lv_fixed(int chunk, int L, int hmax, int smax) {
+    return 16 * LV_NS_MAX + p16(8LL * L) + p16(8LL * chunk) + p16(8LL * hmax) + p16(8LL * (smax + 1)) +
+           p16(4LL * smax) + 128;
+}
+__device__ __forceinline__ bool mtest(unsigned a, unsigned parity) {
+    unsigned ok;
+    asm volatile("{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    return ok;
+}
+__global__ void __launch_bounds__(LV_THREADS, 1)
+    k_trsv_lvl(int n, int ncomp, int chunk, int L, int smax, int hmax, int stage, int ns,
+               const unsigned char *__restrict__ blocks, const long long *__restrict__ boff,
+               const int *__restrict__ tstart, const int *__restrict__ splev, const int *__restrict__ tx,
+               const int *__restrict__ lrows, const double *__restrict__ b, double *__restrict__ x,
+               const double *__restrict__ xadd, double *__restrict__ xout, int l2pf) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long *mfull = reinterpret_cast<unsigned long long *>(smem);
+    unsigned long long *mempty = mfull + LV_NS_MAX;
+    unsigned long long *mlev = mfull + 2 * LV_NS_MAX;
+    double *xh = reinterpret_cast<double *>(smem + 16 * LV_NS_MAX + p16(8LL * L));
+    const int chunkp = pu_chunkp(chunk);
+    long long *boff_s = reinterpret_cast<long long *>(xh + chunkp + p16(8LL * hmax) / 8);
+    int *slev = reinterpret_cast<int *>(boff_s + p16(8LL * (smax + 1)) / 8);
+    unsigned *peer = reinterpret_cast<unsigned *>(slev + p16(4LL * smax) / 4);   // [0,16): halo, [16,32): mlev
+    unsigned char *ring = smem + lv_fixed(chunk, L, hmax, smax);
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
+    const int comp = blockIdx.x / C;
+    const int s0 = tstart[k], S = tstart[k + 1] - s0;
+    const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int base = k * chunk, mine = min(chunk, n - base);
+    const int b0 = k * L;
+    if (threadIdx.x < ns) {   // slot s: full (TMA bytes), empty (every consumer warp passed its step)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mfull[threadIdx.x])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mempty[threadIdx.x])), "r"(LV_TEAMS * (nw / 4)) : "memory");
+    }
+#ifdef DPP_FLOW_PHASES
+    const bool nopush = g_flow_nopush;   // timing experiment only: no remote pushes (results invalid)
+#else
+    constexpr bool nopush = false;
+#endif
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mlev[l])), "r"(lrows[b0 + l] + 1) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mlev[l])), "r"(nopush ? 0 : tx[b0 + l])
+                     : "memory");
+    }
+    if (threadIdx.x < C) {
+        peer[threadIdx.x] = mapa_u32(su32(xh + chunkp), threadIdx.x);
+        peer[16 + threadIdx.x] = mapa_u32(su32(mlev), threadIdx.x);
+    }
+    for (int i = threadIdx.x; i <= S; i += blockDim.x) boff_s[i] = boff[s0 + i];
+    for (int i = threadIdx.x; i < S; i += blockDim.x) slev[i] = splev[s0 + i];
+    pdl_wait();   // b is the previous kernel's output
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = b[(size_t)(base + i) * ncomp + comp];
+    for (int i = threadIdx.x; i < hmax; i += blockDim.x) xh[chunkp + i] = 0.0;   // slot hmax-1: padding
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    // every CTA's level mbarriers are armed before the first push
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    // ring of ns one-block slots in step order: step s lives in slot s % ns.  A slot is refilled
+    // once every consumer warp passed its step -- the owning team after solving the block, the
+    // other teams as soon as they walk past it -- so slots free in level order and the producer
+    // runs up to ns - LV_TEAMS blocks ahead of the teams
+    if (wid == 0) {
+        if (lane == 0) {
+            int pa = 0;   // L2 prefetch cursor
+            const long long t0 = clock64();
+            for (int st = 0; st < S; ++st) {
+                const int sl = st % ns;
+                // poll with back-off: a producer spinning in try_wait steals issue slots from the
+                // team warps on its SM sub-partition (measured: that team's levels 3-5x slower)
+                if (st >= ns)
+                    while (!mtest(su32(&mempty[sl]), (unsigned)((st / ns - 1) & 1))) {
+                        __nanosleep(64);
+                        if (clock64() - t0 > (16ll << 30)) __trap();
+                    }
+                const unsigned bytes = (unsigned)(boff_s[st + 1] - boff_s[st]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mfull[sl])), "r"(bytes)
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(su32(ring + (size_t)sl * stage)), "l"(blocks + boff_s[st]), "r"(bytes), "r"(su32(&mfull[sl]))
+                             : "memory");
+                for (; l2pf && pa < S && pa < st + ns + l2pf; ++pa)
+                    if (pa >= st + ns) {
+                        const unsigned pb = (unsigned)(boff_s[pa + 1] - boff_s[pa]);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[pa]), "r"(pb) : "memory");
+                    }
+            }
+        }
+    } else if (wid % 4 != 0) {   // warps 4, 8, .. stay idle: sub-partition 0 is the producer's
+        // consumer warps in LV_TEAMS teams by level (team = wid % LV_TEAMS = level % LV_TEAMS).  A
+        // team's warps deal a block's 32-row chunks; for its level-l rows a warp sums the early
+        // columns (sources of levels <= l-LV_TEAMS-1, complete before its previous block ended)
+        // right away, the mid columns (levels l-LV_TEAMS .. l-2) once those are complete, and
+        // only the late columns (level l-1) after the last wait -- the other teams' rows run
+        // meanwhile, so a level's critical path is one wake-up plus the late columns.  Index /
+        // value loads of the first mid / late group are issued before the waits; partial sums
+        // regroup the row's dot product (exact-arithmetic equivalent).
+        const int team = wid % 4 - 1, wi = wid / 4;
+        const int nteam = nw / 4;
+        int waited = 0;   // levels [0, waited) known complete by this warp
+#ifdef DPP_FLOW_PHASES
+        long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        long long sink = 0;
+#endif
+        for (int st = 0; st < S; ++st) {
+            const int sl = st % ns;
+            const int lvl = slev[st];
+            // every warp waits for the slot's fill before releasing it: an arrival may not count
+            // toward the slot's previous use
+            mwait(su32(&mfull[sl]), (unsigned)((st / ns) & 1));
+            if (lvl % LV_TEAMS != team) {
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
+                continue;
+            }
+            {
+                const unsigned char *blk = ring + (size_t)sl * stage;
+                const int4 hd = *reinterpret_cast<const int4 *>(blk);
+                const int nr = hd.x, nch = hd.y;
+                if (wi >= nch) goto release;
+                {
+                const int4 *chs = reinterpret_cast<const int4 *>(blk + 16);
+                const int2 *rw = reinterpret_cast<const int2 *>(blk + lv_off_rw(nch));
+                const double *dg = reinterpret_cast<const double *>(blk + lv_off_dq(nch, nr));
+                const unsigned short *code = reinterpret_cast<const unsigned short *>(blk + lv_off_code(nch, nr));
+                int ne = 0;   // the last chunk's end
+                {
+                    const int4 lc = chs[nch - 1];
+                    ne = lc.x + 32 * (lc.y + lc.z + lc.w);
+                }
+                const double *val = reinterpret_cast<const double *>(blk + lv_off_val(nch, nr, ne));
+                const int *pl = reinterpret_cast<const int *>(val + ne);
+                int done = 0;
+#ifdef DPP_FLOW_PHASES
+                long long c_late = 1ll << 62;
+                const long long c_first = clk();
+#endif
+                for (int ci = wi; ci < nch; ci += nteam) {
+                    const int q = 32 * ci + lane;
+                    const bool act = q < nr;
+                    done += min(32, nr - 32 * ci);
+                    const int4 ch = chs[ci];
+                    int2 R = make_int2(0, 0);
+                    double dq = 0.0;
+                    if (act) {
+                        R = rw[q];
+                        dq = dg[q];
+                    }
+                    PH_T(c0);
+                    for (; waited < lvl - LV_TEAMS; ++waited) mwait(su32(&mlev[waited]), 0);   // early levels
+                    PH_T(c1);
+                    PH_ADD(1, c1 - c0);
+                    // early columns (a multiple of 4): two groups of 4 loads in flight, four partial sums
+                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                    int e = ch.x + lane;
+#pragma unroll 2
+                    for (int k = 0; k < ch.y; k += 4, e += 128) {
+                        int cd[4];
+                        double v[4], xv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) { cd[u] = code[e + 32 * u]; v[u] = val[e + 32 * u]; }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) xv[u] = xh[cd[u]];
+                        s0 = fma(v[0], xv[0], s0); s1 = fma(v[1], xv[1], s1);
+                        s2 = fma(v[2], xv[2], s2); s3 = fma(v[3], xv[3], s3);
+                    }
+                    // mid / late columns (multiples of 4): the first group's indices and values are
+                    // fetched before the waits, only the x gathers follow them
+                    const int em = e, el = e + 32 * ch.z;
+                    int mc[4], lc[4];
+                    double mv[4], lv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        mc[u] = ch.z ? code[em + 32 * u] : 0;
+                        mv[u] = ch.z ? val[em + 32 * u] : 0.0;
+                        lc[u] = ch.w ? code[el + 32 * u] : 0;
+                        lv[u] = ch.w ? val[el + 32 * u] : 0.0;
+                    }
+                    const double bq = act ? xh[R.x] : 0.0;
+                    double sum = (s0 + s1) + (s2 + s3);
+#ifdef DPP_FLOW_PHASES
+                    sink ^= (long long)__double_as_longlong(sum);
+#endif
+                    PH_T(c2);
+                    PH_ADD(2, c2 - c1);
+                    for (; waited < lvl - 1; ++waited) mwait(su32(&mlev[waited]), 0);   // mid levels
+                    auto group4 = [&](const int *gc, const double *gv, double &t0, double &t1) {
+                        double gx[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) gx[u] = xh[gc[u]];
+                        t0 = fma(gv[0], gx[0], t0); t1 = fma(gv[1], gx[1], t1);
+                        t0 = fma(gv[2], gx[2], t0); t1 = fma(gv[3], gx[3], t1);
+                    };
+                    auto rest4 = [&](int e0, int n, double &t0, double &t1) {   // groups after the first
+                        for (int k = 4; k < n; k += 4) {
+                            int gc[4];
+                            double gv[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) { gc[u] = code[e0 + 32 * (k + u)]; gv[u] = val[e0 + 32 * (k + u)]; }
+                            group4(gc, gv, t0, t1);
+                        }
+                    };
+                    if (ch.z) {
+                        double t0 = 0.0, t1 = 0.0;
+                        group4(mc, mv, t0, t1);
+                        rest4(em, ch.z, t0, t1);
+                        sum += t0 + t1;
+                    }
+                    PH_T(c3);
+                    PH_ADD(3, c3 - c2);
+                    if (waited < lvl) {   // level l-1
+                        mwait(su32(&mlev[lvl - 1]), 0);
+                        waited = lvl;
+                    }
+                    PH_T(c4);
+                    PH_ADD(5, c4 - c3);
+#ifdef DPP_FLOW_PHASES
+                    c_late = min(c_late, c4);
+#endif
+                    if (ch.w) {
+                        double t0 = 0.0, t1 = 0.0;
+                        group4(lc, lv, t0, t1);
+                        rest4(el, ch.w, t0, t1);
+                        sum += t0 + t1;
+                    }
+#ifdef DPP_FLOW_PHASES
+                    sink ^= (long long)__double_as_longlong(sum);
+                    PH_T(c4a);
+                    PH_ADD(4, c4a - c4);
+#endif
+                    if (act) {
+                        const double xr = (bq - sum) * dq;   // dq = 1/t_ii
+                        xh[R.x] = xr;
+                        const int p0 = R.y >> 4, pc = nopush ? 0 : R.y & 15;
+                        for (int u = 0; u < pc; ++u) {
+                            const int pe = pl[p0 + u];
+                            const int dst = (int)((unsigned)pe >> 28);
+                            const unsigned slh = (unsigned)pe & 0x0fffffffu;
+                            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                                         ::"r"(peer[dst] + 8u * slh), "l"(__double_as_longlong(xr)),
+                                         "r"(peer[16 + dst] + 8u * lvl)
+                                         : "memory");
+                        }
+#ifdef DPP_FLOW_PHASES
+                        sink ^= (long long)__double_as_longlong(xr);
+#endif
+                    }
+                    __syncwarp();
+                    PH_T(c5);
+#ifdef DPP_FLOW_PHASES
+                    PH_ADD(7, c5 - c4a);
+#endif
+                    PH_ADD(6, 1);
+                }
+                __syncwarp();
+                PH_T(c6);
+                if (lane == 0)   // release: this warp's x stores of the level precede the arrival
+                    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mlev[lvl])),
+                                 "r"(done)
+                                 : "memory");
+                PH_T(c7);
+                PH_ADD(0, c7 - c6);
+#ifdef DPP_FLOW_PHASES
+                if (lane == 0 && g_flow_tl) {
+                    unsigned long long *o = g_flow_tl + ((size_t)blockIdx.x * g_flow_smax + st) * 4;
+                    o[0] = lvl;
+                    atomicMin(o + 1, (unsigned long long)c_late);
+                    atomicMax(o + 2, (unsigned long long)c7);
+                    atomicMin(o + 3, (unsigned long long)c_first);
+                }
+#endif
+                }
+            }
+        release:
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
+        }
+#ifdef DPP_FLOW_PHASES
+        if (lane == 0 && g_flow_phase)
+            for (int i = 0; i < 8; ++i) g_flow_phase[((size_t)blockIdx.x * 32 + wid) * 8 + i] = ph[i] + (sink == 0x1234567 ? 1 : 0);
+#endif
     }
     __syncthreads();
     pdl_trigger();
@@ -515,10 +897,14 @@ __global__ void k_pu_headers(int np_, const int *pstart, const int *plev, const 
         h[3] = plev[i];
     }
 }
+// A row's entries are stored with the sources of levels <= l-2 first ("early") and those of
+// level l-1 last ("late"; their count in R.x >> 16): k_trsv_lvl sums the early ones before it
+// waits for level l-1.  Every kernel adds a lane's entries in storage order.
 __global__ void k_pu_fill(int n, int chunk, int chunkp, int np_, const int *pstart, const int *perm,
                           const int *rptr, const int *rpp, const long long *boff, const int *ptr, const int *idx,
                           const double *val, const double *diag, const unsigned long long *h, const int *hstart,
-                          const int *pptr, const unsigned long long *k2s, const int *slots, unsigned char *blocks) {
+                          const int *pptr, const unsigned long long *k2s, const int *slots, const int *lev,
+                          unsigned char *blocks) {
     for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         int lo = 0, hi = np_;   // part holding sorted row q: last part with pstart <= q
         while (hi - lo > 1) {
@@ -538,12 +924,17 @@ __global__ void k_pu_fill(int n, int chunk, int chunkp, int np_, const int *psta
         int *pl = reinterpret_cast<int *>(vv + ne);
         const int e0 = rptr[q] - rptr[q0], e1 = rptr[q + 1] - rptr[q0];
         const int p0 = rpp[q] - rpp[q0], pc = rpp[q + 1] - rpp[q];
-        rows[i] = make_int4(r - owner * chunk, e0, e1, (p0 << 4) | pc);
+        const int lr = lev[r];
+        int nlate = 0;
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) nlate += lev[idx[p]] >= lr - 1;
+        rows[i] = make_int4((r - owner * chunk) | (nlate << 16), e0, e1, (p0 << 4) | pc);
         dg[i] = diag ? 1.0 / diag[r] : 1.0;
         int w = e0;
         const int hs = hstart[owner], he = hstart[owner + 1];
-        for (int p = ptr[r]; p < ptr[r + 1]; ++p, ++w) {
+        for (int pass = 0; pass < 2; ++pass)
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
             const int j = idx[p];
+            if ((lev[j] >= lr - 1) != (pass == 1)) continue;
             const int o = j / chunk;
             if (o == owner) {
                 code[w] = j - o * chunk;
@@ -557,11 +948,127 @@ __global__ void k_pu_fill(int n, int chunk, int chunkp, int np_, const int *psta
                 code[w] = chunkp + (lo - hs);
             }
             vv[w] = val[p];
+            ++w;
         }
         int u = p0;
         for (int t = pptr[r]; t < pptr[r + 1]; ++t, ++u)
             pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28) | (unsigned)slots[t]);
     }
+}
+
+// ---- level-mbarrier (SELL chunk) format
+__device__ __forceinline__ int pu_code(int j, int owner, int chunk, int chunkp, const unsigned long long *h, int hs,
+                                       int he) {
+    const int o = j / chunk;
+    if (o == owner) return j - o * chunk;
+    const unsigned long long key = ((unsigned long long)owner << 32) | (unsigned)j;
+    int lo = hs, hi = he;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (h[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return chunkp + (lo - hs);
+}
+// entry class by source level distance: 0 early (<= l-LV_TEAMS-1), 1 mid (l-LV_TEAMS .. l-2), 2 late (l-1)
+__device__ __forceinline__ int lv_class(int ls, int lr) { return ls >= lr - 1 ? 2 : ls >= lr - LV_TEAMS ? 1 : 0; }
+__global__ void k_lv_counts(int n, const int *perm, const int *ptr, const int *idx, const int *lev, int *cnt) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int r = perm[q], lr = lev[r];
+        int c3[3] = {0, 0, 0};
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) ++c3[lv_class(lev[idx[p]], lr)];
+        cnt[3 * q] = c3[0];
+        cnt[3 * q + 1] = c3[1];
+        cnt[3 * q + 2] = c3[2];
+    }
+}
+// block headers and chunk tables; padding lanes of a partial last chunk get (zero slot, 0.0)
+__global__ void k_lv_headers(int np_, const int *pstart, const int *pch, const int *plev, const int *rpp,
+                             const int4 *ctab, int zero_code, const long long *boff, unsigned char *blocks) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np_; i += gridDim.x * blockDim.x) {
+        unsigned char *B = blocks + boff[i];
+        const int nr = pstart[i + 1] - pstart[i], g0 = pch[i], nch = pch[i + 1] - g0;
+        const int4 lc = ctab[pch[i + 1] - 1];
+        const int ncol = lc.y + lc.z + lc.w;
+        const int ne = lc.x + 32 * ncol;
+        int *h = reinterpret_cast<int *>(B);
+        h[0] = nr;
+        h[1] = nch;
+        h[2] = rpp[pstart[i + 1]] - rpp[pstart[i]];
+        h[3] = plev[i];
+        int4 *chs = reinterpret_cast<int4 *>(B + 16);
+        for (int c = 0; c < nch; ++c) chs[c] = ctab[g0 + c];
+        unsigned short *code = reinterpret_cast<unsigned short *>(B + lv_off_code(nch, nr));
+        double *vv = reinterpret_cast<double *>(B + lv_off_val(nch, nr, ne));
+        const int used = nr - 32 * (nch - 1);
+        for (int k = 0; k < ncol; ++k)
+            for (int l = used; l < 32; ++l) {
+                code[lc.x + 32 * k + l] = zero_code;
+                vv[lc.x + 32 * k + l] = 0.0;
+            }
+    }
+}
+__global__ void k_lv_fill(int n, int chunk, int chunkp, int zero_code, int np_, const int *pstart, const int *pch,
+                          const int *perm, const int *rpp, const long long *boff, const int *ptr, const int *idx,
+                          const double *val, const double *diag, const int *lev, const unsigned long long *h,
+                          const int *hstart, const int *pptr, const unsigned long long *k2s, const int *slots,
+                          const int4 *ctab, unsigned char *blocks) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        int lo = 0, hi = np_;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (pstart[mid] <= q) lo = mid; else hi = mid;
+        }
+        const int part = lo, q0 = pstart[part], nr = pstart[part + 1] - q0, i = q - q0;
+        const int g0 = pch[part], nch = pch[part + 1] - g0;
+        const int4 lc = ctab[pch[part + 1] - 1];
+        const int ne = lc.x + 32 * (lc.y + lc.z + lc.w);
+        const int gc = g0 + i / 32, lane = i % 32;
+        unsigned char *B = blocks + boff[part];
+        int2 *rw = reinterpret_cast<int2 *>(B + lv_off_rw(nch));
+        double *dq = reinterpret_cast<double *>(B + lv_off_dq(nch, nr));
+        unsigned short *code = reinterpret_cast<unsigned short *>(B + lv_off_code(nch, nr));
+        double *vv = reinterpret_cast<double *>(B + lv_off_val(nch, nr, ne));
+        int *pl = reinterpret_cast<int *>(vv + ne);
+        const int r = perm[q], owner = r / chunk, lr = lev[r];
+        const int p0 = rpp[q] - rpp[q0], pc = rpp[q + 1] - rpp[q];
+        rw[i] = make_int2(r - owner * chunk, (p0 << 4) | pc);
+        dq[i] = diag ? 1.0 / diag[r] : 1.0;
+        const int hs = hstart[owner], he = hstart[owner + 1];
+        const int4 ch = ctab[gc];
+        const int nc[3] = {ch.y, ch.z, ch.w};
+        const int c0[3] = {0, ch.y, ch.y + ch.z};
+        int kk[3] = {0, 0, 0};
+        for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
+            const int j = idx[p];
+            const int cl = lv_class(lev[j], lr);
+            const int e = ch.x + 32 * (c0[cl] + kk[cl]++) + lane;
+            code[e] = pu_code(j, owner, chunk, chunkp, h, hs, he);
+            vv[e] = val[p];
+        }
+        for (int cl = 0; cl < 3; ++cl)
+            for (; kk[cl] < nc[cl]; ++kk[cl]) {
+                const int e = ch.x + 32 * (c0[cl] + kk[cl]) + lane;
+                code[e] = zero_code;
+                vv[e] = 0.0;
+            }
+        int u = p0;
+        for (int t = pptr[r]; t < pptr[r + 1]; ++t, ++u)
+            pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28) | (unsigned)slots[t]);
+    }
+}
+
+// sweep kernel: 1 dataflow (default), 0 level-mbarrier (DPP_PU_MODE=lvl; own block format),
+// 2 level-synchronous push (DPP_PU_MODE=push or DPP_PU_FLOW=0)
+int pu_mode() {
+    static const int mode = [] {
+        const char *e = std::getenv("DPP_PU_MODE");
+        const char *f = std::getenv("DPP_PU_FLOW");
+        if (f && *f == '0') return 2;
+        if (e && !std::strcmp(e, "lvl")) return 0;
+        if (e && !std::strcmp(e, "push")) return 2;
+        return 1;
+    }();
+    return mode;
 }
 
 template <typename T>
@@ -577,6 +1084,7 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     const int n = T.n;
     const int chunk = (n + C - 1) / C;
     const int nblk = C * L;
+    if (chunk >= (1 << 16)) return false;   // local row index in 16 bits of the row header
     const Csr &S = T.strict;
     // rows grouped by (owner CTA, level)
     DBuf<int> key(n, c->s), skey(n, c->s), rows(n, c->s), perm(n, c->s), lp((size_t)nblk + 1, c->s);
@@ -651,9 +1159,27 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     counts_to_ptr(c, plen.p, n, rpp);
     // steps: the non-empty (CTA, level) blocks, each cut into parts of at most `cap` bytes
     std::vector<int> hlp = lp.to_host(), hr = rptr.to_host(), hp = rpp.to_host();
+    {
+        std::vector<int> lr((size_t)C * L);
+        for (size_t i = 0; i < lr.size(); ++i) lr[i] = hlp[i + 1] - hlp[i];
+        P->lrows.alloc(lr.size(), c->s);
+        P->lrows.upload(lr.data(), lr.size());
+    }
     auto part_bytes = [&](int q0, int q1) {
         return pu_block_bytes(q1 - q0, (long long)hr[q1] - hr[q0], (long long)hp[q1] - hp[q0]);
     };
+    const int fmt = pu_mode() == 0 ? 1 : 0;
+    if (fmt == 1) ++hmax;   // one zero slot after the halo: the padding entries' source
+    if (fmt == 1 && pu_chunkp(chunk) + hmax >= (1 << 16)) return false;   // 16-bit column codes
+    std::vector<int> hcnt;   // lvl format: per sorted row, entries of class early / mid / late
+    if (fmt == 1) {
+        DBuf<int> dcnt(3 * (size_t)n, c->s);
+        k_lv_counts<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, perm.p, S.ptr.p, S.idx.p, lev.p, dcnt.p);
+        launched(c);
+        hcnt = dcnt.to_host();
+    }
+    std::vector<int> pch;    // lvl format: chunks of part i are ctab[pch[i] .. pch[i+1])
+    std::vector<int4> ctab;  //   {ebase, early, mid, late columns}
     std::vector<int> pstart, plev, sstart(C + 1, 0);
     std::vector<long long> pboff;
     int smax = 0, widest = 1;
@@ -661,18 +1187,52 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     bool ok = false;
     for (int tries = 0; tries < 4 && !ok; ++tries) {
         const int smax_est = tries == 0 ? L : smax;
-        const size_t fixed = pu_fixed(chunk, L, hmax, smax_est);
+        const size_t fixed = fmt == 1 ? lv_fixed(chunk, L, hmax, smax_est) : pu_fixed(chunk, L, hmax, smax_est);
         if (fixed + 2 * 16384 >= PU_SMEM_LIMIT) return false;
         long long cap = (long long)(PU_SMEM_LIMIT - fixed) / 3;
         if (cap < 16384) cap = (long long)(PU_SMEM_LIMIT - fixed) / 2;
+        if (fmt == 1) cap = (long long)(PU_SMEM_LIMIT - fixed) / (LV_TEAMS + 2);   // >= 6 one-block ring slots
         cap &= ~127LL;
         pstart.clear(); plev.clear(); pboff.assign(1, 0);
+        pch.assign(1, 0); ctab.clear();
         smax = 0; mx = 16; widest = 1;
         bool fit = true;
         for (int d = 0; d < C && fit; ++d) {
             sstart[d] = (int)plev.size();
             for (int l = 0; l < L && fit; ++l) {
                 const int a0 = hlp[d * L + l], a1 = hlp[d * L + l + 1];
+                if (fmt == 1) {   // parts grown row by row; chunk maxima tracked incrementally
+                    for (int q = a0; q < a1 && fit;) {
+                        long long nr = 0, nch = 0, ne = 0, np = 0;
+                        int cur[3] = {0, 0, 0}, inc = 0;
+                        const int q0 = q;
+                        while (q < a1) {
+                            const int *rc = &hcnt[3 * (size_t)q];
+                            const bool fresh = nch == 0 || inc == 32;
+                            int nx[3];   // early columns padded to 8, mid / late to 4 (whole load groups)
+                            for (int u = 0; u < 3; ++u) {
+                                const int pad = 4;
+                                const int want = (rc[u] + pad - 1) / pad * pad;
+                                nx[u] = fresh ? want : std::max(cur[u], want);
+                            }
+                            const long long nch2 = nch + (fresh ? 1 : 0);
+                            const long long ne2 = ne + 32LL * ((nx[0] + nx[1] + nx[2]) - (fresh ? 0 : cur[0] + cur[1] + cur[2]));
+                            const long long np2 = np + (hp[q + 1] - hp[q]);
+                            if (lv_block_bytes(nch2, nr + 1, ne2, np2) > cap) break;
+                            if (fresh) ctab.push_back(make_int4((int)ne, nx[0], nx[1], nx[2]));
+                            else ctab.back() = make_int4(ctab.back().x, nx[0], nx[1], nx[2]);
+                            nch = nch2; ne = ne2; np = np2; inc = fresh ? 1 : inc + 1; ++nr; ++q;
+                            for (int u = 0; u < 3; ++u) cur[u] = nx[u];
+                        }
+                        if (nr == 0) { fit = false; break; }
+                        const long long by = lv_block_bytes(nch, nr, ne, np);
+                        pstart.push_back(q0); plev.push_back(l); pboff.push_back(pboff.back() + by);
+                        pch.push_back((int)ctab.size());
+                        mx = std::max(mx, by);
+                        widest = std::max(widest, (int)nch);
+                    }
+                    continue;
+                }
                 for (int q = a0; q < a1;) {
                     int e = q + 1;
                     if (part_bytes(q, e) > cap) { fit = false; break; }
@@ -693,10 +1253,11 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     if (!ok) return false;
     const int np_ = (int)plev.size();
     pstart.push_back(n);
-    const size_t fixed = pu_fixed(chunk, L, hmax, smax);
+    const size_t fixed = fmt == 1 ? lv_fixed(chunk, L, hmax, smax) : pu_fixed(chunk, L, hmax, smax);
     const long long stage = (mx + 127) & ~127LL;
-    const int nst = (int)std::min<long long>(PU_NST_MAX, (long long)(PU_SMEM_LIMIT - fixed) / stage);
-    if (nst < 2) return false;
+    const int nst = fmt == 1 ? (int)std::min<long long>(LV_NS_MAX, (long long)(PU_SMEM_LIMIT - fixed) / stage)
+                             : (int)std::min<long long>(PU_NST_MAX, (long long)(PU_SMEM_LIMIT - fixed) / stage);
+    if (nst < (fmt == 1 ? LV_TEAMS + 2 : 2)) return false;
     const long long total = pboff.back();
     DBuf<int> dpstart((size_t)np_ + 1, c->s), dplev((size_t)std::max(np_, 1), c->s);
     dpstart.upload(pstart.data(), pstart.size());
@@ -705,6 +1266,10 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     P->sstart.upload(sstart.data(), sstart.size());
     P->boff.alloc((size_t)np_ + 1, c->s);
     P->boff.upload(pboff.data(), pboff.size());
+    if (fmt == 1) {
+        P->slev.alloc(std::max(np_, 1), c->s);
+        P->slev.upload(plev.data(), np_);
+    }
     P->C = C;
     P->chunk = chunk;
     P->L = L;
@@ -724,21 +1289,38 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     static const int force_thr = [] { const char *e = std::getenv("DPP_PU_THREADS"); return e ? std::atoi(e) : 0; }();
     if (force_thr) threads = std::min(threads, force_thr);
     P->threads = threads;
+    P->widest = widest;
+    P->fmt = fmt;
     P->blocks.alloc((size_t)total, c->s);
-    if (np_) {
+    if (np_ && fmt == 1) {
+        DBuf<int> dpch(pch.size(), c->s);
+        DBuf<int4> dct(ctab.size(), c->s);
+        dpch.upload(pch.data(), pch.size());
+        dct.upload(ctab.data(), ctab.size());
+        const int zero_code = pu_chunkp(chunk) + hmax - 1;
+        k_lv_headers<<<grid_for(np_, 128, c->sms), 128, 0, c->s>>>(np_, dpstart.p, dpch.p, dplev.p, rpp.p, dct.p,
+                                                                   zero_code, P->boff.p, P->blocks.p);
+        launched(c);
+        k_lv_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, pu_chunkp(chunk), zero_code, np_, dpstart.p,
+                                                              dpch.p, perm.p, rpp.p, P->boff.p, S.ptr.p, S.idx.p,
+                                                              S.val.p, T.diag.n ? T.diag.p : nullptr, lev.p, H.p,
+                                                              hstart.p, pptr.p, k2s.p, slots.p, dct.p, P->blocks.p);
+        launched(c);
+        CK(cudaStreamSynchronize(c->s));   // the chunk tables are freed on return
+    } else if (np_) {
         k_pu_headers<<<grid_for(np_, 256, c->sms), 256, 0, c->s>>>(np_, dpstart.p, dplev.p, rptr.p, rpp.p,
                                                                    P->blocks.p, P->boff.p);
         launched(c);
         k_pu_fill<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, chunk, pu_chunkp(chunk), np_, dpstart.p, perm.p,
                                                               rptr.p, rpp.p, P->boff.p, S.ptr.p, S.idx.p, S.val.p,
                                                               T.diag.n ? T.diag.p : nullptr, H.p, hstart.p, pptr.p,
-                                                              k2s.p, slots.p, P->blocks.p);
+                                                              k2s.p, slots.p, lev.p, P->blocks.p);
         launched(c);
     }
     CK(cudaStreamSynchronize(c->s));
     if (TraceScope::on())
-        std::fprintf(stderr, "[dpp-trace]   push_plan n=%d C=%d L=%d steps max %d G=%d thr=%d halo max %d (pairs %d) stage=%lld nst=%d\n",
-                     n, C, L, smax, P->G, threads, hmax, nh, stage, nst);
+        std::fprintf(stderr, "[dpp-trace]   push_plan n=%d C=%d L=%d steps max %d G=%d thr=%d halo max %d (pairs %d) stage=%lld nst=%d fmt=%d bytes=%lld widest=%d\n",
+                     n, C, L, smax, P->G, threads, hmax, nh, stage, nst, fmt, total, widest);
     T.pu = std::move(P);
     return true;
 }
@@ -764,6 +1346,7 @@ bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
         setk((const void *)k_trsv_flow<8>);
         setk((const void *)k_trsv_flow<16>);
         setk((const void *)k_trsv_flow<32>);
+        setk((const void *)k_trsv_lvl);
         attr = true;
     }
     // as many CTAs as useful: each keeps >= ~2k rows of x
@@ -821,10 +1404,88 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
         CK(cudaMemcpyAsync(fdbg, init.data(), nfd * 8, cudaMemcpyHostToDevice, st));
         CK(cudaStreamSynchronize(st));
     }
+    // level-mbarrier sweep (default): no polling; DPP_PU_MODE=flow|push selects the others
+    const int mode = pu_mode();
+    if (P.fmt == 1) {
+        const size_t lfixed = lv_fixed(P.chunk, P.L, P.hmax, P.smax);
+        if (wp || P.nst < LV_TEAMS + 2 || lfixed + (size_t)P.nst * P.stage > PU_SMEM_LIMIT)
+            DPP_FAIL(DPP_ERR_RUNTIME, "level-mbarrier sweep: plan does not fit");
+        // LV_TEAMS level teams, each wide enough for the widest block (in 32-row chunks) in one round
+        static const int pt_env = [] { const char *e = std::getenv("DPP_LVL_PER_TEAM"); return e ? std::atoi(e) : 0; }();
+        const int per_team = pt_env ? pt_env : std::max(1, std::min(P.widest, LV_THREADS / 128));
+        cfg.blockDim = dim3(128 * per_team, 1, 1);   // per_team warps on each sub-partition
+        cfg.dynamicSmemBytes = lfixed + (size_t)P.nst * P.stage;
+        const int *lr = P.lrows.p, *txp = P.tx.p, *ss = P.sstart.p;
+        const int nn = T.n / T.ncomp;
+#ifdef DPP_FLOW_PHASES
+        static const char *ph_path2 = std::getenv("DPP_FLOW_PHASES");
+        unsigned long long *phb2 = nullptr;
+        const size_t nph2 = (size_t)P.C * T.ncomp * 32 * 8;
+        cudaEvent_t pe0 = nullptr, pe1 = nullptr;
+        unsigned long long *tlb = nullptr;
+        const size_t ntl = (size_t)P.C * T.ncomp * std::max(P.smax, 1) * 4;
+        if (ph_path2 && *ph_path2 && !c->capturing) {
+            CK(cudaStreamSynchronize(st));
+            CK(cudaMalloc((void **)&phb2, nph2 * 8));
+            CK(cudaMemset(phb2, 0, nph2 * 8));
+            CK(cudaMemcpyToSymbol(g_flow_phase, &phb2, sizeof(phb2)));
+            CK(cudaMalloc((void **)&tlb, ntl * 8));
+            std::vector<unsigned long long> init(ntl, 0);
+            for (size_t i = 0; i < ntl; i += 4) { init[i + 1] = ~0ull; init[i + 3] = ~0ull; }
+            CK(cudaMemcpy(tlb, init.data(), ntl * 8, cudaMemcpyHostToDevice));
+            CK(cudaMemcpyToSymbol(g_flow_tl, &tlb, sizeof(tlb)));
+            const int sm_ = P.smax;
+            CK(cudaMemcpyToSymbol(g_flow_smax, &sm_, sizeof(int)));
+            const int np_env = std::getenv("DPP_LVL_NOPUSH") ? 1 : 0;
+            CK(cudaMemcpyToSymbol(g_flow_nopush, &np_env, sizeof(int)));
+            cudaEventCreate(&pe0); cudaEventCreate(&pe1);
+            cudaEventRecord(pe0, st);
+        }
+#endif
+        e = cudaLaunchKernelEx(&cfg, k_trsv_lvl, nn, T.ncomp, P.chunk, P.L, P.smax, P.hmax, P.stage, P.nst, B, O, ss,
+                               (const int *)P.slev.p, txp, lr, b, x, xadd, xout, l2pf);
+#ifdef DPP_FLOW_PHASES
+        if (phb2) {
+            cudaEventRecord(pe1, st);
+            CK(cudaStreamSynchronize(st));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, pe0, pe1);
+            std::vector<unsigned long long> h(nph2);
+            CK(cudaMemcpy(h.data(), phb2, nph2 * 8, cudaMemcpyDeviceToHost));
+            unsigned long long *z = nullptr;
+            CK(cudaMemcpyToSymbol(g_flow_phase, &z, sizeof(z)));
+            CK(cudaMemcpyToSymbol(g_flow_tl, &z, sizeof(z)));
+            cudaFree(phb2);
+            {
+                std::vector<unsigned long long> tl(ntl);
+                CK(cudaMemcpy(tl.data(), tlb, ntl * 8, cudaMemcpyDeviceToHost));
+                cudaFree(tlb);
+                std::string tp = std::string(ph_path2) + ".tl";
+                if (FILE *f = std::fopen(tp.c_str(), "a")) {
+                    std::fprintf(f, "# n=%d C=%d ncomp=%d smax=%d L=%d\n", T.n, P.C, T.ncomp, P.smax, P.L);
+                    for (size_t i = 0; i < ntl / 4; ++i)
+                        if (tl[i * 4 + 2]) std::fprintf(f, "%zu %zu %llu %llu %llu %llu\n", i / P.smax, i % P.smax, tl[i * 4], tl[i * 4 + 3], tl[i * 4 + 1], tl[i * 4 + 2]);
+                    std::fclose(f);
+                }
+            }
+            if (FILE *f = std::fopen(ph_path2, "a")) {
+                std::fprintf(f, "# lvl n=%d C=%d ncomp=%d L=%d G=%d threads=%d us=%.2f\n", T.n, P.C, T.ncomp, P.L, 1, (int)cfg.blockDim.x, ms * 1e3);
+                for (size_t i = 0; i < nph2 / 8; ++i) {
+                    const unsigned long long *o = &h[i * 8];
+                    if (o[6]) std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 32, i % 32, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+                }
+                std::fclose(f);
+            }
+        }
+#endif
+        CK(e);
+        launched(c);
+        return;
+    }
     // dataflow for thin rows (C2: G = 2 / 8); the level-synchronous kernel measured faster for
     // the 32-lane groups of the long-row triangles of configs 3/4 (34.0 vs 37.8 ms per PC apply at C3)
     static const int flow_gmax = [] { const char *e = std::getenv("DPP_FLOW_GMAX"); return e ? std::atoi(e) : 16; }();
-    if (flow && P.G <= flow_gmax && !wp && !dbg && P.L >= nst_f && nst_b >= 2 && nst_f >= 2 &&
+    if (flow && mode != 2 && P.G <= flow_gmax && !wp && !dbg && P.L >= nst_f && nst_b >= 2 && nst_f >= 2 &&
         fixed + flags + (size_t)nst_f * stage_f <= PU_SMEM_LIMIT) {
         cfg.blockDim = dim3(std::min(PU_THREADS, P.threads + 32), 1, 1);
         cfg.dynamicSmemBytes = fixed + (size_t)nst_f * stage_f + flags;
@@ -835,6 +1496,44 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
             case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
             default: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
         }
+#ifdef DPP_FLOW_PHASES
+        static const char *ph_path = std::getenv("DPP_FLOW_PHASES");
+        unsigned long long *phb = nullptr;
+        const size_t nph = (size_t)P.C * T.ncomp * 32 * 8;
+        if (ph_path && *ph_path && !c->capturing) {
+            CK(cudaStreamSynchronize(st));
+            CK(cudaMalloc((void **)&phb, nph * 8));
+            CK(cudaMemset(phb, 0, nph * 8));
+            CK(cudaMemcpyToSymbol(g_flow_phase, &phb, sizeof(phb)));
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0); cudaEventCreate(&e1);
+            cudaEventRecord(e0, st);
+            switch (P.G) {
+                case 2: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<2>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+                case 4: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<4>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+                case 8: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<8>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+                case 16: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<16>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+                default: e = cudaLaunchKernelEx(&cfg, k_trsv_flow<32>, T.n / T.ncomp, T.ncomp, P.chunk, P.L, P.smax, P.hmax, (int)stage_f, nst_f, B, O, (const int *)P.sstart.p, b, x, xadd, xout, l2pf, fdbg); break;
+            }
+            cudaEventRecord(e1, st);
+            CK(cudaStreamSynchronize(st));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            std::vector<unsigned long long> h(nph);
+            CK(cudaMemcpy(h.data(), phb, nph * 8, cudaMemcpyDeviceToHost));
+            unsigned long long *z = nullptr;
+            CK(cudaMemcpyToSymbol(g_flow_phase, &z, sizeof(z)));
+            cudaFree(phb);
+            if (FILE *f = std::fopen(ph_path, "a")) {
+                std::fprintf(f, "# n=%d C=%d ncomp=%d L=%d G=%d threads=%d us=%.2f\n", T.n, P.C, T.ncomp, P.L, P.G, (int)cfg.blockDim.x, ms * 1e3);
+                for (size_t i = 0; i < nph / 8; ++i) {
+                    const unsigned long long *o = &h[i * 8];
+                    if (o[6]) std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / 32, i % 32, o[0], o[1], o[2], o[3], o[4], o[5], o[6], o[7]);
+                }
+                std::fclose(f);
+            }
+        }
+#endif
         CK(e);
         launched(c);
         if (fdbg) {   // "# n C ncomp smax" then per (cta, step): cta step level rows t_land t_done
