@@ -16,7 +16,16 @@ Multi-GPU: the exact preconditioner does not shard, so N GPUs
 run N independent replicas (weak scaling, no collective on the data path).
 
 --impl reference times the CPU oracle (a numpy/scipy/C port of the reference
-path, oracle/) on the host cores on a bounded sample of the same workload.
+path, oracle/; bit-identical to the reference at C2, tests/golden/configs.json) on
+the host cores on the same workload (C2, one solve per step, ~15 s), and quotes the
+unmodified reference's own run_case(repeats=3) time at C2 measured in the build
+container (tests/golden/reference_c2_timing.json).
+
+Every timed solve must converge to rtol with the expected iteration count (a solve
+that stops early would otherwise inflate the throughput).  --gpus N without a
+torchrun environment re-launches itself under torch.distributed.run (N replicas).
+The line also carries the BASELINE config-4 sweep (DG-VMS TET 32^3: 100 SpMV + 100 PC
+applies, c4_sweep; --no-c4 skips it).
 """
 
 from __future__ import annotations
@@ -141,8 +150,15 @@ def gpu_arm(args, rank, world):
         N.call("dpp_pc_destroy", pch)
         N.call("dpp_system_destroy", sysh)
 
+    def check(st):
+        # a solve that stopped early (max_iter / stagnation) must not count as throughput
+        if not st.converged or not st.relative_residual <= config.rtol:
+            raise RuntimeError(f"bench solve did not converge: its={st.iterations} "
+                               f"relres={st.relative_residual:.3e} reason={st.reason}")
+
     for _ in range(args.warmup):
         s, pc, st = device_step()
+        check(st)
         release(s, pc)
     dist_barrier(world)
     clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
@@ -154,6 +170,7 @@ def gpu_arm(args, rank, world):
         s, pc, st = device_step()
         ms = C.c_double()
         N.call("dpp_timer_stop", ctx, C.byref(ms))
+        check(st)
         times.append(ms.value)
         its.append(st.iterations)
         if _ < args.steps - 1:
@@ -177,8 +194,11 @@ def gpu_arm(args, rank, world):
         rep = dpp.solve(bs, config)
         x = rep.solution_vector()
         dt = time.perf_counter() - t0
+        if not rep.converged or not rep.stats.relative_residual <= config.rtol:
+            raise RuntimeError(f"e2e solve did not converge: {rep.stats}")
         if k >= args.warmup:
             e2e_times.append(dt)
+        print(f"[bench] e2e step {k}: {1e3 * dt:.1f} ms", file=sys.stderr, flush=True)
         del bs, rep
     # bytes actually copied each e2e step, as counted by the library: the parts of the mesh's
     # pinned device-layout image the formulation needs plus the boundary data (pressure facet
@@ -188,8 +208,37 @@ def gpu_arm(args, rank, world):
     h2d = mb.value
     d2h = x.nbytes
     e2e_s = dist_max(float(np.mean(e2e_times)), world)
+    if len(set(its)) != 1:
+        raise RuntimeError(f"iteration count changed between identical solves: {its}")
     return dict(dof=dof, ms_step=t_max, its=its, launches=launches, clocks=clk, prof=prof,
                 e2e_s=e2e_s, h2d=h2d, d2h=d2h)
+
+
+def c4_sweep():
+    """BASELINE config 4: DG-VMS TET 32^3 (6.3 M DoF), paper_3d_parameters, scale split; 100 SpMV
+    and 100 PC applies on the assembled system after one warm-up, CUDA events,
+    L2 flushed between applications."""
+    import ctypes as C
+
+    import paper_1808_08328_b200 as dpp
+    from paper_1808_08328_b200 import _native as N
+    p = dpp.paper_3d_parameters()
+    m = dpp.generate_unit_mesh(3, "tet", 32)
+    bs = dpp.assemble(m, "dgvms", p, dpp.boundary_data(dpp.mms_3d(p), m))
+    pc = dpp.build_preconditioner(bs, dpp.method_config("scale", rtol=1e-8))
+    prof = N.StepProfile()
+    N.call("dpp_profile_step", N.ctx(), bs.device().h, pc.handle(), 100, 1, C.byref(prof))
+    peak, _ = measured_peak()
+    gbs = (prof.spmv_bytes + prof.pc_bytes) / ((prof.spmv_ms + prof.pc_ms) * 1e-3) / 1e9
+    out = {"workload": "C4: DG-VMS TET 32^3 P1 disc., paper-3d parameters, scale split; 100 x (SpMV(K) + PC apply)",
+           "dof": int(sum(bs.device().sizes)), "spmv_ms": prof.spmv_ms, "pc_ms": prof.pc_ms,
+           "spmv_gbs": prof.spmv_bytes / (prof.spmv_ms * 1e-3) / 1e9,
+           "pc_gbs": prof.pc_bytes / (prof.pc_ms * 1e-3) / 1e9,
+           "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                        "bytes_per_step": prof.spmv_bytes + prof.pc_bytes},
+           "pc_kernels_per_apply": int(prof.pc_launches)}
+    del pc, bs
+    return out
 
 
 def _sizes(sysh):
@@ -203,7 +252,16 @@ def _sizes(sysh):
 
 # --------------------------------------------------------------------------- CPU arm (oracle)
 
-CPU_SAMPLE_N = 16    # bounded sample of the same workload (CG-VMS TET n^3, k2=0.01, scale)
+CPU_SAMPLE_N = int(os.environ.get("BENCH_CPU_N", "40"))   # the workload itself (C2: n = 40), ~15 s per solve
+
+
+def reference_timing():
+    """The unmodified reference's own C2 time (run_case(repeats=3) in the build container)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "reference_c2_timing.json")) as fh:
+            return json.load(fh)
+    except Exception:
+        return None
 
 
 def cpu_solve(n):
@@ -219,12 +277,21 @@ def cpu_solve(n):
     return bs.size, dt, rep.stats.iterations
 
 
+def _ref_note():
+    r = reference_timing()
+    if not r:
+        return ""
+    return (f"; the unmodified reference at C2 (run_case repeats=3, build container {r['cpu_count']} threads): "
+            f"{r['total_s']:.1f} s = {r['dof_per_s']:.0f} DoF/s, {r['ksp']} its")
+
+
 def cpu_baseline(n=CPU_SAMPLE_N):
     dof, dt, its = cpu_solve(n)
     return {"value": dof / dt, "unit": "DoF/s", "cores": 1, "kind": "port",
-            "sample": f"oracle (numpy/scipy + C port of reference dppflow) CG-VMS TET n={n} "
-                      f"({dof} DoF, {its} its, {dt:.2f} s): assemble + PC setup + GMRES to 1e-8, "
-                      f"scipy sparse kernels are single-threaded"}
+            "same_config": n == CONFIG["n"],
+            "sample": f"oracle (numpy/scipy + C port of reference dppflow, bit-identical to it at C2) CG-VMS TET "
+                      f"n={n} ({dof} DoF, {its} its, {dt:.2f} s): assemble + PC setup + GMRES to 1e-8, "
+                      f"scipy sparse kernels are single-threaded" + _ref_note()}
 
 
 # --------------------------------------------------------------------------- distributed plumbing
@@ -263,7 +330,17 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true", help="skip the config-4 SpMV / PC-apply sweep")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # N replicas, one process per GPU: re-launch under torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     rank, world = dist_init()
     metric = "DoFs solved/sec to rtol 1e-8"
     if args.impl == "reference":
@@ -271,7 +348,7 @@ def main():
             return
         threads = os.cpu_count()
         for _ in range(args.warmup):
-            cpu_solve(8)
+            cpu_solve(8)   # warm-up: imports, the oracle's C helper, allocator
         vals, its = [], []
         for _ in range(args.steps):
             dof, dt, it = cpu_solve(CPU_SAMPLE_N)
@@ -282,11 +359,13 @@ def main():
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * dof / v, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (structured mesh + MMS)",
-                "config": {"workload": CONFIG["workload"] + f" [CPU sample n={CPU_SAMPLE_N}]",
+                "config": {"workload": CONFIG["workload"] + ("" if CPU_SAMPLE_N == CONFIG["n"] else f" [CPU sample n={CPU_SAMPLE_N}]"),
                            "dof": dof, "ksp": its[-1]},
                 "cpu_baseline": {"value": v, "unit": "DoF/s", "kind": "port", "cores": 1,
-                                 "sample": f"oracle port, CG-VMS TET n={CPU_SAMPLE_N} ({dof} DoF) per step; "
-                                           f"host has {threads} threads, scipy sparse is single-threaded"},
+                                 "same_config": CPU_SAMPLE_N == CONFIG["n"],
+                                 "sample": f"oracle port (bit-identical to the reference at C2), CG-VMS TET n={CPU_SAMPLE_N} "
+                                           f"({dof} DoF) per step; host has {threads} threads, scipy sparse is "
+                                           f"single-threaded" + _ref_note()},
                 "e2e": {"value": v, "unit": "DoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -321,6 +400,8 @@ def main():
         "e2e": {"value": world * r["dof"] / r["e2e_s"], "unit": "DoF/s",
                 "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},
     }
+    if not args.no_c4 and world == 1:
+        line["c4_sweep"] = c4_sweep()
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line))

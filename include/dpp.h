@@ -127,6 +127,25 @@ int dpp_facet_points(dpp_ctx *ctx, dpp_mesh *m, int degree, int64_t nf, const in
 /* bc may be NULL (bcs=None).  The mesh is uploaded on first use. */
 int dpp_assemble(dpp_ctx *ctx, dpp_mesh *m, int formulation, const dpp_params *p,
                  const dpp_bc *bc, dpp_system **out);
+/* ---- discrete fields (assembly.py:591-644, spectrum.py:149-176) ----------
+ * field 0..3 = u1, p1, u2, p2 of a formulation; coeffs = that field's segment of the
+ * solution vector (ncoef checked).  ref_points: (nq, dim) reference coordinates, nq <= 128. */
+/* values on every cell, (C, nq) for pressures, (C, nq, dim) for velocities
+ * (DiscreteField.evaluate_all: nodal P1/Q1 sums, Piola map of the RT basis for H(div)) */
+int dpp_field_evaluate(dpp_ctx *ctx, dpp_mesh *m, int formulation, int field, const double *coeffs_host,
+                       int64_t ncoef, int nq, const double *ref_points_host, double *out_host);
+/* physical points origin + J x_q of every cell, (C, nq, dim) (spectrum.py:159-161) */
+int dpp_cell_points(dpp_ctx *ctx, dpp_mesh *m, int nq, const double *ref_points_host, double *X_host);
+/* sqrt(sum_c sum_q w_q |u_h - u|^2 det_c) (spectrum.l2_error).  The exact field is either
+ * exact_values_host (C, nq[, dim]) evaluated by the caller at dpp_cell_points, or, with
+ * exact_kind != 0, the package manufactured solution evaluated on the device:
+ * 1 / 2 = 2-D / 3-D pressure (exact_coef as dpp_bc.p0_coef), 3 / 4 = 2-D / 3-D velocity
+ * -k [X S, X cos(pi y) + c e^{e y}, X cos(pi z) + c e^{e z}] with exact_coef = {k, c, e}. */
+int dpp_field_l2_error(dpp_ctx *ctx, dpp_mesh *m, int formulation, int field, const double *coeffs_host,
+                       int64_t ncoef, int nq, const double *ref_points_host, const double *weights_host,
+                       int exact_kind, const double exact_coef[3], const double *exact_values_host,
+                       double *l2);
+
 /* a system from existing blocks (BlockSystem(...) constructed by the user):
  * blocks are copied; NULL block = empty matrix of the implied shape */
 int dpp_system_from_blocks(dpp_ctx *ctx, const dpp_csr *const blocks[10],
@@ -184,6 +203,11 @@ typedef struct {
 } dpp_split_node;
 int dpp_pc_create(dpp_ctx *ctx, dpp_system *s, const dpp_split_node *nodes, int n_nodes,
                   dpp_randn_fn randn, void *user, dpp_pc **out);
+/* build_preconditioner(bs, config, monolithic=K) (blocksolve.py:288-294): the split tree's
+ * blocks are extracted from the caller's K (n x n, n = the system's total size) by the
+ * system's field index sets instead of from the system's own blocks */
+int dpp_pc_create_explicit(dpp_ctx *ctx, dpp_system *s, const dpp_csr *K, const dpp_split_node *nodes,
+                           int n_nodes, dpp_randn_fn randn, void *user, dpp_pc **out);
 int dpp_pc_apply(dpp_pc *pc, const double *r_host, double *z_host);
 int dpp_pc_describe(const dpp_pc *pc, char *buf, int cap);
 int dpp_pc_setup_ms(const dpp_pc *pc, double *ms);

@@ -9,7 +9,7 @@ entry points raise DeviceUnavailable.
 """
 
 from ._native import DeviceUnavailable, ZeroPivotError
-from .assembly import BlockSystem, assemble, monolithic_view, solution_fields
+from .assembly import BlockSystem, DiscreteField, assemble, monolithic_view, solution_fields
 from .blocksolve import (
     FIELD_SPLIT_OPTIONS,
     SCALE_SPLIT_OPTIONS,
@@ -23,7 +23,7 @@ from .blocksolve import (
     parse_options,
     solve,
 )
-from .elements import ElementFamily, Formulation, dof_count, quadrature_rule
+from .elements import ElementFamily, Formulation, dof_count, eval_basis, quadrature_rule
 from .linalg import (
     KrylovStats,
     amg_setup,
@@ -49,6 +49,23 @@ from .problem import (
     mms_3d,
     paper_2d_parameters,
     paper_3d_parameters,
+)
+from .spectrum import (
+    CSV_COLUMNS,
+    EfficiencySeries,
+    SpectrumRecord,
+    StaticScalingError,
+    convergence_slope,
+    doa,
+    doe,
+    dos,
+    field_errors,
+    l2_error,
+    parallel_efficiency,
+    read_csv,
+    run_case,
+    static_scaling_run,
+    write_csv,
 )
 
 __version__ = "0.1.0"

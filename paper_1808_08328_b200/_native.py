@@ -85,6 +85,9 @@ SIGNATURES = {
     "dpp_facet_rule_size": [I32, I32, I32, C.POINTER(I32)],
     "dpp_facet_points": [P, P, I32, I64, P, P, P],
     "dpp_assemble": [P, P, I32, C.POINTER(Params), C.POINTER(Bc), PP],
+    "dpp_field_evaluate": [P, P, I32, I32, P, I64, I32, P, P],
+    "dpp_cell_points": [P, P, I32, P, P],
+    "dpp_field_l2_error": [P, P, I32, I32, P, I64, I32, P, P, I32, P, P, C.POINTER(D)],
     "dpp_system_eliminate": [P, I32, I64, P, P],
     "dpp_mesh_upload_bytes": [P, C.POINTER(I64)],
     "dpp_system_from_blocks": [P, C.POINTER(P), C.POINTER(P), C.POINTER(I64), PP],
@@ -106,6 +109,7 @@ SIGNATURES = {
     "dpp_amg_vcycle": [P, P, P],
     "dpp_amg_destroy": [P],
     "dpp_pc_create": [P, P, C.POINTER(SplitNode), I32, RANDN_FN, P, PP],
+    "dpp_pc_create_explicit": [P, P, P, C.POINTER(SplitNode), I32, RANDN_FN, P, PP],
     "dpp_pc_apply": [P, P, P],
     "dpp_pc_describe": [P, C.c_char_p, I32],
     "dpp_pc_setup_ms": [P, C.POINTER(D)],

@@ -118,6 +118,13 @@ class BlockSystem:
         return dev
 
 
+def export_matrix_market(block_system: BlockSystem, path) -> None:
+    """Monolithic K in MatrixMarket coordinate format (reference assembly.py:111-116)."""
+    from .linalg import write_matrix_market
+    K, _ = monolithic_view(block_system)
+    write_matrix_market(path, K)
+
+
 def monolithic_view(block_system: BlockSystem):
     """(K, f) in the (u1, p1, u2, p2) ordering (reference assembly.py:102-108).
 
@@ -255,6 +262,22 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
     return bs
 
 
+def assemble_hdiv(mesh: Mesh, params: DppParameters, bcs: BoundarySpec | None, workers: int = 1) -> BlockSystem:
+    """Facet-flux velocities, cellwise-constant pressures (reference assembly.py:233)."""
+    return assemble(mesh, Formulation.HDIV, params, bcs, workers=workers)
+
+
+def assemble_cgvms(mesh: Mesh, params: DppParameters, bcs: BoundarySpec | None, workers: int = 1,
+                   pressure_dirichlet: str = "weak") -> BlockSystem:
+    """Continuous equal-order VMS (reference assembly.py:360)."""
+    return assemble(mesh, Formulation.CG_VMS, params, bcs, workers=workers, pressure_dirichlet=pressure_dirichlet)
+
+
+def assemble_dgvms(mesh: Mesh, params: DppParameters, bcs: BoundarySpec | None, workers: int = 1) -> BlockSystem:
+    """Discontinuous VMS with interior-facet couplings (reference assembly.py:449)."""
+    return assemble(mesh, Formulation.DG_VMS, params, bcs, workers=workers)
+
+
 class _DeviceNnz(dict):
     """nnz per block, read from the device lazily (AssemblyStats.nnz)."""
 
@@ -292,5 +315,48 @@ class _DeviceNnz(dict):
         return super().__len__()
 
 
+# ----------------------------------------------------------------------------- fields
+
+@dataclass
+class DiscreteField:
+    """One solution field with per-cell evaluation (reference assembly.py:591-638).
+
+    evaluate_all runs on the device (csrc/fields.cu): nodal P1/Q1 sums for pressures and
+    CG/DG velocities, the contravariant Piola map of the RT facet-flux basis for H(div)
+    velocities; (C, nq) for pressures, (C, nq, dim) for velocities.
+    """
+
+    mesh: Mesh
+    formulation: Formulation
+    name: str   # u1 | p1 | u2 | p2
+    coeffs: np.ndarray
+
+    @property
+    def is_velocity(self) -> bool:
+        return self.name.startswith("u")
+
+    @property
+    def field_index(self) -> int:
+        return FIELDS.index(self.name)
+
+    def evaluate_all(self, ref_points) -> np.ndarray:
+        mesh = self.mesh
+        pts = N.f64(np.atleast_2d(np.asarray(ref_points, dtype=float)))
+        if pts.shape[1] != mesh.dim:
+            raise ValueError("reference points do not match the mesh dimension")
+        coef = N.f64(np.asarray(self.coeffs, dtype=float).ravel())
+        nc = mesh.dim if self.is_velocity else 1
+        out = np.empty((mesh.n_cells, len(pts), nc))
+        N.call("dpp_field_evaluate", N.ctx(), mesh._h, N.FORMS[Formulation(self.formulation).value],
+               self.field_index, N.ptr(coef), len(coef), len(pts), N.ptr(pts), N.ptr(out))
+        return out if self.is_velocity else out[..., 0]
+
+    def evaluate(self, cell: int, ref_points) -> np.ndarray:
+        return self.evaluate_all(ref_points)[cell]
+
+
 def solution_fields(block_system: BlockSystem, x: np.ndarray) -> dict:
-    return block_system.split_solution(x)
+    """{name: DiscreteField} (reference assembly.py:641-644)."""
+    parts = block_system.split_solution(x)
+    return {name: DiscreteField(block_system.mesh, block_system.formulation, name, parts[name])
+            for name in FIELDS}

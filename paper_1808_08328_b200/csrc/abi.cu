@@ -354,6 +354,10 @@ int dpp_pc_create(dpp_ctx *ctx, dpp_system *s, const dpp_split_node *nodes, int 
                   dpp_randn_fn randn, void *user, dpp_pc **out) {
     return guard([&] { *out = pc_create(&ctx->c, s, nodes, n_nodes, randn, user); });
 }
+int dpp_pc_create_explicit(dpp_ctx *ctx, dpp_system *s, const dpp_csr *K, const dpp_split_node *nodes,
+                           int n_nodes, dpp_randn_fn randn, void *user, dpp_pc **out) {
+    return guard([&] { *out = pc_create(&ctx->c, s, nodes, n_nodes, randn, user, &K->m); });
+}
 int dpp_pc_apply(dpp_pc *pc, const double *r, double *z) {
     return guard([&] {
         const int n = pc_size(pc);

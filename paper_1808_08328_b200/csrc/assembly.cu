@@ -21,6 +21,7 @@
 #include <cstring>
 
 #include "abi_guard.cuh"
+#include "devmesh.cuh"
 #include "mesh.h"
 #include "system.cuh"
 
@@ -187,18 +188,7 @@ static Elem make_elem(int kind) {
     return e;
 }
 
-// ------------------------------------------------------------------ device mesh
-struct DevMesh {
-    Ctx *c = nullptr;
-    int dim = 0, kind = 0, nn = 0, nf = 0, nvf = 0;
-    int64_t V = 0, C = 0, F = 0;
-    DBuf<double> verts, det, Jinv;
-    DBuf<int> cells, cf, fv, fplus, fminus;
-    DBuf<signed char> cs;
-    DBuf<double> fn, fm;
-    bool facets = false;   // facet arrays uploaded (H(div), DG-VMS, facet queries); CG-VMS needs none
-    size_t foff[7] = {0}, fbytes[7] = {0};   // facet parts in the pinned image
-};
+// ------------------------------------------------------------------ device mesh (devmesh.cuh)
 
 // J (mesh.py:175-183) and J^-1 by LU with partial pivoting (numpy.linalg.inv)
 __global__ void k_geom(int64_t C, int dim, int kind, int nn, const double *V, const int *cells,
@@ -247,7 +237,7 @@ __global__ void k_geom(int64_t C, int dim, int kind, int nn, const double *V, co
     }
 }
 
-static DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
+DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
     if (m.dev && m.dev->c == c) return *m.dev;
     auto d = std::make_shared<DevMesh>();
     d->c = c;
@@ -315,7 +305,7 @@ static DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
     return *d;
 }
 
-static void ensure_facets(Ctx *c, HostMesh &hm, DevMesh &d) {
+void ensure_facets(Ctx *c, HostMesh &hm, DevMesh &d) {
     if (d.facets) return;
     const unsigned char *B = static_cast<const unsigned char *>(hm.pinned.get());
     auto up = [&](auto &buf, int q, size_t count) {
@@ -1362,6 +1352,8 @@ static const int BLK_RC[10][2] = {{0, 0}, {0, 1}, {1, 0}, {1, 1}, {2, 2}, {2, 3}
 void eliminate(Ctx *c, dpp_system &S, int field, int64_t n, const int64_t *idx_h, const double *vals_h) {
     if (n <= 0) return;
     const int64_t nf = S.sizes[field];
+    for (int64_t i = 0; i < n; ++i)   // out-of-range ids would scatter out of bounds on the device
+        if (idx_h[i] < 0 || idx_h[i] >= nf) DPP_FAIL(DPP_ERR_VALUE, "eliminated dof out of range");
     DBuf<int64_t> idx(n, c->s);
     DBuf<double> vals(n, c->s), lift(nf, c->s);
     DBuf<unsigned char> pin(nf, c->s);
@@ -1439,6 +1431,9 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
                 hm.bc_pinned = std::shared_ptr<void>(h, [](void *q) { cudaFreeHost(q); });
                 hm.bc_pinned_bytes = 2 * tot + 64;
             }
+            // the staging may still feed a copy of an earlier assembly (one that failed before its
+            // final synchronisation, or another context's): wait for its last recorded copies
+            if (hm.bc_done) CK(cudaEventSynchronize(static_cast<cudaEvent_t>(hm.bc_done.get())));
             unsigned char *B = static_cast<unsigned char *>(hm.bc_pinned.get()) + (net ? hm.bc_pinned_bytes / 2 : 0);
             int *hv = reinterpret_cast<int *>(B + o_v), *hp = reinterpret_cast<int *>(B + o_p);
             double *hn = reinterpret_cast<double *>(B + o_n), *hmz = reinterpret_cast<double *>(B + o_m);
@@ -1450,8 +1445,7 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
                 for (int k = 0; k < m.dim; ++k) hn[(size_t)i * m.dim + k] = hm.facet_normals[(size_t)g * m.dim + k];
                 hmz[i] = hm.facet_measures[g];
             }
-            // asynchronous copies: the staging is reused only by the next assembly, which
-            // starts after this one's final stream synchronisation
+            // asynchronous copies; the next fill of the staging waits on bc_done
             cfv.alloc((size_t)nfp * m.nvf, c->s);
             cfp.alloc(nfp, c->s);
             cfn.alloc((size_t)nfp * m.dim, c->s);
@@ -1460,6 +1454,12 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
             CK(cudaMemcpyAsync(cfp.p, hp, bp, cudaMemcpyHostToDevice, c->s));
             CK(cudaMemcpyAsync(cfn.p, hn, bn, cudaMemcpyHostToDevice, c->s));
             CK(cudaMemcpyAsync(cfm.p, hmz, bm, cudaMemcpyHostToDevice, c->s));
+            if (!hm.bc_done) {
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                hm.bc_done = std::shared_ptr<void>(ev, [](void *q) { cudaEventDestroy(static_cast<cudaEvent_t>(q)); });
+            }
+            CK(cudaEventRecord(static_cast<cudaEvent_t>(hm.bc_done.get()), c->s));
             hm.bc_bytes += bv + bp + bn + bm;
             iota.alloc(nfp, c->s);
             k_iota64<<<grid_for(nfp, 256, c->sms), 256, 0, c->s>>>(nfp, iota.p);
@@ -1501,7 +1501,6 @@ static void boundary_rhs(Ctx *c, HostMesh &hm, DevMesh &m, int formulation, cons
 // ------------------------------------------------------------------ C ABI
 using namespace dpp;
 
-struct dpp_mesh { HostMesh m; };
 
 
 extern "C" {
@@ -1599,6 +1598,8 @@ int dpp_facet_points(dpp_ctx *ctx, dpp_mesh *mm, int degree, int64_t nf, const i
                      double *X, double *W) {
     return guard([&] {
         Ctx *c = &ctx->c;
+        for (int64_t i = 0; i < nf; ++i)
+            if (facets[i] < 0 || facets[i] >= mm->m.n_facets) DPP_FAIL(DPP_ERR_VALUE, "facet id out of range");
         DevMesh &m = dev_mesh(c, mm->m);
         ensure_facets(c, mm->m, m);
         FRule R = frule(m.kind, degree);
@@ -1631,6 +1632,18 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
         Ctx *c = &ctx->c;
         HostMesh &hm = mm->m;
         if (p->mu <= 0 || p->k1 <= 0 || p->k2 <= 0) DPP_FAIL(DPP_ERR_VALUE, "mu, k1, k2 must be positive");
+        if (bc)   // every boundary facet id is checked on the host before anything reaches the device
+            for (int n = 0; n < 2; ++n) {
+                if (bc->n_pfacets[n] < 0 || bc->n_vfacets[n] < 0) DPP_FAIL(DPP_ERR_VALUE, "negative facet count");
+                if (bc->n_pfacets[n] && !bc->pfacets[n]) DPP_FAIL(DPP_ERR_VALUE, "pressure facets missing");
+                if (bc->n_vfacets[n] && (!bc->vfacets[n] || !bc->vdata[n])) DPP_FAIL(DPP_ERR_VALUE, "velocity facets missing");
+                for (int64_t i = 0; i < bc->n_pfacets[n]; ++i)
+                    if (bc->pfacets[n][i] < 0 || bc->pfacets[n][i] >= hm.n_facets)
+                        DPP_FAIL(DPP_ERR_VALUE, "pressure facet id out of range");
+                for (int64_t i = 0; i < bc->n_vfacets[n]; ++i)
+                    if (bc->vfacets[n][i] < 0 || bc->vfacets[n][i] >= hm.n_facets)
+                        DPP_FAIL(DPP_ERR_VALUE, "velocity facet id out of range");
+            }
         DPP_TRACE_SCOPE(c, "assemble.total");
         DevMesh *mp;
         {

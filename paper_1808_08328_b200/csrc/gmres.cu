@@ -265,7 +265,10 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
             // end the cycle (estimate far above the target, not the last column), so the
             // speculative work is always the next iteration's (a breakdown leaves it unused)
             static const bool spec_on = [] { const char *e = std::getenv("DPP_GMRES_AHEAD"); return !(e && *e == '0'); }();
-            if (spec_on && j + 1 < m && total + 1 < max_iter && std::fabs(gg[j]) > 1e3 * rtol * norm_mb) {
+            // (device operators only: a host callback would be called on a column that may be
+            // thrown away, and its synchronous round trip gains no overlap)
+            if (spec_on && A.A && M.pc && j + 1 < m && total + 1 < max_iter &&
+                std::fabs(gg[j]) > 1e3 * rtol * norm_mb) {
                 double *Vn = V.p + (size_t)(j + 1) * n;
                 scale_by_dev(c, n, w.p, hcol + j + 1, Vn);
                 g.matvec(Vn, tmp.p);
@@ -294,7 +297,14 @@ void gmres_dev(Ctx *c, int64_t n, const Operator &A, const PcOp &M, const double
             ++total;
             k_used = j + 1;
             if (history) history->push_back(std::fabs(gg[j + 1]) / norm_mb);
-            if (happy || std::fabs(gg[j + 1]) <= rtol * norm_mb) break;
+            if (happy || std::fabs(gg[j + 1]) <= rtol * norm_mb) {
+                if (ahead) {   // the speculative column is discarded: it is not counted
+                    --g.mv;
+                    --g.pcs;
+                    ahead = false;
+                }
+                break;
+            }
         }
         // y = R^-1 g by column-oriented back substitution (LAPACK getrs on triu(R))
         std::vector<double> y(gg.begin(), gg.begin() + k_used);

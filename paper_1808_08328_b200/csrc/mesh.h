@@ -25,8 +25,9 @@ struct HostMesh {
     size_t pinned_bytes = 0;
     size_t dev_bytes = 0;                     // host->device bytes of the current device image
     size_t bc_bytes = 0;                      //   + the last assembly's compact boundary-facet data
-    std::shared_ptr<void> bc_pinned;          // pinned staging of that data (reused; assembly syncs at its end)
+    std::shared_ptr<void> bc_pinned;          // pinned staging of that data (reused)
     size_t bc_pinned_bytes = 0;
+    std::shared_ptr<void> bc_done;            // event (cudaEvent_t) after the staging's last copies
     void build();
 };
 

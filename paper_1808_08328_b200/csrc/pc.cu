@@ -297,8 +297,11 @@ struct dpp_pc {
 namespace dpp {
 
 dpp_pc *pc_create(Ctx *c, dpp_system *s, const dpp_split_node *nodes, int n_nodes,
-                  dpp_randn_fn randn, void *user) {
+                  dpp_randn_fn randn, void *user, const Csr *K) {
     if (n_nodes < 1) DPP_FAIL(DPP_ERR_VALUE, "empty split tree");
+    const int64_t ntot = s->sizes[0] + s->sizes[1] + s->sizes[2] + s->sizes[3];
+    if (K && (K->rows != ntot || K->cols != ntot))
+        DPP_FAIL(DPP_ERR_VALUE, "monolithic matrix does not match the system's field sizes");
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -307,7 +310,9 @@ dpp_pc *pc_create(Ctx *c, dpp_system *s, const dpp_split_node *nodes, int n_node
     pc->ctx = c;
     DPP_TRACE_SCOPE(c, "pc.total");
     Builder b{c, nodes, n_nodes, s, randn, user};
-    pc->root = b.node(0, {0, 1, 2, 3});
+    // K given: the tree's blocks are extracted from it by field index sets, as the reference
+    // does with the matrix its caller passes (blocksolve.py:288-294); else from the system's blocks
+    pc->root = b.node(0, {0, 1, 2, 3}, K);
     pc->n = (int)(s->sizes[0] + s->sizes[1] + s->sizes[2] + s->sizes[3]);
     pc->r.alloc(pc->n, c->s);
     pc->z.alloc(pc->n, c->s);

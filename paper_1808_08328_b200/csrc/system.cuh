@@ -27,7 +27,7 @@ const Csr &system_Kc(Ctx *c, dpp_system *s);
 const double *system_f(Ctx *c, dpp_system *s);
 
 dpp_pc *pc_create(Ctx *c, dpp_system *s, const dpp_split_node *nodes, int n_nodes,
-                  dpp_randn_fn randn, void *user);
+                  dpp_randn_fn randn, void *user, const Csr *K = nullptr);
 void pc_apply_dev(dpp_pc *pc, const double *r_dev, double *z_dev);
 std::string pc_desc(const dpp_pc *pc);
 double pc_setup_ms(const dpp_pc *pc);

@@ -36,6 +36,81 @@ SCALAR_FAMILY = {CellKind.TRI: ElementFamily.P1, CellKind.QUAD: ElementFamily.Q1
                  CellKind.TET: ElementFamily.P1, CellKind.HEX: ElementFamily.Q1}
 HDIV_FAMILY = {CellKind.TRI: ElementFamily.RT_TRI, CellKind.QUAD: ElementFamily.RT_QUAD,
                CellKind.TET: ElementFamily.RT_TET, CellKind.HEX: ElementFamily.RT_HEX}
+_VECTOR_DIM = {ElementFamily.RT_TRI: 2, ElementFamily.RT_QUAD: 2, ElementFamily.RT_TET: 3,
+               ElementFamily.RT_HEX: 3}
+# vertex opposite each local facet (LOCAL_FACETS order) of the simplex flux bases
+_TRI_OPPOSITE = ((0.0, 1.0), (1.0, 0.0), (0.0, 0.0))
+_TET_OPPOSITE = ((0.0, 0.0, 1.0), (0.0, 1.0, 0.0), (1.0, 0.0, 0.0), (0.0, 0.0, 0.0))
+
+
+def family_dim(family):
+    """Vector dimension of an H(div) family, None for scalar families."""
+    return _VECTOR_DIM.get(ElementFamily(family))
+
+
+def is_vector_family(family) -> bool:
+    return ElementFamily(family) in _VECTOR_DIM
+
+
+def piola_map(geometry, reference_vector_values: np.ndarray) -> np.ndarray:
+    """Contravariant Piola transform (J v_ref) / det J (reference elements.py:141-149)."""
+    if geometry.det <= 0:
+        raise ValueError("singular or inverted cell geometry")
+    return np.einsum("ij,...j->...i", geometry.jacobian, reference_vector_values) / geometry.det
+
+
+def piola_divergence(geometry, reference_divergences: np.ndarray) -> np.ndarray:
+    if geometry.det <= 0:
+        raise ValueError("singular or inverted cell geometry")
+    return np.asarray(reference_divergences) / geometry.det
+
+
+def eval_basis(family, points):
+    """Reference basis at reference points (reference elements.py:79-138): scalar families ->
+    (values (n, nd), gradients (n, nd, dim)); RT families -> (values (n, nd, dim), divergences
+    (nd,)).  A host-side table utility; the device kernels (csrc/fields.cu, assembly.cu) carry
+    the same formulas."""
+    fam = ElementFamily(family)
+    pts = np.atleast_2d(np.asarray(points, dtype=float))
+    n, dim = pts.shape
+    tol = 1e-12
+    simplex = fam in (ElementFamily.P1, ElementFamily.RT_TRI, ElementFamily.RT_TET)
+    inside = (np.all(pts >= -tol) and np.all(pts.sum(axis=-1) <= 1 + tol)) if simplex else \
+        (np.all(pts >= -tol) and np.all(pts <= 1 + tol))
+    if not inside:
+        raise ValueError("reference point outside reference cell")
+    if fam is ElementFamily.P1:
+        vals = np.empty((n, dim + 1))
+        vals[:, 0] = 1.0 - pts.sum(axis=1)
+        vals[:, 1:] = pts
+        grads = np.empty((n, dim + 1, dim))
+        grads[:, 0, :] = -1.0
+        grads[:, 1:, :] = np.eye(dim)
+        return vals, grads
+    if fam is ElementFamily.Q1:
+        nd = 2 ** dim
+        vals, grads = np.ones((n, nd)), np.ones((n, nd, dim))
+        for a in range(nd):
+            for axis in range(dim):
+                s = (a >> axis) & 1
+                f = pts[:, axis] if s else 1.0 - pts[:, axis]
+                vals[:, a] *= f
+                for other in range(dim):
+                    grads[:, a, other] *= (1.0 if s else -1.0) if other == axis else f
+        return vals, grads
+    if fam is ElementFamily.DP0_DQ0:
+        return np.ones((n, 1)), np.zeros((n, 1, dim))
+    if dim != _VECTOR_DIM[fam]:
+        raise ValueError("point dimension does not match element family")
+    if fam is ElementFamily.RT_TRI:
+        return pts[:, None, :] - np.array(_TRI_OPPOSITE)[None], np.full(3, 2.0)
+    if fam is ElementFamily.RT_TET:
+        return 2.0 * (pts[:, None, :] - np.array(_TET_OPPOSITE)[None]), np.full(4, 6.0)
+    vals = np.zeros((n, 2 * dim, dim))
+    for axis in range(dim):
+        vals[:, 2 * axis, axis] = pts[:, axis] - 1.0
+        vals[:, 2 * axis + 1, axis] = pts[:, axis]
+    return vals, np.ones(2 * dim)
 
 
 @dataclass(frozen=True)

@@ -13,7 +13,7 @@ reference returns as scipy matrices are exported back to scipy.
 
 from __future__ import annotations
 
-import ctypes as C
+import ctypes as ct
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -80,7 +80,7 @@ def _host_cb(fn, n):
     def cb(inp, out, _u):
         x = np.ctypeslib.as_array(inp, shape=(n,)).copy()
         y = np.asarray(fn(x), dtype=np.float64)
-        C.memmove(out, y.ctypes.data, 8 * n)
+        ct.memmove(out, y.ctypes.data, 8 * n)
     return N.APPLY_FN(cb)
 
 
@@ -112,7 +112,7 @@ def gmres(operator, b: np.ndarray, *, preconditioner=None, rtol: float = 1e-7,
     null_cb = N.APPLY_FN()
     N.call("dpp_gmres", N.ctx(), None if A is None else A.h, Acb or null_cb, None, pc,
            pcb or null_cb, None, n, N.ptr(b), N.ptr(x0a), N.ptr(x), float(rtol), int(max_iter),
-           int(restart), C.byref(st), N.ptr(hist), len(hist))
+           int(restart), ct.byref(st), N.ptr(hist), len(hist))
     return x, _stats(st, hist[:st.iterations])
 
 
@@ -127,8 +127,8 @@ class Ilu0Factorization:
         self._L = self._U = None
 
     def _export(self):
-        lh, uh = C.c_void_p(), C.c_void_p()
-        N.call("dpp_ilu0_factors", self.h, C.byref(lh), C.byref(uh))
+        lh, uh = ct.c_void_p(), ct.c_void_p()
+        N.call("dpp_ilu0_factors", self.h, ct.byref(lh), ct.byref(uh))
         self._L, self._U = DeviceCsr(lh).to_scipy(), DeviceCsr(uh).to_scipy()
 
     @property
@@ -154,8 +154,8 @@ def ilu0(A) -> Ilu0Factorization:
     if A.shape[0] != A.shape[1]:
         raise ValueError("ilu0 requires a square matrix")
     d = as_device(A)
-    h = C.c_void_p()
-    N.call("dpp_ilu0_create", N.ctx(), d.h, C.byref(h))
+    h = ct.c_void_p()
+    N.call("dpp_ilu0_create", N.ctx(), d.h, ct.byref(h))
     return Ilu0Factorization(h, A.shape[0])
 
 
@@ -179,16 +179,16 @@ def diag_lump(A) -> np.ndarray:
     return d
 
 
-def schur_selfp(D, C_, diagA: np.ndarray, B) -> sp.csr_matrix:
+def schur_selfp(D, C, diagA: np.ndarray, B) -> sp.csr_matrix:
     """S = D - C diag(diagA)^-1 B with scipy's accumulation order (bitwise)."""
     diagA = N.f64(diagA)
     if np.any(diagA == 0.0):
         raise ZeroPivotError("zero entry in diagA")
-    if C_.shape[1] != len(diagA) or B.shape[0] != len(diagA) or D.shape != (C_.shape[0], B.shape[1]):
+    if C.shape[1] != len(diagA) or B.shape[0] != len(diagA) or D.shape != (C.shape[0], B.shape[1]):
         raise ValueError("schur_selfp: non-conforming block dimensions")
-    h = C.c_void_p()
-    dD, dC, dB = as_device(D), as_device(C_), as_device(B)
-    N.call("dpp_schur_selfp", N.ctx(), dD.h, dC.h, N.ptr(diagA), dB.h, C.byref(h))
+    h = ct.c_void_p()
+    dD, dC, dB = as_device(D), as_device(C), as_device(B)
+    N.call("dpp_schur_selfp", N.ctx(), dD.h, dC.h, N.ptr(diagA), dB.h, ct.byref(h))
     return DeviceCsr(h).to_scipy()
 
 
@@ -209,8 +209,8 @@ class AmgHierarchy:
 
     def __init__(self, handle):
         self.h = handle
-        n = C.c_int()
-        N.call("dpp_amg_levels", handle, C.byref(n))
+        n = ct.c_int()
+        N.call("dpp_amg_levels", handle, ct.byref(n))
         self._count = n.value
         self._levels = None
         self.coarse_lu = None   # the coarsest solve is a device dense inverse
@@ -224,10 +224,10 @@ class AmgHierarchy:
         if self._levels is None:
             out = []
             for l in range(self._count):
-                a, p = C.c_void_p(), C.c_void_p()
-                rho = C.c_double()
+                a, p = ct.c_void_p(), ct.c_void_p()
+                rho = ct.c_double()
                 coarse = l + 1 == self._count
-                N.call("dpp_amg_level", self.h, l, C.byref(a), C.byref(p), None, C.byref(rho))
+                N.call("dpp_amg_level", self.h, l, ct.byref(a), ct.byref(p), None, ct.byref(rho))
                 A0 = DeviceCsr(a, owner=self).to_scipy()
                 if not coarse:
                     agg = np.empty(A0.shape[0], dtype=np.int64)
@@ -252,10 +252,10 @@ def amg_setup(A, *, theta: float = 0.5, omega: float = 2.0 / 3.0, max_coarse: in
     """Smoothed-aggregation hierarchy on the device (reference linalg.py:341-380)."""
     if A.shape[0] != A.shape[1]:
         raise ValueError("amg_setup requires a square matrix")
-    h = C.c_void_p()
+    h = ct.c_void_p()
     dA = as_device(A)
     N.call("dpp_amg_create", N.ctx(), dA.h, float(theta), float(omega), int(max_coarse),
-           int(max_levels), N.RANDN, None, C.byref(h))
+           int(max_levels), N.RANDN, None, ct.byref(h))
     return AmgHierarchy(h)
 
 

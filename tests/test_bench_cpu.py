@@ -14,9 +14,10 @@ from tests.conftest import ROOT
 
 
 def test_reference_arm_json_contract():
+    # BENCH_CPU_N shrinks the oracle sample for this contract check (the arm times n = 40)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                           "--steps", "1", "--warmup", "1"], capture_output=True, text=True,
-                         timeout=600, cwd=ROOT)
+                         timeout=600, cwd=ROOT, env=dict(os.environ, BENCH_CPU_N="8"))
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
@@ -24,6 +25,12 @@ def test_reference_arm_json_contract():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    assert line["cpu_baseline"]["same_config"] is False   # n = 8 here; the default sample is C2 itself
+
+
+def test_bench_defaults_time_config2_on_cpu_arm():
+    import bench
+    assert bench.CPU_SAMPLE_N == bench.CONFIG["n"] == 40 or "BENCH_CPU_N" in os.environ
 
 
 def _free_port():
@@ -60,3 +67,19 @@ def test_replica_max_over_ranks_gloo_world2(tmp_path):
     res = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
     assert sorted(r["rank"] for r in res) == [0, 1]
     assert all(r["max"] == 20.0 for r in res)   # max over ranks, as bench.py reports
+
+
+@pytest.mark.timeout(600)
+def test_gpus_flag_spawns_replicas_without_torchrun():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with torch.distributed.run: two
+    ranks (gloo here), rank 0 prints the one JSON line (reference arm: rank 0 alone works)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["BENCH_CPU_N"] = "8"
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--impl", "reference",
+                          "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=540,
+                         cwd=ROOT, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2

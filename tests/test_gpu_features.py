@@ -146,3 +146,25 @@ def test_device_mms_traces_match_host(dim, kind, n, form):
     b = dpp.assemble(m, form, p, dpp.boundary_data(host, m))
     for name in ("f1_u", "f1_p", "f2_u", "f2_p"):
         assert rel_close(getattr(a, name), getattr(b, name), 1e-13), name
+
+
+@pytest.mark.gpu
+def test_build_preconditioner_honours_monolithic():
+    """build_preconditioner(bs, config, monolithic=K) builds the tree from the caller's matrix
+    (reference blocksolve.py:288-294): the system's own K gives the same operator bit for bit,
+    2K gives (up to rounding) half of it, a wrong shape is rejected."""
+    import scipy.sparse as sp
+    p = dpp.DppParameters(k2=0.01, gamma_b=(0.0, 0.0, 0.0))
+    m = dpp.generate_unit_mesh(3, "tet", 4)
+    bs = dpp.assemble(m, "cgvms", p, dpp.boundary_data(dpp.mms_3d(p), m))
+    K, _ = dpp.monolithic_view(bs)
+    r = np.random.default_rng(3).standard_normal(K.shape[0])
+    for meth in ("scale", "field"):
+        cfg = dpp.method_config(meth)
+        z0 = dpp.build_preconditioner(bs, cfg)(r)
+        z1 = dpp.build_preconditioner(bs, cfg, monolithic=K)(r)
+        assert np.array_equal(z0, z1)
+        z2 = dpp.build_preconditioner(bs, cfg, monolithic=(2.0 * K).tocsr())(r)
+        assert np.linalg.norm(z2 - 0.5 * z0) <= 1e-12 * np.linalg.norm(z0)
+    with pytest.raises(ValueError):
+        dpp.build_preconditioner(bs, dpp.method_config("scale"), monolithic=sp.identity(5, format="csr"))
