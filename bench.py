@@ -24,8 +24,9 @@ container (tests/golden/reference_c2_timing.json).
 Every timed solve must converge to rtol with the expected iteration count (a solve
 that stops early would otherwise inflate the throughput).  --gpus N without a
 torchrun environment re-launches itself under torch.distributed.run (N replicas).
-The line also carries the BASELINE config-4 sweep (DG-VMS TET 32^3: 100 SpMV + 100 PC
-applies, c4_sweep; --no-c4 skips it).
+The line also carries BASELINE config 3 as stated (c3_solve: per-cell permeability + no-flow
+walls, the extension; --no-c3 skips it) and the config-4 sweep (DG-VMS TET 32^3: 100 SpMV +
+100 PC applies, c4_sweep; --no-c4 skips it).
 """
 
 from __future__ import annotations
@@ -214,6 +215,34 @@ def gpu_arm(args, rank, world):
                 e2e_s=e2e_s, h2d=h2d, d2h=d2h)
 
 
+def c3_solve():
+    """BASELINE config 3 as stated (the per-cell-permeability / no-flow extension; parity
+    unpinned): HEX 64^3 CG-VMS, field split, rtol 1e-8; assemble + setup + GMRES, device-timed."""
+    import ctypes as C
+
+    import paper_1808_08328_b200 as dpp
+    from paper_1808_08328_b200 import _native as N
+    m = dpp.generate_unit_mesh(3, "hex", 64)
+    params, bcs, ck = dpp.problem.heterogeneous_channel(m)
+    cfg = dpp.method_config("field", rtol=1e-8)
+    out = None
+    for _ in range(2):   # warm-up + timed
+        N.call("dpp_timer_start", N.ctx())
+        bs = dpp.assemble(m, "cgvms", params, bcs, cell_permeability=ck, velocity_dirichlet="strong")
+        rep = dpp.solve(bs, cfg, want_solution=False)
+        ms = C.c_double()
+        N.call("dpp_timer_stop", N.ctx(), C.byref(ms))
+        if not rep.converged or not rep.stats.relative_residual <= cfg.rtol:
+            raise RuntimeError(f"config 3 solve did not converge: {rep.stats}")
+        dof = bs.size
+        out = {"workload": "C3: HEX 64^3 CG-VMS, log-normal k1 per cell (seed 20240817), k2 = 1e-2 k1, "
+                           "p = 1/0 on x = 0/1, no flow elsewhere, field split, rtol 1e-8 (extension, parity unpinned)",
+               "dof": dof, "ksp": rep.stats.iterations, "ms_per_step": ms.value,
+               "dof_per_s": dof / (ms.value * 1e-3)}
+        del bs, rep
+    return out
+
+
 def c4_sweep():
     """BASELINE config 4: DG-VMS TET 32^3 (6.3 M DoF), paper_3d_parameters, scale split; 100 SpMV
     and 100 PC applies on the assembled system after one warm-up, CUDA events,
@@ -331,6 +360,7 @@ def main():
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 SpMV / PC-apply sweep")
+    ap.add_argument("--no-c3", action="store_true", help="skip the config-3 solve")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # N replicas, one process per GPU: re-launch under torch.distributed.run
@@ -400,6 +430,8 @@ def main():
         "e2e": {"value": world * r["dof"] / r["e2e_s"], "unit": "DoF/s",
                 "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},
     }
+    if not args.no_c3 and world == 1:
+        line["c3_solve"] = c3_solve()
     if not args.no_c4 and world == 1:
         line["c4_sweep"] = c4_sweep()
     if not args.no_cpu_baseline and world == 1:

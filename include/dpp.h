@@ -127,6 +127,14 @@ int dpp_facet_points(dpp_ctx *ctx, dpp_mesh *m, int degree, int64_t nf, const in
 /* bc may be NULL (bcs=None).  The mesh is uploaded on first use. */
 int dpp_assemble(dpp_ctx *ctx, dpp_mesh *m, int formulation, const dpp_params *p,
                  const dpp_bc *bc, dpp_system **out);
+/* Config-3 extension (the reference has scalar k only, problem.py:26-45):
+ * per-cell permeabilities cell_k1 / cell_k2 (n_cells each, > 0; both or neither) replace
+ * params.k1 / k2 cell by cell in the H(div) and CG-VMS cell integrals (assembly.py:274-276,
+ * :338-342: mu/k in the velocity mass, k/mu in the pressure Laplacian and body force).
+ * NULL -> dpp_assemble.  Parity for heterogeneous k is "unpinned" (no reference answer); with
+ * every cell at params' k the system is bit-for-bit dpp_assemble's. */
+int dpp_assemble_ext(dpp_ctx *ctx, dpp_mesh *m, int formulation, const dpp_params *p,
+                     const double *cell_k1, const double *cell_k2, const dpp_bc *bc, dpp_system **out);
 /* ---- discrete fields (assembly.py:591-644, spectrum.py:149-176) ----------
  * field 0..3 = u1, p1, u2, p2 of a formulation; coeffs = that field's segment of the
  * solution vector (ncoef checked).  ref_points: (nq, dim) reference coordinates, nq <= 128. */

@@ -162,8 +162,12 @@ def _eliminate(table, rhs, sizes, field, idx, values):
     rhs[field][idx] = values
 
 
-def _vms_cells(mesh, p):
-    """Cell integrals of the stabilised forms (assembly.py:318-349)."""
+def _vms_cells(mesh, p, cell_k=None):
+    """Cell integrals of the stabilised forms (assembly.py:318-349).
+
+    cell_k = (k1_cells, k2_cells): the config-3 extension (per-cell permeability; the reference
+    has scalar k only) -- mu/k_c and k_c/mu per cell, in the scalar path's operation order, so
+    constant arrays reproduce the reference bit for bit."""
     dim = mesh.dim
     q, w = quadrature_rule(mesh.kind, 2)
     N, G = scalar_basis(mesh.kind, q)
@@ -177,10 +181,17 @@ def _vms_cells(mesh, p):
     C = len(det)
     out = {}
     for net, k in ((1, p.k1), (2, p.k2)):
-        uu = 0.5 * p.mu / k * np.einsum("cab,ij->caibj", mass, np.eye(dim))
+        if cell_k is None:
+            uu = 0.5 * p.mu / k * np.einsum("cab,ij->caibj", mass, np.eye(dim))
+        else:
+            kc = np.asarray(cell_k[net - 1], dtype=float)
+            uu = (0.5 * p.mu / kc)[:, None, None, None, None] * np.einsum("cab,ij->caibj", mass, np.eye(dim))
         up = -(gn + 0.5 * gn.transpose(0, 2, 1, 3)).transpose(0, 1, 3, 2)
         pu = gn.transpose(0, 2, 1, 3) + 0.5 * gn
-        pp = 0.5 * k / p.mu * gg + p.beta / p.mu * mass
+        if cell_k is None:
+            pp = 0.5 * k / p.mu * gg + p.beta / p.mu * mass
+        else:
+            pp = (0.5 * kc / p.mu)[:, None, None] * gg + p.beta / p.mu * mass
         out[net] = (uu.reshape(C, nn * dim, nn * dim), up.reshape(C, nn * dim, nn),
                     pu.reshape(C, nn, nn * dim), pp)
     return out, mass, N, Gp, w, det, Jinv
@@ -189,8 +200,31 @@ def _vms_cells(mesh, p):
 def _body_force(p, k, N, Gp, w, det, gb):
     iN = np.einsum("q,qa->a", w, N)
     fu = 0.5 * det[:, None, None] * iN[None, :, None] * gb[None, None, :]
-    fp = 0.5 * k / p.mu * det[:, None] * np.einsum("q,cqai,i->ca", w, Gp, gb)
+    kk = np.asarray(k, dtype=float)
+    fp = ((0.5 * kk / p.mu * det)[:, None] if kk.ndim else 0.5 * k / p.mu * det[:, None]) * \
+        np.einsum("q,cqai,i->ca", w, Gp, gb)
     return fu, fp
+
+
+def _normal_velocity_dofs(mesh, bcs, net):
+    """Config-3 extension (CG-VMS, velocity_dirichlet="strong"): component d = axis of the
+    normal of every velocity-facet vertex, value g n_d (u.n = g from un_data, 0 = no flow)."""
+    vel = np.array(sorted(bcs.velocity_facets[net - 1]), dtype=np.int64)
+    if not len(vel):
+        return np.empty(0, np.int64), np.empty(0)
+    out = {}
+    for f in vel:
+        nrm = mesh.facet_normals[f]
+        d = int(np.argmax(np.abs(nrm)))
+        if abs(abs(nrm[d]) - 1.0) > 1e-12:
+            raise ValueError("strong velocity conditions need axis-aligned boundary facets")
+        vs = mesh.facet_vertex_ids[f]
+        un = bcs.un_data[net - 1] if bcs.un_data is not None else None
+        g = np.zeros(len(vs)) if un is None else np.asarray(un(mesh.vertices[vs], nrm), dtype=float) * nrm[d]
+        for v, val in zip(vs, g):
+            out.setdefault(int(v) * mesh.dim + d, float(val))
+    idx = np.array(sorted(out), dtype=np.int64)
+    return idx, np.array([out[i] for i in idx])
 
 
 def _nodal_pressure_rhs(mesh, bcs, Jinv, origin, dm_u, rhs):
@@ -206,16 +240,20 @@ def _nodal_pressure_rhs(mesh, bcs, Jinv, origin, dm_u, rhs):
         np.add.at(rhs[f"u{net}"], dm_u[cells].ravel(), c.reshape(len(pf), -1).ravel())
 
 
-def assemble(mesh, formulation, p, bcs, pressure_dirichlet="weak"):
+def assemble(mesh, formulation, p, bcs, pressure_dirichlet="weak", cell_k=None, velocity_dirichlet="natural"):
     formulation = getattr(formulation, "value", formulation)
     t0 = time.perf_counter()
     gb = np.asarray(p.gamma_b, dtype=float)
     if gb.shape != (mesh.dim,):
         raise ValueError("gamma_b dimension does not match the mesh")
+    if cell_k is not None and formulation == "dgvms":
+        raise ValueError("per-cell permeability is implemented for H(div) and CG-VMS")
+    if velocity_dirichlet == "strong" and formulation != "cgvms":
+        raise ValueError("velocity_dirichlet='strong' is a CG-VMS option")
     if formulation == "hdiv":
-        table, rhs = _hdiv(mesh, p, bcs, gb)
+        table, rhs = _hdiv(mesh, p, bcs, gb, cell_k)
     elif formulation == "cgvms":
-        table, rhs = _cgvms(mesh, p, bcs, gb, pressure_dirichlet)
+        table, rhs = _cgvms(mesh, p, bcs, gb, pressure_dirichlet, cell_k, velocity_dirichlet)
     elif formulation == "dgvms":
         table, rhs = _dgvms(mesh, p, bcs, gb)
     else:
@@ -228,7 +266,7 @@ def assemble(mesh, formulation, p, bcs, pressure_dirichlet="weak"):
     return OBlockSystem(formulation, mesh, p, blocks, rhs, time.perf_counter() - t0)
 
 
-def _hdiv(mesh, p, bcs, gb):
+def _hdiv(mesh, p, bcs, gb, cell_k=None):
     dim, C = mesh.dim, mesh.n_cells
     J, det = mesh.J, mesh.det
     nu, npr = mesh.n_facets, C
@@ -245,7 +283,10 @@ def _hdiv(mesh, p, bcs, gb):
     vol = det * w.sum()
     ones = np.ones((C, 1, 1))
     for net, k in ((1, p.k1), (2, p.k2)):
-        acc[f"uu{net}"].add(p.mu / k * mass, dm_u, dm_u)
+        if cell_k is None:
+            acc[f"uu{net}"].add(p.mu / k * mass, dm_u, dm_u)
+        else:
+            acc[f"uu{net}"].add((p.mu / np.asarray(cell_k[net - 1], dtype=float))[:, None, None] * mass, dm_u, dm_u)
         acc[f"up{net}"].add(-sc[:, :, None], dm_u, dm_p)
         acc[f"pu{net}"].add(sc[:, None, :], dm_p, dm_u)
         acc[f"pp{net}"].add(p.beta / p.mu * vol[:, None, None] * ones, dm_p, dm_p)
@@ -273,7 +314,7 @@ def _hdiv(mesh, p, bcs, gb):
     return table, rhs
 
 
-def _cgvms(mesh, p, bcs, gb, pressure_dirichlet):
+def _cgvms(mesh, p, bcs, gb, pressure_dirichlet, cell_k=None, velocity_dirichlet="natural"):
     dim, C, V = mesh.dim, mesh.n_cells, mesh.n_vertices
     nu, npr = V * dim, V
     dm_p = mesh.cells
@@ -281,7 +322,7 @@ def _cgvms(mesh, p, bcs, gb, pressure_dirichlet):
     acc = _blocks(nu, npr)
     fu = {1: np.zeros(nu), 2: np.zeros(nu)}
     fp = {1: np.zeros(npr), 2: np.zeros(npr)}
-    nets, mass, N, Gp, w, det, Jinv = _vms_cells(mesh, p)
+    nets, mass, N, Gp, w, det, Jinv = _vms_cells(mesh, p, cell_k)
     for net, k in ((1, p.k1), (2, p.k2)):
         uu, up, pu, pp = nets[net]
         acc[f"uu{net}"].add(uu, dm_u, dm_u)
@@ -289,7 +330,7 @@ def _cgvms(mesh, p, bcs, gb, pressure_dirichlet):
         acc[f"pu{net}"].add(pu, dm_p, dm_u)
         acc[f"pp{net}"].add(pp, dm_p, dm_p)
         if np.any(gb):
-            a, b = _body_force(p, k, N, Gp, w, det, gb)
+            a, b = _body_force(p, k if cell_k is None else cell_k[net - 1], N, Gp, w, det, gb)
             np.add.at(fu[net], dm_u.ravel(), a.ravel())
             np.add.at(fp[net], dm_p.ravel(), b.ravel())
     cross = -p.beta / p.mu * mass
@@ -312,6 +353,13 @@ def _cgvms(mesh, p, bcs, gb, pressure_dirichlet):
                            bcs.p_data[net - 1](mesh.vertices[verts]))
         elif pressure_dirichlet != "weak":
             raise ValueError("pressure_dirichlet must be 'weak' or 'strong'")
+        if velocity_dirichlet == "strong":
+            sizes = {"u1": nu, "p1": npr, "u2": nu, "p2": npr}
+            for net in (1, 2):
+                idx, vals = _normal_velocity_dofs(mesh, bcs, net)
+                _eliminate(table, rhs, sizes, f"u{net}", idx, vals)
+        elif velocity_dirichlet != "natural":
+            raise ValueError("velocity_dirichlet must be 'natural' or 'strong'")
     return table, rhs
 
 

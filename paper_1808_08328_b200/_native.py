@@ -85,6 +85,7 @@ SIGNATURES = {
     "dpp_facet_rule_size": [I32, I32, I32, C.POINTER(I32)],
     "dpp_facet_points": [P, P, I32, I64, P, P, P],
     "dpp_assemble": [P, P, I32, C.POINTER(Params), C.POINTER(Bc), PP],
+    "dpp_assemble_ext": [P, P, I32, C.POINTER(Params), P, P, C.POINTER(Bc), PP],
     "dpp_field_evaluate": [P, P, I32, I32, P, I64, I32, P, P],
     "dpp_cell_points": [P, P, I32, P, P],
     "dpp_field_l2_error": [P, P, I32, I32, P, I64, I32, P, P, I32, P, P, C.POINTER(D)],

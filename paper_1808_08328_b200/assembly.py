@@ -206,10 +206,52 @@ def _pressure_dirichlet_vertices(mesh: Mesh, bcs: BoundarySpec, net: int) -> np.
     return np.unique(mesh.facet_vertex_ids[bf].ravel()).astype(np.int64)
 
 
+def _normal_velocity_dofs(mesh: Mesh, bcs: BoundarySpec, net: int):
+    """Config-3 extension: the nodal velocity components normal to the network's velocity
+    facets and their prescribed values (u.n = g, bcs.un_data; 0 = no flow).  The structured
+    unit meshes have axis-aligned boundary facets, so u.n = g pins component d of every facet
+    vertex to g n_d (n = +-e_d)."""
+    vel = np.array(sorted(bcs.velocity_facets[net - 1]), dtype=np.int64)
+    if not len(vel):
+        return np.empty(0, np.int64), np.empty(0)
+    nrm = mesh.facet_normals[vel]
+    axis = np.argmax(np.abs(nrm), axis=1)
+    nd = nrm[np.arange(len(vel)), axis]
+    if np.any(np.abs(np.abs(nd) - 1.0) > 1e-12):
+        raise ValueError("strong velocity conditions need axis-aligned boundary facets")
+    verts = mesh.facet_vertex_ids[vel]                     # (F, nvf)
+    dofs = verts * mesh.dim + axis[:, None]
+    un = bcs.un_data[net - 1] if bcs.un_data is not None else None
+    if un is None:
+        vals = np.zeros(verts.shape)
+    else:
+        vals = np.stack([np.asarray(un(mesh.vertices[verts[i]], nrm[i]), dtype=float) * nd[i]
+                         for i in range(len(vel))])
+    dofs, vals = dofs.ravel(), vals.ravel()
+    order = np.argsort(dofs, kind="stable")
+    dofs, vals = dofs[order], vals[order]
+    first = np.ones(len(dofs), bool)
+    first[1:] = dofs[1:] != dofs[:-1]
+    u_d, u_v = dofs[first], vals[first]
+    if np.any(np.abs(vals - np.repeat(u_v, np.diff(np.append(np.flatnonzero(first), len(dofs))))) > 1e-12):
+        raise ValueError("inconsistent normal velocity data at a shared vertex")
+    return u_d.astype(np.int64), u_v
+
+
 def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec | None,
-             workers: int = 1, pressure_dirichlet: str = "weak") -> BlockSystem:
+             workers: int = 1, pressure_dirichlet: str = "weak", *, cell_permeability=None,
+             velocity_dirichlet: str = "natural") -> BlockSystem:
     """Device assembly (reference assembly.py:564-566).  `workers` is accepted
-    for API compatibility; the device assembles all cells at once."""
+    for API compatibility; the device assembles all cells at once.
+
+    Beyond the reference (BASELINE config 3; parity unpinned):
+      cell_permeability=(k1_cells, k2_cells) -- per-cell permeabilities (H(div), CG-VMS)
+        replacing params.k1 / k2 cell by cell (mu/k_c and k_c/mu in the cell integrals);
+      velocity_dirichlet="strong" (CG-VMS) -- the velocity facets' normal velocity is imposed
+        strongly (u.n = bcs.un_data, 0 = no flow) by the reference's symmetric elimination
+        (assembly.py:200-226) of the normal components at those facets' vertices.  The
+        reference's CG-VMS only drops the pressure functional there ("natural", the default).
+    """
     t0 = time.perf_counter()
     form = Formulation(formulation)
     gb = np.asarray(params.gamma_b, dtype=float)
@@ -219,6 +261,18 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
         raise ValueError("pressure_dirichlet must be 'weak' or 'strong'")
     if pressure_dirichlet == "strong" and form != Formulation.CG_VMS:
         raise ValueError("pressure_dirichlet='strong' is a CG-VMS option (reference assemble_cgvms)")
+    if velocity_dirichlet not in ("natural", "strong"):
+        raise ValueError("velocity_dirichlet must be 'natural' or 'strong'")
+    if velocity_dirichlet == "strong" and form != Formulation.CG_VMS:
+        raise ValueError("velocity_dirichlet='strong' is a CG-VMS option (H(div) / DG-VMS impose the flux already)")
+    ck = None
+    if cell_permeability is not None:
+        k1c, k2c = (N.f64(np.asarray(a, dtype=float).ravel()) for a in cell_permeability)
+        if len(k1c) != mesh.n_cells or len(k2c) != mesh.n_cells:
+            raise ValueError("cell_permeability needs one k1 and one k2 per cell")
+        if not (np.all(k1c > 0) and np.all(k2c > 0)):
+            raise ValueError("cell permeabilities must be positive")
+        ck = (k1c, k2c)
     p = N.Params(params.mu, params.beta, params.k1, params.k2, params.eta_u, params.eta_p,
                  (C.c_double * 3)(*(list(gb) + [0.0] * (3 - len(gb)))))
     keep = []
@@ -247,7 +301,11 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
                 bc.vdata[net - 1] = un.ctypes.data
         bcp = C.byref(bc)
     h = C.c_void_p()
-    N.call("dpp_assemble", N.ctx(), mesh._h, N.FORMS[form.value], C.byref(p), bcp, C.byref(h))
+    if ck is None:
+        N.call("dpp_assemble", N.ctx(), mesh._h, N.FORMS[form.value], C.byref(p), bcp, C.byref(h))
+    else:
+        N.call("dpp_assemble_ext", N.ctx(), mesh._h, N.FORMS[form.value], C.byref(p), N.ptr(ck[0]),
+               N.ptr(ck[1]), bcp, C.byref(h))
     dev = DeviceSystem(h)
     if bcs is not None and pressure_dirichlet == "strong":
         # strong boundary pressure: eliminate p1 then p2 (reference assembly.py:410-415)
@@ -255,6 +313,12 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
             verts = _pressure_dirichlet_vertices(mesh, bcs, net)
             vals = N.f64(np.asarray(bcs.p_data[net - 1](mesh.vertices[verts]), dtype=float))
             N.call("dpp_system_eliminate", h, 1 if net == 1 else 3, len(verts), N.ptr(verts), N.ptr(vals))
+    if bcs is not None and velocity_dirichlet == "strong":
+        for net in (1, 2):   # u1 then u2, after the pressure data (as the strong pressure route)
+            dofs, vals = _normal_velocity_dofs(mesh, bcs, net)
+            if len(dofs):
+                dofs, vals = N.i64(dofs), N.f64(vals)
+                N.call("dpp_system_eliminate", h, 0 if net == 1 else 2, len(dofs), N.ptr(dofs), N.ptr(vals))
     bs = BlockSystem(formulation=form, mesh=mesh, params=params)
     object.__setattr__(bs, "_dev", dev)
     wall = time.perf_counter() - t0
@@ -262,15 +326,17 @@ def assemble(mesh: Mesh, formulation, params: DppParameters, bcs: BoundarySpec |
     return bs
 
 
-def assemble_hdiv(mesh: Mesh, params: DppParameters, bcs: BoundarySpec | None, workers: int = 1) -> BlockSystem:
+def assemble_hdiv(mesh: Mesh, params: DppParameters, bcs: BoundarySpec | None, workers: int = 1,
+                  **extension) -> BlockSystem:
     """Facet-flux velocities, cellwise-constant pressures (reference assembly.py:233)."""
-    return assemble(mesh, Formulation.HDIV, params, bcs, workers=workers)
+    return assemble(mesh, Formulation.HDIV, params, bcs, workers=workers, **extension)
 
 
 def assemble_cgvms(mesh: Mesh, params: DppParameters, bcs: BoundarySpec | None, workers: int = 1,
-                   pressure_dirichlet: str = "weak") -> BlockSystem:
+                   pressure_dirichlet: str = "weak", **extension) -> BlockSystem:
     """Continuous equal-order VMS (reference assembly.py:360)."""
-    return assemble(mesh, Formulation.CG_VMS, params, bcs, workers=workers, pressure_dirichlet=pressure_dirichlet)
+    return assemble(mesh, Formulation.CG_VMS, params, bcs, workers=workers, pressure_dirichlet=pressure_dirichlet,
+                    **extension)
 
 
 def assemble_dgvms(mesh: Mesh, params: DppParameters, bcs: BoundarySpec | None, workers: int = 1) -> BlockSystem:

@@ -499,6 +499,8 @@ struct VmsArgs {
     const int *pay;
     int64_t nnz;
     double s_uu[2], s_pp_gg[2], s_pp_m, s_cross;
+    const double *ck[2];         // per-cell k1 / k2 (config-3 extension) or null: s_uu, s_pp_gg per cell
+    double mu;
     double c_uu[2], c_pp[2];     // DG facet coefficients (before side signs)
     // DG facet tables
     const int *interior;
@@ -575,10 +577,13 @@ __global__ void __launch_bounds__(128) k_vms_values(VmsArgs A) {
                 for (int i = 0; i < dim; ++i) { gnab[i] *= det; gnba[i] *= det; }
                 #pragma unroll
                 for (int n = 0; n < 2; ++n) {
-                    const double v = A.s_uu[n] * mass;
+                    // per-cell k: (0.5 mu) / k_c and (0.5 k_c) / mu, the scalar path's operation order
+                    const double suu = A.ck[n] ? 0.5 * A.mu / A.ck[n][c] : A.s_uu[n];
+                    const double spp = A.ck[n] ? 0.5 * A.ck[n][c] / A.mu : A.s_pp_gg[n];
+                    const double v = suu * mass;
                     #pragma unroll
                     for (int i = 0; i < dim; ++i) uu[n][i][i] += v;
-                    pp[n] += A.s_pp_gg[n] * gg + A.s_pp_m * mass;
+                    pp[n] += spp * gg + A.s_pp_m * mass;
                 }
                 #pragma unroll
                 for (int i = 0; i < dim; ++i) {
@@ -757,6 +762,8 @@ struct HdivArgs {
     double w[8];
     double Vref[8][6][3];   // [q][f][j]
     double s_uu[2];
+    const double *ck[2];   // per-cell k1 / k2 or null: mu / k_c
+    double mu;
     const double *V, *det;
     const int *cells, *cf;
     const signed char *cs;
@@ -814,7 +821,7 @@ __global__ void k_hdiv_uu(HdivArgs A) {
             const int lf = (int)((p / A.nf) % A.nf), lg = (int)(p % A.nf);
             const double m = hdiv_mass(A, c, lf, lg);
             for (int n = 0; n < 2; ++n) {
-                const double v = __dmul_rn(A.s_uu[n], m);
+                const double v = __dmul_rn(A.ck[n] ? __ddiv_rn(A.mu, A.ck[n][c]) : A.s_uu[n], m);
                 acc[n] = first ? v : __dadd_rn(acc[n], v);
             }
             first = false;
@@ -949,8 +956,8 @@ static void add_at(Ctx *c, int64_t n, DBuf<int64_t> &dof, DBuf<double> &val, dou
 // ------------------------------------------------------------------ body force (gamma_b)
 // VMS (assembly.py:352-356): fu[c,a,i] = 0.5 det intN_a g_i ; fp[c,a] = 0.5 k/mu det sum_q w_q (Gp_qa . g)
 __global__ void k_body_vms(int64_t C, Elem E, const double *det, const double *Jinv, const int *cells, int dg,
-                           double g0, double g1, double g2, double kmu, int64_t *du, double *vu, int64_t *dp,
-                           double *vp) {
+                           double g0, double g1, double g2, double kmu, const double *ck, double mu, int64_t *du,
+                           double *vu, int64_t *dp, double *vp) {
     const int dim = E.dim, nn = E.nn;
     const double gb[3] = {g0, g1, g2};
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C; c += (int64_t)gridDim.x * blockDim.x) {
@@ -974,7 +981,7 @@ __global__ void k_body_vms(int64_t C, Elem E, const double *det, const double *J
                 s += E.w[q] * t;
             }
             dp[c * nn + a] = node;
-            vp[c * nn + a] = kmu * d * s;
+            vp[c * nn + a] = (ck ? 0.5 * ck[c] / mu : kmu) * d * s;
         }
     }
 }
@@ -1063,7 +1070,7 @@ __global__ void k_scatter_vals(int64_t n, const int64_t *idx, const double *v, d
 static void alloc_blk(Ctx *c, Csr &B, int rows, int cols, int64_t nnz) { B.alloc(rows, cols, nnz, c->s); }
 
 static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, bool dg,
-                         const dpp_bc *bc, dpp_system &S) {
+                         const dpp_bc *bc, dpp_system &S, const double *ck1 = nullptr, const double *ck2 = nullptr) {
     const Elem E = make_elem(m.kind);
     const int dim = m.dim, nn = m.nn;
     const int64_t C = m.C;
@@ -1172,6 +1179,9 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
     }
     A.s_pp_m = p.beta / p.mu;
     A.s_cross = -p.beta / p.mu;
+    A.mu = p.mu;
+    A.ck[0] = ck1;
+    A.ck[1] = ck2;
     A.interior = dinter.p;
     A.fW = fW.p;
     A.fNp = fNp.p;
@@ -1208,7 +1218,8 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
             DBuf<double> vu(nu_c, c->s), vp(np_c, c->s);
             k_body_vms<<<grid_for(C, 128, c->sms), 128, 0, c->s>>>(C, E, m.det.p, m.Jinv.p, m.cells.p, dg,
                                                                  p.gamma_b[0], p.gamma_b[1], p.gamma_b[2],
-                                                                 0.5 * ks[n] / p.mu, du.p, vu.p, dpi.p, vp.p);
+                                                                 0.5 * ks[n] / p.mu, n == 0 ? ck1 : ck2, p.mu,
+                                                                 du.p, vu.p, dpi.p, vp.p);
             launched(c);
             add_at(c, nu_c, du, vu, S.rhs[n == 0 ? 0 : 2].p);
             add_at(c, np_c, dpi, vp, S.rhs[n == 0 ? 1 : 3].p);
@@ -1233,7 +1244,8 @@ static void assemble_vms(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, 
     CK(cudaStreamSynchronize(c->s));
 }
 
-static void assemble_hdiv(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, dpp_system &S) {
+static void assemble_hdiv(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p, dpp_system &S,
+                          const double *ck1 = nullptr, const double *ck2 = nullptr) {
     const int dim = m.dim, nf = m.nf;
     const int64_t C = m.C, F = m.F;
     Rule r = cell_rule(m.kind, 2);
@@ -1264,6 +1276,9 @@ static void assemble_hdiv(Ctx *c, HostMesh &hm, DevMesh &m, const dpp_params &p,
     for (int q = 0; q < r.nq; ++q) ws += r.w[q];
     A.s_uu[0] = p.mu / p.k1;
     A.s_uu[1] = p.mu / p.k2;
+    A.ck[0] = ck1;
+    A.ck[1] = ck2;
+    A.mu = p.mu;
     A.V = m.verts.p;
     A.det = m.det.p;
     A.cells = m.cells.p;
@@ -1627,6 +1642,11 @@ int dpp_system_eliminate(dpp_system *s, int field, int64_t n, const int64_t *idx
 
 int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *p, const dpp_bc *bc,
                  dpp_system **out) {
+    return dpp_assemble_ext(ctx, mm, formulation, p, nullptr, nullptr, bc, out);
+}
+
+int dpp_assemble_ext(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *p, const double *cell_k1,
+                     const double *cell_k2, const dpp_bc *bc, dpp_system **out) {
     return guard([&] {
         const auto t0 = std::chrono::steady_clock::now();
         Ctx *c = &ctx->c;
@@ -1645,6 +1665,12 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
                         DPP_FAIL(DPP_ERR_VALUE, "velocity facet id out of range");
             }
         DPP_TRACE_SCOPE(c, "assemble.total");
+        if ((cell_k1 == nullptr) != (cell_k2 == nullptr)) DPP_FAIL(DPP_ERR_VALUE, "give both cell_k1 and cell_k2 or neither");
+        if (cell_k1 && formulation == DPP_DGVMS)
+            DPP_FAIL(DPP_ERR_VALUE, "per-cell permeability is implemented for H(div) and CG-VMS");
+        if (cell_k1)
+            for (int64_t i = 0; i < hm.n_cells; ++i)
+                if (!(cell_k1[i] > 0) || !(cell_k2[i] > 0)) DPP_FAIL(DPP_ERR_VALUE, "cell permeabilities must be positive");
         DevMesh *mp;
         {
             DPP_TRACE_SCOPE(c, "assemble.mesh_upload");
@@ -1674,8 +1700,16 @@ int dpp_assemble(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_params *
             ensure_facets(c, hm, m);
         {
             DPP_TRACE_SCOPE(c, "assemble.blocks");
-            if (formulation == DPP_HDIV) assemble_hdiv(c, hm, m, *p, *S);
-            else assemble_vms(c, hm, m, *p, formulation == DPP_DGVMS, bc, *S);
+            DBuf<double> ck1, ck2;   // per-cell permeabilities (config-3 extension)
+            if (cell_k1) {
+                ck1.alloc(hm.n_cells, c->s);
+                ck2.alloc(hm.n_cells, c->s);
+                ck1.upload(cell_k1, hm.n_cells);
+                ck2.upload(cell_k2, hm.n_cells);
+            }
+            if (formulation == DPP_HDIV) assemble_hdiv(c, hm, m, *p, *S, ck1.p, ck2.p);
+            else assemble_vms(c, hm, m, *p, formulation == DPP_DGVMS, bc, *S, ck1.p, ck2.p);
+            CK(cudaStreamSynchronize(c->s));
         }
         {
             DPP_TRACE_SCOPE(c, "assemble.rhs");

@@ -1,8 +1,10 @@
 """Full-size runs of BASELINE configs on the device (no oracle): assemble + solve, twice.
 
-  python tools/run_config.py C3 | C4 [n]
-C3 = parity-pinned variant (HEX 64^3 CG-VMS, homogeneous k1=1, k2=0.01, MMS BCs, field split);
-C4 = DG-VMS TET 32^3, paper_3d_parameters, scale split, plus the 100x SpMV / PC-apply sweep.
+  python tools/run_config.py C3 | C3h | C4 [n]
+C3  = config 3 as BASELINE.json states it (HEX 64^3 CG-VMS, per-cell log-normal k1, k2 = 1e-2 k1,
+      p = 1 / 0 on x = 0 / 1, no flow elsewhere; field split) -- the extension, parity unpinned;
+C3h = its parity-pinned variant (homogeneous k1=1, k2=0.01, MMS BCs, field split);
+C4  = DG-VMS TET 32^3, paper_3d_parameters, scale split, plus the 100x SpMV / PC-apply sweep.
 """
 import ctypes as C
 import os
@@ -14,7 +16,8 @@ import paper_1808_08328_b200 as dpp
 from paper_1808_08328_b200 import _native as N
 
 name = sys.argv[1]
-if name == "C3":
+ext = {}
+if name in ("C3", "C3h"):
     form, dim, kind, n, meth = "cgvms", 3, "hex", 64, "field"
     p = dpp.DppParameters(k2=0.01, gamma_b=(0.0, 0.0, 0.0))
 else:
@@ -25,10 +28,13 @@ if len(sys.argv) > 2:
 t0 = time.perf_counter()
 m = dpp.generate_unit_mesh(dim, kind, n)
 bcs = dpp.boundary_data(dpp.manufactured_solution(dim, p), m)
+if name == "C3":
+    p, bcs, ck = dpp.problem.heterogeneous_channel(m)
+    ext = dict(cell_permeability=ck, velocity_dirichlet="strong")
 print(f"{name} n={n}: mesh {time.perf_counter() - t0:.2f} s", flush=True)
 for rep in range(int(os.environ.get("REPS", "2"))):
     t0 = time.perf_counter()
-    bs = dpp.assemble(m, form, p, bcs)
+    bs = dpp.assemble(m, form, p, bcs, **ext)
     N.sync()
     t1 = time.perf_counter()
     r = dpp.solve(bs, dpp.method_config(meth, rtol=1e-8), want_solution=False)
