@@ -83,6 +83,15 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// Checked build (-DDPP_CHECKED, tools/checked_build.sh): device-side bounds / invariant checks in
+// the lock-free kernels (shared-memory slot ranges, push targets, ring offsets, dependency ids);
+// a violated check traps.  Stands in for compute-sanitizer, which is closed on the GPU pool.
+#ifdef DPP_CHECKED
+#define DPP_DCHECK(cond) do { if (!(cond)) __trap(); } while (0)
+#else
+#define DPP_DCHECK(cond) do { } while (0)
+#endif
+
 // record one kernel launch (checks launch errors outside graph capture)
 inline void launched(Ctx *c) {
     c->launches++;

@@ -389,8 +389,10 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
           if (dbg && lane == 0) t_land = gtimer();
           for (int t = a; t < e_run; ++t) {
             const unsigned char *blk = ring + (size_t)sl * stage + (boff_s[t] - boff_s[a]);
+            DPP_DCHECK(boff_s[t + 1] - boff_s[a] <= stage);   // the block lies inside its ring slot
             const int4 hd = *reinterpret_cast<const int4 *>(blk);
             const int nr = hd.x, ne = hd.y;
+            DPP_DCHECK(nr >= 0 && ne >= 0 && hd.w >= 0 && hd.w < L && pu_block_bytes(nr, ne, hd.z) <= boff_s[t + 1] - boff_s[t]);
             const int4 *rows = reinterpret_cast<const int4 *>(blk + 16);
             const double *dg = reinterpret_cast<const double *>(blk + 16 + 16LL * nr);
             const int *code = reinterpret_cast<const int *>(blk + pu_off_code(nr));
@@ -411,6 +413,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                 if (act) {
                     R = rows[q];
                     dq = dg[q];
+                    DPP_DCHECK((R.x & 0xffff) < mine && R.y >= 0 && R.y <= R.z && R.z <= ne);
                     bi = bsl[R.x & 0xffff];
                 }
                 int len = R.z - R.y;
@@ -429,6 +432,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                     for (int r = 0; r < RND; ++r) {
                         const int e = R.y + e0 + r * G + gl;
                         has[r] = act && e < R.z;
+                        DPP_DCHECK(!has[r] || (code[e] >= 0 && (code[e] < mine || (code[e] >= chunkp && code[e] < chunkp + hmax))));
                         xa[r] = has[r] ? xh_s + 8u * (unsigned)code[e] : 0u;
                         v[r] = has[r] ? val[e] : 0.0;
                     }
@@ -468,6 +472,7 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
                     const int p0 = R.w >> 4, pc = R.w & 15;
                     for (int u = gl; u < pc; u += G) {
                         const int pe = pl[p0 + u];
+                        DPP_DCHECK((int)((unsigned)pe >> 28) < C && (int)((unsigned)pe & 0x0fffffffu) < hmax);
                         st_remote(peer[(unsigned)pe >> 28] + 8u * ((unsigned)pe & 0x0fffffffu), xr);
                     }
                 }

@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256) k_levels(int n, int backward, const int *
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 pj[u] = backward ? re - 1 - (k0 + u) : rs + k0 + u;
+                DPP_DCHECK(u >= cnt || (backward ? idx[pj[u]] > row : idx[pj[u]] < row));   // a strict triangle
                 lj[u] = u < cnt ? ld_relaxed_i(level + idx[pj[u]]) : 0;
             }
 #pragma unroll
@@ -630,12 +631,14 @@ __global__ void __launch_bounds__(32 * ILU_WPB) k_ilu0(int n, const int *__restr
         for (int q = 0; q < len; ++q) {
             const int k = cols[q];
             if (k >= i) break;
+            DPP_DCHECK(k >= 0);
             const double a = v[q];
             if (a == 0.0) continue;   // l_ik = 0: no update, no dependency (exact)
             long long spins = 0;
             while (ld_acquire(done + k) == 0)
                 if (++spins > SPIN_LIMIT) __trap();
             const int dk = dpos[k];
+            DPP_DCHECK(dk >= ptr[k] && dk < ptr[k + 1] && idx[dk] == k);   // k's diagonal, k already factored
             const double piv = __ldcg(val + dk);
             if (piv == 0.0) {
                 if (lane == 0) atomicMin(err_row, k);

@@ -155,8 +155,9 @@ def test_rt0_reference_triangle_known_answer():
 
 
 def test_hdiv_tri256_bitwise_diag_and_schur():
-    # config 1 needs bitwise level-0 S_p
-    bs, obs = systems("hdiv", 2, "tri", 64)
+    # config 1 (H(div) TRI 256^2) needs bitwise level-0 S_p: its blocks and
+    # S_p at the config's own size, bit for bit
+    bs, obs = systems("hdiv", 2, "tri", 256)
     for b in BLOCKS:
         assert np.array_equal(getattr(bs, b).data, getattr(obs, b).data), b
     S = dpp.schur_selfp(bs.k1_pp, bs.k1_pu, dpp.diag_lump(bs.k1_uu), bs.k1_up)
