@@ -272,6 +272,7 @@ __device__ unsigned long long *g_flow_phase = nullptr;
 __device__ unsigned long long *g_flow_tl = nullptr;   // per (CTA, step): {level, min t late-wait done, max t arrive}
 __device__ int g_flow_smax = 0;
 __device__ int g_flow_nopush = 0;
+__device__ int g_flow_rot = 0;
 __device__ __forceinline__ long long clk() { long long t; asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)); return t; }
 #define PH_T(v) const long long v = clk()
 #define PH_ADD(i, d) ph[i] += (d)
@@ -524,17 +525,15 @@ __global__ void __launch_bounds__(PU_THREADS, 1)
 // Warps without rows in a step do nothing for it, so no warp spins on shared memory and the
 // critical path per level is one wake-up + one row (measured phase breakdown: DESIGN.md §5).
 constexpr int LV_THREADS = 512;
-// Warp layout: warp w sits on SM sub-partition w % 4.  Warp 0 is the TMA producer and has
-// sub-partition 0 to itself (warps 4, 8, .. idle): a producer sharing a sub-partition with a team
-// slowed that team's levels 3-5x (bulk-copy issue).  Team t (= level % LV_TEAMS) = warps w with
-// w % 4 == t + 1, so each team owns one sub-partition.
-constexpr int LV_TEAMS = 3;   // level teams of k_trsv_lvl (and the plan's column classes)
+// Warp layout: warp w sits on SM sub-partition w % 4 and belongs to level team w % LV_TEAMS, so
+// each team owns one sub-partition; there is no producer warp (the ring refills itself).
+constexpr int LV_TEAMS = 4;   // level teams of k_trsv_lvl (and the plan's column classes)
 constexpr int LV_NS_MAX = 16;  // ring slots (one block each)
 // shared memory: ring mbarriers [2][LV_NS_MAX] | level mbarriers [L] | x slice | halo |
 //                step offsets [smax+1] | step levels [smax] | peer addresses [32] | ring [ns][stage]
 __host__ __device__ inline size_t lv_fixed(int chunk, int L, int hmax, int smax) {
     return 16 * LV_NS_MAX + p16(8LL * L) + p16(8LL * chunk) + p16(8LL * hmax) + p16(8LL * (smax + 1)) +
-           p16(4LL * smax) + 128;
+           p16(4LL * smax) + 128 + 4 * LV_NS_MAX + 16;
 }
 __device__ __forceinline__ bool mtest(unsigned a, unsigned parity) {
     unsigned ok;
@@ -565,10 +564,11 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
     const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int base = k * chunk, mine = min(chunk, n - base);
     const int b0 = k * L;
-    if (threadIdx.x < ns) {   // slot s: full (TMA bytes), empty (every consumer warp passed its step)
+    if (threadIdx.x < ns) {   // slot s: full when the block's bytes landed
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mfull[threadIdx.x])) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(&mempty[threadIdx.x])), "r"(LV_TEAMS * (nw / 4)) : "memory");
+        reinterpret_cast<int *>(peer + 32)[threadIdx.x] = 0;   // release counter
     }
+    if (threadIdx.x == 0) reinterpret_cast<int *>(peer + 32)[LV_NS_MAX] = 0;   // completed-level prefix
 #ifdef DPP_FLOW_PHASES
     const bool nopush = g_flow_nopush;   // timing experiment only: no remote pushes (results invalid)
 #else
@@ -592,48 +592,65 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
     __syncthreads();
     // every CTA's level mbarriers are armed before the first push
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-    // ring of ns one-block slots in step order: step s lives in slot s % ns.  A slot is refilled
-    // once every consumer warp passed its step -- the owning team after solving the block, the
-    // other teams as soon as they walk past it -- so slots free in level order and the producer
-    // runs up to ns - LV_TEAMS blocks ahead of the teams
-    if (wid == 0) {
+    // Ring of ns one-block slots in step order (step s in slot s % ns) without a producer warp:
+    // every warp passes every step (the owning team after solving the block, the others as soon
+    // as the block landed) and the LAST warp to release a slot issues the bulk copy of step
+    // s + ns into it.  (A dedicated producer warp made the team sharing its SM sub-partition
+    // 3-5x slower per level; the copy issue itself costs nothing measurable,
+    // tools/micro/tma_interference.cu.)
+    int *rel = reinterpret_cast<int *>(peer + 32);   // ns release counters
+    auto issue = [&](int st) {
+        const int sl = st % ns;
+        const unsigned bytes = (unsigned)(boff_s[st + 1] - boff_s[st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mfull[sl])), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su32(ring + (size_t)sl * stage)), "l"(blocks + boff_s[st]), "r"(bytes), "r"(su32(&mfull[sl]))
+                     : "memory");
+        const int pf = st + l2pf;
+        if (l2pf && pf < S)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[pf]),
+                         "r"((unsigned)(boff_s[pf + 1] - boff_s[pf]))
+                         : "memory");
+    };
+    auto release = [&](int st) {
+        __syncwarp();
         if (lane == 0) {
-            int pa = 0;   // L2 prefetch cursor
-            const long long t0 = clock64();
-            for (int st = 0; st < S; ++st) {
-                const int sl = st % ns;
-                // poll with back-off: a producer spinning in try_wait steals issue slots from the
-                // team warps on its SM sub-partition (measured: that team's levels 3-5x slower)
-                if (st >= ns)
-                    while (!mtest(su32(&mempty[sl]), (unsigned)((st / ns - 1) & 1))) {
-                        __nanosleep(64);
-                        if (clock64() - t0 > (16ll << 30)) __trap();
-                    }
-                const unsigned bytes = (unsigned)(boff_s[st + 1] - boff_s[st]);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mfull[sl])), "r"(bytes)
-                             : "memory");
-                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                             ::"r"(su32(ring + (size_t)sl * stage)), "l"(blocks + boff_s[st]), "r"(bytes), "r"(su32(&mfull[sl]))
-                             : "memory");
-                for (; l2pf && pa < S && pa < st + ns + l2pf; ++pa)
-                    if (pa >= st + ns) {
-                        const unsigned pb = (unsigned)(boff_s[pa + 1] - boff_s[pa]);
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(blocks + boff_s[pa]), "r"(pb) : "memory");
-                    }
+            const int sl = st % ns;
+            if (atomicAdd(&rel[sl], 1) == nw - 1) {   // every warp passed step st
+                atomicExch(&rel[sl], 0);
+                if (st + ns < S) issue(st + ns);
             }
         }
-    } else if (wid % 4 != 0) {   // warps 4, 8, .. stay idle: sub-partition 0 is the producer's
-        // consumer warps in LV_TEAMS teams by level (team = wid % LV_TEAMS = level % LV_TEAMS).  A
-        // team's warps deal a block's 32-row chunks; for its level-l rows a warp sums the early
-        // columns (sources of levels <= l-LV_TEAMS-1, complete before its previous block ended)
-        // right away, the mid columns (levels l-LV_TEAMS .. l-2) once those are complete, and
-        // only the late columns (level l-1) after the last wait -- the other teams' rows run
-        // meanwhile, so a level's critical path is one wake-up plus the late columns.  Index /
-        // value loads of the first mid / late group are issued before the waits; partial sums
-        // regroup the row's dot product (exact-arithmetic equivalent).
-        const int team = wid % 4 - 1, wi = wid / 4;
-        const int nteam = nw / 4;
+    };
+    if (threadIdx.x == 0)
+        for (int st = 0; st < min(ns, S); ++st) issue(st);
+    {
+        // warps in LV_TEAMS teams by level (team = wid % LV_TEAMS = level % LV_TEAMS), one team
+        // per sub-partition.  A team's warps deal a block's 32-row chunks; for its level-l rows a
+        // warp sums the early columns (sources of levels <= l-LV_TEAMS-1, complete before its
+        // previous block ended) right away, the mid columns (levels l-LV_TEAMS .. l-2) once those
+        // are complete, and only the late columns (level l-1) after the last wait -- the other
+        // teams' rows run meanwhile, so a level's critical path is one wake-up plus the late
+        // columns.  Index / value loads of the first mid / late group are issued before the
+        // waits; partial sums regroup the row's dot product (exact-arithmetic equivalent).
+#ifdef DPP_FLOW_PHASES
+        const int team = (wid + g_flow_rot * k) % LV_TEAMS, wi = wid / LV_TEAMS;   // experiment: rotate by rank
+#else
+        const int team = wid % LV_TEAMS, wi = wid / LV_TEAMS;
+#endif
+        const int nteam = nw / LV_TEAMS;
         int waited = 0;   // levels [0, waited) known complete by this warp
+        // levels [0, *lvdone) are known complete CTA-wide (the largest prefix any warp waited
+        // through): a warp that skipped many levels starts its waits there instead of
+        // re-checking every completed barrier (~100 cycles each)
+        int *lvdone = rel + LV_NS_MAX;
+        auto wait_levels = [&](int upto) {   // all levels < upto complete
+            if (waited >= upto) return;
+            waited = max(waited, *reinterpret_cast<volatile int *>(lvdone));
+            if (waited >= upto) return;
+            for (; waited < upto; ++waited) mwait(su32(&mlev[waited]), 0);
+            if (lane == 0) atomicMax(lvdone, waited);
+        };
 #ifdef DPP_FLOW_PHASES
         long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         long long sink = 0;
@@ -641,12 +658,14 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
         for (int st = 0; st < S; ++st) {
             const int sl = st % ns;
             const int lvl = slev[st];
-            // every warp waits for the slot's fill before releasing it: an arrival may not count
-            // toward the slot's previous use
+            // every warp waits for the slot's fill before releasing it, so a release always
+            // counts toward the slot's current use
+            PH_T(cr0);
             mwait(su32(&mfull[sl]), (unsigned)((st / ns) & 1));
+            PH_T(cr1);
+            PH_ADD(0, cr1 - cr0);
             if (lvl % LV_TEAMS != team) {
-                __syncwarp();
-                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
+                release(st);
                 continue;
             }
             {
@@ -683,7 +702,7 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                         dq = dg[q];
                     }
                     PH_T(c0);
-                    for (; waited < lvl - LV_TEAMS; ++waited) mwait(su32(&mlev[waited]), 0);   // early levels
+                    wait_levels(lvl - LV_TEAMS);   // early levels
                     PH_T(c1);
                     PH_ADD(1, c1 - c0);
                     // early columns (a multiple of 4): two groups of 4 loads in flight, four partial sums
@@ -719,7 +738,7 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
 #endif
                     PH_T(c2);
                     PH_ADD(2, c2 - c1);
-                    for (; waited < lvl - 1; ++waited) mwait(su32(&mlev[waited]), 0);   // mid levels
+                    wait_levels(lvl - 1);   // mid levels
                     auto group4 = [&](const int *gc, const double *gv, double &t0, double &t1) {
                         double gx[4];
 #pragma unroll
@@ -744,10 +763,7 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                     }
                     PH_T(c3);
                     PH_ADD(3, c3 - c2);
-                    if (waited < lvl) {   // level l-1
-                        mwait(su32(&mlev[lvl - 1]), 0);
-                        waited = lvl;
-                    }
+                    wait_levels(lvl);   // level l-1
                     PH_T(c4);
                     PH_ADD(5, c4 - c3);
 #ifdef DPP_FLOW_PHASES
@@ -795,7 +811,6 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                                  "r"(done)
                                  : "memory");
                 PH_T(c7);
-                PH_ADD(0, c7 - c6);
 #ifdef DPP_FLOW_PHASES
                 if (lane == 0 && g_flow_tl) {
                     unsigned long long *o = g_flow_tl + ((size_t)blockIdx.x * g_flow_smax + st) * 4;
@@ -808,8 +823,7 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                 }
             }
         release:
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&mempty[sl])) : "memory");
+            release(st);
         }
 #ifdef DPP_FLOW_PHASES
         if (lane == 0 && g_flow_phase)
@@ -1417,8 +1431,8 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
             DPP_FAIL(DPP_ERR_RUNTIME, "level-mbarrier sweep: plan does not fit");
         // LV_TEAMS level teams, each wide enough for the widest block (in 32-row chunks) in one round
         static const int pt_env = [] { const char *e = std::getenv("DPP_LVL_PER_TEAM"); return e ? std::atoi(e) : 0; }();
-        const int per_team = pt_env ? pt_env : std::max(1, std::min(P.widest, LV_THREADS / 128));
-        cfg.blockDim = dim3(128 * per_team, 1, 1);   // per_team warps on each sub-partition
+        const int per_team = pt_env ? pt_env : std::max(1, std::min(P.widest, LV_THREADS / (32 * LV_TEAMS)));
+        cfg.blockDim = dim3(32 * LV_TEAMS * per_team, 1, 1);   // per_team warps on each sub-partition
         cfg.dynamicSmemBytes = lfixed + (size_t)P.nst * P.stage;
         const int *lr = P.lrows.p, *txp = P.tx.p, *ss = P.sstart.p;
         const int nn = T.n / T.ncomp;
@@ -1443,6 +1457,8 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
             CK(cudaMemcpyToSymbol(g_flow_smax, &sm_, sizeof(int)));
             const int np_env = std::getenv("DPP_LVL_NOPUSH") ? 1 : 0;
             CK(cudaMemcpyToSymbol(g_flow_nopush, &np_env, sizeof(int)));
+            const int rot_env = std::getenv("DPP_LVL_ROT") ? std::atoi(std::getenv("DPP_LVL_ROT")) : 0;
+            CK(cudaMemcpyToSymbol(g_flow_rot, &rot_env, sizeof(int)));
             cudaEventCreate(&pe0); cudaEventCreate(&pe1);
             cudaEventRecord(pe0, st);
         }
