@@ -640,6 +640,7 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
 #endif
         const int nteam = nw / LV_TEAMS;
         int waited = 0;   // levels [0, waited) known complete by this warp
+        int part_of_lvl = 0;
         // levels [0, *lvdone) are known complete CTA-wide (the largest prefix any warp waited
         // through): a warp that skipped many levels starts its waits there instead of
         // re-checking every completed barrier (~100 cycles each)
@@ -658,6 +659,8 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
         for (int st = 0; st < S; ++st) {
             const int sl = st % ns;
             const int lvl = slev[st];
+            // the parts of a level (consecutive steps) are dealt to the team's warps in turn
+            const int pidx = (st > 0 && slev[st - 1] == lvl) ? ++part_of_lvl : (part_of_lvl = 0);
             // every warp waits for the slot's fill before releasing it, so a release always
             // counts toward the slot's current use
             PH_T(cr0);
@@ -672,16 +675,17 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                 const unsigned char *blk = ring + (size_t)sl * stage;
                 const int4 hd = *reinterpret_cast<const int4 *>(blk);
                 const int nr = hd.x, nch = hd.y;
-                if (wi >= nch) goto release;
+                const int ci0 = ((wi - pidx) % nteam + nteam) % nteam;   // chunks ci = ci0 (mod nteam)
+                if (ci0 >= nch) goto release;
                 {
                 const int4 *chs = reinterpret_cast<const int4 *>(blk + 16);
                 const int2 *rw = reinterpret_cast<const int2 *>(blk + lv_off_rw(nch));
                 const double *dg = reinterpret_cast<const double *>(blk + lv_off_dq(nch, nr));
                 const unsigned short *code = reinterpret_cast<const unsigned short *>(blk + lv_off_code(nch, nr));
-                int ne = 0;   // the last chunk's end
+                int ne = 0;   // the last chunk's end (its width: the block's remaining rows)
                 {
                     const int4 lc = chs[nch - 1];
-                    ne = lc.x + 32 * (lc.y + lc.z + lc.w);
+                    ne = lc.x + (nr - 32 * (nch - 1)) * (lc.y + lc.z + lc.w);
                 }
                 const double *val = reinterpret_cast<const double *>(blk + lv_off_val(nch, nr, ne));
                 const int *pl = reinterpret_cast<const int *>(val + ne);
@@ -690,7 +694,7 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                 long long c_late = 1ll << 62;
                 const long long c_first = clk();
 #endif
-                for (int ci = wi; ci < nch; ci += nteam) {
+                for (int ci = ci0; ci < nch; ci += nteam) {
                     const int q = 32 * ci + lane;
                     const bool act = q < nr;
                     done += min(32, nr - 32 * ci);
@@ -707,13 +711,15 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                     PH_ADD(1, c1 - c0);
                     // early columns (a multiple of 4): two groups of 4 loads in flight, four partial sums
                     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                    int e = ch.x + lane;
+                    // a chunk's columns are w = its rows (<= 32) entries apart
+                    const int w = min(32, nr - 32 * ci);
+                    int e = ch.x + (act ? lane : 0);
 #pragma unroll 2
-                    for (int k = 0; k < ch.y; k += 4, e += 128) {
+                    for (int k = 0; k < ch.y; k += 4, e += 4 * w) {
                         int cd[4];
                         double v[4], xv[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) { cd[u] = code[e + 32 * u]; v[u] = val[e + 32 * u]; }
+                        for (int u = 0; u < 4; ++u) { cd[u] = code[e + w * u]; v[u] = val[e + w * u]; }
 #pragma unroll
                         for (int u = 0; u < 4; ++u) xv[u] = xh[cd[u]];
                         s0 = fma(v[0], xv[0], s0); s1 = fma(v[1], xv[1], s1);
@@ -721,15 +727,15 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                     }
                     // mid / late columns (multiples of 4): the first group's indices and values are
                     // fetched before the waits, only the x gathers follow them
-                    const int em = e, el = e + 32 * ch.z;
+                    const int em = e, el = e + w * ch.z;
                     int mc[4], lc[4];
                     double mv[4], lv[4];
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        mc[u] = ch.z ? code[em + 32 * u] : 0;
-                        mv[u] = ch.z ? val[em + 32 * u] : 0.0;
-                        lc[u] = ch.w ? code[el + 32 * u] : 0;
-                        lv[u] = ch.w ? val[el + 32 * u] : 0.0;
+                        mc[u] = ch.z ? code[em + w * u] : 0;
+                        mv[u] = ch.z ? val[em + w * u] : 0.0;
+                        lc[u] = ch.w ? code[el + w * u] : 0;
+                        lv[u] = ch.w ? val[el + w * u] : 0.0;
                     }
                     const double bq = act ? xh[R.x] : 0.0;
                     double sum = (s0 + s1) + (s2 + s3);
@@ -751,7 +757,7 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
                             int gc[4];
                             double gv[4];
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) { gc[u] = code[e0 + 32 * (k + u)]; gv[u] = val[e0 + 32 * (k + u)]; }
+                            for (int u = 0; u < 4; ++u) { gc[u] = code[e0 + w * (k + u)]; gv[u] = val[e0 + w * (k + u)]; }
                             group4(gc, gv, t0, t1);
                         }
                     };
@@ -1008,7 +1014,7 @@ __global__ void k_lv_headers(int np_, const int *pstart, const int *pch, const i
         const int nr = pstart[i + 1] - pstart[i], g0 = pch[i], nch = pch[i + 1] - g0;
         const int4 lc = ctab[pch[i + 1] - 1];
         const int ncol = lc.y + lc.z + lc.w;
-        const int ne = lc.x + 32 * ncol;
+        const int ne = lc.x + (nr - 32 * (nch - 1)) * ncol;
         int *h = reinterpret_cast<int *>(B);
         h[0] = nr;
         h[1] = nch;
@@ -1018,12 +1024,7 @@ __global__ void k_lv_headers(int np_, const int *pstart, const int *pch, const i
         for (int c = 0; c < nch; ++c) chs[c] = ctab[g0 + c];
         unsigned short *code = reinterpret_cast<unsigned short *>(B + lv_off_code(nch, nr));
         double *vv = reinterpret_cast<double *>(B + lv_off_val(nch, nr, ne));
-        const int used = nr - 32 * (nch - 1);
-        for (int k = 0; k < ncol; ++k)
-            for (int l = used; l < 32; ++l) {
-                code[lc.x + 32 * k + l] = zero_code;
-                vv[lc.x + 32 * k + l] = 0.0;
-            }
+        (void)code; (void)vv; (void)zero_code;   // chunks are exactly as wide as their rows: no padding lanes
     }
 }
 __global__ void k_lv_fill(int n, int chunk, int chunkp, int zero_code, int np_, const int *pstart, const int *pch,
@@ -1040,8 +1041,8 @@ __global__ void k_lv_fill(int n, int chunk, int chunkp, int zero_code, int np_, 
         const int part = lo, q0 = pstart[part], nr = pstart[part + 1] - q0, i = q - q0;
         const int g0 = pch[part], nch = pch[part + 1] - g0;
         const int4 lc = ctab[pch[part + 1] - 1];
-        const int ne = lc.x + 32 * (lc.y + lc.z + lc.w);
-        const int gc = g0 + i / 32, lane = i % 32;
+        const int ne = lc.x + (nr - 32 * (nch - 1)) * (lc.y + lc.z + lc.w);
+        const int gc = g0 + i / 32, lane = i % 32, wch = min(32, nr - 32 * (i / 32));
         unsigned char *B = blocks + boff[part];
         int2 *rw = reinterpret_cast<int2 *>(B + lv_off_rw(nch));
         double *dq = reinterpret_cast<double *>(B + lv_off_dq(nch, nr));
@@ -1060,13 +1061,13 @@ __global__ void k_lv_fill(int n, int chunk, int chunkp, int zero_code, int np_, 
         for (int p = ptr[r]; p < ptr[r + 1]; ++p) {
             const int j = idx[p];
             const int cl = lv_class(lev[j], lr);
-            const int e = ch.x + 32 * (c0[cl] + kk[cl]++) + lane;
+            const int e = ch.x + wch * (c0[cl] + kk[cl]++) + lane;
             code[e] = pu_code(j, owner, chunk, chunkp, h, hs, he);
             vv[e] = val[p];
         }
         for (int cl = 0; cl < 3; ++cl)
             for (; kk[cl] < nc[cl]; ++kk[cl]) {
-                const int e = ch.x + 32 * (c0[cl] + kk[cl]) + lane;
+                const int e = ch.x + wch * (c0[cl] + kk[cl]) + lane;
                 code[e] = zero_code;
                 vv[e] = 0.0;
             }
@@ -1210,7 +1211,9 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
         if (fixed + 2 * 16384 >= PU_SMEM_LIMIT) return false;
         long long cap = (long long)(PU_SMEM_LIMIT - fixed) / 3;
         if (cap < 16384) cap = (long long)(PU_SMEM_LIMIT - fixed) / 2;
-        if (fmt == 1) cap = (long long)(PU_SMEM_LIMIT - fixed) / (LV_TEAMS + 2);   // >= 6 one-block ring slots
+        // >= LV_TEAMS + 2 one-block ring slots (12 smaller slots measured slower: 2.69 vs 1.78 ms per
+        // C2 PC apply); a level bigger than a slot becomes several parts, dealt to the team's warps
+        if (fmt == 1) cap = (long long)(PU_SMEM_LIMIT - fixed) / (LV_TEAMS + 2);
         cap &= ~127LL;
         pstart.clear(); plev.clear(); pboff.assign(1, 0);
         pch.assign(1, 0); ctab.clear();
@@ -1235,7 +1238,10 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
                                 nx[u] = fresh ? want : std::max(cur[u], want);
                             }
                             const long long nch2 = nch + (fresh ? 1 : 0);
-                            const long long ne2 = ne + 32LL * ((nx[0] + nx[1] + nx[2]) - (fresh ? 0 : cur[0] + cur[1] + cur[2]));
+                            // a chunk occupies (its rows) x (its padded columns) entries
+                            const long long ne2 = fresh ? ne + (nx[0] + nx[1] + nx[2])
+                                                        : ne - (long long)inc * (cur[0] + cur[1] + cur[2]) +
+                                                              (long long)(inc + 1) * (nx[0] + nx[1] + nx[2]);
                             const long long np2 = np + (hp[q + 1] - hp[q]);
                             if (lv_block_bytes(nch2, nr + 1, ne2, np2) > cap) break;
                             if (fresh) ctab.push_back(make_int4((int)ne, nx[0], nx[1], nx[2]));
