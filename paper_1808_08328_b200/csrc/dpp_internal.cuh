@@ -51,10 +51,15 @@ struct TraceScope {
     double t0;
     static bool on();
     static double now();
+    cudaEvent_t ev0 = nullptr;   // DPP_TRACE=ev: events on the scope's stream, no syncs
+    static bool ev_on();
+    static void ev_flush(const char *title);   // resolve + print every recorded scope (stream idle)
     TraceScope(Ctx *cc, const char *n) : c(cc), name(n), t0(0) {
         if (on()) { cudaStreamSynchronize(c->s); t0 = now(); }
+        else if (ev_on()) ev_begin();
     }
     ~TraceScope();
+    void ev_begin();
 };
 #define DPP_CAT2(a, b) a##b
 #define DPP_CAT(a, b) DPP_CAT2(a, b)

@@ -308,11 +308,13 @@ dpp_pc *pc_create(Ctx *c, dpp_system *s, const dpp_split_node *nodes, int n_node
     CK(cudaEventRecord(e0, c->s));
     auto pc = std::make_unique<dpp_pc>();
     pc->ctx = c;
-    DPP_TRACE_SCOPE(c, "pc.total");
-    Builder b{c, nodes, n_nodes, s, randn, user};
-    // K given: the tree's blocks are extracted from it by field index sets, as the reference
-    // does with the matrix its caller passes (blocksolve.py:288-294); else from the system's blocks
-    pc->root = b.node(0, {0, 1, 2, 3}, K);
+    {
+        DPP_TRACE_SCOPE(c, "pc.total");
+        Builder b{c, nodes, n_nodes, s, randn, user};
+        // K given: the tree's blocks are extracted from it by field index sets, as the reference
+        // does with the matrix its caller passes (blocksolve.py:288-294); else from the system's blocks
+        pc->root = b.node(0, {0, 1, 2, 3}, K);
+    }
     pc->n = (int)(s->sizes[0] + s->sizes[1] + s->sizes[2] + s->sizes[3]);
     pc->r.alloc(pc->n, c->s);
     pc->z.alloc(pc->n, c->s);
@@ -323,6 +325,7 @@ dpp_pc *pc_create(Ctx *c, dpp_system *s, const dpp_split_node *nodes, int n_node
     pc->setup_ms = ms;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    TraceScope::ev_flush("pc_create");
     return pc.release();
 }
 

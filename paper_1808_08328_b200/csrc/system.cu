@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <exception>
 #include <mutex>
+#include <string>
 #include <thread>
 #include <vector>
 
@@ -17,10 +18,59 @@ bool TraceScope::on() {
     if (v < 0) { const char *e = std::getenv("DPP_TRACE"); v = e && *e && *e != '0'; }
     return v == 1;
 }
+bool TraceScope::ev_on() {
+    static int v = -1;
+    if (v < 0) { const char *e = std::getenv("DPP_TRACE"); v = e && std::string(e) == "ev"; }
+    return v == 1;
+}
+namespace {
+struct EvRec {
+    std::string name;
+    cudaEvent_t a, b;
+    size_t tid;
+};
+std::mutex g_ev_mu;
+std::vector<EvRec> g_ev;
+cudaEvent_t g_ev_origin = nullptr;
+}  // namespace
+void TraceScope::ev_begin() {
+    std::lock_guard<std::mutex> g(g_ev_mu);
+    if (!g_ev_origin) {
+        cudaEventCreate(&g_ev_origin);
+        cudaEventRecord(g_ev_origin, c->s);
+    }
+    cudaEventCreate(&ev0);
+    cudaEventRecord(ev0, c->s);
+}
+void TraceScope::ev_flush(const char *title) {
+    std::lock_guard<std::mutex> g(g_ev_mu);
+    if (!g_ev_origin) return;
+    cudaDeviceSynchronize();
+    std::fprintf(stderr, "[dpp-evtrace] == %s ==\n", title);
+    for (auto &r : g_ev) {
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, g_ev_origin, r.a);
+        cudaEventElapsedTime(&b, g_ev_origin, r.b);
+        std::fprintf(stderr, "[dpp-evtrace] %9.3f %9.3f %8.3f t%03zu %s\n", a, b, b - a, r.tid, r.name.c_str());
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_ev.clear();
+    cudaEventDestroy(g_ev_origin);
+    g_ev_origin = nullptr;
+}
 double TraceScope::now() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 TraceScope::~TraceScope() {
+    if (ev0) {
+        cudaEvent_t e1;
+        cudaEventCreate(&e1);
+        cudaEventRecord(e1, c->s);
+        std::lock_guard<std::mutex> g(g_ev_mu);
+        g_ev.push_back({name, ev0, e1, std::hash<std::thread::id>{}(std::this_thread::get_id()) % 1000});
+        return;
+    }
     if (!on()) return;
     cudaStreamSynchronize(c->s);
     cudaMemPool_t pool;

@@ -424,6 +424,7 @@ void tri_dense_inverse(Ctx *c, Tri &T) {
 }
 
 bool bd_plan(Ctx *c, Tri &T, int B) {
+    DPP_TRACE_SCOPE(c, "tri.bd_plan");
     const int n = T.n;
     if (n == 0 || B <= 0) return false;
     auto P = std::make_unique<BdPlan>();

@@ -1353,6 +1353,7 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
 }  // namespace
 
 bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
+    DPP_TRACE_SCOPE(c, "tri.push_plan");
     const int n = T.n;
     if (n == 0 || L < 1 || L > PU_LMAX) return false;
     static bool attr = false;

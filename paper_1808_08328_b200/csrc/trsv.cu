@@ -519,7 +519,10 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf
     Tri T;
     T.n = A.rows;
     T.backward = !lower;
-    T.strict = csr_part(c, A, lower ? -1 : 1, true);
+    {
+        DPP_TRACE_SCOPE(c, "tri.strict_part");
+        T.strict = csr_part(c, A, lower ? -1 : 1, true);
+    }
     if (!unit) {
         T.diag.alloc(A.rows, c->s);
         csr_diag(c, A, T.diag.p, nullptr);
@@ -527,6 +530,7 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf
     if (allow_dense && T.n <= DENSE_TRI_MAX) {
         // exact-arithmetic rewrite for small, deep coarse levels: x = T^-1 b as a GEMV
         const int n = T.n;
+        DPP_TRACE_SCOPE(c, "tri.dense_inverse");
         tri_dense_inverse(c, T);
         CK(cudaStreamSynchronize(c->s));
         T.nlev = n;
