@@ -193,6 +193,11 @@ typedef void (*dpp_randn_fn)(int64_t n, double *out, void *user);
 int dpp_amg_create(dpp_ctx *ctx, const dpp_csr *A, double theta, double omega, int max_coarse,
                    int max_levels, dpp_randn_fn randn, void *user, dpp_amg **out);
 int dpp_amg_levels(const dpp_amg *h, int *levels);
+/* strength-graph greedy aggregation alone (linalg.py:279-324 _strength_aggregates): agg_host (n)
+ * receives the aggregate id of every row, *n_agg their count; path 0 = automatic (device passes
+ * from 32768 rows), 1 = host greedy over the device strength graph, 2 = device passes */
+int dpp_strength_aggregates(dpp_ctx *ctx, const dpp_csr *A, double theta, int path, int64_t *agg_host,
+                            int64_t *n_agg);
 /* borrowed A_l and P_l (P NULL on the coarsest level); agg_host (n_l) may be NULL */
 int dpp_amg_level(dpp_amg *h, int level, dpp_csr **A, dpp_csr **P, int64_t *agg_host,
                   double *rho);

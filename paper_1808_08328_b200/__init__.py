@@ -27,6 +27,7 @@ from .elements import ElementFamily, Formulation, dof_count, eval_basis, quadrat
 from .linalg import (
     KrylovStats,
     amg_setup,
+    strength_aggregates,
     amg_vcycle,
     apply_ilu0,
     diag_lump,

@@ -106,6 +106,7 @@ SIGNATURES = {
     "dpp_schur_selfp": [P, P, P, P, P, PP],
     "dpp_amg_create": [P, P, D, D, I32, I32, RANDN_FN, P, PP],
     "dpp_amg_levels": [P, C.POINTER(I32)],
+    "dpp_strength_aggregates": [P, P, D, I32, P, C.POINTER(I64)],
     "dpp_amg_level": [P, I32, PP, PP, P, C.POINTER(D)],
     "dpp_amg_vcycle": [P, P, P],
     "dpp_amg_destroy": [P],

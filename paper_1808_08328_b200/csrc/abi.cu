@@ -320,6 +320,16 @@ int dpp_amg_create(dpp_ctx *ctx, const dpp_csr *A, double theta, double omega, i
         *out = h.release();
     });
 }
+int dpp_strength_aggregates(dpp_ctx *ctx, const dpp_csr *A, double theta, int path, int64_t *agg_host,
+                            int64_t *n_agg) {
+    return guard([&] {
+        DBuf<int> agg;
+        *n_agg = strength_aggregates(&ctx->c, M(A), theta, path, agg);
+        TraceScope::ev_flush("strength_aggregates");
+        std::vector<int> a = agg.to_host();
+        std::copy(a.begin(), a.end(), agg_host);
+    });
+}
 int dpp_amg_levels(const dpp_amg *h, int *levels) { return guard([&] { *levels = (int)h->h->lv.size(); }); }
 int dpp_amg_level(dpp_amg *h, int level, dpp_csr **A, dpp_csr **P, int64_t *agg, double *rho) {
     return guard([&] {
@@ -328,7 +338,10 @@ int dpp_amg_level(dpp_amg *h, int level, dpp_csr **A, dpp_csr **P, int64_t *agg,
         const bool coarsest = level + 1 == (int)h->h->lv.size();
         if (A) *A = borrow(h->c, L.A);
         if (P) *P = coarsest ? nullptr : borrow(h->c, L.P);
-        if (agg && !coarsest) std::copy(L.agg.begin(), L.agg.end(), agg);
+        if (agg && !coarsest) {
+            std::vector<int> a = L.agg.to_host();
+            std::copy(a.begin(), a.end(), agg);
+        }
         if (rho) *rho = L.rho;
     });
 }

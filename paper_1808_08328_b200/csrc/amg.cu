@@ -15,7 +15,11 @@
 #include <cstdlib>
 #include <exception>
 #include <functional>
+#include <memory>
 #include <thread>
+
+#include <cub/cub.cuh>
+#include <thrust/iterator/transform_iterator.h>
 
 #include "dpp_internal.cuh"
 
@@ -74,7 +78,7 @@ static int64_t greedy(int n, const std::vector<int> &sp, const std::vector<int> 
     return next;
 }
 
-static int64_t aggregate(Ctx *c, const Csr &A, double theta, std::vector<int64_t> &agg) {
+static int64_t aggregate_host(Ctx *c, const Csr &A, double theta, DBuf<int> &dagg) {
     const int n = A.rows;
     DBuf<int> cnt(n, c->s);
     const int grid = grid_for((int64_t)n * 32, 256, c->sms, 8);
@@ -92,7 +96,308 @@ static int64_t aggregate(Ctx *c, const Csr &A, double theta, std::vector<int64_t
         hi = sidx.to_host();
     }
     DPP_TRACE_SCOPE(c, "amg.greedy_host");
-    return greedy(n, hp, hi, agg);
+    std::vector<int64_t> agg;
+    const int64_t nc = greedy(n, hp, hi, agg);
+    std::vector<int> agg32(agg.begin(), agg.end());
+    dagg.alloc(n, c->s);
+    dagg.upload(agg32.data(), n);
+    return nc;
+}
+
+// ---------------------------------------------------------------- device aggregation
+// The same three passes on the device, bit for bit.  N[i] = {i} + strong(i).
+//  pass 1: i seeds iff no earlier seed j has N[j] & N[i] != {} (an earlier seed that
+//          took i or one of its neighbours).  The owners of a node k are k itself and
+//          the rows whose strong list holds k (the transposed strength pattern); i waits
+//          only on the states of lower owners of its N[i], and decides "not a seed" as
+//          soon as one of them is a seed.  Seeds' N[] are disjoint, so a seed's
+//          aggregate id is its rank among the seeds and it stamps its whole N[].
+//  pass 2: i (untaken) takes the aggregate of its first strong neighbour, in stored
+//          order, that is taken at that point of the sequential loop: taken in pass 1,
+//          or a lower row that took one in pass 2 (i waits for that row's pass 2).
+//  pass 3: the rest become singletons, numbered after the seeds in row order.
+// Spinning rows only wait on lower rows and every thread walks its rows in ascending
+// order (the level-analysis dealing), so the lowest undecided row is always runnable;
+// the grid is co-resident (cooperative launch).
+namespace {
+constexpr long long AGG_SPIN_LIMIT = 1ll << 26;
+__device__ __forceinline__ int agg_ld(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void agg_st(int *p, int v) {
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// wait until x[j] != undecided; returns the value
+__device__ __forceinline__ int agg_wait(const int *x, int j, int undecided) {
+    int v = agg_ld(x + j);
+    long long spins = 0;
+    while (v == undecided) {
+        __nanosleep(32);
+        v = agg_ld(x + j);
+        if (++spins > AGG_SPIN_LIMIT) __trap();
+    }
+    return v;
+}
+__global__ void k_tcount(int n, const int *__restrict__ sp, const int *__restrict__ si, int *tc) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        for (int p = sp[j]; p < sp[j + 1]; ++p) atomicAdd(tc + si[p], 1);
+}
+__global__ void k_tfill(int n, const int *__restrict__ sp, const int *__restrict__ si, const int *__restrict__ tp,
+                        int *tcur, int *ti) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        for (int p = sp[j]; p < sp[j + 1]; ++p) {
+            const int k = si[p];
+            ti[tp[k] + atomicAdd(tcur + k, 1)] = j;
+        }
+}
+// Pass 1 as a dataflow: pending[i] counts the (k, j) pairs with k in N[i] and j a lower
+// owner of k (j conflicts with i through k).  A row that decides pushes to its higher
+// conflicting rows: a seed marks them (not seeds), a non-seed decrements their pending
+// count.  A row waits until it is marked or its count drains, i.e. until one lower
+// conflicting row is a seed or all of them are not -- the lexicographically-first MIS,
+// decided along its own dependency depth (148 steps on C2's S_p).
+template <typename F>
+__device__ __forceinline__ void agg_pairs(int i, const int *__restrict__ sp, const int *__restrict__ si,
+                                          const int *__restrict__ tp, const int *__restrict__ ti, F f) {
+    const int s0 = sp[i], s1 = sp[i + 1];
+    for (int q = s0 - 1; q < s1; ++q) {
+        const int k = q < s0 ? i : si[q];
+        f(k);
+        for (int p = tp[k], pe = tp[k + 1]; p < pe; ++p) f(ti[p]);
+    }
+}
+// per row: pending = lower conflicting pairs, hc = higher conflicting pairs
+__global__ void k_agg_count(int n, const int *__restrict__ sp, const int *__restrict__ si,
+                            const int *__restrict__ tp, const int *__restrict__ ti, int *pending, int *hc) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int lo = 0, hi = 0;
+        agg_pairs(i, sp, si, tp, ti, [&](int j) {
+            lo += j < i;
+            hi += j > i;
+        });
+        pending[i] = lo;
+        hc[i] = hi;
+    }
+}
+// the higher conflicting rows of every row, flattened (the push list of pass 1)
+__global__ void k_agg_hfill(int n, const int *__restrict__ sp, const int *__restrict__ si,
+                            const int *__restrict__ tp, const int *__restrict__ ti, const int *__restrict__ hp,
+                            int *hl) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        int o = hp[i];
+        agg_pairs(i, sp, si, tp, ti, [&](int h) {
+            if (h > i) hl[o++] = h;
+        });
+    }
+}
+// state: 1 seed, 0 not a seed
+__global__ void __launch_bounds__(256) k_agg_pass1(int n, const int *__restrict__ hp, const int *__restrict__ hl,
+                                                   int *pending, int *mark, int *state) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t W = T >> 5, w = g >> 5, lane = g & 31;
+    for (int64_t base = 0; base < n; base += T) {
+        const int64_t t = base + lane * W + w;
+        if (t >= n) continue;
+        const int i = (int)t;
+        int mk = agg_ld(mark + i), pd = agg_ld(pending + i);
+        long long spins = 0;
+        while (!mk && pd > 0) {
+            __nanosleep(20);
+            mk = agg_ld(mark + i);
+            pd = agg_ld(pending + i);
+            if (++spins > AGG_SPIN_LIMIT) __trap();
+        }
+        const bool seed = !mk;
+        state[i] = seed ? 1 : 0;
+        const int p0 = hp[i], p1 = hp[i + 1];
+        if (seed)
+            for (int p = p0; p < p1; ++p) agg_st(mark + hl[p], 1);
+        else
+            for (int p = p0; p < p1; ++p) atomicSub(pending + hl[p], 1);
+    }
+}
+// a1[k] = rank of the seed whose N[] holds k (pass 1), else -1
+__global__ void k_agg_stamp(int n, const int *__restrict__ sp, const int *__restrict__ si,
+                            const int *__restrict__ state, const int *__restrict__ rank, int *a1) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        if (state[j] != 1) continue;
+        const int id = rank[j];
+        a1[j] = id;
+        for (int p = sp[j]; p < sp[j + 1]; ++p) a1[si[p]] = id;
+    }
+}
+// fin: -2 undecided, -1 untaken after pass 2, else the aggregate
+__global__ void __launch_bounds__(256) k_agg_pass2(int n, const int *__restrict__ sp, const int *__restrict__ si,
+                                                   const int *__restrict__ a1, int *fin) {
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t W = T >> 5, w = g >> 5, lane = g & 31;
+    for (int64_t base = 0; base < n; base += T) {
+        const int64_t t = base + lane * W + w;
+        if (t >= n) continue;
+        const int i = (int)t;
+        int v = a1[i];
+        if (v < 0) {
+            for (int p = sp[i]; p < sp[i + 1]; ++p) {
+                const int k = si[p];
+                const int ak = a1[k];
+                if (ak >= 0) { v = ak; break; }
+                if (k < i) {
+                    const int fk = agg_wait(fin, k, -2);
+                    if (fk >= 0) { v = fk; break; }
+                }
+            }
+        }
+        agg_st(fin + i, v);
+    }
+}
+struct IsSeed {
+    __host__ __device__ int operator()(int s) const { return s == 1; }
+};
+struct IsLeft {
+    __host__ __device__ int operator()(int f) const { return f == -1; }
+};
+__global__ void k_fill_i(int *x, int n, int v) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) x[i] = v;
+}
+// pass 3 + count: agg = fin, or nseed + rank among the untaken
+__global__ void k_agg_final(int n, const int *__restrict__ state, const int *__restrict__ srank,
+                            const int *__restrict__ lrank, int *fin, int *nc) {
+    const int nseed = srank[n - 1] + (state[n - 1] == 1);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const bool left = fin[i] == -1;
+        if (i == n - 1) *nc = nseed + lrank[i] + (left ? 1 : 0);
+        if (left) fin[i] = nseed + lrank[i];
+    }
+}
+}  // namespace
+
+// threads of the spinning pass kernels (DPP_AGG_THREADS, default 16384): the waits
+// follow the MIS dependency depth, not the thread count, and a small co-resident grid
+// neither waits for half the device to drain nor keeps it spinning
+static int64_t agg_threads() {
+    static const int64_t t = [] { const char *e = std::getenv("DPP_AGG_THREADS"); return e ? std::atoll(e) : 16384LL; }();
+    return t;
+}
+static void coop_launch(Ctx *c, const void *k, int n, void **args, int64_t max_threads = agg_threads()) {
+    const int block = 256;
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, 0));
+    if (per_sm < 1) DPP_FAIL(DPP_ERR_CUDA, "aggregation kernels cannot be resident");
+    per_sm = std::max(1, per_sm / 2);   // leave room for the other setup branches
+    const int64_t need = std::min<int64_t>(((int64_t)n + 31) / 32 * 32, std::max<int64_t>(max_threads, 256));
+    const int64_t cap = (int64_t)c->sms * per_sm * block;
+    const int grid = (int)((std::min(need, cap) + block - 1) / block);
+    CK(cudaLaunchCooperativeKernel(k, grid, block, args, 0, c->s));
+    launched(c);
+}
+
+template <typename Op>
+static void flag_scan(Ctx *c, const int *in, int *out, int n) {
+    auto it = thrust::make_transform_iterator(in, Op());
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, out, n, c->s));
+    DBuf<char> t(std::max<size_t>(tb, 1), c->s);
+    CK(cub::DeviceScan::ExclusiveSum(t.p, tb, it, out, n, c->s));
+    launched(c);
+}
+
+static int64_t aggregate_dev(Ctx *c, const Csr &A, double theta, DBuf<int> &agg) {
+    const int n = A.rows;
+    agg.alloc(n, c->s);
+    if (!n) return 0;
+    // strength graph: counts -> int32 scan (total <= nnz(A), no read back) -> fill
+    std::unique_ptr<TraceScope> ph(new TraceScope(c, "agg.strength"));
+    DBuf<int> cnt(n, c->s), sp(n + 1, c->s), si(std::max<int64_t>(A.nnz, 1), c->s);
+    const int grid = grid_for((int64_t)n * 32, 256, c->sms, 8);
+    k_strength<<<grid, 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, theta, nullptr, cnt.p, nullptr);
+    launched(c);
+    scan_to_ptr32(c, cnt.p, n, sp.p);
+    k_strength<<<grid, 256, 0, c->s>>>(n, A.ptr.p, A.idx.p, A.val.p, theta, sp.p, nullptr, si.p);
+    launched(c);
+    // transposed pattern (owners)
+    ph.reset(new TraceScope(c, "agg.transpose"));
+    DBuf<int> tc(n, c->s), tp(n + 1, c->s), ti(std::max<int64_t>(A.nnz, 1), c->s);
+    CK(cudaMemsetAsync(tc.p, 0, sizeof(int) * n, c->s));
+    const int g1 = grid_for(n, 256, c->sms);
+    k_tcount<<<g1, 256, 0, c->s>>>(n, sp.p, si.p, tc.p);
+    launched(c);
+    scan_to_ptr32(c, tc.p, n, tp.p);
+    CK(cudaMemsetAsync(tc.p, 0, sizeof(int) * n, c->s));
+    k_tfill<<<g1, 256, 0, c->s>>>(n, sp.p, si.p, tp.p, tc.p, ti.p);
+    launched(c);
+    // pass 1
+    ph.reset(new TraceScope(c, "agg.pass1"));
+    DBuf<int> state(n, c->s), srank(n, c->s), lrank(n, c->s), nc(1, c->s), pend(n, c->s), mark(n, c->s);
+    DBuf<int> hc(n, c->s), hp(n + 1, c->s);
+    CK(cudaMemsetAsync(mark.p, 0, sizeof(int) * n, c->s));
+    k_agg_count<<<g1, 256, 0, c->s>>>(n, sp.p, si.p, tp.p, ti.p, pend.p, hc.p);
+    launched(c);
+    scan_to_ptr32(c, hc.p, n, hp.p);
+    int nh = 0;
+    CK(cudaMemcpyAsync(&nh, hp.p + n, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    // dense strong hubs make the push lists quadratic: the host loop has no such term
+    if (nh < 0 || nh > (1 << 28)) {
+        ph.reset();
+        return aggregate_host(c, A, theta, agg);
+    }
+    DBuf<int> hl(std::max(nh, 1), c->s);
+    k_agg_hfill<<<g1, 256, 0, c->s>>>(n, sp.p, si.p, tp.p, ti.p, hp.p, hl.p);
+    launched(c);
+    {
+        int nn = n;
+        const int *a = hp.p, *b = hl.p;
+        int *pe = pend.p, *mk = mark.p, *st = state.p;
+        void *args[] = {&nn, &a, &b, &pe, &mk, &st};
+        coop_launch(c, (const void *)k_agg_pass1, n, args, agg_threads());
+    }
+    ph.reset(new TraceScope(c, "agg.stamp"));
+    flag_scan<IsSeed>(c, state.p, srank.p, n);
+    DBuf<int> a1(n, c->s);
+    CK(cudaMemsetAsync(a1.p, 0xFF, sizeof(int) * n, c->s));
+    k_agg_stamp<<<g1, 256, 0, c->s>>>(n, sp.p, si.p, state.p, srank.p, a1.p);
+    launched(c);
+    // pass 2 (into agg, -2 = undecided)
+    ph.reset(new TraceScope(c, "agg.pass2"));
+    k_fill_i<<<g1, 256, 0, c->s>>>(agg.p, n, -2);
+    launched(c);
+    {
+        int nn = n;
+        const int *a = sp.p, *b = si.p, *d = a1.p;
+        int *f = agg.p;
+        void *args[] = {&nn, &a, &b, &d, &f};
+        coop_launch(c, (const void *)k_agg_pass2, n, args);
+    }
+    // pass 3
+    ph.reset(new TraceScope(c, "agg.pass3"));
+    flag_scan<IsLeft>(c, agg.p, lrank.p, n);
+    k_agg_final<<<g1, 256, 0, c->s>>>(n, state.p, srank.p, lrank.p, agg.p, nc.p);
+    launched(c);
+    ph.reset();
+    int h = 0;
+    CK(cudaMemcpyAsync(&h, nc.p, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return h;
+}
+
+// Device passes from DPP_AGG_DEV_MIN rows up (default 32768): below it the strength graph
+// is small enough that its read back + the host loop beat the cooperative launches, which
+// must wait for half the device to drain while the other setup branches run.
+// DPP_AGG_HOST=1 / =0 forces either path (read per call); path 1 / 2 force them per call.
+int64_t strength_aggregates(Ctx *c, const Csr &A, double theta, int path, DBuf<int> &agg) {
+    static const int dev_min = [] { const char *v = std::getenv("DPP_AGG_DEV_MIN"); return v ? std::atoi(v) : 32768; }();
+    bool host = A.rows < dev_min;
+    const char *e = std::getenv("DPP_AGG_HOST");
+    if (e && *e) host = *e == '1';
+    if (path == 1 || path == 2) host = path == 1;
+    return host ? aggregate_host(c, A, theta, agg) : aggregate_dev(c, A, theta, agg);
+}
+static int64_t aggregate(Ctx *c, const Csr &A, double theta, DBuf<int> &agg) {
+    return strength_aggregates(c, A, theta, 0, agg);
 }
 
 // ---------------------------------------------------------------- P construction
@@ -512,9 +817,7 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
         }
         L->rho = rho;
         const double damping = 2.0 * omega / L->rho;
-        std::vector<int> agg32(L->agg.begin(), L->agg.end());
-        DBuf<int> dagg(n, c->s);
-        dagg.upload(agg32.data(), n);
+        DBuf<int> &dagg = L->agg;
         static const bool p_generic = [] { const char *e = std::getenv("DPP_P_GENERIC"); return e && *e == '1'; }();
         L->P.rows = n;
         L->P.cols = (int)nc;

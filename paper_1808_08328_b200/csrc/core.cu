@@ -2,6 +2,9 @@
 // Reference semantics: scipy.sparse CSR as used by dppflow (linalg.py:27-32,
 // blocksolve.py:227-228, assembly.py:102-108, linalg.py:218-219, :372-374).
 #include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+#include <thrust/iterator/transform_output_iterator.h>
 
 #include <climits>
 #include <cstdlib>
@@ -14,32 +17,36 @@ namespace dpp {
 static inline cudaStream_t S(Ctx *c, cudaStream_t st) { return st ? st : c->s; }
 
 // ---------------------------------------------------------------- scans
-__global__ void k_widen(const int *a, int64_t *b, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
-        b[i] = i < n ? a[i] : 0;
-}
-__global__ void k_narrow(const int64_t *a, int *b, int n) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += gridDim.x * blockDim.x)
-        b[i] = (int)a[i];
+// One decoupled-look-back scan: counts widened to int64 on the fly (element n reads as
+// 0), the running sum narrowed on the way out with saturation to -1, so a total of
+// 2^31 or more shows up as a negative ptr[n] instead of wrapping silently.
+namespace {
+struct CountAt {
+    const int *c;
+    int n;
+    __host__ __device__ long long operator()(int i) const { return i < n ? (long long)c[i] : 0LL; }
+};
+struct Narrow {
+    __host__ __device__ int operator()(long long v) const { return v > INT_MAX ? -1 : (int)v; }
+};
+}  // namespace
+void scan_to_ptr32(Ctx *c, const int *counts, int n, int *ptr) {
+    auto in = thrust::make_transform_iterator(thrust::make_counting_iterator<int>(0), CountAt{counts, n});
+    auto out = thrust::make_transform_output_iterator(ptr, Narrow{});
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n + 1, c->s));
+    DBuf<char> t(std::max<size_t>(tb, 1), c->s);
+    CK(cub::DeviceScan::ExclusiveSum(t.p, tb, in, out, n + 1, c->s));
+    launched(c);
 }
 // counts[n] -> ptr[n+1] (int32), returns total; errors if total >= 2^31
 int64_t counts_to_ptr(Ctx *c, const int *counts, int n, DBuf<int> &ptr) {
-    DBuf<int64_t> tmp64((size_t)n + 1, c->s);
-    DBuf<int64_t> in64((size_t)n + 1, c->s);
-    k_widen<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(counts, in64.p, n);
-    launched(c);
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, in64.p, tmp64.p, n + 1, c->s));
-    DBuf<char> t(tb, c->s);
-    CK(cub::DeviceScan::ExclusiveSum(t.p, tb, in64.p, tmp64.p, n + 1, c->s));
-    launched(c);
-    int64_t total = 0;
-    CK(cudaMemcpyAsync(&total, tmp64.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, c->s));
-    CK(cudaStreamSynchronize(c->s));
-    if (total > INT_MAX) DPP_FAIL(DPP_ERR_VALUE, "CSR with more than 2^31-1 entries");
     ptr.alloc((size_t)n + 1, c->s);
-    k_narrow<<<grid_for(n + 1, 256, c->sms), 256, 0, c->s>>>(tmp64.p, ptr.p, n);
-    launched(c);
+    scan_to_ptr32(c, counts, n, ptr.p);
+    int total = 0;
+    CK(cudaMemcpyAsync(&total, ptr.p + n, sizeof(int), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    if (total < 0) DPP_FAIL(DPP_ERR_VALUE, "CSR with more than 2^31-1 entries");
     return total;
 }
 

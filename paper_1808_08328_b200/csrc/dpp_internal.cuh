@@ -225,6 +225,8 @@ void fork_join(Ctx *c, SideStream &owner, const std::function<void(Ctx *)> &side
                const std::function<void()> &main_fn, int kind);
 
 int64_t counts_to_ptr(Ctx *c, const int *counts, int n, DBuf<int> &ptr);
+// counts[n] -> ptr[n+1] without a read back (caller bounds the total below 2^31)
+void scan_to_ptr32(Ctx *c, const int *counts, int n, int *ptr);
 
 inline int grid_for(int64_t work, int block, int sms, int per_sm = 16) {
     int64_t g = (work + block - 1) / block;
@@ -362,7 +364,7 @@ void ilu_apply(Ctx *c, Ilu &f, const double *r, double *z, cudaStream_t st = nul
 struct AmgLevel {
     Csr A, P, R;               // R = P^T
     Tri lo, up;                // D+L, D+U
-    std::vector<int64_t> agg;  // host copy of aggregates
+    DBuf<int> agg;             // aggregates (device)
     double rho = 0;
     DBuf<double> b, x, r, t, y; // workspace
     DBuf<int> ticket;
@@ -377,6 +379,8 @@ struct Amg {
     int nc = 0;
 };
 // A0_steal: optional; its storage becomes level 0 (no copy) when the caller is done with it
+// greedy strength aggregation (path 0 auto, 1 host greedy, 2 device passes); returns the count
+int64_t strength_aggregates(Ctx *c, const Csr &A, double theta, int path, DBuf<int> &agg);
 std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A, double theta, double omega, int max_coarse,
                                int max_levels, dpp_randn_fn randn, void *user, Csr *A0_steal = nullptr);
 void amg_vcycle(Ctx *c, Amg &h, const double *r, double *z, cudaStream_t st = nullptr);

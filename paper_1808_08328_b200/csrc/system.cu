@@ -15,7 +15,7 @@ namespace dpp {
 
 bool TraceScope::on() {
     static int v = -1;
-    if (v < 0) { const char *e = std::getenv("DPP_TRACE"); v = e && *e && *e != '0'; }
+    if (v < 0) { const char *e = std::getenv("DPP_TRACE"); v = e && *e && *e != '0' && std::string(e) != "ev"; }
     return v == 1;
 }
 bool TraceScope::ev_on() {

@@ -24,6 +24,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 
@@ -237,6 +238,109 @@ __global__ void __launch_bounds__(32 * BD_INV_WPB)
     for (int i = lane; i < m; i += 32) D[(size_t)i * B + c] = xc[i];
 }
 
+// Same inverse, G columns per CTA at once: X[rows][G] lives in shared memory and the
+// block's rows are dealt to G-lane workers in substitution order; a worker waits (on a
+// per-row flag in shared memory) only for the rows its row reads, so independent rows of
+// the block proceed in parallel instead of one warp walking every row of one column.
+// Forward: column group [c0, c0+G) is zero above row c0; backward: zero below c0+G-1.
+// Entries of a row are loaded G at a time by the worker's lanes and only the in-window
+// ones are broadcast (ballot).  Rows outside the window are written as zeros.
+constexpr int BDI_THREADS = 512;
+template <int G>
+__global__ void __launch_bounds__(BDI_THREADS)
+    k_bd_inv_tile(int n, int B, int backward, const int *__restrict__ ptr, const int *__restrict__ idx,
+                  const double *__restrict__ val, const double *__restrict__ diag, double *__restrict__ dense) {
+    extern __shared__ double X[];
+    const int blk = blockIdx.y, s = blk * B, m = min(B, n - s);
+    const int c0 = blockIdx.x * G;
+    if (c0 >= m) return;
+    int *done = reinterpret_cast<int *>(X + (size_t)m * G);
+    const int lo = backward ? 0 : c0, hi = backward ? min(m, c0 + G) : m;
+    for (int i = threadIdx.x; i < hi - lo; i += blockDim.x) done[lo + i] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, q = lane % G, sub = lane / G;
+    const int wk = threadIdx.x / G, nwk = blockDim.x / G;
+    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (sub * G));
+    const unsigned done_base = (unsigned)__cvta_generic_to_shared(done);
+    for (int t = wk; t < hi - lo; t += nwk) {
+        const int a = backward ? hi - 1 - t : lo + t, r = s + a;
+        const int pe = ptr[r + 1];
+        double acc = 0.0;
+        for (int p0 = ptr[r]; p0 < pe; p0 += G) {
+            const int p = p0 + q;
+            int j = -1;
+            double v = 0.0;
+            if (p < pe) {
+                j = idx[p] - s;
+                v = val[p];
+            }
+            const bool keep = j >= lo && j < hi;
+            unsigned km = (__ballot_sync(gmask, keep) & gmask) >> (sub * G);
+            while (km) {
+                const int e = __ffs(km) - 1;
+                km &= km - 1;
+                const int jj = __shfl_sync(gmask, j, e, G);
+                const double vv = __shfl_sync(gmask, v, e, G);
+                int f;
+                long long spins = 0;
+                do {
+                    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(f) : "r"(done_base + 4u * jj) : "memory");
+                    if (++spins > (1ll << 28)) __trap();
+                } while (!f);
+                acc += vv * X[(size_t)jj * G + q];
+            }
+        }
+        const double d = diag ? diag[r] : 1.0;
+        X[(size_t)a * G + q] = ((a == c0 + q ? 1.0 : 0.0) - acc) / d;
+        __syncwarp(gmask);
+        if (q == 0) asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(done_base + 4u * a), "r"(1) : "memory");
+    }
+    __syncthreads();
+    const int ncol = min(G, m - c0);
+    double *D = dense + (size_t)blk * B * B;
+    for (int i = threadIdx.x; i < m * G; i += blockDim.x) {
+        const int row = i / G, cc = i % G;
+        if (cc < ncol) D[(size_t)row * B + c0 + cc] = row >= lo && row < hi ? X[(size_t)row * G + cc] : 0.0;
+    }
+}
+
+// G for an m-row block: the X tile plus flags within 200 KB
+static int bd_inv_g(int m) {
+    for (int g : {32, 16, 8, 4})
+        if ((size_t)m * (8 * g + 4) <= 200 * 1024) return g;
+    return 0;
+}
+static bool bd_inverse_tiles(Ctx *c, int n, int B, int nb, const Tri &T, double *dense) {
+    // opt-in (DPP_BD_INV_TILE=1, read per call): measured slower than the column-per-warp
+    // kernel on C2 (setup 24.9 vs 18.4 ms median): a row's entries stream in G-wide chunks
+    // behind its dependency waits, so each row costs several L2 round trips on the chain
+    const char *oe = std::getenv("DPP_BD_INV_TILE");
+    const bool old = !(oe && *oe == '1');
+    const int m = std::min(B, n);
+    const int G = old ? 0 : bd_inv_g(m);
+    if (!G) return false;
+    const size_t sm = (size_t)m * (8 * G + 4);
+    dim3 grid((m + G - 1) / G, nb);
+    auto go = [&](auto gtag) {
+        constexpr int GG = decltype(gtag)::value;
+        static const bool attr = [] {   // thread-safe once per G (setups run on several host threads)
+            CK(cudaFuncSetAttribute(k_bd_inv_tile<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            return true;
+        }();
+        (void)attr;
+        k_bd_inv_tile<GG><<<grid, BDI_THREADS, sm, c->s>>>(n, B, T.backward, T.strict.ptr.p, T.strict.idx.p,
+                                                          T.strict.val.p, T.diag.n ? T.diag.p : nullptr, dense);
+    };
+    switch (G) {
+        case 32: go(std::integral_constant<int, 32>{}); break;
+        case 16: go(std::integral_constant<int, 16>{}); break;
+        case 8: go(std::integral_constant<int, 8>{}); break;
+        default: go(std::integral_constant<int, 4>{}); break;
+    }
+    launched(c);
+    return true;
+}
+
 // ---------------------------------------------------------------- sweep
 // Values move between the cluster's CTAs only by st.async pushes that count
 // their bytes on the receiving CTA's mbarrier (no cluster barrier, no fence):
@@ -409,6 +513,7 @@ static int bd_cluster_size() {
 void tri_dense_inverse(Ctx *c, Tri &T) {
     const int n = T.n;
     T.dense.alloc((size_t)n * n, c->s);
+    if (bd_inverse_tiles(c, n, n, 1, T, T.dense.p)) return;   // writes every entry
     CK(cudaMemsetAsync(T.dense.p, 0, sizeof(double) * (size_t)n * n, c->s));
     const size_t sm = (size_t)BD_INV_WPB * n * sizeof(double);
     static bool attr = false;
@@ -466,10 +571,12 @@ bool bd_plan(Ctx *c, Tri &T, int B) {
             CK(cudaFuncSetAttribute(k_trsv_bd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD_SMEM_LIMIT));
             attr = true;
         }
-        dim3 grid((B + BD_INV_WPB - 1) / BD_INV_WPB, P->nb);
-        k_bd_inverse<<<grid, 32 * BD_INV_WPB, sm, c->s>>>(n, B, T.backward, T.strict.ptr.p, T.strict.idx.p,
-                                                           T.strict.val.p, T.diag.n ? T.diag.p : nullptr, dense.p);
-        launched(c);
+        if (!bd_inverse_tiles(c, n, B, P->nb, T, dense.p)) {
+            dim3 grid((B + BD_INV_WPB - 1) / BD_INV_WPB, P->nb);
+            k_bd_inverse<<<grid, 32 * BD_INV_WPB, sm, c->s>>>(n, B, T.backward, T.strict.ptr.p, T.strict.idx.p,
+                                                               T.strict.val.p, T.diag.n ? T.diag.p : nullptr, dense.p);
+            launched(c);
+        }
         k_bd_seg_fill<<<nseg, 256, 0, c->s>>>(n, B, C, P->W, T.backward, T.strict.ptr.p, T.strict.idx.p,
                                                T.strict.val.p, dense.p, P->soff.p, P->segs.p);
         launched(c);

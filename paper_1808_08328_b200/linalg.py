@@ -247,6 +247,20 @@ class AmgHierarchy:
             self.h = None
 
 
+def strength_aggregates(A, theta: float = 0.5, *, path: str = "auto") -> np.ndarray:
+    """Greedy aggregation over the strength graph (reference linalg.py:279-324
+    _strength_aggregates): int64 aggregate id per row.  path: "auto" (device passes from
+    32768 rows), "host" (greedy loop over the device-built strength graph) or "device"."""
+    if A.shape[0] != A.shape[1]:
+        raise ValueError("aggregation requires a square matrix")
+    dA = as_device(A)
+    agg = np.empty(A.shape[0], dtype=np.int64)
+    nagg = ct.c_int64()
+    N.call("dpp_strength_aggregates", N.ctx(), dA.h, float(theta), {"auto": 0, "host": 1, "device": 2}[path],
+           N.ptr(agg), ct.byref(nagg))
+    return agg
+
+
 def amg_setup(A, *, theta: float = 0.5, omega: float = 2.0 / 3.0, max_coarse: int = 64,
               max_levels: int = 25) -> AmgHierarchy:
     """Smoothed-aggregation hierarchy on the device (reference linalg.py:341-380)."""

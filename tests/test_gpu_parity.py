@@ -11,6 +11,7 @@ import pytest
 import scipy.sparse as sp
 
 import oracle
+import oracle.solvers as oracle_solvers
 from tests.conftest import csr_from
 
 pytestmark = pytest.mark.gpu
@@ -262,6 +263,54 @@ def test_amg_prolongator_bitwise(form, dim, kind, n):
         Ac = (P.T.tocsr() @ (A @ P)).tocsr()
         Ac.sort_indices()
         assert abs(nx.A - Ac).max() <= 1e-14 * abs(Ac).max()
+
+
+def _agg_case(kind, n, rng):
+    """Strength graphs the mesh operators do not produce: asymmetric patterns, rows with
+    no off-diagonal entries, ties at the threshold, long chains, dense hubs."""
+    if kind == "random_asym":
+        A = sp.random(n, n, density=6.0 / n, random_state=int(rng.integers(1 << 30)), format="csr")
+        A = A + sp.diags(np.full(n, 10.0))
+    elif kind == "chain":   # a path in reverse order plus a few long-range ties
+        i = np.arange(n - 1)
+        A = sp.coo_matrix((-np.ones(n - 1), (i + 1, i)), shape=(n, n)) + sp.diags(np.full(n, 2.0))
+        A = A + sp.coo_matrix((-np.ones(20), (rng.integers(0, n, 20), rng.integers(0, n, 20))), shape=(n, n))
+    elif kind == "ties":    # integer magnitudes: many |a_ij| == theta * max exactly
+        A = sp.random(n, n, density=8.0 / n, random_state=int(rng.integers(1 << 30)), format="csr")
+        A.data = np.round(A.data * 4.0) + 1.0
+        A = A + sp.diags(np.full(n, 50.0))
+    elif kind == "hubs":    # a few rows / columns strongly tied to everything
+        A = sp.random(n, n, density=3.0 / n, random_state=int(rng.integers(1 << 30)), format="lil")
+        for h in rng.integers(0, n, 4):
+            A[h, :] = 0.5
+            A[:, h] = 0.5
+        A = sp.csr_matrix(A) + sp.diags(np.full(n, 20.0))
+    A = sp.csr_matrix(A)
+    A.sum_duplicates()
+    A.sort_indices()
+    # isolated rows: diagonal only
+    iso = rng.integers(0, n, max(1, n // 50))
+    A = sp.lil_matrix(A)
+    for r in iso:
+        d = A[r, r]
+        A[r, :] = 0.0
+        A[r, r] = d
+    A = sp.csr_matrix(A)
+    A.eliminate_zeros()
+    A.sort_indices()
+    return A
+
+
+@pytest.mark.parametrize("kind", ["random_asym", "chain", "ties", "hubs"])
+@pytest.mark.parametrize("n", [300, 20000])
+def test_device_aggregation_bitwise(kind, n, rng):
+    """Device aggregation (three passes: seeds by owner waits, first-taken neighbour,
+    singletons) == the reference's sequential greedy (linalg.py:279-324) via the oracle,
+    on patterns chosen to stress its order dependence (device passes forced at every size)."""
+    A = _agg_case(kind, n, rng)
+    ref = oracle_solvers.aggregate(A, 0.5)
+    for path in ("device", "host"):
+        assert np.array_equal(dpp.strength_aggregates(A, 0.5, path=path), ref)
 
 
 def test_amg_known_answers(rng):
