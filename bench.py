@@ -26,7 +26,8 @@ that stops early would otherwise inflate the throughput).  --gpus N without a
 torchrun environment re-launches itself under torch.distributed.run (N replicas).
 The line also carries BASELINE config 3 as stated (c3_solve: per-cell permeability + no-flow
 walls, the extension; --no-c3 skips it) and the config-4 sweep (DG-VMS TET 32^3: 100 SpMV +
-100 PC applies, c4_sweep; --no-c4 skips it).
+100 PC applies, c4_sweep; --no-c4 skips it) and, labelled NON-PARITY, the same C2 step with
+the preconditioner's triangular solves as Jacobi sweeps (fast_mode; --no-fast skips it).
 """
 
 from __future__ import annotations
@@ -215,6 +216,53 @@ def gpu_arm(args, rank, world):
                 e2e_s=e2e_s, h2d=h2d, d2h=d2h)
 
 
+FAST_TRI = os.environ.get("BENCH_FAST_TRI", "jacobi4")
+
+
+def fast_mode():
+    """NON-PARITY fast mode (extension): the same C2 step with every triangular
+    solve of the preconditioner as k Jacobi sweeps (triangular="jacobi<k>"); assemble + setup +
+    GMRES to rtol 1e-8 on the true residual, device-timed like `value`, plus its Arnoldi-step
+    roofline.  Iterates and iteration counts are NOT the reference's."""
+    import ctypes as C
+
+    import paper_1808_08328_b200 as dpp
+    from paper_1808_08328_b200 import _native as N
+    cfg = CONFIG
+    p = dpp.DppParameters(k2=cfg["k2"], gamma_b=(0.0, 0.0, 0.0))
+    mesh = dpp.generate_unit_mesh(cfg["dim"], cfg["kind"], cfg["n"])
+    bcs = dpp.boundary_data(dpp.manufactured_solution(cfg["dim"], p), mesh)
+    conf = dpp.method_config(cfg["method"], rtol=cfg["rtol"], triangular=FAST_TRI)
+    times, its = [], []
+    for k in range(5):   # 2 warm-up + 3 timed
+        N.call("dpp_timer_start", N.ctx())
+        bs = dpp.assemble(mesh, cfg["formulation"], p, bcs)
+        rep = dpp.solve(bs, conf, want_solution=False)
+        ms = C.c_double()
+        N.call("dpp_timer_stop", N.ctx(), C.byref(ms))
+        if not rep.converged or not rep.stats.relative_residual <= conf.rtol:
+            raise RuntimeError(f"fast-mode solve did not converge: {rep.stats}")
+        if k >= 2:
+            times.append(ms.value)
+            its.append(rep.stats.iterations)
+        if k < 4:
+            del bs, rep
+    pc = dpp.build_preconditioner(bs, conf)
+    prof = N.StepProfile()
+    N.call("dpp_profile_step", N.ctx(), bs.device().h, pc.handle(), 20, 1, C.byref(prof))
+    peak, _ = measured_peak()
+    gbs = (prof.spmv_bytes + prof.pc_bytes) / ((prof.spmv_ms + prof.pc_ms) * 1e-3) / 1e9
+    dof = bs.size
+    ms_step = float(np.mean(times))
+    del pc, bs, rep
+    return {"label": "NON-PARITY extension: triangular solves as Jacobi sweeps; iterates differ from the reference",
+            "triangular": FAST_TRI, "workload": CONFIG["workload"], "dof": dof, "ksp": its[-1],
+            "ms_per_step": ms_step, "dof_per_s": dof / (ms_step * 1e-3),
+            "pc_ms": prof.pc_ms, "spmv_ms": prof.spmv_ms, "pc_kernels_per_apply": int(prof.pc_launches),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "bytes_per_step": prof.spmv_bytes + prof.pc_bytes}}
+
+
 def c3_solve():
     """BASELINE config 3 as stated (the per-cell-permeability / no-flow extension; parity
     unpinned): HEX 64^3 CG-VMS, field split, rtol 1e-8; assemble + setup + GMRES, device-timed."""
@@ -266,7 +314,13 @@ def c4_sweep():
            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                         "bytes_per_step": prof.spmv_bytes + prof.pc_bytes},
            "pc_kernels_per_apply": int(prof.pc_launches)}
-    del pc, bs
+    del pc
+    pcf = dpp.build_preconditioner(bs, dpp.method_config("scale", rtol=1e-8, triangular=FAST_TRI))
+    N.call("dpp_profile_step", N.ctx(), bs.device().h, pcf.handle(), 100, 1, C.byref(prof))
+    out["fast_mode"] = {"label": "NON-PARITY extension (Jacobi triangular sweeps)", "triangular": FAST_TRI,
+                        "pc_ms": prof.pc_ms, "pc_gbs": prof.pc_bytes / (prof.pc_ms * 1e-3) / 1e9,
+                        "pc_kernels_per_apply": int(prof.pc_launches)}
+    del pcf, bs
     return out
 
 
@@ -361,6 +415,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 SpMV / PC-apply sweep")
     ap.add_argument("--no-c3", action="store_true", help="skip the config-3 solve")
+    ap.add_argument("--no-fast", action="store_true", help="skip the non-parity fast-mode C2 step")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # N replicas, one process per GPU: re-launch under torch.distributed.run
@@ -430,6 +485,8 @@ def main():
         "e2e": {"value": world * r["dof"] / r["e2e_s"], "unit": "DoF/s",
                 "h2d_bytes_per_step": int(r["h2d"]), "d2h_bytes_per_step": int(r["d2h"])},
     }
+    if not args.no_fast and world == 1:
+        line["fast_mode"] = fast_mode()
     if not args.no_c3 and world == 1:
         line["c3_solve"] = c3_solve()
     if not args.no_c4 and world == 1:

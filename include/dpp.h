@@ -59,6 +59,10 @@ int dpp_timer_start(dpp_ctx *ctx);
 int dpp_timer_stop(dpp_ctx *ctx, double *ms);
 /* number of libdpp kernel launches issued on this context so far */
 int dpp_ctx_launches(const dpp_ctx *ctx, int64_t *count);
+/* NON-PARITY fast mode (no reference counterpart): triangular solves of
+ * preconditioners built afterwards on this context become `sweeps` Jacobi sweeps
+ * (x0 = D^-1 b, x <- D^-1 (b - S x)); 0 restores the reference's exact substitution */
+int dpp_ctx_set_tri_jacobi(dpp_ctx *ctx, int sweeps);
 
 /* ---- CSR matrices (scipy.sparse.csr_matrix on the device) --------------- */
 int dpp_csr_create(dpp_ctx *ctx, int rows, int cols, int64_t nnz, const int32_t *indptr_host,

@@ -70,6 +70,7 @@ SIGNATURES = {
     "dpp_timer_start": [P],
     "dpp_timer_stop": [P, C.POINTER(D)],
     "dpp_ctx_launches": [P, C.POINTER(I64)],
+    "dpp_ctx_set_tri_jacobi": [P, I32],
     "dpp_csr_create": [P, I32, I32, I64, P, P, P, PP],
     "dpp_csr_info": [P, C.POINTER(I32), C.POINTER(I32), C.POINTER(I64)],
     "dpp_csr_download": [P, P, P, P],

@@ -94,6 +94,12 @@ int dpp_ctx_sync(dpp_ctx *ctx) { return guard([&] { CK(cudaStreamSynchronize(ctx
 int dpp_ctx_launches(const dpp_ctx *ctx, int64_t *count) {
     return guard([&] { *count = ctx->c.launches; });
 }
+int dpp_ctx_set_tri_jacobi(dpp_ctx *ctx, int sweeps) {
+    return guard([&] {
+        if (sweeps < 0 || sweeps > 64) DPP_FAIL(DPP_ERR_VALUE, "Jacobi sweep count must be in [0, 64]");
+        ctx->c.tri_jacobi = sweeps;
+    });
+}
 
 // ---------------------------------------------------------------- CSR
 int dpp_csr_create(dpp_ctx *ctx, int rows, int cols, int64_t nnz, const int32_t *indptr,

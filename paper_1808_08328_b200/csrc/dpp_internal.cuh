@@ -40,6 +40,8 @@ struct Ctx {
     double *nrm_part = nullptr;  // NRM_BLOCKS partial sums (norm reductions on s)
     double *nrm_part2 = nullptr; // same for s2
     cudaEvent_t t0 = nullptr, t1 = nullptr;   // dpp_timer_*
+    int tri_jacobi = 0;          // non-parity fast mode: triangular solves built at setup become
+                                 // this many Jacobi sweeps (0 = exact substitution, the reference)
 };
 constexpr int NRM_BLOCKS = 296;
 
@@ -320,7 +322,9 @@ struct Tri {              // one sweep: strict part (zero-free) + optional diago
     int ncomp = 1;        // Kronecker form: the triangle is this one (x) I_ncomp, rows interleaved
     Csr W;                // level-merged form (merge_levels): x = solve_unit(strict, W b)
     DBuf<double> wb;      //   scratch for W b
+    DBuf<double> wb2;     // Jacobi mode: x0 = D^-1 b
     int64_t nnz_alg = -1; // stored entries of the original strict triangle (algorithmic bytes)
+    int jacobi = 0;       // non-parity fast mode: x = k Jacobi sweeps on (strict, diag), ncomp-interleaved
     bool backward = false;
     int n = 0, nlev = 0;
 };
@@ -345,6 +349,8 @@ constexpr int DENSE_TRI_MAX = 4096;   // dense inverse up to 134 MB per factor: 
 // (e.g. ILU(0)'s stored lower pattern for its L factor), reused as the schedule
 Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense = false,
              DBuf<int> *pre_order = nullptr, DBuf<int> *pre_lev = nullptr, int pre_nlev = 0);
+// non-parity fast mode (Ctx::tri_jacobi): the triangle M (x) I_d as k Jacobi sweeps
+Tri make_tri_jacobi(Ctx *c, const Csr &M, bool lower, bool unit, int d, int k);
 // x = T^{-1} b  (xout = xadd + x when xadd given); x/ticket are scratch of size n / 1
 void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const double *xadd,
           double *xout, cudaStream_t st = nullptr);

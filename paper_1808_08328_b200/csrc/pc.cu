@@ -396,6 +396,11 @@ void pc_destroy(dpp_pc *pc) { delete pc; }
 namespace dpp {
 static double b_spmv(const Csr &A) { return 12.0 * A.nnz + 4.0 * (A.rows + 1) + 8.0 * A.cols + 8.0 * A.rows; }
 static double b_tri(const Tri &T) {   // of the reference triangle, not of a merged form
+    if (T.jacobi) {   // non-parity fast mode: init pass + k sweeps over the (scalar) strict part
+        const double dg = T.diag.n ? 8.0 * T.strict.rows : 0.0;
+        const double sweep = 12.0 * T.strict.nnz + 4.0 * (T.strict.rows + 1) + 24.0 * T.n + dg;
+        return 16.0 * T.n + dg + T.jacobi * sweep;
+    }
     const double nz = T.nnz_alg >= 0 ? (double)T.nnz_alg : (double)T.strict.nnz;
     return 12.0 * (nz + T.n) + 4.0 * (T.n + 1) + 16.0 * T.n;
 }

@@ -21,6 +21,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdio>
+#include <type_traits>
 #include <cstdlib>
 
 #include <cooperative_groups.h>
@@ -312,10 +313,162 @@ __global__ void __launch_bounds__(128) k_trsv(int n, const int *__restrict__ ord
     }
 }
 
+// ------------------------------------------------------------------ non-parity fast mode
+// the exact substitution replaced by k Jacobi sweeps on the triangle,
+//     x_0 = D^-1 b,   x_{s+1} = D^-1 (b - S x_s)      (S strict part, D = I for unit factors)
+// -- a fixed linear operator, so GMRES stays valid, but iterates and iteration counts
+// differ from the reference's (never used unless asked for).  Every sweep is one
+// bandwidth-bound pass over S with no dependency chain.  G lanes per scalar row; the
+// Kronecker form M (x) I_d is swept on M with d interleaved components per row.
+template <int G, int D>
+__global__ void __launch_bounds__(256) k_jacobi(int rows, int d, const int *__restrict__ ptr,
+                                                const int *__restrict__ idx, const double *__restrict__ val,
+                                                const double *__restrict__ diag, const double *__restrict__ b,
+                                                const double *__restrict__ xin, double *__restrict__ xo,
+                                                const double *__restrict__ xadd, double *__restrict__ xout) {
+    pdl_wait();
+    // every lane of a warp runs the same trip count (the width-G shuffles stay full)
+    const int gl = threadIdx.x % G, gw = (threadIdx.x & 31) / G;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = warp * (32 / G); base < rows; base += nwarp * (32 / G)) {
+        const int64_t r = base + gw;
+        const bool act = r < rows;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (xin && act) {
+            const int pe = ptr[r + 1];
+            for (int p = ptr[r] + gl; p < pe; p += G) {
+                const int j = idx[p];
+                const double v = val[p];
+                const double *xj = xin + (int64_t)j * d;
+                s0 += v * xj[0];
+                if (D > 1) s1 += v * xj[1];
+                if (D > 2) s2 += v * xj[2];
+                if (D > 3) s3 += v * xj[3];
+            }
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            s0 += __shfl_xor_sync(0xffffffffu, s0, o, G);
+            if (D > 1) s1 += __shfl_xor_sync(0xffffffffu, s1, o, G);
+            if (D > 2) s2 += __shfl_xor_sync(0xffffffffu, s2, o, G);
+            if (D > 3) s3 += __shfl_xor_sync(0xffffffffu, s3, o, G);
+        }
+        if (act && gl < D) {
+            const double sq = gl == 0 ? s0 : gl == 1 ? s1 : gl == 2 ? s2 : s3;
+            const int64_t R = r * d + gl;
+            double y = b[R] - sq;
+            if (diag) y = y / diag[r];
+            xo[R] = y;
+            if (xout) xout[R] = xadd[R] + y;
+        }
+    }
+}
+
+// S' = D^-1 S (rows divided by the diagonal) and x0 = D^-1 b: the sweeps of a scalar
+// triangle are then x <- x0 - S' x, plain planned SpMVs
+__global__ void k_rowdiv(int rows, const int *__restrict__ ptr, double *val, const double *__restrict__ d) {
+    for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows;
+         r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const double dr = d[r];
+        for (int p = ptr[r] + (threadIdx.x & 31); p < ptr[r + 1]; p += 32) val[p] = val[p] / dr;
+    }
+}
+__global__ void k_vdiv(int64_t n, const double *__restrict__ b, const double *__restrict__ d, double *o) {
+    pdl_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = b[i] / d[i];
+    pdl_trigger();
+}
+
+Tri make_tri_jacobi(Ctx *c, const Csr &M, bool lower, bool unit, int d, int k) {
+    if (d < 1 || d > 4) DPP_FAIL(DPP_ERR_VALUE, "Jacobi sweeps support up to 4 interleaved components");
+    Tri T;
+    T.backward = !lower;
+    T.strict = csr_part(c, M, lower ? -1 : 1, true);
+    if (!unit) {
+        T.diag.alloc(M.rows, c->s);
+        csr_diag(c, M, T.diag.p, nullptr);
+    }
+    T.ncomp = d;
+    T.n = M.rows * d;
+    T.nnz_alg = T.strict.nnz * d;
+    T.jacobi = k;
+    T.nlev = 1;
+    T.wb.alloc(T.n, c->s);
+    if (d == 1) {
+        if (!unit) {
+            k_rowdiv<<<grid_for((int64_t)M.rows * 32, 256, c->sms, 8), 256, 0, c->s>>>(M.rows, T.strict.ptr.p,
+                                                                                      T.strict.val.p, T.diag.p);
+            launched(c);
+        }
+        spmv_plan(c, T.strict);
+        T.W.rows = 0;
+        T.wb2.alloc(T.n, c->s);
+    }
+    return T;
+}
+
+static void trsv_jacobi(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+                        cudaStream_t st) {
+    const int rows = T.strict.rows, d = T.ncomp, k = T.jacobi;
+    const double *dg = T.diag.n ? T.diag.p : nullptr;
+    // the last sweep lands in x: start in x when k is even, in the scratch when odd
+    double *buf[2] = {x, T.wb.p};
+    int cur = k % 2;
+    if (d == 1) {   // x0 = D^-1 b (b itself when unit); sweeps x <- x0 - S' x as planned SpMVs
+        const double *x0 = b;
+        if (dg) {
+            CK(launch_pdl(k_vdiv, dim3(grid_for(rows, 256, c->sms)), dim3(256), 0, st, (int64_t)rows, b, dg,
+                          T.wb2.p));
+            launched(c);
+            x0 = T.wb2.p;
+        }
+        const double *xin = x0;
+        for (int s = 0; s < k; ++s) {
+            double *xo = buf[(k - 1 - s) % 2 == 0 ? 0 : 1];
+            spmv(c, T.strict, xin, xo, x0, -1.0, st);
+            xin = xo;
+        }
+        if (k == 0 && xin != x) CK(cudaMemcpyAsync(x, xin, sizeof(double) * rows, cudaMemcpyDeviceToDevice, st));
+        if (xout) axpby_to(c, rows, xadd, 1.0, x, xout, st);
+        return;
+    }
+    const double avg = rows ? (double)T.strict.nnz / rows : 0.0;
+    auto sweep = [&](const double *xin, double *xo, bool last) {
+        auto go = [&](auto kern, int G) {
+            const int64_t thr = ((int64_t)rows * G + 255) / 256 * 256;
+            const int grid = (int)std::min<int64_t>(thr / 256, (int64_t)c->sms * 8);
+            CK(launch_pdl(kern, dim3(grid), dim3(256), 0, st, rows, d, (const int *)T.strict.ptr.p,
+                          (const int *)T.strict.idx.p, (const double *)T.strict.val.p, dg, b, xin, xo,
+                          last ? xadd : (const double *)nullptr, last ? xout : (double *)nullptr));
+            launched(c);
+        };
+        auto pick = [&](auto dtag) {
+            constexpr int DD = decltype(dtag)::value;
+            if (avg > 24) go(k_jacobi<32, DD>, 32);
+            else if (avg > 10) go(k_jacobi<16, DD>, 16);
+            else go(k_jacobi<8, DD>, 8);
+        };
+        if (d == 2) pick(std::integral_constant<int, 2>{});
+        else if (d == 3) pick(std::integral_constant<int, 3>{});
+        else pick(std::integral_constant<int, 4>{});
+    };
+    sweep(nullptr, buf[cur], k == 0);
+    for (int s = 0; s < k; ++s) {
+        sweep(buf[cur], buf[cur ^ 1], s == k - 1);
+        cur ^= 1;
+    }
+}
+
 void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const double *xadd,
           double *xout, cudaStream_t st) {
     st = st ? st : c->s;
     if (T.n == 0) return;
+    if (T.jacobi) {
+        trsv_jacobi(c, T, b, x, xadd, xout, st);
+        return;
+    }
     if (T.W.rows && !T.pu) {   // level-merged form: sweep on W b (the push sweep folds W in)
         spmv(c, T.W, b, T.wb.p, nullptr, 1.0, st);
         b = T.wb.p;
@@ -516,6 +669,9 @@ static int merge_factor() {
 
 Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf<int> *pre_order,
              DBuf<int> *pre_lev, int pre_nlev) {
+    // non-parity fast mode: Jacobi sweeps (small dense coarse levels stay exact)
+    if (c->tri_jacobi > 0 && !(allow_dense && A.rows <= DENSE_TRI_MAX))
+        return make_tri_jacobi(c, A, lower, unit, 1, c->tri_jacobi);
     Tri T;
     T.n = A.rows;
     T.backward = !lower;
@@ -861,6 +1017,14 @@ std::unique_ptr<Ilu> ilu0(Ctx *c, const Csr &A) {
         k_ilu_kron_expand<<<grid_for(n, 256, c->sms), 256, 0, c->s>>>(n, d, A.ptr.p, A.idx.p, M.ptr.p, M.idx.p,
                                                                       M.val.p, f->LU.val.p);
         launched(c);
+        if (c->tri_jacobi > 0) {
+            f->L = make_tri_jacobi(c, M, true, true, d, c->tri_jacobi);
+            f->U = make_tri_jacobi(c, M, false, false, d, c->tri_jacobi);
+            f->y.alloc(n, c->s);
+            f->tmp.alloc(n, c->s);
+            f->ticket.alloc(2, c->s);
+            return f;
+        }
         bool okl = false, oku = false;
         f->L = make_tri_kron(c, M, true, true, d, &order, &lev, nlev, okl);
         if (okl) f->U = make_tri_kron(c, M, false, false, d, nullptr, nullptr, 0, oku);
