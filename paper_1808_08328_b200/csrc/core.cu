@@ -137,6 +137,73 @@ __global__ void k_sell_fill(int rows, const int *__restrict__ ptr, const int *__
     }
 }
 
+// 16-bit column codes: a slice's columns fall in at most 4 windows of 2^14 columns
+// (mesh operators: the node's neighbourhood in each field block the row couples to), so
+// each entry stores a 2-bit window id and a 14-bit offset -- 10 bytes per entry instead
+// of 12.  Windows start at the smallest column not yet covered (greedy); a slice that
+// needs a fifth window fails the whole matrix back to 32-bit columns.
+constexpr int SELL_WIN = 1 << 14;
+__global__ void k_sell_bases(int rows, const int *__restrict__ ptr, const int *__restrict__ idx, int nsl,
+                             int4 *base, int *fail) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nsl;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t r = k * 32 + lane;
+        const int a = r < rows ? ptr[r] : 0, e = r < rows ? ptr[r + 1] : 0;
+        int b[4] = {0, 0, 0, 0}, nb = 0;
+        auto covered = [&](int c) {
+            bool cv = false;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) cv |= s < nb && c >= b[s] && c - b[s] < SELL_WIN;
+            return cv;
+        };
+        for (int s = 0; s < 4; ++s) {
+            int m = INT_MAX;
+            for (int p = a; p < e; ++p) {
+                const int c = idx[p];
+                if (!covered(c)) m = min(m, c);
+            }
+            for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (m == INT_MAX) break;
+            b[nb++] = m;
+        }
+        bool bad = false;
+        for (int p = a; p < e; ++p) bad |= !covered(idx[p]);
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(fail, 1);
+        if (lane == 0) base[k] = make_int4(b[0], nb > 1 ? b[1] : b[0], nb > 2 ? b[2] : b[0], nb > 3 ? b[3] : b[0]);
+    }
+}
+__global__ void k_sell_fill16(int rows, const int *__restrict__ ptr, const int *__restrict__ idx,
+                              const double *__restrict__ val, int nsl, const int *__restrict__ sp,
+                              const int4 *__restrict__ base, uint16_t *sc, double *sv) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < nsl;
+         k += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t r = k * 32 + lane;
+        const int a = r < rows ? ptr[r] : 0, len = r < rows ? ptr[r + 1] - a : 0;
+        const int w = (sp[k + 1] - sp[k]) >> 5;
+        const int4 B = base[k];
+        const int bs[4] = {B.x, B.y, B.z, B.w};
+        uint16_t last = 0;   // padding: window 0, offset 0 (a valid column: the slice's smallest)
+        for (int t = 0; t < w; ++t) {
+            const int64_t o = sp[k] + (int64_t)t * 32 + lane;
+            if (t < len) {
+                const int c = idx[a + t];
+                int sel = 3;
+#pragma unroll
+                for (int s = 3; s >= 0; --s)
+                    if (c >= bs[s] && c - bs[s] < SELL_WIN) sel = s;
+                last = (uint16_t)((sel << 14) | (c - bs[sel]));
+                sc[o] = last;
+                sv[o] = val[a + t];
+            } else {
+                sc[o] = last;
+                sv[o] = 0.0;
+            }
+        }
+    }
+}
+
 // SELL-32 is used when padding stays under this factor of the stored entries
 constexpr double SELL_MAX_FILL = 1.25;
 // DPP_SPMV=row|stream|sell (default sell): kernel selection for A/B measurements
@@ -149,9 +216,15 @@ static int spmv_mode() {
     return m;
 }
 
+// DPP_SELL16=0 keeps 32-bit SELL columns (A/B); read per plan
+static bool sell16_on() {
+    const char *e = std::getenv("DPP_SELL16");
+    return !(e && *e == '0');
+}
+
 void spmv_plan(Ctx *c, Csr &A, int kind) {
     A.rb.release(); A.nrb = 0;
-    A.sp.release(); A.sc.release(); A.sv.release(); A.nsl = 0;
+    A.sp.release(); A.sc.release(); A.sv.release(); A.sc16.release(); A.sbase.release(); A.nsl = 0;
     if (kind == 3) kind = spmv_mode() == 0 ? 0 : spmv_mode() == 1 ? 1 : 3;
     if (A.rows == 0 || A.nnz == 0 || kind == 0) return;
     if (kind >= 2) {
@@ -164,9 +237,25 @@ void spmv_plan(Ctx *c, Csr &A, int kind) {
         const int64_t tot = counts_to_ptr(c, wcnt.p, nsl, sp);
         if (kind == 2 || (double)tot <= SELL_MAX_FILL * (double)A.nnz) {
             A.sp = std::move(sp);
-            A.sc.alloc((size_t)tot, c->s);
             A.sv.alloc((size_t)tot, c->s);
-            k_sell_fill<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, nsl, A.sp.p, A.sc.p, A.sv.p);
+            bool narrow = sell16_on();
+            if (narrow) {
+                A.sbase.alloc((size_t)nsl, c->s);
+                DBuf<int> fail(1, c->s);
+                CK(cudaMemsetAsync(fail.p, 0, sizeof(int), c->s));
+                k_sell_bases<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, nsl, A.sbase.p, fail.p);
+                launched(c);
+                narrow = fail.to_host()[0] == 0;
+            }
+            if (narrow) {
+                A.sc16.alloc((size_t)tot, c->s);
+                k_sell_fill16<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, nsl, A.sp.p, A.sbase.p,
+                                                     A.sc16.p, A.sv.p);
+            } else {
+                A.sbase.release();
+                A.sc.alloc((size_t)tot, c->s);
+                k_sell_fill<<<grid, 256, 0, c->s>>>(A.rows, A.ptr.p, A.idx.p, A.val.p, nsl, A.sp.p, A.sc.p, A.sv.p);
+            }
             launched(c);
             A.nsl = nsl;
             return;
@@ -237,29 +326,47 @@ __global__ void __launch_bounds__(SB_THREADS) k_spmv_stream(const int *__restric
 // sequentially; the T partial sums are added in q order (T = 1: one sequential sum
 // per row in column order).  Up to SELL_U columns of a lane are in flight at once.
 constexpr int SELL_U = 8;
-template <int T>
+template <int T, bool C16>
 __global__ void __launch_bounds__(256) k_spmv_sell(int rows, int nsl, const int *__restrict__ sp,
-                                                   const int *__restrict__ sc, const double *__restrict__ sv,
+                                                   const int *__restrict__ sc, const uint16_t *__restrict__ sc16,
+                                                   const int4 *__restrict__ sbase, const double *__restrict__ sv,
                                                    const double *__restrict__ x, double *__restrict__ y,
                                                    const double *__restrict__ b, double alpha) {
     constexpr int SPB = 8 / T;   // slices per CTA
     __shared__ double part[T > 1 ? 8 : 1][32];
+    __shared__ int sbw[8][4];    // 16-bit codes: the slice's column windows, per warp
     pdl_wait();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = warp % T;
     const int64_t k = (int64_t)blockIdx.x * SPB + warp / T;
     double sum = 0.0;
     if (k < nsl) {
         const int o0 = __ldg(sp + k), w = (__ldg(sp + k + 1) - o0) >> 5;
+        if (C16 && lane < 4) sbw[warp][lane] = __ldg(reinterpret_cast<const int *>(sbase + k) + lane);
+        if (C16) __syncwarp();
         const int *J = sc + o0 + lane;
+        const uint16_t *J16 = sc16 + o0 + lane;
         const double *V = sv + o0 + lane;
         for (int t = q; t < w; t += T * SELL_U) {
             double v[SELL_U], xv[SELL_U];
             int j[SELL_U];
+            if (C16) {   // all code loads in flight first, then the decode (window base from smem)
+                unsigned cd[SELL_U];
 #pragma unroll
-            for (int u = 0; u < SELL_U; ++u) {
-                const int tt = t + u * T;
-                v[u] = tt < w ? __ldg(V + tt * 32) : 0.0;
-                j[u] = tt < w ? __ldg(J + tt * 32) : -1;
+                for (int u = 0; u < SELL_U; ++u) {
+                    const int tt = t + u * T;
+                    v[u] = tt < w ? __ldg(V + tt * 32) : 0.0;
+                    cd[u] = tt < w ? (unsigned)__ldg(J16 + tt * 32) : 0xffffffffu;
+                }
+#pragma unroll
+                for (int u = 0; u < SELL_U; ++u)
+                    j[u] = cd[u] == 0xffffffffu ? -1 : sbw[warp][cd[u] >> 14] + (int)(cd[u] & 0x3fffu);
+            } else {
+#pragma unroll
+                for (int u = 0; u < SELL_U; ++u) {
+                    const int tt = t + u * T;
+                    v[u] = tt < w ? __ldg(V + tt * 32) : 0.0;
+                    j[u] = tt < w ? __ldg(J + tt * 32) : -1;
+                }
             }
 #pragma unroll
             for (int u = 0; u < SELL_U; ++u) xv[u] = j[u] >= 0 ? __ldg(x + j[u]) : 0.0;
@@ -287,16 +394,29 @@ void spmv(Ctx *c, const Csr &A, const double *x, double *y, const double *b, dou
     if (A.nsl > 0) {
         // warps per slice: about SELL_U columns per lane (one round of loads per row)
         static const int tenv = [] { const char *e = std::getenv("DPP_SELL_T"); return e && *e ? atoi(e) : 0; }();
-        const int wavg = (int)(A.sc.n / ((size_t)A.nsl * 32));
-        const int T = tenv ? tenv : wavg <= SELL_U ? 1 : wavg <= 2 * SELL_U ? 2 : wavg <= 4 * SELL_U ? 4 : 8;
         auto go = [&](auto kern, int spb) {
             CK(launch_pdl(kern, dim3((A.nsl + spb - 1) / spb), dim3(256), 0, st, A.rows, A.nsl, (const int *)A.sp.p,
-                          (const int *)A.sc.p, (const double *)A.sv.p, x, y, b, alpha));
+                          (const int *)A.sc.p, (const uint16_t *)A.sc16.p, (const int4 *)A.sbase.p,
+                          (const double *)A.sv.p, x, y, b, alpha));
         };
-        if (T == 1) go(k_spmv_sell<1>, 8);
-        else if (T == 2) go(k_spmv_sell<2>, 4);
-        else if (T == 4) go(k_spmv_sell<4>, 2);
-        else go(k_spmv_sell<8>, 1);
+        const size_t ent = A.sc16.n ? A.sc16.n : A.sc.n;
+        const int wavg = (int)(ent / ((size_t)A.nsl * 32));
+        // warps per slice: about rpw rounds of SELL_U columns per warp (DPP_SELL_RPW; 3 measured
+        // best on C2's K with 16-bit codes: 59.3 us against 69.8 at 1)
+        static const int rpw = [] { const char *e = std::getenv("DPP_SELL_RPW"); return e && *e ? atoi(e) : 3; }();
+        const int cpw = SELL_U * rpw;
+        const int T = tenv ? tenv : wavg <= cpw ? 1 : wavg <= 2 * cpw ? 2 : wavg <= 4 * cpw ? 4 : 8;
+        if (A.sc16.n) {
+            if (T == 1) go(k_spmv_sell<1, true>, 8);
+            else if (T == 2) go(k_spmv_sell<2, true>, 4);
+            else if (T == 4) go(k_spmv_sell<4, true>, 2);
+            else go(k_spmv_sell<8, true>, 1);
+        } else {
+            if (T == 1) go(k_spmv_sell<1, false>, 8);
+            else if (T == 2) go(k_spmv_sell<2, false>, 4);
+            else if (T == 4) go(k_spmv_sell<4, false>, 2);
+            else go(k_spmv_sell<8, false>, 1);
+        }
         launched(c);
         return;
     }

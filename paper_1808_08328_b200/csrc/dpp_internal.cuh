@@ -192,12 +192,14 @@ struct Csr {
     DBuf<int> sp;         // SELL-32: slice k = rows [32k, 32k+32), entries sp[k] .. sp[k+1]
     DBuf<int> sc;         //   column of (slice k, column t, lane l) at sp[k] + 32 t + l
     DBuf<double> sv;      //   value (padding: 0.0 with a valid column)
+    DBuf<uint16_t> sc16;  //   or 16-bit column codes (sc then empty): sel = code >> 14,
+    DBuf<int4> sbase;     //   column = sbase[k][sel] + (code & 0x3fff)
     int nsl = 0;
     DBuf<int> rb;         // CSR-stream row blocks: block k = rows starting in [k*T, (k+1)*T)
     int nrb = 0;
     void alloc(int r, int c, int64_t z, cudaStream_t s) {
         rb.release(); nrb = 0;
-        sp.release(); sc.release(); sv.release(); nsl = 0;
+        sp.release(); sc.release(); sv.release(); sc16.release(); sbase.release(); nsl = 0;
         rows = r; cols = c; nnz = z;
         ptr.alloc((size_t)r + 1, s);
         idx.alloc((size_t)z, s);

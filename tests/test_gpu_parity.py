@@ -88,16 +88,26 @@ def _spmv_cases(rng):
     # a CG-VMS K (explicit zeros, the structured gathers SELL-32 is built for)
     bs, _ = systems("cgvms", 3, "tet", 3)
     yield "K", dpp.monolithic_view(bs)[0]
+    # 16-bit SELL codes: four 2^14-column windows per slice exactly at their edges (coded),
+    # and a fifth window (the whole matrix falls back to 32-bit columns)
+    for name, starts in (("windows4", [0, 20000, 40000, 60000]), ("windows5", [0, 20000, 40000, 60000, 90000])):
+        cols = np.concatenate([[s0, s0 + 16383] for s0 in starts])
+        nr = 70
+        rr = np.repeat(np.arange(nr), cols.size)
+        cc = np.tile(cols, nr) + np.repeat(np.arange(nr) % 3, cols.size) * 0
+        yield name, sp.csr_matrix((rng.standard_normal(rr.size), (rr, cc)), shape=(nr, 120000))
 
 
+@pytest.mark.parametrize("sell16", ["1", "0"])
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
-def test_spmv_plans_match_scipy(kind, rng):
+def test_spmv_plans_match_scipy(kind, sell16, rng, monkeypatch):
     """Every SpMV kernel (row / CSR-stream / SELL-32 / auto) against scipy's csr_matvec
     (linalg.py:27-32): 1e-14 relative per row; SELL-32 with one warp per slice sums each
     row sequentially in column order and is bitwise equal."""
     import ctypes as C
     from paper_1808_08328_b200 import _native as N
     from paper_1808_08328_b200.device import DeviceCsr
+    monkeypatch.setenv("DPP_SELL16", sell16)   # 16-bit SELL column codes (default) / 32-bit
     for name, A in _spmv_cases(rng):
         A = sp.csr_matrix(A)
         A.sort_indices()
