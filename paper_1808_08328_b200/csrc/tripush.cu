@@ -845,6 +845,202 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
     }
 }
 
+
+// ----------------------------------------------------------------- warp-stream dataflow variant
+// Lane-per-row dataflow sweep (DPP_PU_MODE=ws).  Same partition and halo / push tables as the
+// other kernels of this file, but:
+//   * a CTA's rows of one level are cut into chunks of <= 32 rows, and chunk g of the CTA (in
+//     level order) belongs to warp g % nw -- consecutive levels sit on different warps;
+//   * lane l of the warp owns row l of the chunk and walks its entries four columns at a time
+//     (SELL layout: column t of the chunk is w consecutive (code, value) pairs), the entries of
+//     a row sorted by source level and right-aligned, so every lane meets its level l-1 sources
+//     in the chunk's last group;
+//   * readiness is the x slot itself (NaN sentinel until the value lands: own rows by a
+//     volatile shared store, remote rows by a plain cluster store into the halo), polled
+//     warp-uniformly -- the lanes of a chunk never depend on one another;
+//   * every warp streams its own chunks through a private ring of TMA slots that it refills
+//     itself (pieces of <= slot bytes, sizes in a per-warp offset table), so no warp waits for
+//     another one's ring and there is no CTA-wide step;
+//   * b is read and x written straight from / to global memory by the owning lane (loads issued
+//     at the chunk's first piece, far ahead of their use).
+// A level therefore costs one poll hit + one group of FMAs + the row's store on the critical
+// path.  Arithmetic: four partial sums per row (exact-arithmetic regrouping of the dot product).
+//
+// piece (16-byte aligned): int4 {groups, w, flags (1 first piece of a chunk, 2 last), np} |
+//   first: u16 local row[w] | groups x { u16 code[4][w] | f64 val[4][w] } |
+//   last: f64 1/diag[w] | int (p0 << 4 | npush)[w] | int push[np]
+constexpr int WS_NS_MAX = 8;
+__host__ __device__ inline long long ws_group_bytes(int w) { return p16(8LL * w) + 32LL * w; }
+__host__ __device__ inline long long ws_head_bytes(int w) { return 16 + p16(2LL * w); }
+__host__ __device__ inline long long ws_tail_bytes(int w, int np) { return p16(8LL * w) + p16(4LL * w) + p16(4LL * np); }
+__host__ __device__ inline size_t ws_fixed(int chunk, int hmax, int nw, int ns) {
+    return (size_t)((p16(8LL * nw * ns) + p16(8LL * chunk) + p16(8LL * hmax) + 64 + 127) & ~127LL);
+}
+struct WsWalk {   // the pieces of one chunk (w rows, ngr column groups, np push entries), greedy in slot bytes
+    int w, ngr, np, slot;
+    long long off, bytes;   // the current piece: offset from the chunk's start, size
+    int g0, ng, flags;
+    __host__ __device__ void place(bool fst) {
+        long long sz = fst ? ws_head_bytes(w) : 16;
+        const long long gb = ws_group_bytes(w);
+        ng = 0;
+        while (g0 + ng < ngr && sz + gb <= slot) { sz += gb; ++ng; }
+        flags = fst ? 1 : 0;
+        if (g0 + ng == ngr && sz + ws_tail_bytes(w, np) <= slot) { flags |= 2; sz += ws_tail_bytes(w, np); }
+        bytes = sz;
+    }
+    __host__ __device__ void first() { off = 0; g0 = 0; place(true); }
+    __host__ __device__ bool next() {
+        if (flags & 2) return false;
+        off += bytes; g0 += ng;
+        place(false);
+        return true;
+    }
+    __host__ __device__ long long data() const { return off + ((flags & 1) ? ws_head_bytes(w) : 16); }   // first group
+};
+
+__global__ void __launch_bounds__(512, 1)
+    k_trsv_ws(int n, int ncomp, int chunk, int hmax, int slot, int ns, const unsigned char *__restrict__ blocks,
+              const long long *__restrict__ poff, const int *__restrict__ pidx, const double *__restrict__ b,
+              double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout, int nap) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long *mb = reinterpret_cast<unsigned long long *>(smem) + wid * ns;
+    const int chunkp = pu_chunkp(chunk);
+    double *xh = reinterpret_cast<double *>(smem + p16(8LL * nw * ns));
+    unsigned *peer = reinterpret_cast<unsigned *>(xh + chunkp + p16(8LL * hmax) / 8);
+    unsigned char *ring = smem + ws_fixed(chunk, hmax, nw, ns) + (size_t)wid * ns * slot;
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
+    const int comp = blockIdx.x / C;
+    const int base = k * chunk, mine = max(0, min(chunk, n - base));
+    const int pi0 = pidx[k * nw + wid], NP = pidx[k * nw + wid + 1] - pi0 - 1;
+    const long long *po = poff + pi0;
+    auto issue = [&](int i, long long o0, long long o1) {
+        const int sl = i % ns;
+        const unsigned bytes = (unsigned)(o1 - o0);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&mb[sl])), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su32(ring + (size_t)sl * slot)), "l"(blocks + o0), "r"(bytes), "r"(su32(&mb[sl]))
+                     : "memory");
+    };
+    // the plan is static: the ring's first pieces are in flight before the predecessor ends
+    if (lane == 0) {
+        for (int s = 0; s < ns; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&mb[s])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int i = 0; i < min(ns, NP); ++i) issue(i, po[i], po[i + 1]);
+    }
+    if (threadIdx.x < C) peer[threadIdx.x] = mapa_u32(su32(xh + chunkp), threadIdx.x);
+    const double sent = __longlong_as_double((long long)PU_SENT);
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = sent;
+    for (int i = threadIdx.x; i < hmax - 1; i += blockDim.x) xh[chunkp + i] = sent;
+    if (threadIdx.x == 0) xh[chunkp + hmax - 1] = 0.0;   // the padding entries' source
+    __syncthreads();
+    // every CTA's slots hold the sentinel before anyone pushes
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    pdl_wait();   // b is the previous kernel's output
+    const unsigned xh_s = su32(xh);
+    const int zero_code = chunkp + hmax - 1;
+    int row = 0;
+    size_t g = 0;
+    double bq = 0.0, xa = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int pi = 0; pi < NP; ++pi) {
+        const int sl = pi % ns;
+        long long n0 = 0, n1 = 0;   // the refill's extent, fetched before it is needed
+        if (pi + ns < NP) { n0 = po[pi + ns]; n1 = po[pi + ns + 1]; }
+        mwait(su32(&mb[sl]), (unsigned)((pi / ns) & 1));
+        const unsigned char *pc = ring + (size_t)sl * slot;
+        const int4 hd = *reinterpret_cast<const int4 *>(pc);
+        const int ng = hd.x, w = hd.y, fl = hd.z;
+        DPP_DCHECK(w >= 1 && w <= 32 && ng >= 0 && hd.w >= 0);
+        const bool act = lane < w;
+        int o = 16;
+        if (fl & 1) {
+            const unsigned short *rows = reinterpret_cast<const unsigned short *>(pc + 16);
+            row = act ? rows[lane] : 0;
+            DPP_DCHECK(row < mine);
+            g = (size_t)(base + row) * ncomp + comp;
+            bq = act ? b[g] : 0.0;
+            xa = (act && xout) ? xadd[g] : 0.0;
+            s0 = s1 = s2 = s3 = 0.0;
+            o += (int)p16(2LL * w);
+        }
+        const int cb = (int)p16(8LL * w), gb = cb + 32 * w;
+        DPP_DCHECK(o + (long long)ng * gb + ((fl & 2) ? ws_tail_bytes(w, hd.w) : 0) <= slot);
+        double dq = 0.0;
+        int pinf = 0;
+        const int *pl = nullptr;
+        if (fl & 2) {
+            const unsigned char *t = pc + o + ng * gb;
+            dq = act ? reinterpret_cast<const double *>(t)[lane] : 0.0;
+            pinf = act ? reinterpret_cast<const int *>(t + cb)[lane] : 0;
+            pl = reinterpret_cast<const int *>(t + cb + p16(4LL * w));
+        }
+        int cd[4];
+        double v[4];
+#define WS_LOAD_CV(gi)                                                                                  \
+    {                                                                                                   \
+        const unsigned short *code_ = reinterpret_cast<const unsigned short *>(pc + o + (gi) * gb);     \
+        const double *val_ = reinterpret_cast<const double *>(pc + o + (gi) * gb + cb);                 \
+        _Pragma("unroll") for (int u = 0; u < 4; ++u) {                                                 \
+            cd[u] = act ? (int)code_[u * w + lane] : zero_code;                                         \
+            v[u] = act ? val_[u * w + lane] : 0.0;                                                      \
+        }                                                                                               \
+    }
+        if (ng) WS_LOAD_CV(0);
+        for (int gi = 0; gi < ng; ++gi) {
+            unsigned a[4];
+            double cv[4], xv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                DPP_DCHECK(cd[u] >= 0 && (cd[u] < mine || (cd[u] >= chunkp && cd[u] < chunkp + hmax)));
+                a[u] = xh_s + 8u * (unsigned)cd[u];
+                cv[u] = v[u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) xv[u] = ld_vol_shared(a[u]);
+            if (gi + 1 < ng) WS_LOAD_CV(gi + 1);
+            long long spins = 0;
+            while (true) {
+                bool pend = false;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) pend |= __double_as_longlong(xv[u]) == (long long)PU_SENT;
+                if (!__any_sync(0xffffffffu, pend)) break;
+                // far from the chunk's last groups the missing sources are levels away
+                if (nap && (!(fl & 2) || gi + 2 < ng)) __nanosleep(nap);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (__double_as_longlong(xv[u]) == (long long)PU_SENT) xv[u] = ld_vol_shared(a[u]);
+                if (++spins > (1ll << 26)) __trap();
+            }
+            s0 = fma(cv[0], xv[0], s0);
+            s1 = fma(cv[1], xv[1], s1);
+            s2 = fma(cv[2], xv[2], s2);
+            s3 = fma(cv[3], xv[3], s3);
+        }
+#undef WS_LOAD_CV
+        if ((fl & 2) && act) {
+            double xr = (bq - ((s0 + s1) + (s2 + s3))) * dq;   // dq = 1/t_ii
+            if (__double_as_longlong(xr) == (long long)PU_SENT) xr = __longlong_as_double(0x7ff8000000000000ll);
+            st_vol_shared(xh_s + 8u * (unsigned)row, xr);
+            const int p0 = pinf >> 4, pn = pinf & 15;
+            for (int u = 0; u < pn; ++u) {
+                const int pe = pl[p0 + u];
+                DPP_DCHECK((int)((unsigned)pe >> 28) < C && (int)((unsigned)pe & 0x0fffffffu) < hmax - 1);
+                st_remote(peer[(unsigned)pe >> 28] + 8u * ((unsigned)pe & 0x0fffffffu), xr);
+            }
+            x[g] = xr;
+            if (xout) xout[g] = xa + xr;
+        }
+        __syncwarp();
+        if (lane == 0 && pi + ns < NP) issue(pi + ns, n0, n1);
+    }
+    pdl_trigger();
+    // a CTA's shared memory must outlive the pushes aimed at it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ----------------------------------------------------------------- setup
 __global__ void k_pu_keys(int n, int chunk, int L, const int *lev, int *key, int *rows) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
@@ -1077,6 +1273,72 @@ __global__ void k_lv_fill(int n, int chunk, int chunkp, int zero_code, int np_, 
     }
 }
 
+
+// ---- warp-stream format (k_trsv_ws): one thread per sorted row writes its lane of the chunk
+// ctab[gc] = {first sorted row, rows, column groups, push entries}, cbase[gc] = the chunk's bytes
+__device__ inline long long ws_group_off(int w, int ngr, int np, int slot, int gi) {   // from the chunk's start
+    WsWalk wk{w, ngr, np, slot};
+    wk.first();
+    while (gi >= wk.g0 + wk.ng) wk.next();
+    return wk.data() + (long long)(gi - wk.g0) * ws_group_bytes(w);
+}
+__global__ void k_ws_fill(int n, int chunk, int chunkp, int zero_code, int slot, int nchunks, const int4 *ctab,
+                          const long long *cbase, const int *perm, const int *rpp, const int *ptr, const int *idx,
+                          const double *val, const double *diag, const int *lev, const unsigned long long *h,
+                          const int *hstart, const int *pptr, const unsigned long long *k2s, const int *slots,
+                          unsigned char *blocks) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        int lo = 0, hi = nchunks;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (ctab[mid].x <= q) lo = mid; else hi = mid;
+        }
+        const int4 ct = ctab[lo];
+        const int q0 = ct.x, w = ct.y, ngr = ct.z, np = ct.w, lane = q - q0;
+        unsigned char *B = blocks + cbase[lo];
+        const int r = perm[q], owner = r / chunk;
+        const int a0 = ptr[r], len = ptr[r + 1] - a0, pad = 4 * ngr - len;
+        const int hs = hstart[owner], he = hstart[owner + 1];
+        const long long cb = p16(8LL * w);
+        // pieces: headers (lane 0), local rows (first piece), 1/diag + push list (last piece)
+        WsWalk wk{w, ngr, np, slot};
+        wk.first();
+        while (true) {
+            unsigned char *pc = B + wk.off;
+            if (lane == 0) *reinterpret_cast<int4 *>(pc) = make_int4(wk.ng, w, wk.flags, np);
+            if (wk.flags & 1) reinterpret_cast<unsigned short *>(pc + 16)[lane] = (unsigned short)(r - owner * chunk);
+            if (wk.flags & 2) {
+                unsigned char *t = B + wk.data() + (long long)wk.ng * ws_group_bytes(w);
+                const int p0 = rpp[q] - rpp[q0], pn = rpp[q + 1] - rpp[q];
+                reinterpret_cast<double *>(t)[lane] = diag ? 1.0 / diag[r] : 1.0;
+                reinterpret_cast<int *>(t + cb)[lane] = (p0 << 4) | pn;
+                int *pl = reinterpret_cast<int *>(t + cb + p16(4LL * w));
+                int u = p0;
+                for (int tt = pptr[r]; tt < pptr[r + 1]; ++tt, ++u)
+                    pl[u] = (int)(((unsigned)(k2s[tt] & 15u) << 28) | (unsigned)slots[tt]);
+                break;
+            }
+            wk.next();
+        }
+        // entries by source level (ties in storage order), right-aligned in the chunk's columns
+        auto put = [&](int col, int code, double vv) {
+            unsigned char *gp = B + ws_group_off(w, ngr, np, slot, col >> 2);
+            reinterpret_cast<unsigned short *>(gp)[(col & 3) * w + lane] = (unsigned short)code;
+            reinterpret_cast<double *>(gp + cb)[(col & 3) * w + lane] = vv;
+        };
+        for (int col = 0; col < pad; ++col) put(col, zero_code, 0.0);
+        for (int p = a0; p < a0 + len; ++p) {
+            const int j = idx[p], lj = lev[j];
+            int rank = 0;
+            for (int t = a0; t < a0 + len; ++t) {
+                const int lt = lev[idx[t]];
+                rank += (lt < lj) || (lt == lj && t < p);
+            }
+            put(pad + rank, pu_code(j, owner, chunk, chunkp, h, hs, he), val[p]);
+        }
+    }
+}
+
 // sweep kernel: 1 dataflow (default), 0 level-mbarrier (DPP_PU_MODE=lvl; own block format),
 // 2 level-synchronous push (DPP_PU_MODE=push or DPP_PU_FLOW=0)
 int pu_mode() {
@@ -1086,6 +1348,7 @@ int pu_mode() {
         if (f && *f == '0') return 2;
         if (e && !std::strcmp(e, "lvl")) return 0;
         if (e && !std::strcmp(e, "push")) return 2;
+        if (e && !std::strcmp(e, "ws")) return 3;
         return 1;
     }();
     return mode;
@@ -1188,9 +1451,77 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     auto part_bytes = [&](int q0, int q1) {
         return pu_block_bytes(q1 - q0, (long long)hr[q1] - hr[q0], (long long)hp[q1] - hp[q0]);
     };
-    const int fmt = pu_mode() == 0 ? 1 : 0;
-    if (fmt == 1) ++hmax;   // one zero slot after the halo: the padding entries' source
-    if (fmt == 1 && pu_chunkp(chunk) + hmax >= (1 << 16)) return false;   // 16-bit column codes
+    const int fmt = pu_mode() == 0 ? 1 : (pu_mode() == 3 && !T.W.rows) ? 2 : 0;
+    if (fmt) ++hmax;   // one zero slot after the halo: the padding entries' source
+    if (fmt && pu_chunkp(chunk) + hmax >= (1 << 16)) return false;   // 16-bit column codes
+    if (fmt == 2) {   // warp streams (k_trsv_ws)
+        static const int nw_env = [] { const char *e = std::getenv("DPP_WS_WARPS"); return e ? std::atoi(e) : 8; }();
+        static const int ns_env = [] { const char *e = std::getenv("DPP_WS_SLOTS"); return e ? std::atoi(e) : 3; }();
+        const int NW = std::max(1, std::min(16, nw_env)), NS = std::max(2, std::min(WS_NS_MAX, ns_env));
+        const size_t fixed = ws_fixed(chunk, hmax, NW, NS);
+        if (fixed + (size_t)NW * NS * 2048 > PU_SMEM_LIMIT) return false;
+        const int slot = (int)(((PU_SMEM_LIMIT - fixed) / ((size_t)NW * NS)) & ~(size_t)127);
+        // chunks: the rows of a (CTA, level) cut evenly into ceil(rows / 32) chunks
+        std::vector<int4> ctab;
+        std::vector<int> cstart(C + 1, 0);
+        for (int d = 0; d < C; ++d) {
+            cstart[d] = (int)ctab.size();
+            for (int l = 0; l < L; ++l) {
+                const int a0 = hlp[d * L + l], nr = hlp[d * L + l + 1] - a0;
+                const int nch = (nr + 31) / 32;
+                for (int cc = 0; cc < nch; ++cc) {
+                    const int q0 = a0 + (int)((long long)nr * cc / nch), q1 = a0 + (int)((long long)nr * (cc + 1) / nch);
+                    int mxl = 0;
+                    for (int q = q0; q < q1; ++q) mxl = std::max(mxl, hr[q + 1] - hr[q]);
+                    const int w = q1 - q0, ngr = (mxl + 3) / 4, np = hp[q1] - hp[q0];
+                    if (16 + ws_group_bytes(w) > slot || 16 + ws_tail_bytes(w, np) > slot || np >= (1 << 27)) return false;
+                    ctab.push_back(make_int4(q0, w, ngr, np));
+                }
+            }
+        }
+        cstart[C] = (int)ctab.size();
+        const int nchunks = (int)ctab.size();
+        if (nchunks == 0) return false;
+        // streams: chunk g of CTA d belongs to warp g % NW; a stream's pieces are contiguous
+        std::vector<long long> cbase(nchunks), poffs;
+        std::vector<int> pidx((size_t)C * NW + 1, 0);
+        long long cur = 0;
+        for (int d = 0; d < C; ++d)
+            for (int wv = 0; wv < NW; ++wv) {
+                pidx[(size_t)d * NW + wv] = (int)poffs.size();
+                for (int gc = cstart[d] + wv; gc < cstart[d + 1]; gc += NW) {
+                    cbase[gc] = cur;
+                    WsWalk wk{ctab[gc].y, ctab[gc].z, ctab[gc].w, slot};
+                    wk.first();
+                    do poffs.push_back(cur + wk.off); while (wk.next());
+                    cur += wk.off + wk.bytes;
+                }
+                poffs.push_back(cur);
+            }
+        pidx[(size_t)C * NW] = (int)poffs.size();
+        P->C = C; P->chunk = chunk; P->L = L; P->hmax = hmax; P->smax = 0;
+        P->stage = slot; P->nst = NS; P->threads = 32 * NW; P->fmt = 2; P->G = 1; P->widest = 1;
+        P->blocks.alloc((size_t)std::max<long long>(cur, 16), c->s);
+        P->boff.alloc(poffs.size(), c->s);
+        P->boff.upload(poffs.data(), poffs.size());
+        P->sstart.alloc(pidx.size(), c->s);
+        P->sstart.upload(pidx.data(), pidx.size());
+        DBuf<int4> dct(ctab.size(), c->s);
+        DBuf<long long> dcb(cbase.size(), c->s);
+        dct.upload(ctab.data(), ctab.size());
+        dcb.upload(cbase.data(), cbase.size());
+        k_ws_fill<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, chunk, pu_chunkp(chunk), pu_chunkp(chunk) + hmax - 1, slot,
+                                                              nchunks, dct.p, dcb.p, perm.p, rpp.p, S.ptr.p, S.idx.p,
+                                                              S.val.p, T.diag.n ? T.diag.p : nullptr, lev.p, H.p,
+                                                              hstart.p, pptr.p, k2s.p, slots.p, P->blocks.p);
+        launched(c);
+        CK(cudaStreamSynchronize(c->s));
+        if (TraceScope::on())
+            std::fprintf(stderr, "[dpp-trace]   ws_plan n=%d C=%d L=%d chunks %d pieces %zu warps %d slots %d x %d B halo max %d bytes=%lld\n",
+                         n, C, L, nchunks, poffs.size() - (size_t)C * NW, NW, NS, slot, hmax, cur);
+        T.pu = std::move(P);
+        return true;
+    }
     std::vector<int> hcnt;   // lvl format: per sorted row, entries of class early / mid / late
     if (fmt == 1) {
         DBuf<int> dcnt(3 * (size_t)n, c->s);
@@ -1373,6 +1704,7 @@ bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
         setk((const void *)k_trsv_flow<16>);
         setk((const void *)k_trsv_flow<32>);
         setk((const void *)k_trsv_lvl);
+        setk((const void *)k_trsv_ws);
         attr = true;
     }
     // as many CTAs as useful: each keeps >= ~2k rows of x
@@ -1432,6 +1764,15 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     }
     // level-mbarrier sweep (default): no polling; DPP_PU_MODE=flow|push selects the others
     const int mode = pu_mode();
+    if (P.fmt == 2) {
+        static const int nap = [] { const char *e = std::getenv("DPP_WS_NAP"); return e ? std::atoi(e) : 0; }();
+        cfg.blockDim = dim3(P.threads, 1, 1);
+        cfg.dynamicSmemBytes = ws_fixed(P.chunk, P.hmax, P.threads / 32, P.nst) + (size_t)(P.threads / 32) * P.nst * P.stage;
+        CK(cudaLaunchKernelEx(&cfg, k_trsv_ws, T.n / T.ncomp, T.ncomp, P.chunk, P.hmax, P.stage, P.nst, B, O,
+                              (const int *)P.sstart.p, b, x, xadd, xout, nap));
+        launched(c);
+        return;
+    }
     if (P.fmt == 1) {
         const size_t lfixed = lv_fixed(P.chunk, P.L, P.hmax, P.smax);
         if (wp || P.nst < LV_TEAMS + 2 || lfixed + (size_t)P.nst * P.stage > PU_SMEM_LIMIT)
