@@ -722,6 +722,142 @@ static void coarse_setup(Ctx *c, Amg &h, const Csr &A) {
     CK(cudaStreamSynchronize(c->s));
 }
 
+// ---------------------------------------------------------------- tail collapse
+// The last levels of the hierarchy are tiny (C2: 590 / 80 / 12 rows) and their V-cycle is a chain
+// of ~25 dependent launches that each run for a few microseconds.  Where both smoother
+// triangles of every remaining level already are dense inverses Li = (D+L)^-1, Ui = (D+U)^-1,
+// the cycle below that level is a fixed linear map and is formed once at setup (reference
+// linalg.py:383-400 composed symbolically, level by level from the coarsest):
+//   T = Li + Ui (I - A Li)                      one symmetric Gauss-Seidel sweep from x = 0
+//   Y = T + P M_c R (I - A T)                   + coarse correction
+//   M = Y - Li (A Y);  M = M - Ui (A M);  M += T   post-smoothing sweep from Y b
+// An exact-arithmetic rewrite like the dense triangular inverses themselves; DPP_AMG_TAIL=0
+// (or a level above the row limit) keeps the launch-by-launch cycle.
+// Y = Z + alpha * A X (+ I): A CSR (rows x k), X dense k x m, row-major
+__global__ void k_spmm(int rows, int m, const int *__restrict__ ptr, const int *__restrict__ idx,
+                       const double *__restrict__ val, const double *__restrict__ X, const double *Z, double alpha,
+                       int add_identity, double *Y) {
+    const int r = blockIdx.y;
+    const int p0 = ptr[r], p1 = ptr[r + 1];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int p = p0; p < p1; ++p) s += val[p] * X[(int64_t)idx[p] * m + j];
+        double y = alpha * s;
+        if (Z) y += Z[(int64_t)r * m + j];
+        if (add_identity && j == r) y += 1.0;
+        Y[(int64_t)r * m + j] = y;
+    }
+}
+// C = Cin + alpha * A B: A n x k, B k x m, row-major; tri = 1 / 2: A is lower / upper triangular
+// (k == n) and the zero tiles are skipped
+constexpr int GT = 64, GK = 16;
+__global__ void __launch_bounds__(256) k_dgemm(int n, int m, int k, const double *__restrict__ A,
+                                               const double *__restrict__ B, const double *Cin, double alpha,
+                                               double *C, int tri) {
+    __shared__ double As[GK][GT + 1], Bs[GK][GT];
+    const int bi = blockIdx.y * GT, bj = blockIdx.x * GT;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    const int k_begin = tri == 2 ? (bi / GK) * GK : 0;
+    const int k_end = tri == 1 ? min(k, bi + GT) : k;
+    for (int k0 = k_begin; k0 < k_end; k0 += GK) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = threadIdx.x + 256 * q;
+            const int ar = e >> 4, ak = e & 15;
+            As[ak][ar] = (bi + ar < n && k0 + ak < k) ? A[(int64_t)(bi + ar) * k + k0 + ak] : 0.0;
+            const int bk = e >> 6, bc = e & 63;
+            Bs[bk][bc] = (k0 + bk < k && bj + bc < m) ? B[(int64_t)(k0 + bk) * m + bj + bc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < GK; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) av[a] = As[kk][ty + 16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][tx + 16 * b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int i = bi + ty + 16 * a;
+        if (i >= n) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = bj + tx + 16 * b;
+            if (j >= m) continue;
+            const double cin = Cin ? Cin[(int64_t)i * m + j] : 0.0;
+            C[(int64_t)i * m + j] = cin + alpha * acc[a][b];
+        }
+    }
+}
+__global__ void k_add_to(int64_t n, const double *a, double *y) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] += a[i];
+}
+
+static void tail_collapse(Ctx *c, Amg &h) {
+    static const int tail_max = [] { const char *e = std::getenv("DPP_AMG_TAIL"); return e ? std::atoi(e) : 1024; }();
+    const int nl = (int)h.lv.size();
+    h.tail_level = -1;
+    if (tail_max <= 0 || nl < 2 || h.nc <= 0) return;
+    int l0 = nl - 1;   // first level of the collapsed tail
+    while (l0 > 0) {
+        const AmgLevel &L = *h.lv[l0 - 1];
+        if (L.A.rows > tail_max || !L.lo.dense.n || !L.up.dense.n || L.lo.ncomp != 1 || L.up.ncomp != 1) break;
+        --l0;
+    }
+    if (l0 == nl - 1) return;   // only the coarse solve: already one GEMV
+    DPP_TRACE_SCOPE(c, "amg.tail_collapse");
+    auto spmm = [&](const Csr &A, int m, const double *X, const double *Z, double alpha, int addI, double *Y) {
+        if (!A.rows || !m) return;
+        k_spmm<<<dim3((m + 127) / 128, A.rows), 128, 0, c->s>>>(A.rows, m, A.ptr.p, A.idx.p, A.val.p, X, Z, alpha, addI, Y);
+        launched(c);
+    };
+    auto gemm = [&](int n, int m, int k, const double *A, const double *B, const double *Cin, double alpha, double *C,
+                    int tri) {
+        if (!n || !m) return;
+        k_dgemm<<<dim3((m + GT - 1) / GT, (n + GT - 1) / GT), 256, 0, c->s>>>(n, m, k, A, B, Cin, alpha, C, tri);
+        launched(c);
+    };
+    DBuf<double> Mc;   // the collapsed cycle of level l+1
+    const double *mc = h.coarse_inv.p;
+    for (int l = nl - 2; l >= l0; --l) {
+        AmgLevel &L = *h.lv[l];
+        const int n = L.A.rows, nc = L.P.cols;
+        const size_t nn = (size_t)n * n;
+        const double *Li = L.lo.dense.p, *Ui = L.up.dense.p;
+        DBuf<double> E(nn, c->s), T(nn, c->s), W(nn, c->s), G1((size_t)nc * n, c->s), G2((size_t)nc * n, c->s), M(nn, c->s);
+        spmm(L.A, n, Li, nullptr, -1.0, 1, E.p);                 // E = I - A Li
+        gemm(n, n, n, Ui, E.p, Li, 1.0, T.p, 2);                 // T = Li + Ui E
+        spmm(L.A, n, T.p, nullptr, -1.0, 1, W.p);                // W = I - A T
+        spmm(L.R, n, W.p, nullptr, 1.0, 0, G1.p);                // G1 = R W
+        gemm(nc, n, nc, mc, G1.p, nullptr, 1.0, G2.p, 0);        // G2 = M_c G1
+        spmm(L.P, n, G2.p, T.p, 1.0, 0, E.p);                    // Y = T + P G2            (in E)
+        spmm(L.A, n, E.p, nullptr, 1.0, 0, W.p);                 // W = A Y
+        gemm(n, n, n, Li, W.p, E.p, -1.0, M.p, 1);               // Z1 = Y - Li W           (in M)
+        spmm(L.A, n, M.p, nullptr, 1.0, 0, W.p);                 // W = A Z1
+        gemm(n, n, n, Ui, W.p, M.p, -1.0, E.p, 2);               // Z2 = Z1 - Ui W          (in E)
+        k_add_to<<<grid_for((int64_t)nn, 256, c->sms), 256, 0, c->s>>>((int64_t)nn, T.p, E.p);   // M = Z2 + T
+        launched(c);
+        CK(cudaStreamSynchronize(c->s));   // the temporaries are freed on scope exit
+        Mc = std::move(E);
+        mc = Mc.p;
+    }
+    h.tail_M = std::move(Mc);
+    h.tail_level = l0;
+}
+
 // ---------------------------------------------------------------- setup
 std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega, int max_coarse,
                                int max_levels, dpp_randn_fn randn, void *user, Csr *A0_steal) {
@@ -931,6 +1067,7 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
     for (DBuf<double> *b : {&last->b, &last->x}) b->alloc(n, c->s);
     last->A = std::move(cur);
     h->lv.push_back(std::move(last));
+    tail_collapse(c, *h);
     CK(cudaStreamSynchronize(c->s));
     return h;
 }
@@ -939,6 +1076,11 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
 static void vc(Ctx *c, Amg &h, size_t l, const double *b, double *xo, cudaStream_t st) {
     AmgLevel &L = *h.lv[l];
     const int n = L.A.rows;
+    if ((int)l == h.tail_level) {   // the collapsed tail: one dense operator
+        k_gemv<<<grid_for((int64_t)n * 32, 128, c->sms, 4), 128, 0, st>>>(n, h.tail_M.p, b, xo);
+        launched(c);
+        return;
+    }
     if (l + 1 == h.lv.size()) {
         if (n) {
             k_gemv<<<grid_for((int64_t)n * 32, 128, c->sms, 4), 128, 0, st>>>(n, h.coarse_inv.p, b, xo);

@@ -385,6 +385,10 @@ struct Amg {
     std::vector<std::unique_ptr<AmgLevel>> lv;
     DBuf<double> coarse_inv;   // dense inverse of the coarsest operator (row-major)
     int nc = 0;
+    // tail collapse: the V-cycle of levels >= tail_level as one dense operator (row-major);
+    // exact-arithmetic rewrite of the small, launch-latency-bound tail of the hierarchy
+    DBuf<double> tail_M;
+    int tail_level = -1;
 };
 // A0_steal: optional; its storage becomes level 0 (no copy) when the caller is done with it
 // greedy strength aggregation (path 0 auto, 1 host greedy, 2 device passes); returns the count

@@ -870,6 +870,11 @@ __global__ void __launch_bounds__(LV_THREADS, 1)
 //   first: u16 local row[w] | groups x { u16 code[4][w] | f64 val[4][w] } |
 //   last: f64 1/diag[w] | int (p0 << 4 | npush)[w] | int push[np]
 constexpr int WS_NS_MAX = 8;
+#ifdef DPP_WS_TL
+// timeline build: per (CTA, warp, chunk ordinal) {t first piece landed, t last group entered, t inputs ready, t stored}
+constexpr int WS_TL_MAXC = 1024;
+__device__ unsigned long long *g_ws_tl = nullptr;
+#endif
 __host__ __device__ inline long long ws_group_bytes(int w) { return p16(8LL * w) + 32LL * w; }
 __host__ __device__ inline long long ws_head_bytes(int w) { return 16 + p16(2LL * w); }
 __host__ __device__ inline long long ws_tail_bytes(int w, int np) { return p16(8LL * w) + p16(4LL * w) + p16(4LL * np); }
@@ -945,18 +950,33 @@ __global__ void __launch_bounds__(512, 1)
     int row = 0;
     size_t g = 0;
     double bq = 0.0, xa = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#ifdef DPP_WS_TL
+    int tl_ord = -1;
+    unsigned long long tl0 = 0, tl1 = 0, tl2 = 0, tlw = 0, tlm = 0, tlq = 0;   // tlw: poll time of the earlier groups, tlm: mbarrier waits
+#endif
     for (int pi = 0; pi < NP; ++pi) {
         const int sl = pi % ns;
         long long n0 = 0, n1 = 0;   // the refill's extent, fetched before it is needed
         if (pi + ns < NP) { n0 = po[pi + ns]; n1 = po[pi + ns + 1]; }
+#ifdef DPP_WS_TL
+        tlq = clock64();
+#endif
         mwait(su32(&mb[sl]), (unsigned)((pi / ns) & 1));
         const unsigned char *pc = ring + (size_t)sl * slot;
         const int4 hd = *reinterpret_cast<const int4 *>(pc);
         const int ng = hd.x, w = hd.y, fl = hd.z;
         DPP_DCHECK(w >= 1 && w <= 32 && ng >= 0 && hd.w >= 0);
+#ifdef DPP_WS_TL
+        if (fl & 1) { tlw = 0; tlm = 0; }
+        tlm += clock64() - tlq;
+#endif
         const bool act = lane < w;
         int o = 16;
         if (fl & 1) {
+#ifdef DPP_WS_TL
+            ++tl_ord;
+            tl0 = clock64();
+#endif
             const unsigned short *rows = reinterpret_cast<const unsigned short *>(pc + 16);
             row = act ? rows[lane] : 0;
             DPP_DCHECK(row < mine);
@@ -1002,18 +1022,28 @@ __global__ void __launch_bounds__(512, 1)
             for (int u = 0; u < 4; ++u) xv[u] = ld_vol_shared(a[u]);
             if (gi + 1 < ng) WS_LOAD_CV(gi + 1);
             long long spins = 0;
+#ifdef DPP_WS_TL
+            tlq = clock64();
+            if ((fl & 2) && gi == ng - 1) tl1 = tlq;
+#endif
+            // the sentinel is the only stored value whose high word is all ones (a computed NaN is
+            // stored as the canonical quiet NaN), and 8-byte shared accesses are single transactions
             while (true) {
                 bool pend = false;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) pend |= __double_as_longlong(xv[u]) == (long long)PU_SENT;
+                for (int u = 0; u < 4; ++u) pend |= __double2hiint(xv[u]) == -1;
                 if (!__any_sync(0xffffffffu, pend)) break;
                 // far from the chunk's last groups the missing sources are levels away
                 if (nap && (!(fl & 2) || gi + 2 < ng)) __nanosleep(nap);
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
-                    if (__double_as_longlong(xv[u]) == (long long)PU_SENT) xv[u] = ld_vol_shared(a[u]);
+                    if (__double2hiint(xv[u]) == -1) xv[u] = ld_vol_shared(a[u]);
                 if (++spins > (1ll << 26)) __trap();
             }
+#ifdef DPP_WS_TL
+            if ((fl & 2) && gi == ng - 1) tl2 = clock64();
+            else tlw += clock64() - tlq;
+#endif
             s0 = fma(cv[0], xv[0], s0);
             s1 = fma(cv[1], xv[1], s1);
             s2 = fma(cv[2], xv[2], s2);
@@ -1022,7 +1052,7 @@ __global__ void __launch_bounds__(512, 1)
 #undef WS_LOAD_CV
         if ((fl & 2) && act) {
             double xr = (bq - ((s0 + s1) + (s2 + s3))) * dq;   // dq = 1/t_ii
-            if (__double_as_longlong(xr) == (long long)PU_SENT) xr = __longlong_as_double(0x7ff8000000000000ll);
+            if (__double2hiint(xr) == -1) xr = __longlong_as_double(0x7ff8000000000000ll);   // a NaN that looks pending
             st_vol_shared(xh_s + 8u * (unsigned)row, xr);
             const int p0 = pinf >> 4, pn = pinf & 15;
             for (int u = 0; u < pn; ++u) {
@@ -1034,6 +1064,15 @@ __global__ void __launch_bounds__(512, 1)
             if (xout) xout[g] = xa + xr;
         }
         __syncwarp();
+#ifdef DPP_WS_TL
+        if (fl & 2) {
+            const unsigned long long tl3 = clock64();
+            if (lane == 0 && g_ws_tl && tl_ord < WS_TL_MAXC) {
+                unsigned long long *o = g_ws_tl + (((size_t)blockIdx.x * nw + wid) * WS_TL_MAXC + tl_ord) * 6;
+                o[0] = tl0; o[1] = tl1; o[2] = tl2; o[3] = tl3; o[4] = tlw; o[5] = tlm;
+            }
+        }
+#endif
         if (lane == 0 && pi + ns < NP) issue(pi + ns, n0, n1);
     }
     pdl_trigger();
@@ -1339,8 +1378,9 @@ __global__ void k_ws_fill(int n, int chunk, int chunkp, int zero_code, int slot,
     }
 }
 
-// sweep kernel: 1 dataflow (default), 0 level-mbarrier (DPP_PU_MODE=lvl; own block format),
-// 2 level-synchronous push (DPP_PU_MODE=push or DPP_PU_FLOW=0)
+// sweep kernel: 4 auto (default: warp streams for thin rows, lane-group dataflow otherwise),
+// 1 lane-group dataflow (DPP_PU_MODE=flow), 3 warp streams everywhere (ws), 0 level-mbarrier
+// (lvl; own block format), 2 level-synchronous push (push or DPP_PU_FLOW=0)
 int pu_mode() {
     static const int mode = [] {
         const char *e = std::getenv("DPP_PU_MODE");
@@ -1349,9 +1389,22 @@ int pu_mode() {
         if (e && !std::strcmp(e, "lvl")) return 0;
         if (e && !std::strcmp(e, "push")) return 2;
         if (e && !std::strcmp(e, "ws")) return 3;
-        return 1;
+        if (e && !std::strcmp(e, "flow")) return 1;
+        return 4;
     }();
     return mode;
+}
+// lane groups the row-major kernels would use for rows of this average length
+inline int pu_lane_group(double avg) {
+    int G = 2;
+    while (G < 32 && G * 4 < avg) G *= 2;
+    return G;
+}
+// a lane per row pays off while a row is a few 4-column groups long (C2: ILU 7, AMG level 0
+// 26 entries per row); the long rows of configs 3/4 measured slower (C4 PC apply 47 -> 68 ms)
+inline bool pu_use_ws(double avg) {
+    static const int gmax = [] { const char *e = std::getenv("DPP_WS_GMAX"); return e ? std::atoi(e) : 8; }();
+    return pu_mode() == 3 || (pu_mode() == 4 && pu_lane_group(avg) <= gmax);
 }
 
 template <typename T>
@@ -1451,12 +1504,10 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     auto part_bytes = [&](int q0, int q1) {
         return pu_block_bytes(q1 - q0, (long long)hr[q1] - hr[q0], (long long)hp[q1] - hp[q0]);
     };
-    const int fmt = pu_mode() == 0 ? 1 : (pu_mode() == 3 && !T.W.rows) ? 2 : 0;
-    if (fmt) ++hmax;   // one zero slot after the halo: the padding entries' source
-    if (fmt && pu_chunkp(chunk) + hmax >= (1 << 16)) return false;   // 16-bit column codes
-    if (fmt == 2) {   // warp streams (k_trsv_ws)
+    int fmt = pu_mode() == 0 ? 1 : (pu_use_ws((double)S.nnz / n) && !T.W.rows) ? 2 : 0;
+    auto ws_plan = [&]() -> bool {   // warp streams (k_trsv_ws)
         static const int nw_env = [] { const char *e = std::getenv("DPP_WS_WARPS"); return e ? std::atoi(e) : 8; }();
-        static const int ns_env = [] { const char *e = std::getenv("DPP_WS_SLOTS"); return e ? std::atoi(e) : 3; }();
+        static const int ns_env = [] { const char *e = std::getenv("DPP_WS_SLOTS"); return e ? std::atoi(e) : 2; }();
         const int NW = std::max(1, std::min(16, nw_env)), NS = std::max(2, std::min(WS_NS_MAX, ns_env));
         const size_t fixed = ws_fixed(chunk, hmax, NW, NS);
         if (fixed + (size_t)NW * NS * 2048 > PU_SMEM_LIMIT) return false;
@@ -1521,7 +1572,16 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
                          n, C, L, nchunks, poffs.size() - (size_t)C * NW, NW, NS, slot, hmax, cur);
         T.pu = std::move(P);
         return true;
+    };
+    if (fmt == 2) {
+        ++hmax;   // one zero slot after the halo: the padding entries' source
+        if (pu_chunkp(chunk) + hmax < (1 << 16) && ws_plan()) return true;   // 16-bit column codes
+        if (pu_mode() == 3) return false;
+        --hmax;   // auto: the row-major plan instead
+        fmt = 0;
     }
+    if (fmt) ++hmax;
+    if (fmt && pu_chunkp(chunk) + hmax >= (1 << 16)) return false;
     std::vector<int> hcnt;   // lvl format: per sorted row, entries of class early / mid / late
     if (fmt == 1) {
         DBuf<int> dcnt(3 * (size_t)n, c->s);
@@ -1633,9 +1693,7 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     P->hmax = hmax;
     P->stage = (int)stage;
     P->nst = nst;
-    const double avg = (double)S.nnz / n;
-    P->G = 2;
-    while (P->G < 32 && P->G * 4 < avg) P->G *= 2;
+    P->G = pu_lane_group((double)S.nnz / n);
     static const int force_g = [] { const char *e = std::getenv("DPP_PU_G"); return e ? std::atoi(e) : 0; }();
     if (force_g && P->G < force_g) P->G = force_g;   // experiment: wider lane groups for thin rows
     static const int set_g = [] { const char *e = std::getenv("DPP_PU_GSET"); return e ? std::atoi(e) : 0; }();
@@ -1768,9 +1826,47 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
         static const int nap = [] { const char *e = std::getenv("DPP_WS_NAP"); return e ? std::atoi(e) : 0; }();
         cfg.blockDim = dim3(P.threads, 1, 1);
         cfg.dynamicSmemBytes = ws_fixed(P.chunk, P.hmax, P.threads / 32, P.nst) + (size_t)(P.threads / 32) * P.nst * P.stage;
+#ifdef DPP_WS_TL
+        static const char *tl_path = std::getenv("DPP_WS_TL");
+        unsigned long long *tlb = nullptr;
+        const size_t ntl = (size_t)P.C * T.ncomp * (P.threads / 32) * WS_TL_MAXC * 6;
+        cudaEvent_t te0 = nullptr, te1 = nullptr;
+        if (tl_path && *tl_path && !c->capturing) {
+            CK(cudaStreamSynchronize(st));
+            CK(cudaMalloc((void **)&tlb, ntl * 8));
+            CK(cudaMemset(tlb, 0, ntl * 8));
+            CK(cudaMemcpyToSymbol(g_ws_tl, &tlb, sizeof(tlb)));
+            cudaEventCreate(&te0); cudaEventCreate(&te1);
+            cudaEventRecord(te0, st);
+        }
+#endif
         CK(cudaLaunchKernelEx(&cfg, k_trsv_ws, T.n / T.ncomp, T.ncomp, P.chunk, P.hmax, P.stage, P.nst, B, O,
                               (const int *)P.sstart.p, b, x, xadd, xout, nap));
         launched(c);
+#ifdef DPP_WS_TL
+        if (tlb) {
+            cudaEventRecord(te1, st);
+            CK(cudaStreamSynchronize(st));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, te0, te1);
+            std::vector<unsigned long long> h(ntl);
+            CK(cudaMemcpy(h.data(), tlb, ntl * 8, cudaMemcpyDeviceToHost));
+            unsigned long long *z = nullptr;
+            CK(cudaMemcpyToSymbol(g_ws_tl, &z, sizeof(z)));
+            cudaFree(tlb);
+            if (FILE *f = std::fopen(tl_path, "a")) {
+                std::fprintf(f, "# ws n=%d C=%d ncomp=%d L=%d warps=%d slots=%d slot=%d us=%.2f\n", T.n, P.C, T.ncomp, P.L,
+                             P.threads / 32, P.nst, P.stage, ms * 1e3);
+                const int nwv = P.threads / 32;
+                for (size_t i = 0; i < ntl / 6; ++i) {
+                    const unsigned long long *o = &h[i * 6];
+                    if (o[3]) std::fprintf(f, "%zu %zu %zu %llu %llu %llu %llu %llu %llu\n", i / WS_TL_MAXC / nwv,
+                                           (i / WS_TL_MAXC) % nwv, i % WS_TL_MAXC, o[0], o[1], o[2], o[3], o[4], o[5]);
+                }
+                std::fclose(f);
+            }
+        }
+#endif
         return;
     }
     if (P.fmt == 1) {

@@ -3,7 +3,10 @@ triangle; these force the others).  Each variant runs in a fresh process (the
 switches are read once per process) and must match the CPU oracle to the usual
 bars: solution within 1e-9 relative, iterations within +-2.
 
-  default                     dataflow cluster sweeps (k_trsv_flow, polled x slots) + block-dense / dense smoothers
+  default                     warp-stream dataflow sweeps for thin rows (k_trsv_ws, lane per row), lane-group
+                              dataflow sweeps otherwise (k_trsv_flow) + block-dense / dense smoothers
+  DPP_PU_MODE=flow            lane-group dataflow sweeps everywhere (k_trsv_flow, polled x slots)
+  DPP_PU_MODE=ws              warp-stream sweeps everywhere
   DPP_PU_MODE=lvl             level-mbarrier cluster sweeps (k_trsv_lvl: level teams, SELL chunks)
   DPP_PU_FLOW=0               level-synchronous push-exchange cluster sweeps (k_trsv_push)
   DPP_NO_PUSH=1               barrier-per-level cluster sweeps (tricluster.cu)
@@ -39,6 +42,8 @@ print(json.dumps({{"its": r.stats.iterations, "converged": bool(r.stats.converge
 
 VARIANTS = {
     "default": {},
+    "lane_group_flow": {"DPP_PU_MODE": "flow"},
+    "warp_stream": {"DPP_PU_MODE": "ws"},
     "level_mbarrier": {"DPP_PU_MODE": "lvl"},
     "level_sync_push": {"DPP_PU_FLOW": "0"},
     "pull_cluster": {"DPP_NO_PUSH": "1"},
@@ -75,12 +80,13 @@ def test_sweep_strategy(name, oracle_ref, tmp_path):
 
 @pytest.mark.timeout(600)
 def test_cluster_sweeps_bitwise(tmp_path):
-    """The dataflow and level-synchronous push sweeps only change when a row is computed, not
-    how: per-lane products in entry order, the same xor-shuffle reduction, (b - sum) * (1/t_ii)
-    -- so the whole solve is bit-for-bit the same.  (The level-mbarrier sweep regroups the
-    row sums into partial sums: tolerance-checked in test_sweep_strategy.)"""
+    """The lane-group dataflow and level-synchronous push sweeps only change when a row is
+    computed, not how: per-lane products in entry order, the same xor-shuffle reduction,
+    (b - sum) * (1/t_ii) -- so the whole solve is bit-for-bit the same.  (The warp-stream and
+    level-mbarrier sweeps regroup the row sums into partial sums: tolerance-checked in
+    test_sweep_strategy.)"""
     xs = []
-    for k, extra in enumerate(({}, {"DPP_PU_MODE": "push"})):
+    for k, extra in enumerate(({"DPP_PU_MODE": "flow"}, {"DPP_PU_MODE": "push"})):
         out = str(tmp_path / f"x{k}.npy")
         res = subprocess.run([sys.executable, "-c", SCRIPT.format(root=ROOT, out=out)],
                              env=dict(os.environ, **extra), capture_output=True, text=True, timeout=500)
