@@ -1080,6 +1080,200 @@ __global__ void __launch_bounds__(512, 1)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// ----------------------------------------------------------------- global-stream dataflow variant
+// Lane-per-row dataflow sweep without a shared-memory ring (the default for thin rows).  The
+// warp-stream kernel above was measured (-DDPP_WS_PH) to be bound by the SM's shared-memory
+// pipe, not by the dependency chain: per chunk a warp spends ~3,800 cycles of which only ~800
+// wait for inputs, and doubling the warps (shared ring) made every phase 4-5x slower -- the TMA
+// writes, the code / value reads back out of the ring and the x-slot polls all go through the
+// same banks.  Here only x lives in shared memory: every lane streams its own row's entries
+// straight from global memory (coalesced SELL columns, whole batches of 4-column groups in
+// flight in registers, the next chunk's header / rows and an L2 prefetch issued a chunk ahead),
+// so the shared-memory traffic is the x gathers alone and 16+ warps hide the load latency.
+// Same partition, halo / push tables, level-sorted right-aligned rows, NaN-sentinel readiness
+// and arithmetic (four partial sums per row) as k_trsv_ws.
+//
+// chunk (16-byte aligned segments): int4 {groups, w, np, 0} | u16 local row[w] | f64 1/diag[w] |
+//   int (p0 << 4 | npush)[w] | int2 first two push entries[w] | int push[np] |
+//   groups x { u16 code[w][4] | f64 val[4][w] }
+#ifndef DPP_GS_WARPS_MAX
+#define DPP_GS_WARPS_MAX 16   // 512 threads: up to 128 registers each (a batch of groups lives in registers)
+#endif
+#ifndef DPP_GS_GB
+#define DPP_GS_GB 4
+#endif
+constexpr int GS_WARPS_MAX = DPP_GS_WARPS_MAX, GS_GB = DPP_GS_GB;
+__host__ __device__ inline long long gs_group_bytes(int w) { return p16(8LL * w) + 32LL * w; }
+__host__ __device__ inline long long gs_off_dq(int w) { return 16 + p16(2LL * w); }
+__host__ __device__ inline long long gs_off_pinf(int w) { return gs_off_dq(w) + p16(8LL * w); }
+__host__ __device__ inline long long gs_off_p2(int w) { return gs_off_pinf(w) + p16(4LL * w); }
+__host__ __device__ inline long long gs_off_pl(int w) { return gs_off_p2(w) + p16(8LL * w); }
+__host__ __device__ inline long long gs_off_groups(int w, int np) { return gs_off_pl(w) + p16(4LL * np); }
+__host__ __device__ inline long long gs_chunk_bytes(int w, int ngr, int np) {
+    return gs_off_groups(w, np) + (long long)ngr * gs_group_bytes(w);
+}
+__host__ __device__ inline size_t gs_smem(int chunk, int hmax) {   // x slice | halo | peers
+    return (size_t)((p16(8LL * chunk) + p16(8LL * hmax) + 64 + 127) & ~127LL);
+}
+#ifdef DPP_WS_PH
+// phase build: per (CTA, warp) cycles summed over its chunks {head, loads + groups, tail, -, -, polls, chunks, -}
+__device__ unsigned long long *g_ws_ph = nullptr;
+#define GS_PH(i, t0_) { const unsigned long long t_ = clock64(); ph[i] += t_ - (t0_); (t0_) = t_; }
+#else
+#define GS_PH(i, t0_)
+#endif
+__device__ __forceinline__ unsigned long long ldg_u64(const void *p) {
+    unsigned long long v;
+    asm volatile("ld.global.nc.L1::no_allocate.b64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ldg_f64(const void *p) { return __longlong_as_double((long long)ldg_u64(p)); }
+
+__global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
+    k_trsv_gs(int n, int ncomp, int chunk, int hmax, const unsigned char *__restrict__ blocks,
+              const long long *__restrict__ soff, const int *__restrict__ scnt, const double *__restrict__ b,
+              double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout, int nap) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int chunkp = pu_chunkp(chunk);
+    double *xh = reinterpret_cast<double *>(smem);
+    unsigned *peer = reinterpret_cast<unsigned *>(xh + chunkp + p16(8LL * hmax) / 8);
+    cg::cluster_group cl = cg::this_cluster();
+    const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
+    const int comp = blockIdx.x / C;
+    const int base = k * chunk, mine = max(0, min(chunk, n - base));
+    // the plan is static: this warp's first header and rows are in flight before the predecessor ends
+    const unsigned char *pc = blocks + soff[k * nw + wid];
+    const int NCH = scnt[k * nw + wid];
+    int4 hd = make_int4(0, 0, 0, 0);
+    int rown = 0;
+    if (NCH) {
+        hd = *reinterpret_cast<const int4 *>(pc);
+        rown = reinterpret_cast<const unsigned short *>(pc + 16)[lane];
+    }
+    if (threadIdx.x < C) peer[threadIdx.x] = mapa_u32(su32(xh + chunkp), threadIdx.x);
+    const double sent = __longlong_as_double((long long)PU_SENT);
+    for (int i = threadIdx.x; i < mine; i += blockDim.x) xh[i] = sent;
+    for (int i = threadIdx.x; i < hmax - 1; i += blockDim.x) xh[chunkp + i] = sent;
+    if (threadIdx.x == 0) xh[chunkp + hmax - 1] = 0.0;   // the padding entries' source
+    __syncthreads();
+    // every CTA's slots hold the sentinel before anyone pushes
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    pdl_wait();   // b is the previous kernel's output
+    const unsigned xh_s = su32(xh);
+    const unsigned long long zero4 = 0x0001000100010001ull * (unsigned long long)(chunkp + hmax - 1);
+#ifdef DPP_WS_PH
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt = clock64(), pq = 0;
+#endif
+    for (int ci = 0; ci < NCH; ++ci) {
+        const int ng = hd.x, w = hd.y, np = hd.z;
+        DPP_DCHECK(w >= 1 && w <= 32 && ng >= 0 && np >= 0);
+        const bool act = lane < w;
+        const int row = act ? rown : 0;
+        DPP_DCHECK(row < mine);
+        const size_t g = (size_t)(base + row) * ncomp + comp;
+        const double bq = act ? b[g] : 0.0;
+        const double xa = (act && xout) ? xadd[g] : 0.0;
+        const double dq = act ? ldg_f64(pc + gs_off_dq(w) + 8 * lane) : 0.0;
+        const int pinf = act ? reinterpret_cast<const int *>(pc + gs_off_pinf(w))[lane] : 0;
+        const unsigned long long p2 = act ? ldg_u64(pc + gs_off_p2(w) + 8 * lane) : 0ull;
+        const int *pl = reinterpret_cast<const int *>(pc + gs_off_pl(w));
+        const unsigned char *gp = pc + gs_off_groups(w, np);
+        const long long cb = p16(8LL * w), gb = cb + 32LL * w;
+        const unsigned char *pnx = gp + (long long)ng * gb;   // the next chunk of this warp's stream
+        if (ci + 1 < NCH) {
+            hd = *reinterpret_cast<const int4 *>(pnx);
+            rown = reinterpret_cast<const unsigned short *>(pnx + 16)[lane];
+            // and its entries on their way into L2 (128 B per lane and instruction)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pnx + 128 * lane));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pnx + 4096 + 128 * lane));
+        }
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        GS_PH(0, pt);
+        // batches of GS_GB groups: a batch's codes / values are all in flight before its first group is
+        // polled (double-buffering the batches measured slower: 1.11 vs 1.07 ms per C2 PC apply -- the
+        // sweep is bound by the ~300-cycle shared-memory hand-off between the warps of consecutive
+        // levels, tools/micro/fp64lat.cu, not by load latency)
+        for (int g0 = 0; g0 < ng; g0 += GS_GB) {
+            unsigned long long c4[GS_GB];
+            double v[GS_GB][4];
+#pragma unroll
+            for (int j = 0; j < GS_GB; ++j) {
+                const unsigned char *q = gp + (long long)(g0 + j) * gb;
+                const bool on = act && g0 + j < ng;
+                c4[j] = on ? ldg_u64(q + 8 * lane) : zero4;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[j][u] = on ? ldg_f64(q + cb + 8 * (u * w + lane)) : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < GS_GB; ++j) {
+                if (g0 + j >= ng) break;
+                unsigned a[4];
+                double xv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cd = (int)((c4[j] >> (16 * u)) & 0xffffu);
+                    DPP_DCHECK(cd < mine || (cd >= chunkp && cd < chunkp + hmax));
+                    a[u] = xh_s + 8u * (unsigned)cd;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xv[u] = ld_vol_shared(a[u]);
+                long long spins = 0;
+#ifdef DPP_WS_PH
+                pq = clock64();
+#endif
+                // the sentinel is the only stored value whose high word is all ones (a computed NaN is
+                // stored as the canonical quiet NaN), and 8-byte shared accesses are single transactions
+                while (true) {
+                    bool pend = false;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) pend |= __double2hiint(xv[u]) == -1;
+                    if (!__any_sync(0xffffffffu, pend)) break;
+                    if (nap) __nanosleep(nap);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (__double2hiint(xv[u]) == -1) xv[u] = ld_vol_shared(a[u]);
+                    if (++spins > (1ll << 26)) __trap();
+                }
+#ifdef DPP_WS_PH
+                ph[5] += clock64() - pq;
+#endif
+                s0 = fma(v[j][0], xv[0], s0);
+                s1 = fma(v[j][1], xv[1], s1);
+                s2 = fma(v[j][2], xv[2], s2);
+                s3 = fma(v[j][3], xv[3], s3);
+            }
+        }
+        GS_PH(1, pt);
+        if (act) {
+            double xr = (bq - ((s0 + s1) + (s2 + s3))) * dq;   // dq = 1/t_ii
+            if (__double2hiint(xr) == -1) xr = __longlong_as_double(0x7ff8000000000000ll);   // a NaN that looks pending
+            st_vol_shared(xh_s + 8u * (unsigned)row, xr);
+            const int p0 = pinf >> 4, pn = pinf & 15;
+            for (int u = 0; u < pn; ++u) {
+                const int pe = u < 2 ? (int)(p2 >> (32 * u)) : pl[p0 + u];
+                DPP_DCHECK((int)((unsigned)pe >> 28) < C && (int)((unsigned)pe & 0x0fffffffu) < hmax - 1);
+                st_remote(peer[(unsigned)pe >> 28] + 8u * ((unsigned)pe & 0x0fffffffu), xr);
+            }
+            x[g] = xr;
+            if (xout) xout[g] = xa + xr;
+        }
+        __syncwarp();
+        pc = pnx;
+#ifdef DPP_WS_PH
+        ph[6] += 1;
+#endif
+        GS_PH(2, pt);
+    }
+#ifdef DPP_WS_PH
+    if (lane == 0 && g_ws_ph)
+        for (int i = 0; i < 8; ++i) g_ws_ph[((size_t)blockIdx.x * nw + wid) * 8 + i] = ph[i];
+#endif
+    pdl_trigger();
+    // a CTA's shared memory must outlive the pushes aimed at it
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ----------------------------------------------------------------- setup
 __global__ void k_pu_keys(int n, int chunk, int L, const int *lev, int *key, int *rows) {
     for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
@@ -1378,8 +1572,63 @@ __global__ void k_ws_fill(int n, int chunk, int chunkp, int zero_code, int slot,
     }
 }
 
-// sweep kernel: 4 auto (default: warp streams for thin rows, lane-group dataflow otherwise),
-// 1 lane-group dataflow (DPP_PU_MODE=flow), 3 warp streams everywhere (ws), 0 level-mbarrier
+// ---- global-stream format (k_trsv_gs): one thread per sorted row writes its lane of the chunk
+// ctab[gc] = {first sorted row, rows, column groups, push entries}, cbase[gc] = the chunk's bytes
+__global__ void k_gs_fill(int n, int chunk, int chunkp, int zero_code, int nchunks, const int4 *ctab,
+                          const long long *cbase, const int *perm, const int *rpp, const int *ptr, const int *idx,
+                          const double *val, const double *diag, const int *lev, const unsigned long long *h,
+                          const int *hstart, const int *pptr, const unsigned long long *k2s, const int *slots,
+                          unsigned char *blocks) {
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        int lo = 0, hi = nchunks;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (ctab[mid].x <= q) lo = mid; else hi = mid;
+        }
+        const int4 ct = ctab[lo];
+        const int q0 = ct.x, w = ct.y, ngr = ct.z, np = ct.w, lane = q - q0;
+        unsigned char *B = blocks + cbase[lo];
+        const int r = perm[q], owner = r / chunk;
+        const int a0 = ptr[r], len = ptr[r + 1] - a0, pad = 4 * ngr - len;
+        const int hs = hstart[owner], he = hstart[owner + 1];
+        if (lane == 0) *reinterpret_cast<int4 *>(B) = make_int4(ngr, w, np, 0);
+        reinterpret_cast<unsigned short *>(B + 16)[lane] = (unsigned short)(r - owner * chunk);
+        reinterpret_cast<double *>(B + gs_off_dq(w))[lane] = diag ? 1.0 / diag[r] : 1.0;
+        const int p0 = rpp[q] - rpp[q0], pn = rpp[q + 1] - rpp[q];
+        reinterpret_cast<int *>(B + gs_off_pinf(w))[lane] = (p0 << 4) | pn;
+        int *pl = reinterpret_cast<int *>(B + gs_off_pl(w));
+        int first2[2] = {0, 0};
+        int u = 0;
+        for (int tt = pptr[r]; tt < pptr[r + 1]; ++tt, ++u) {
+            const int pe = (int)(((unsigned)(k2s[tt] & 15u) << 28) | (unsigned)slots[tt]);
+            pl[p0 + u] = pe;
+            if (u < 2) first2[u] = pe;
+        }
+        reinterpret_cast<int2 *>(B + gs_off_p2(w))[lane] = make_int2(first2[0], first2[1]);
+        // entries by source level (ties in storage order), right-aligned in the chunk's columns
+        unsigned char *G = B + gs_off_groups(w, np);
+        const long long cb = p16(8LL * w), gb = cb + 32LL * w;
+        auto put = [&](int col, int code, double vv) {
+            unsigned char *gq = G + (long long)(col >> 2) * gb;
+            reinterpret_cast<unsigned short *>(gq)[4 * lane + (col & 3)] = (unsigned short)code;
+            reinterpret_cast<double *>(gq + cb)[(col & 3) * w + lane] = vv;
+        };
+        for (int col = 0; col < pad; ++col) put(col, zero_code, 0.0);
+        for (int p = a0; p < a0 + len; ++p) {
+            const int j = idx[p], lj = lev[j];
+            int rank = 0;
+            for (int t = a0; t < a0 + len; ++t) {
+                const int lt = lev[idx[t]];
+                rank += (lt < lj) || (lt == lj && t < p);
+            }
+            put(pad + rank, pu_code(j, owner, chunk, chunkp, h, hs, he), val[p]);
+        }
+    }
+}
+
+// sweep kernel: 4 auto (default: global streams for thin rows, lane-group dataflow otherwise),
+// 1 lane-group dataflow (DPP_PU_MODE=flow), 3 warp streams through TMA rings everywhere (ws),
+// 5 global streams everywhere (gs), 0 level-mbarrier
 // (lvl; own block format), 2 level-synchronous push (push or DPP_PU_FLOW=0)
 int pu_mode() {
     static const int mode = [] {
@@ -1389,6 +1638,7 @@ int pu_mode() {
         if (e && !std::strcmp(e, "lvl")) return 0;
         if (e && !std::strcmp(e, "push")) return 2;
         if (e && !std::strcmp(e, "ws")) return 3;
+        if (e && !std::strcmp(e, "gs")) return 5;
         if (e && !std::strcmp(e, "flow")) return 1;
         return 4;
     }();
@@ -1404,7 +1654,7 @@ inline int pu_lane_group(double avg) {
 // 26 entries per row); the long rows of configs 3/4 measured slower (C4 PC apply 47 -> 68 ms)
 inline bool pu_use_ws(double avg) {
     static const int gmax = [] { const char *e = std::getenv("DPP_WS_GMAX"); return e ? std::atoi(e) : 8; }();
-    return pu_mode() == 3 || (pu_mode() == 4 && pu_lane_group(avg) <= gmax);
+    return pu_mode() == 3 || pu_mode() == 5 || (pu_mode() == 4 && pu_lane_group(avg) <= gmax);
 }
 
 template <typename T>
@@ -1573,10 +1823,72 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
         T.pu = std::move(P);
         return true;
     };
+    auto gs_plan = [&]() -> bool {   // global streams (k_trsv_gs): no ring, x slice + halo in shared memory
+        static const int nw_env = [] { const char *e = std::getenv("DPP_GS_WARPS"); return e ? std::atoi(e) : 16; }();
+        const int NW = std::max(1, std::min(GS_WARPS_MAX, nw_env));
+        if (gs_smem(chunk, hmax) > PU_SMEM_LIMIT) return false;
+        // chunks: the rows of a (CTA, level) cut evenly into ceil(rows / 32) chunks
+        std::vector<int4> ctab;
+        std::vector<int> cstart(C + 1, 0);
+        for (int d = 0; d < C; ++d) {
+            cstart[d] = (int)ctab.size();
+            for (int l = 0; l < L; ++l) {
+                const int a0 = hlp[d * L + l], nr = hlp[d * L + l + 1] - a0;
+                const int nch = (nr + 31) / 32;
+                for (int cc = 0; cc < nch; ++cc) {
+                    const int q0 = a0 + (int)((long long)nr * cc / nch), q1 = a0 + (int)((long long)nr * (cc + 1) / nch);
+                    int mxl = 0;
+                    for (int q = q0; q < q1; ++q) mxl = std::max(mxl, hr[q + 1] - hr[q]);
+                    const int np = hp[q1] - hp[q0];
+                    if (np >= (1 << 27)) return false;
+                    ctab.push_back(make_int4(q0, q1 - q0, (mxl + 3) / 4, np));
+                }
+            }
+        }
+        cstart[C] = (int)ctab.size();
+        const int nchunks = (int)ctab.size();
+        if (nchunks == 0) return false;
+        // streams: chunk g of CTA d belongs to warp g % NW; a stream's chunks are contiguous
+        std::vector<long long> cbase(nchunks), soff((size_t)C * NW, 0);
+        std::vector<int> scnt((size_t)C * NW, 0);
+        long long cur = 0;
+        for (int d = 0; d < C; ++d)
+            for (int wv = 0; wv < NW; ++wv) {
+                soff[(size_t)d * NW + wv] = cur;
+                for (int gc = cstart[d] + wv; gc < cstart[d + 1]; gc += NW) {
+                    cbase[gc] = cur;
+                    cur += gs_chunk_bytes(ctab[gc].y, ctab[gc].z, ctab[gc].w);
+                    ++scnt[(size_t)d * NW + wv];
+                }
+            }
+        P->C = C; P->chunk = chunk; P->L = L; P->hmax = hmax; P->smax = 0;
+        P->stage = 128; P->nst = 1;   // unused (no ring); kept non-zero for the shared launch arithmetic
+        P->threads = 32 * NW; P->fmt = 3; P->G = 1; P->widest = 1;
+        P->blocks.alloc((size_t)cur + 8192 + 4096, c->s);   // slack: the L2 prefetch of a stream's last chunk
+        P->boff.alloc(soff.size(), c->s);
+        P->boff.upload(soff.data(), soff.size());
+        P->sstart.alloc(scnt.size(), c->s);
+        P->sstart.upload(scnt.data(), scnt.size());
+        DBuf<int4> dct(ctab.size(), c->s);
+        DBuf<long long> dcb(cbase.size(), c->s);
+        dct.upload(ctab.data(), ctab.size());
+        dcb.upload(cbase.data(), cbase.size());
+        k_gs_fill<<<grid_for(n, 128, c->sms), 128, 0, c->s>>>(n, chunk, pu_chunkp(chunk), pu_chunkp(chunk) + hmax - 1,
+                                                              nchunks, dct.p, dcb.p, perm.p, rpp.p, S.ptr.p, S.idx.p,
+                                                              S.val.p, T.diag.n ? T.diag.p : nullptr, lev.p, H.p,
+                                                              hstart.p, pptr.p, k2s.p, slots.p, P->blocks.p);
+        launched(c);
+        CK(cudaStreamSynchronize(c->s));
+        if (TraceScope::on())
+            std::fprintf(stderr, "[dpp-trace]   gs_plan n=%d C=%d L=%d chunks %d warps %d halo max %d bytes=%lld\n", n, C, L,
+                         nchunks, NW, hmax, cur);
+        T.pu = std::move(P);
+        return true;
+    };
     if (fmt == 2) {
         ++hmax;   // one zero slot after the halo: the padding entries' source
-        if (pu_chunkp(chunk) + hmax < (1 << 16) && ws_plan()) return true;   // 16-bit column codes
-        if (pu_mode() == 3) return false;
+        if (pu_chunkp(chunk) + hmax < (1 << 16) && (pu_mode() == 3 ? ws_plan() : gs_plan())) return true;   // 16-bit column codes
+        if (pu_mode() == 3 || pu_mode() == 5) return false;
         --hmax;   // auto: the row-major plan instead
         fmt = 0;
     }
@@ -1763,6 +2075,7 @@ bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
         setk((const void *)k_trsv_flow<32>);
         setk((const void *)k_trsv_lvl);
         setk((const void *)k_trsv_ws);
+        setk((const void *)k_trsv_gs);
         attr = true;
     }
     // as many CTAs as useful: each keeps >= ~2k rows of x
@@ -1822,6 +2135,52 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
     }
     // level-mbarrier sweep (default): no polling; DPP_PU_MODE=flow|push selects the others
     const int mode = pu_mode();
+    if (P.fmt == 3) {
+        static const int nap = [] { const char *e = std::getenv("DPP_GS_NAP"); return e ? std::atoi(e) : 0; }();
+        cfg.blockDim = dim3(P.threads, 1, 1);
+        cfg.dynamicSmemBytes = gs_smem(P.chunk, P.hmax);
+#ifdef DPP_WS_PH
+        static const char *ph_pathw = std::getenv("DPP_WS_PH");
+        unsigned long long *phw = nullptr;
+        const size_t nphw = (size_t)P.C * T.ncomp * (P.threads / 32) * 8;
+        cudaEvent_t pe0w = nullptr, pe1w = nullptr;
+        if (ph_pathw && *ph_pathw && !c->capturing) {
+            CK(cudaStreamSynchronize(st));
+            CK(cudaMalloc((void **)&phw, nphw * 8));
+            CK(cudaMemset(phw, 0, nphw * 8));
+            CK(cudaMemcpyToSymbol(g_ws_ph, &phw, sizeof(phw)));
+            cudaEventCreate(&pe0w); cudaEventCreate(&pe1w);
+            cudaEventRecord(pe0w, st);
+        }
+#endif
+        CK(cudaLaunchKernelEx(&cfg, k_trsv_gs, T.n / T.ncomp, T.ncomp, P.chunk, P.hmax, B, O, (const int *)P.sstart.p, b, x,
+                              xadd, xout, nap));
+        launched(c);
+#ifdef DPP_WS_PH
+        if (phw) {
+            cudaEventRecord(pe1w, st);
+            CK(cudaStreamSynchronize(st));
+            float ms = 0;
+            cudaEventElapsedTime(&ms, pe0w, pe1w);
+            std::vector<unsigned long long> h(nphw);
+            CK(cudaMemcpy(h.data(), phw, nphw * 8, cudaMemcpyDeviceToHost));
+            unsigned long long *z = nullptr;
+            CK(cudaMemcpyToSymbol(g_ws_ph, &z, sizeof(z)));
+            cudaFree(phw);
+            if (FILE *f = std::fopen(ph_pathw, "a")) {
+                const int nwv = P.threads / 32;
+                std::fprintf(f, "# gs n=%d C=%d ncomp=%d L=%d warps=%d us=%.2f\n", T.n, P.C, T.ncomp, P.L, nwv, ms * 1e3);
+                for (size_t i = 0; i < nphw / 8; ++i) {
+                    const unsigned long long *o = &h[i * 8];
+                    std::fprintf(f, "%zu %zu %llu %llu %llu %llu %llu %llu %llu %llu\n", i / nwv, i % nwv, o[0], o[1], o[2],
+                                 o[3], o[4], o[5], o[6], o[7]);
+                }
+                std::fclose(f);
+            }
+        }
+#endif
+        return;
+    }
     if (P.fmt == 2) {
         static const int nap = [] { const char *e = std::getenv("DPP_WS_NAP"); return e ? std::atoi(e) : 0; }();
         cfg.blockDim = dim3(P.threads, 1, 1);

@@ -3,10 +3,13 @@ triangle; these force the others).  Each variant runs in a fresh process (the
 switches are read once per process) and must match the CPU oracle to the usual
 bars: solution within 1e-9 relative, iterations within +-2.
 
-  default                     warp-stream dataflow sweeps for thin rows (k_trsv_ws, lane per row), lane-group
-                              dataflow sweeps otherwise (k_trsv_flow) + block-dense / dense smoothers
+  default                     global-stream dataflow sweeps for thin rows (k_trsv_gs, lane per row, entries
+                              streamed from global memory), lane-group dataflow sweeps otherwise
+                              (k_trsv_flow) + block-dense / dense smoothers + collapsed AMG tail
   DPP_PU_MODE=flow            lane-group dataflow sweeps everywhere (k_trsv_flow, polled x slots)
-  DPP_PU_MODE=ws              warp-stream sweeps everywhere
+  DPP_PU_MODE=gs              global-stream sweeps everywhere
+  DPP_PU_MODE=ws              warp-stream sweeps (lane per row, per-warp TMA rings) everywhere
+  DPP_AMG_TAIL=0              launch-by-launch V-cycle on the small tail levels (no dense collapse)
   DPP_PU_MODE=lvl             level-mbarrier cluster sweeps (k_trsv_lvl: level teams, SELL chunks)
   DPP_PU_FLOW=0               level-synchronous push-exchange cluster sweeps (k_trsv_push)
   DPP_NO_PUSH=1               barrier-per-level cluster sweeps (tricluster.cu)
@@ -43,7 +46,9 @@ print(json.dumps({{"its": r.stats.iterations, "converged": bool(r.stats.converge
 VARIANTS = {
     "default": {},
     "lane_group_flow": {"DPP_PU_MODE": "flow"},
+    "global_stream": {"DPP_PU_MODE": "gs"},
     "warp_stream": {"DPP_PU_MODE": "ws"},
+    "no_tail_collapse": {"DPP_AMG_TAIL": "0"},
     "level_mbarrier": {"DPP_PU_MODE": "lvl"},
     "level_sync_push": {"DPP_PU_FLOW": "0"},
     "pull_cluster": {"DPP_NO_PUSH": "1"},

@@ -1,6 +1,6 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
-bash tools/ab_pc.sh "X=0" "DPP_WS_SLOTS=3" "DPP_WS_WARPS=10" "DPP_WS_WARPS=12" "DPP_WS_WARPS=6" "DPP_WS_WARPS=16" > gpurun_out/ws_ab.txt 2>&1
+L=$PWD/ab_libs
+bash tools/ab_pc.sh "X=0" "DPP_GS_NAP=10" "DPP_GS_NAP=20" "DPP_GS_NAP=40" "DPP_GS_NAP=80" "DPP_GS_NAP=160" "DPP_GS_WARPS=12 DPP_GS_NAP=20" "DPP_LIB=$L/gs_16_4.so" "DPP_LIB=$L/gs_16_4.so DPP_GS_NAP=20" > gpurun_out/ws_ab.txt 2>&1
 cat gpurun_out/ws_ab.txt
-python tools/ws_check.py 16 "DPP_PU_MODE=flow" "X=0" "DPP_PU_MODE=ws" 2>&1 | tail -4
-WS_TL_EXTRA="" bash tools/ws_tl.sh 2>&1 | grep -A2 "n=68921" | cut -c1-330
+nvcc -arch=sm_100a -O3 -o /tmp/fp64lat tools/micro/fp64lat.cu && /tmp/fp64lat
