@@ -14,5 +14,5 @@ PROF_REPS=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file gpurun_out/pc_dram.csv python tools/prof_pc.py > gpurun_out/prof_pc_dram.log 2>&1
 echo "dram pass rc=$?"
 PROF_RANGE=1 PROF_REPS=1 ncu --profile-from-start off --set full --clock-control none --import-source on \
-    -k regex:"k_trsv_flow|k_spmv|k_trsv_bd" -c 8 -o gpurun_out/${ROUND:-r02}_full python tools/prof_pc.py > gpurun_out/prof_full.log 2>&1
+    -k regex:"k_trsv_gs|k_spmv_sell|k_trsv_bd" -c 10 -o gpurun_out/${ROUND:-r02}_full python tools/prof_pc.py > gpurun_out/prof_full.log 2>&1
 echo "full capture rc=$?"

@@ -117,7 +117,7 @@ def full_summary(tag):
             if key in per:
                 per[key]["dram bytes (read+write)"] = d.get("dram__bytes_read.sum", "?") + " + " + \
                     d.get("dram__bytes_write.sum", "?")
-    lines = [f"ncu --set full --clock-control none --import-source on, kernels k_trsv_flow|k_spmv|k_trsv_bd "
+    lines = [f"ncu --set full --clock-control none --import-source on, kernels k_trsv_gs|k_spmv_sell|k_trsv_bd "
              f"of tools/prof_pc.py (C2 scale-split PC), report gpurun_out/{tag}_full.ncu-rep", ""]
     for k, d in per.items():
         lines.append(f"[{k}] {d.pop('name')}")
