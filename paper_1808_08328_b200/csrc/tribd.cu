@@ -304,6 +304,158 @@ __global__ void __launch_bounds__(BDI_THREADS)
     }
 }
 
+// ---------------------------------------------------------------- blocked dense inversion
+// inv(T[blk, blk]) by recursive doubling on the densified block (the default; the sparse
+// substitutions above cost ~0.4-0.55 ms per triangle, a third of the setup's kernel time at C2):
+//   32 x 32 diagonal sub-blocks by substitution (one warp each), then for s = 32, 64, ...
+//   [[A, 0], [C, B]]^-1 = [[A^-1, 0], [-B^-1 C A^-1, B^-1]]   (upper: [[A, C], [0, B]] -> -A^-1 C B^-1)
+// as two batched tile GEMMs per size over every pair of every block, in place (C is untouched
+// until its own size comes up).  Exact-arithmetic equal to the substitution; DPP_BD_INV=sparse
+// selects the old kernels.
+__global__ void k_ti_densify(int n, int B, const int *__restrict__ ptr, const int *__restrict__ idx,
+                             const double *__restrict__ val, const double *__restrict__ diag, double *D) {
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+        const int blk = r / B, a = r - blk * B;
+        double *row = D + ((size_t)blk * B + a) * B;
+        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32) {
+            const int j = idx[p];
+            if (j / B == blk) row[j - blk * B] = val[p];
+        }
+        if (lane == 0) row[a] = diag ? diag[r] : 1.0;
+    }
+}
+__global__ void __launch_bounds__(32) k_ti_inv32(int n, int B, int backward, double *D) {
+    __shared__ double Ts[32][33], Xs[32][33];
+    const int blk = blockIdx.y, m = min(B, n - blk * B), r0 = blockIdx.x * 32;
+    if (r0 >= m) return;
+    const int sz = min(32, m - r0), c = threadIdx.x;
+    double *Db = D + (size_t)blk * B * B + (size_t)r0 * B + r0;
+    for (int i = 0; i < sz; ++i) Ts[i][c] = c < sz ? Db[(size_t)i * B + c] : 0.0;
+    __syncwarp();
+    if (c < sz) {
+        if (!backward) {
+            Xs[c][c] = 1.0 / Ts[c][c];
+            for (int i = c + 1; i < sz; ++i) {
+                double acc = 0.0;
+                for (int j = c; j < i; ++j) acc += Ts[i][j] * Xs[j][c];
+                Xs[i][c] = -acc / Ts[i][i];
+            }
+        } else {
+            Xs[c][c] = 1.0 / Ts[c][c];
+            for (int i = c - 1; i >= 0; --i) {
+                double acc = 0.0;
+                for (int j = i + 1; j <= c; ++j) acc += Ts[i][j] * Xs[j][c];
+                Xs[i][c] = -acc / Ts[i][i];
+            }
+        }
+    }
+    __syncwarp();
+    for (int i = 0; i < sz; ++i)
+        if (c < sz) {
+            const bool in = backward ? i <= c : i >= c;
+            Db[(size_t)i * B + c] = in ? Xs[i][c] : 0.0;
+        }
+}
+// one 64 x 64 output tile of out = alpha X Y for pair blockIdx.z of size s (phase 0: W = C A or C B,
+// phase 1: C = -B W or -A W)
+constexpr int TI_T = 64, TI_K = 16;
+__global__ void __launch_bounds__(256) k_ti_gemm(int n, int B, int s, int phase, int backward, double *D, double *Wb) {
+    __shared__ double Xs[TI_K][TI_T + 1], Ys[TI_K][TI_T];
+    const int npairs = (B + 2 * s - 1) / (2 * s);
+    const int blk = blockIdx.z / npairs, pr = blockIdx.z % npairs;
+    const int m = min(B, n - blk * B), r0 = pr * 2 * s;
+    const int s2 = min(s, m - r0 - s);
+    if (s2 <= 0) return;
+    double *Db = D + (size_t)blk * B * B;
+    double *W = Wb + (size_t)blockIdx.z * s * s;
+    double *Ab = Db + (size_t)r0 * B + r0, *Bb = Db + (size_t)(r0 + s) * B + r0 + s;
+    double *Cb = backward ? Db + (size_t)r0 * B + r0 + s : Db + (size_t)(r0 + s) * B + r0;
+    // out (on x om, ldo) = alpha X (on x ok, ldx) Y (ok x om, ldy)
+    const double *X, *Y;
+    double *O;
+    int on, om, ok, ldx, ldy, ldo;
+    double alpha;
+    if (!backward) {
+        on = s2; om = s;
+        if (phase == 0) { X = Cb; ldx = B; Y = Ab; ldy = B; ok = s; O = W; ldo = s; alpha = 1.0; }
+        else { X = Bb; ldx = B; Y = W; ldy = s; ok = s2; O = Cb; ldo = B; alpha = -1.0; }
+    } else {
+        on = s; om = s2;
+        if (phase == 0) { X = Cb; ldx = B; Y = Bb; ldy = B; ok = s2; O = W; ldo = s; alpha = 1.0; }
+        else { X = Ab; ldx = B; Y = W; ldy = s; ok = s; O = Cb; ldo = B; alpha = -1.0; }
+    }
+    const int bi = blockIdx.y * TI_T, bj = blockIdx.x * TI_T;
+    if (bi >= on || bj >= om) return;
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < ok; k0 += TI_K) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = threadIdx.x + 256 * q;
+            const int ar = e >> 4, ak = e & 15;
+            Xs[ak][ar] = (bi + ar < on && k0 + ak < ok) ? X[(size_t)(bi + ar) * ldx + k0 + ak] : 0.0;
+            const int bk = e >> 6, bc = e & 63;
+            Ys[bk][bc] = (k0 + bk < ok && bj + bc < om) ? Y[(size_t)(k0 + bk) * ldy + bj + bc] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < TI_K; ++kk) {
+            double av[4], bv[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) av[a] = Xs[kk][ty + 16 * a];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) bv[b] = Ys[kk][tx + 16 * b];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int i = bi + ty + 16 * a;
+        if (i >= on) continue;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = bj + tx + 16 * b;
+            if (j < om) O[(size_t)i * ldo + j] = alpha * acc[a][b];
+        }
+    }
+}
+// dense = inv of every diagonal block (nb blocks of B x B, row-major, zero outside the triangle)
+static bool bd_inverse_gemm(Ctx *c, int n, int B, int nb, const Tri &T, double *dense) {
+    static const bool off = [] { const char *e = std::getenv("DPP_BD_INV"); return e && !std::strcmp(e, "sparse"); }();
+    if (off || T.ncomp != 1) return false;
+    const int mmax = std::min(B, n);
+    CK(cudaMemsetAsync(dense, 0, sizeof(double) * (size_t)nb * B * B, c->s));
+    k_ti_densify<<<grid_for((int64_t)n * 32, 256, c->sms, 8), 256, 0, c->s>>>(n, B, T.strict.ptr.p, T.strict.idx.p,
+                                                                            T.strict.val.p, T.diag.n ? T.diag.p : nullptr,
+                                                                            dense);
+    launched(c);
+    k_ti_inv32<<<dim3((mmax + 31) / 32, nb), 32, 0, c->s>>>(n, B, (int)T.backward, dense);
+    launched(c);
+    if (mmax > 32) {
+        size_t wmax = 0;
+        for (int s = 32; s < mmax; s *= 2) wmax = std::max(wmax, (size_t)nb * ((B + 2 * s - 1) / (2 * s)) * s * s);
+        DBuf<double> W(wmax, c->s);
+        for (int s = 32; s < mmax; s *= 2) {
+            const int npairs = (B + 2 * s - 1) / (2 * s), tiles = (s + TI_T - 1) / TI_T;
+            for (int phase = 0; phase < 2; ++phase) {
+                k_ti_gemm<<<dim3(tiles, tiles, nb * npairs), 256, 0, c->s>>>(n, B, s, phase, (int)T.backward, dense, W.p);
+                launched(c);
+            }
+        }
+        CK(cudaStreamSynchronize(c->s));   // W is freed on return
+    }
+    return true;
+}
+
 // G for an m-row block: the X tile plus flags within 200 KB
 static int bd_inv_g(int m) {
     for (int g : {32, 16, 8, 4})
@@ -513,6 +665,7 @@ static int bd_cluster_size() {
 void tri_dense_inverse(Ctx *c, Tri &T) {
     const int n = T.n;
     T.dense.alloc((size_t)n * n, c->s);
+    if (bd_inverse_gemm(c, n, n, 1, T, T.dense.p)) return;    // writes every entry
     if (bd_inverse_tiles(c, n, n, 1, T, T.dense.p)) return;   // writes every entry
     CK(cudaMemsetAsync(T.dense.p, 0, sizeof(double) * (size_t)n * n, c->s));
     const size_t sm = (size_t)BD_INV_WPB * n * sizeof(double);
@@ -571,7 +724,7 @@ bool bd_plan(Ctx *c, Tri &T, int B) {
             CK(cudaFuncSetAttribute(k_trsv_bd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD_SMEM_LIMIT));
             attr = true;
         }
-        if (!bd_inverse_tiles(c, n, B, P->nb, T, dense.p)) {
+        if (!bd_inverse_gemm(c, n, B, P->nb, T, dense.p) && !bd_inverse_tiles(c, n, B, P->nb, T, dense.p)) {
             dim3 grid((B + BD_INV_WPB - 1) / BD_INV_WPB, P->nb);
             k_bd_inverse<<<grid, 32 * BD_INV_WPB, sm, c->s>>>(n, B, T.backward, T.strict.ptr.p, T.strict.idx.p,
                                                                T.strict.val.p, T.diag.n ? T.diag.p : nullptr, dense.p);
