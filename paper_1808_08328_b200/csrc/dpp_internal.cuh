@@ -311,6 +311,12 @@ struct BdPlan {           // block-dense sweep: per-(block, CTA) segments of inv
     DBuf<unsigned char> segs;
     DBuf<long long> soff;
 };
+struct GbdPlan {          // global block-dense sweep: dense diagonal-block inverses + off-block CSR, two launches per block (tribd.cu)
+    int B = 0, nb = 0;
+    DBuf<double> dinv;    // nb x B x B, row-major, inverse of every diagonal block
+    Csr off;              // strict entries outside the row's diagonal block
+    DBuf<double> y;       // b - off x of the current block
+};
 struct Tri {              // one sweep: strict part (zero-free) + optional diagonal
     Csr strict;
     DBuf<double> diag;    // empty -> unit diagonal
@@ -320,6 +326,7 @@ struct Tri {              // one sweep: strict part (zero-free) + optional diago
     std::unique_ptr<PushPlan> pu;      // cluster-resident sweep, push exchange (preferred)
     std::unique_ptr<BlockPlan> bl;     // block-sequential sweep (small n, narrow levels)
     std::unique_ptr<BdPlan> bd;        // block-dense sweep (AMG smoother factors)
+    std::unique_ptr<GbdPlan> gbd;      // global block-dense sweep (long-row factors too large for one cluster's window)
     DBuf<double> dense;   // optional dense inverse (small coarse levels): sweep = triangular GEMV
     int ncomp = 1;        // Kronecker form: the triangle is this one (x) I_ncomp, rows interleaved
     Csr W;                // level-merged form (merge_levels): x = solve_unit(strict, W b)
@@ -342,6 +349,9 @@ bool bd_plan(Ctx *c, Tri &T, int B);
 void tri_dense_inverse(Ctx *c, Tri &T);
 void trsv_bd(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
              cudaStream_t st);
+bool gbd_plan(Ctx *c, Tri &T, int B);
+void trsv_gbd(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
+              cudaStream_t st);
 void trsv_block(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
                 cudaStream_t st);
 void trsv_cluster(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,

@@ -742,6 +742,126 @@ bool bd_plan(Ctx *c, Tri &T, int B) {
     return true;
 }
 
+// ---------------------------------------------------------------- global block-dense sweep
+// AMG smoother factors with long rows whose x window does not fit one cluster (C4: 16,604 rows,
+// 485 entries per row, 2,524 levels; C3: 44,433 rows, 3,065 levels): the same block recurrence
+// x_k = inv(T_kk) (b_k - sum_{j != k} T_kj x_j) as the cluster kernel above, but every block step
+// is two ordinary launches over the whole device -- the off-block rows as a warp-per-row SpMV
+// against x in global memory, then the block's rows of the dense inverse -- chained by
+// programmatic dependent launches inside the preconditioner's CUDA graph.  ceil(n / B) dependent
+// steps of a few microseconds each instead of thousands of levels.
+__global__ void k_gbd_count(int n, int B, const int *__restrict__ ptr, const int *__restrict__ idx, int *cnt) {
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+        int e = 0;
+        for (int p = ptr[r] + lane; p < ptr[r + 1]; p += 32) e += (idx[p] / B) != (r / B);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (lane == 0) cnt[r] = e;
+    }
+}
+__global__ void k_gbd_fill(int n, int B, const int *__restrict__ ptr, const int *__restrict__ idx,
+                           const double *__restrict__ val, const int *__restrict__ optr, int *oidx, double *oval) {
+    const int lane = threadIdx.x & 31;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += (gridDim.x * blockDim.x) >> 5) {
+        int w = optr[r];
+        for (int base = ptr[r]; base < ptr[r + 1]; base += 32) {
+            const int p = base + lane;
+            const bool keep = p < ptr[r + 1] && (idx[p] / B) != (r / B);
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int pos = w + __popc(m & ((1u << lane) - 1));
+                oidx[pos] = idx[p];
+                oval[pos] = val[p];
+            }
+            w += __popc(m);
+        }
+    }
+}
+// y[r] = b[r] - sum off[r, :] x for the rows [r0, r1) of one block (warp per row, entries in storage order per lane)
+__global__ void __launch_bounds__(256) k_gbd_off(int r0, int r1, const int *__restrict__ ptr, const int *__restrict__ idx,
+                                                 const double *__restrict__ val, const double *__restrict__ b,
+                                                 const double *x, double *y) {
+    const int lane = threadIdx.x & 31;
+    const int r = r0 + ((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (r >= r1) return;
+    const int p0 = ptr[r], p1 = ptr[r + 1];   // the plan is static: read before the predecessor ends
+    pdl_wait();
+    double acc = 0.0;
+    for (int p = p0 + lane; p < p1; p += 32) acc = fma(val[p], __ldcg(x + idx[p]), acc);   // x: other launches' output
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) y[r] = b[r] - acc;
+    pdl_trigger();
+}
+// x[r] = sum_j inv(T_kk)[a, j] y[s + j] over the triangle's half; xout = xadd + x
+__global__ void __launch_bounds__(256) k_gbd_inv(int s, int m, int B, int backward, const double *__restrict__ Di,
+                                                 const double *y, double *x, const double *xadd, double *xout) {
+    const int lane = threadIdx.x & 31;
+    const int a = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (a >= m) return;
+    const int j0 = backward ? a : 0, j1 = backward ? m : a + 1;
+    const double *row = Di + (size_t)a * B;
+    double dv[4];   // the first entries of the inverse's row while the predecessor finishes
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { const int j = j0 + lane + 32 * u; dv[u] = j < j1 ? row[j] : 0.0; }
+    pdl_wait();
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { const int j = j0 + lane + 32 * u; if (j < j1) acc = fma(dv[u], __ldcg(y + s + j), acc); }
+    for (int j = j0 + lane + 128; j < j1; j += 32) acc = fma(row[j], __ldcg(y + s + j), acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+        x[s + a] = acc;
+        if (xout) xout[s + a] = xadd[s + a] + acc;
+    }
+    pdl_trigger();
+}
+bool gbd_plan(Ctx *c, Tri &T, int B) {
+    DPP_TRACE_SCOPE(c, "tri.gbd_plan");
+    const int n = T.n;
+    if (n == 0 || B <= 0 || T.ncomp != 1) return false;
+    auto P = std::make_unique<GbdPlan>();
+    P->B = B;
+    P->nb = (n + B - 1) / B;
+    P->dinv.alloc((size_t)P->nb * B * B, c->s);
+    if (!bd_inverse_gemm(c, n, B, P->nb, T, P->dinv.p)) return false;
+    DBuf<int> cnt(n, c->s);
+    const int grid = grid_for((int64_t)n * 32, 256, c->sms, 8);
+    k_gbd_count<<<grid, 256, 0, c->s>>>(n, B, T.strict.ptr.p, T.strict.idx.p, cnt.p);
+    launched(c);
+    P->off.rows = n;
+    P->off.cols = n;
+    P->off.nnz = counts_to_ptr(c, cnt.p, n, P->off.ptr);
+    P->off.idx.alloc((size_t)P->off.nnz, c->s);
+    P->off.val.alloc((size_t)P->off.nnz, c->s);
+    k_gbd_fill<<<grid, 256, 0, c->s>>>(n, B, T.strict.ptr.p, T.strict.idx.p, T.strict.val.p, P->off.ptr.p, P->off.idx.p,
+                                       P->off.val.p);
+    launched(c);
+    P->y.alloc(n, c->s);
+    CK(cudaStreamSynchronize(c->s));
+    if (TraceScope::on())
+        std::fprintf(stderr, "[dpp-trace]   gbd_plan n=%d B=%d nb=%d off-block nnz %lld of %lld\n", n, B, P->nb,
+                     (long long)P->off.nnz, (long long)T.strict.nnz);
+    T.gbd = std::move(P);
+    return true;
+}
+void trsv_gbd(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout, cudaStream_t st) {
+    const GbdPlan &P = *T.gbd;
+    const int n = T.n, B = P.B;
+    for (int t = 0; t < P.nb; ++t) {
+        const int k = T.backward ? P.nb - 1 - t : t;
+        const int s = k * B, m = std::min(B, n - s);
+        CK(launch_pdl(k_gbd_off, dim3((m * 32 + 255) / 256), dim3(256), 0, st, s, s + m, (const int *)P.off.ptr.p,
+                      (const int *)P.off.idx.p, (const double *)P.off.val.p, b, (const double *)x, P.y.p));
+        launched(c);
+        CK(launch_pdl(k_gbd_inv, dim3((m * 32 + 255) / 256), dim3(256), 0, st, s, m, B, (int)T.backward,
+                      (const double *)(P.dinv.p + (size_t)k * B * B), (const double *)P.y.p, x, xadd, xout));
+        launched(c);
+    }
+}
+
 void trsv_bd(Ctx *c, const Tri &T, const double *b, double *x, const double *xadd, double *xout,
              cudaStream_t st) {
     const BdPlan &P = *T.bd;

@@ -483,6 +483,10 @@ void trsv(Ctx *c, const Tri &T, const double *b, double *x, int *ticket, const d
         trsv_bd(c, T, b, x, xadd, xout, st);
         return;
     }
+    if (T.gbd) {
+        trsv_gbd(c, T, b, x, xadd, xout, st);
+        return;
+    }
     if (T.bl) {
         trsv_block(c, T, b, x, xadd, xout, st);
         return;
@@ -700,6 +704,14 @@ Tri make_tri(Ctx *c, const Csr &A, bool lower, bool unit, bool allow_dense, DBuf
     static const int bd_b = [] { const char *e = std::getenv("DPP_BD_B"); return e ? std::atoi(e) : 512; }();
     if (allow_dense && T.n <= bd_max && bd_plan(c, T, std::min(bd_b, 1024))) {
         T.nlev = T.bd->nb;
+        return T;
+    }
+    // long-row smoother factors beyond that (deep coarse levels of configs 3/4: hundreds of entries
+    // per row, thousands of levels): the block recurrence with two device-wide launches per block
+    static const int gbd_max = [] { const char *e = std::getenv("DPP_GBD_MAX"); return e ? std::atoi(e) : 65536; }();
+    static const int gbd_row = [] { const char *e = std::getenv("DPP_GBD_ROW"); return e ? std::atoi(e) : 128; }();
+    if (allow_dense && T.n <= gbd_max && (double)T.strict.nnz >= (double)gbd_row * T.n && gbd_plan(c, T, 512)) {
+        T.nlev = T.gbd->nb;
         return T;
     }
     static const bool kron_on = [] { const char *e = std::getenv("DPP_KRON"); return !(e && *e == '0'); }();
