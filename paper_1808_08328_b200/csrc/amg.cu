@@ -1006,6 +1006,7 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
         L->A = std::move(cur);
         for (DBuf<double> *b : {&L->b, &L->x, &L->r, &L->t, &L->y}) b->alloc(n, c->s);
         L->ticket.alloc(4, c->s);
+        L->dg = std::move(d);   // this level's diagonal (kept for the smoother's shortcut residuals)
         CK(cudaStreamSynchronize(c->s));
         // level setup off the critical path, on two side streams / host threads: the
         // (D+L) sweep plan + SpMV plans, and the (D+U) sweep plan
@@ -1073,6 +1074,12 @@ std::unique_ptr<Amg> amg_setup(Ctx *c, const Csr &A0, double theta, double omega
 }
 
 // ---------------------------------------------------------------- V(1,1) cycle
+__global__ void k_mul_to(int64_t n, const double *__restrict__ a, const double *__restrict__ x, double *o) {
+    pdl_wait();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = a[i] * x[i];
+    pdl_trigger();
+}
 static void vc(Ctx *c, Amg &h, size_t l, const double *b, double *xo, cudaStream_t st) {
     AmgLevel &L = *h.lv[l];
     const int n = L.A.rows;
@@ -1089,6 +1096,34 @@ static void vc(Ctx *c, Amg &h, size_t l, const double *b, double *xo, cudaStream
         return;
     }
     AmgLevel &C = *h.lv[l + 1];
+    // Symmetric Gauss-Seidel as x += (D+L)^-1 (b - A x); x += (D+U)^-1 (b - A x) (reference
+    // linalg.py:383-385).  After the forward half-sweep with d = (D+L)^-1 r the new residual is
+    // r - A d = r - (D+L) d - U_s d = -U_s d, and (D+U)^-1 (-U_s d) = (D+U)^-1 D d - d: the backward
+    // half-sweep is x_old + (D+U)^-1 (D d) -- the same numbers in exact arithmetic without the
+    // second product with A (two SpMVs per level and cycle instead of four).  DPP_SGS_PLAIN=1 keeps
+    // the literal sequence.
+    static const bool plain = [] { const char *e = std::getenv("DPP_SGS_PLAIN"); return e && *e == '1'; }();
+    if (!plain && L.dg.n == (size_t)n && !L.lo.jacobi && !L.up.jacobi) {   // exact sweeps only
+        // pre-smoothing from x = 0: d = (D+L)^-1 b, x2 = (D+U)^-1 (D d)
+        trsv(c, L.lo, b, L.x.p, L.ticket.p, nullptr, nullptr, st);
+        CK(launch_pdl(k_mul_to, dim3(grid_for(n, 256, c->sms)), dim3(256), 0, st, (int64_t)n, (const double *)L.dg.p,
+                      (const double *)L.x.p, L.r.p));
+        launched(c);
+        trsv(c, L.up, L.r.p, L.t.p, L.ticket.p + 1, nullptr, nullptr, st);
+        // restriction of the residual, coarse correction, prolongation
+        spmv(c, L.A, L.t.p, L.r.p, b, -1.0, st);
+        spmv(c, L.R, L.r.p, C.b.p, nullptr, 1.0, st);
+        vc(c, h, l + 1, C.b.p, C.x.p, st);
+        spmv(c, L.P, C.x.p, L.x.p, L.t.p, 1.0, st);
+        // post-smoothing: d = (D+L)^-1 (b - A x3), x5 = x3 + (D+U)^-1 (D d)
+        spmv(c, L.A, L.x.p, L.r.p, b, -1.0, st);
+        trsv(c, L.lo, L.r.p, L.y.p, L.ticket.p + 2, nullptr, nullptr, st);
+        CK(launch_pdl(k_mul_to, dim3(grid_for(n, 256, c->sms)), dim3(256), 0, st, (int64_t)n, (const double *)L.dg.p,
+                      (const double *)L.y.p, L.r.p));
+        launched(c);
+        trsv(c, L.up, L.r.p, L.y.p, L.ticket.p + 3, L.x.p, xo, st);
+        return;
+    }
     // pre-smoothing, x starts at 0: x1 = (D+L)^-1 b ; x2 = x1 + (D+U)^-1 (b - A x1)
     trsv(c, L.lo, b, L.x.p, L.ticket.p, nullptr, nullptr, st);
     spmv(c, L.A, L.x.p, L.r.p, b, -1.0, st);

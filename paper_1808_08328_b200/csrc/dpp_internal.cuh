@@ -385,6 +385,7 @@ struct AmgLevel {
     DBuf<int> agg;             // aggregates (device)
     double rho = 0;
     DBuf<double> b, x, r, t, y; // workspace
+    DBuf<double> dg;           // diag(A): the Gauss-Seidel sweeps' shortcut residuals
     DBuf<int> ticket;
 };
 struct Amg {

@@ -10,6 +10,7 @@ bars: solution within 1e-9 relative, iterations within +-2.
   DPP_PU_MODE=gs              global-stream sweeps everywhere
   DPP_PU_MODE=ws              warp-stream sweeps (lane per row, per-warp TMA rings) everywhere
   DPP_AMG_TAIL=0              launch-by-launch V-cycle on the small tail levels (no dense collapse)
+  DPP_SGS_PLAIN=1             Gauss-Seidel half-sweeps with the literal residual b - A x (four SpMVs per level)
   DPP_PU_MODE=lvl             level-mbarrier cluster sweeps (k_trsv_lvl: level teams, SELL chunks)
   DPP_PU_FLOW=0               level-synchronous push-exchange cluster sweeps (k_trsv_push)
   DPP_NO_PUSH=1               barrier-per-level cluster sweeps (tricluster.cu)
@@ -49,6 +50,7 @@ VARIANTS = {
     "global_stream": {"DPP_PU_MODE": "gs"},
     "warp_stream": {"DPP_PU_MODE": "ws"},
     "no_tail_collapse": {"DPP_AMG_TAIL": "0"},
+    "plain_sgs_residuals": {"DPP_SGS_PLAIN": "1"},
     "level_mbarrier": {"DPP_PU_MODE": "lvl"},
     "level_sync_push": {"DPP_PU_FLOW": "0"},
     "pull_cluster": {"DPP_NO_PUSH": "1"},
