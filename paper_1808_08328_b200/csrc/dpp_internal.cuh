@@ -299,7 +299,12 @@ struct PushPlan {         // cluster sweep with st.async point-to-point x exchan
     DBuf<int> lrows;      // rows of each (CTA, level)
     DBuf<int> slev;       // fmt 1: level of each step
     int widest = 1;       // most rows (fmt 1: 32-row chunks) in one block (step)
-    int fmt = 0;          // block format: 0 row-major (k_trsv_flow / k_trsv_push), 1 SELL chunks (k_trsv_lvl)
+    int fmt = 0;          // block format: 0 row-major (k_trsv_flow / k_trsv_push), 1 SELL chunks (k_trsv_lvl),
+                          // 2 warp streams (k_trsv_ws), 3 global streams (k_trsv_gs)
+    // multi-cluster global streams (C > 16 CTA slices in clusters of 16): sources in another cluster
+    // are imported from x in global memory by an extra warp of the consumer CTA
+    DBuf<unsigned long long> imp;   // (source row << 32 | halo slot), by consumer CTA and source level
+    DBuf<int> istart;               // first import entry of each CTA slice (C + 1)
 };
 struct BlockPlan {        // block-sequential sweep with dense diagonal-block inverses (triblock.cu)
     int nblk = 0, stage = 0, nst = 0;

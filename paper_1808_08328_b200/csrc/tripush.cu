@@ -1130,21 +1130,29 @@ __device__ __forceinline__ unsigned long long ldg_u64(const void *p) {
 __device__ __forceinline__ double ldg_f64(const void *p) { return __longlong_as_double((long long)ldg_u64(p)); }
 
 __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
-    k_trsv_gs(int n, int ncomp, int chunk, int hmax, const unsigned char *__restrict__ blocks,
-              const long long *__restrict__ soff, const int *__restrict__ scnt, const double *__restrict__ b,
-              double *__restrict__ x, const double *__restrict__ xadd, double *__restrict__ xout, int nap) {
+    k_trsv_gs(int n, int ncomp, int chunk, int hmax, int CT, int rev, const unsigned char *__restrict__ blocks,
+              const long long *__restrict__ soff, const int *__restrict__ scnt,
+              const unsigned long long *__restrict__ imp, const int *__restrict__ istart,
+              const double *__restrict__ b, double *x, const double *__restrict__ xadd, double *__restrict__ xout,
+              int nap) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int nw = blockDim.x >> 5, wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = (blockDim.x >> 5) - (imp ? 1 : 0), wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int chunkp = pu_chunkp(chunk);
     double *xh = reinterpret_cast<double *>(smem);
     unsigned *peer = reinterpret_cast<unsigned *>(xh + chunkp + p16(8LL * hmax) / 8);
     cg::cluster_group cl = cg::this_cluster();
-    const int k = (int)cl.block_rank(), C = (int)cl.num_blocks();
-    const int comp = blockIdx.x / C;
+    const int C = (int)cl.num_blocks();
+    const int comp = blockIdx.x / CT;
+    // CTA slice of this block.  With several clusters the one without cross-cluster sources gets the
+    // lowest block index (a backward sweep's sources have higher rows), so a resident cluster only
+    // ever waits for clusters that were dispatched before it.
+    const int cid = (blockIdx.x % CT) / C, ncl = CT / C;
+    const int k = (rev ? ncl - 1 - cid : cid) * C + (int)cl.block_rank();
     const int base = k * chunk, mine = max(0, min(chunk, n - base));
     // the plan is static: this warp's first header and rows are in flight before the predecessor ends
-    const unsigned char *pc = blocks + soff[k * nw + wid];
-    const int NCH = scnt[k * nw + wid];
+    const bool importer = imp && wid == nw;
+    const unsigned char *pc = blocks + (importer ? 0 : soff[k * nw + wid]);
+    const int NCH = importer ? 0 : scnt[k * nw + wid];
     int4 hd = make_int4(0, 0, 0, 0);
     int rown = 0;
     if (NCH) {
@@ -1161,6 +1169,43 @@ __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     pdl_wait();   // b is the previous kernel's output
     const unsigned xh_s = su32(xh);
+    if (importer) {
+        // sources solved by another cluster: x in global memory (sentinel-filled before the launch,
+        // written by the owning lane) is polled and copied into this CTA's halo slots, 64 entries in
+        // flight, in the order of the sources' levels
+        const int i0 = istart[k], i1 = istart[k + 1];
+        for (int pos = i0; pos < i1; pos += 64) {
+            unsigned long long e[2];
+            bool done[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int i = pos + 32 * u + lane;
+                e[u] = i < i1 ? imp[i] : 0ull;
+                done[u] = i >= i1;
+            }
+            long long spins = 0;
+            while (true) {
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+                    if (!done[u]) {
+                        unsigned long long v;
+                        asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];"
+                                     : "=l"(v) : "l"(x + (size_t)(e[u] >> 32) * ncomp + comp) : "memory");
+                        if ((int)(v >> 32) != -1) {
+                            st_vol_shared(xh_s + 8u * (unsigned)(chunkp + (int)(e[u] & 0xffffffffu)),
+                                          __longlong_as_double((long long)v));
+                            done[u] = true;
+                        }
+                    }
+                if (__all_sync(0xffffffffu, done[0] && done[1])) break;
+                __nanosleep(100);
+                if (++spins > (1ll << 24)) __trap();
+            }
+        }
+        pdl_trigger();
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
     const unsigned long long zero4 = 0x0001000100010001ull * (unsigned long long)(chunkp + hmax - 1);
 #ifdef DPP_WS_PH
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pt = clock64(), pq = 0;
@@ -1306,7 +1351,7 @@ __global__ void k_pu_cross_fill(int n, int chunk, const int *ptr, const int *idx
 }
 // hstart[d] = first halo pair of consumer d (pairs sorted by (d, j))
 __global__ void k_pu_hstart(int nh, const unsigned long long *h, int C, int *hstart) {
-    const int d = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.x * blockDim.x + threadIdx.x;   // one thread per CTA slice (+ the terminator)
     if (d > C) return;
     const unsigned long long key = (unsigned long long)d << 32;
     int lo = 0, hi = nh;
@@ -1316,21 +1361,36 @@ __global__ void k_pu_hstart(int nh, const unsigned long long *h, int C, int *hst
     }
     hstart[d] = lo;
 }
-// push pairs keyed by source row: (j << 4 | d) -> slot; byte counts per (consumer, level of j)
-__global__ void k_pu_push_keys(int nh, const unsigned long long *h, const int *hstart, int L, const int *lev,
-                               unsigned long long *k2, int *slot, int *tx) {
+// push pairs keyed by source row: (j << 8 | d) -> slot; byte counts per (consumer, level of j).
+// A pair whose source row lives in another cluster (multi-cluster sweeps: CTA slices beyond 16)
+// cannot be pushed through distributed shared memory: it leaves the push lists (key past every
+// row) and goes to the consumer's import list (k_pu_import_keys).
+__global__ void k_pu_push_keys(int nh, const unsigned long long *h, const int *hstart, int L, const int *lev, int n,
+                               int chunk, unsigned long long *k2, int *slot, int *tx) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
         const int d = (int)(h[i] >> 32), j = (int)(h[i] & 0xffffffffu);
-        k2[i] = ((unsigned long long)j << 4) | (unsigned)d;
+        const bool cross = (d >> 4) != ((j / chunk) >> 4);
+        k2[i] = ((unsigned long long)(cross ? n : j) << 8) | (unsigned)d;   // cross-cluster pairs sort past every row
         slot[i] = i - hstart[d];
-        atomicAdd(&tx[d * L + lev[j]], 8);
+        if (!cross) atomicAdd(&tx[d * L + lev[j]], 8);
+    }
+}
+// import pairs keyed by (consumer CTA, level of the source row) -> (source row << 32 | halo slot)
+__global__ void k_pu_import_keys(int nh, const unsigned long long *h, const int *hstart, const int *lev, int chunk,
+                                 unsigned long long *ik, unsigned long long *iv, int *ncross) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nh; i += gridDim.x * blockDim.x) {
+        const int d = (int)(h[i] >> 32), j = (int)(h[i] & 0xffffffffu);
+        const bool cross = (d >> 4) != ((j / chunk) >> 4);
+        ik[i] = cross ? (((unsigned long long)d << 32) | (unsigned)lev[j]) : ~0ull;
+        iv[i] = ((unsigned long long)j << 32) | (unsigned)(i - hstart[d]);
+        if (cross) atomicAdd(ncross, 1);
     }
 }
 // pptr[j] = first push pair of source row j
 __global__ void k_pu_pptr(int nh, const unsigned long long *k2s, int n, int *pptr) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= nh; i += gridDim.x * blockDim.x) {
-        const int v = i < nh ? (int)(k2s[i] >> 4) : n;
-        const int prev = i ? (int)(k2s[i - 1] >> 4) : -1;
+        const int v = i < nh ? (int)(k2s[i] >> 8) : n;
+        const int prev = i ? (int)(k2s[i - 1] >> 8) : -1;
         for (int j = prev + 1; j <= v && j <= n; ++j) pptr[j] = i;
     }
 }
@@ -1406,7 +1466,7 @@ __global__ void k_pu_fill(int n, int chunk, int chunkp, int np_, const int *psta
         }
         int u = p0;
         for (int t = pptr[r]; t < pptr[r + 1]; ++t, ++u)
-            pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28) | (unsigned)slots[t]);
+            pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28 /* rank in the cluster */) | (unsigned)slots[t]);
     }
 }
 
@@ -1502,7 +1562,7 @@ __global__ void k_lv_fill(int n, int chunk, int chunkp, int zero_code, int np_, 
             }
         int u = p0;
         for (int t = pptr[r]; t < pptr[r + 1]; ++t, ++u)
-            pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28) | (unsigned)slots[t]);
+            pl[u] = (int)(((unsigned)(k2s[t] & 15u) << 28 /* rank in the cluster */) | (unsigned)slots[t]);
     }
 }
 
@@ -1671,6 +1731,7 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     const int chunk = (n + C - 1) / C;
     const int nblk = C * L;
     if (chunk >= (1 << 16)) return false;   // local row index in 16 bits of the row header
+    if (C > 16 && gs_smem(chunk, 1024) > PU_SMEM_LIMIT) return false;   // before any work: the x slice alone is too large
     const Csr &S = T.strict;
     // rows grouped by (owner CTA, level)
     DBuf<int> key(n, c->s), skey(n, c->s), rows(n, c->s), perm(n, c->s), lp((size_t)nblk + 1, c->s);
@@ -1711,7 +1772,7 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
         nh = nsel.to_host()[0];
     }
     DBuf<int> hstart(C + 1, c->s);
-    k_pu_hstart<<<1, 32, 0, c->s>>>(nh, H.p, C, hstart.p);
+    k_pu_hstart<<<(C + 32) / 32, 32, 0, c->s>>>(nh, H.p, C, hstart.p);
     launched(c);
     std::vector<int> hh = hstart.to_host();
     int hmax = 0;
@@ -1724,15 +1785,15 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     P->tx.alloc((size_t)C * L, c->s);
     CK(cudaMemsetAsync(P->tx.p, 0, sizeof(int) * (size_t)C * L, c->s));
     if (nh > 0) {
-        k_pu_push_keys<<<grid_for(nh, 256, c->sms), 256, 0, c->s>>>(nh, H.p, hstart.p, L, lev.p, k2.p, slot.p,
+        k_pu_push_keys<<<grid_for(nh, 256, c->sms), 256, 0, c->s>>>(nh, H.p, hstart.p, L, lev.p, n, chunk, k2.p, slot.p,
                                                                     P->tx.p);
         launched(c);
         int nb = 1;
         while (nb < 31 && (1LL << nb) <= n) ++nb;
         size_t tb = 0;
-        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k2.p, k2s.p, slot.p, slots.p, nh, 0, 4 + nb, c->s));
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, k2.p, k2s.p, slot.p, slots.p, nh, 0, 8 + nb, c->s));
         DBuf<char> t(tb, c->s);
-        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, k2.p, k2s.p, slot.p, slots.p, nh, 0, 4 + nb, c->s));
+        CK(cub::DeviceRadixSort::SortPairs(t.p, tb, k2.p, k2s.p, slot.p, slots.p, nh, 0, 8 + nb, c->s));
         launched(c);
     }
     k_pu_pptr<<<grid_for(nh + 1, 256, c->sms), 256, 0, c->s>>>(nh, k2s.p, n, pptr.p);
@@ -1825,7 +1886,7 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     };
     auto gs_plan = [&]() -> bool {   // global streams (k_trsv_gs): no ring, x slice + halo in shared memory
         static const int nw_env = [] { const char *e = std::getenv("DPP_GS_WARPS"); return e ? std::atoi(e) : 16; }();
-        const int NW = std::max(1, std::min(GS_WARPS_MAX, nw_env));
+        const int NW = std::max(1, std::min(GS_WARPS_MAX - (C > 16 ? 1 : 0), nw_env));   // + an importer warp beyond one cluster
         if (gs_smem(chunk, hmax) > PU_SMEM_LIMIT) return false;
         // chunks: the rows of a (CTA, level) cut evenly into ceil(rows / 32) chunks
         std::vector<int4> ctab;
@@ -1864,6 +1925,26 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
         P->C = C; P->chunk = chunk; P->L = L; P->hmax = hmax; P->smax = 0;
         P->stage = 128; P->nst = 1;   // unused (no ring); kept non-zero for the shared launch arithmetic
         P->threads = 32 * NW; P->fmt = 3; P->G = 1; P->widest = 1;
+        if (C > 16) {   // several clusters: the cross-cluster halo pairs, by consumer and source level
+            if (nh == 0) return false;
+            DBuf<unsigned long long> ik(nh, c->s), iks(nh, c->s), iv(nh, c->s);
+            DBuf<int> ncross(1, c->s);
+            CK(cudaMemsetAsync(ncross.p, 0, sizeof(int), c->s));
+            P->imp.alloc(nh, c->s);
+            k_pu_import_keys<<<grid_for(nh, 256, c->sms), 256, 0, c->s>>>(nh, H.p, hstart.p, lev.p, chunk, ik.p, iv.p,
+                                                                          ncross.p);
+            launched(c);
+            size_t tb = 0;
+            CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ik.p, iks.p, iv.p, P->imp.p, nh, 0, 64, c->s));
+            DBuf<char> t(tb, c->s);
+            CK(cub::DeviceRadixSort::SortPairs(t.p, tb, ik.p, iks.p, iv.p, P->imp.p, nh, 0, 64, c->s));
+            launched(c);
+            P->istart.alloc(C + 1, c->s);
+            k_pu_hstart<<<(C + 32) / 32, 32, 0, c->s>>>(nh, iks.p, C, P->istart.p);
+            launched(c);
+            CK(cudaStreamSynchronize(c->s));   // the key buffers are freed on return
+            P->threads = 32 * (NW + 1);        // + the importer warp
+        }
         P->blocks.alloc((size_t)cur + 8192 + 4096, c->s);   // slack: the L2 prefetch of a stream's last chunk
         P->boff.alloc(soff.size(), c->s);
         P->boff.upload(soff.data(), soff.size());
@@ -1880,15 +1961,16 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
         launched(c);
         CK(cudaStreamSynchronize(c->s));
         if (TraceScope::on())
-            std::fprintf(stderr, "[dpp-trace]   gs_plan n=%d C=%d L=%d chunks %d warps %d halo max %d bytes=%lld\n", n, C, L,
-                         nchunks, NW, hmax, cur);
+            std::fprintf(stderr, "[dpp-trace]   gs_plan n=%d C=%d (%d clusters) L=%d chunks %d warps %d halo max %d bytes=%lld\n",
+                         n, C, (C + 15) / 16, L, nchunks, NW, hmax, cur);
         T.pu = std::move(P);
         return true;
     };
+    if (C > 16 && (fmt != 2 || pu_mode() == 3)) return false;   // only the global-stream kernel spans clusters
     if (fmt == 2) {
         ++hmax;   // one zero slot after the halo: the padding entries' source
         if (pu_chunkp(chunk) + hmax < (1 << 16) && (pu_mode() == 3 ? ws_plan() : gs_plan())) return true;   // 16-bit column codes
-        if (pu_mode() == 3 || pu_mode() == 5) return false;
+        if (pu_mode() == 3 || pu_mode() == 5 || C > 16) return false;
         --hmax;   // auto: the row-major plan instead
         fmt = 0;
     }
@@ -2080,8 +2162,18 @@ bool push_plan(Ctx *c, Tri &T, const DBuf<int> &lev, int L) {
     }
     // as many CTAs as useful: each keeps >= ~2k rows of x
     const int C0 = std::max(2, std::min(PU_MAX, (n + 2047) / 2048));
-    for (int C = C0; C <= PU_MAX; ++C)
+    // DPP_GS_MIN_CLUSTERS > 1 (tests): skip the single-cluster plans
+    static const int cl_min = [] { const char *e = std::getenv("DPP_GS_MIN_CLUSTERS"); return e ? std::atoi(e) : 1; }();
+    for (int C = C0; C <= PU_MAX && cl_min <= 1; ++C)
         if (try_push(c, T, lev, L, C)) return true;
+    // x too large for one cluster's shared memory: thin-row triangles spread over several clusters
+    // of 16 (global-stream kernel, cross-cluster sources imported from global memory)
+    static const int cl_max = [] { const char *e = std::getenv("DPP_GS_CLUSTERS"); return e ? std::atoi(e) : 9; }();
+    if (pu_use_ws((double)T.strict.nnz / n) && pu_mode() != 3 && !T.W.rows)
+        for (int ncl = std::max(2, cl_min); ncl <= cl_max; ++ncl) {
+            if ((n + 16 * ncl - 1) / (16 * ncl) >= (1 << 16)) continue;   // slices still too long
+            if (try_push(c, T, lev, L, 16 * ncl)) return true;
+        }
     return false;
 }
 
@@ -2153,8 +2245,15 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
             cudaEventRecord(pe0w, st);
         }
 #endif
-        CK(cudaLaunchKernelEx(&cfg, k_trsv_gs, T.n / T.ncomp, T.ncomp, P.chunk, P.hmax, B, O, (const int *)P.sstart.p, b, x,
-                              xadd, xout, nap));
+        const bool multi = P.C > 16;
+        if (multi) {   // the importers poll x: nothing of the previous sweep may look solved
+            CK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)T.n, st));
+            cfg.gridDim = dim3(P.C * T.ncomp, 1, 1);
+            at[0].val.clusterDim.x = 16;
+        }
+        CK(cudaLaunchKernelEx(&cfg, k_trsv_gs, T.n / T.ncomp, T.ncomp, P.chunk, P.hmax, P.C, (int)T.backward, B, O,
+                              (const int *)P.sstart.p, multi ? (const unsigned long long *)P.imp.p : nullptr,
+                              multi ? (const int *)P.istart.p : nullptr, b, x, xadd, xout, nap));
         launched(c);
 #ifdef DPP_WS_PH
         if (phw) {

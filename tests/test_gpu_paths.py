@@ -8,6 +8,9 @@ bars: solution within 1e-9 relative, iterations within +-2.
                               (k_trsv_flow) + block-dense / dense smoothers + collapsed AMG tail
   DPP_PU_MODE=flow            lane-group dataflow sweeps everywhere (k_trsv_flow, polled x slots)
   DPP_PU_MODE=gs              global-stream sweeps everywhere
+  DPP_GS_MIN_CLUSTERS=2       global-stream sweeps spread over two clusters of 16 CTAs (the form triangles too
+                              large for one cluster's shared memory take): cross-cluster sources imported from
+                              global memory by an extra warp
   DPP_PU_MODE=ws              warp-stream sweeps (lane per row, per-warp TMA rings) everywhere
   DPP_AMG_TAIL=0              launch-by-launch V-cycle on the small tail levels (no dense collapse)
   DPP_SGS_PLAIN=1             Gauss-Seidel half-sweeps with the literal residual b - A x (four SpMVs per level)
@@ -48,6 +51,7 @@ VARIANTS = {
     "default": {},
     "lane_group_flow": {"DPP_PU_MODE": "flow"},
     "global_stream": {"DPP_PU_MODE": "gs"},
+    "multi_cluster_stream": {"DPP_GS_MIN_CLUSTERS": "2"},
     "warp_stream": {"DPP_PU_MODE": "ws"},
     "no_tail_collapse": {"DPP_AMG_TAIL": "0"},
     "plain_sgs_residuals": {"DPP_SGS_PLAIN": "1"},
