@@ -1710,10 +1710,12 @@ inline int pu_lane_group(double avg) {
     while (G < 32 && G * 4 < avg) G *= 2;
     return G;
 }
-// a lane per row pays off while a row is a few 4-column groups long (C2: ILU 7, AMG level 0
-// 26 entries per row); the long rows of configs 3/4 measured slower (C4 PC apply 47 -> 68 ms)
+// a lane per row: measured on the global-stream kernel for every row length the configs have
+// (C2: 7 / 26 entries per row; C3 level 0: 58, PC apply 18.7 -> 12.2 ms; C4 level 1: 74, 26.2 -> 25.5 ms).
+// The TMA-ring warp streams were slower on the long rows (C4 PC apply 47 -> 68 ms): DPP_WS_GMAX caps
+// the lane-group width (4 entries per lane) up to which a lane-per-row kernel is chosen.
 inline bool pu_use_ws(double avg) {
-    static const int gmax = [] { const char *e = std::getenv("DPP_WS_GMAX"); return e ? std::atoi(e) : 8; }();
+    static const int gmax = [] { const char *e = std::getenv("DPP_WS_GMAX"); return e ? std::atoi(e) : 32; }();
     return pu_mode() == 3 || pu_mode() == 5 || (pu_mode() == 4 && pu_lane_group(avg) <= gmax);
 }
 
