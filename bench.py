@@ -71,12 +71,46 @@ def measured_peak():
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region."""
+    """SM clock / throttle-reason sampler for the timed region: NVML in-process (a thread
+    polling every 20 ms; initialised before the warm-up so that no process start-up or
+    NVML initialisation falls into the timed steps), nvidia-smi -lms as the fallback."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index=0):
         self.rows, self.proc, self.index = [], None, index
+        self.nvml, self.handle, self.run, self.thread, self.mx = None, None, False, None, None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
+            self.nvml = pynvml
+        except Exception:
+            self.nvml = None
+
+    def _poll(self):
+        nv = self.nvml
+        while self.run:
+            try:
+                sm = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
+                rs = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle))
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def mark(self):
+        """Start of the timed region: earlier samples (taken during the warm-up, so that the sampler's
+        own start-up cost stays outside the timed steps) are dropped."""
+        self.rows = []
 
     def start(self):
+        if self.nvml:
+            self.run = True
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index),
@@ -94,6 +128,18 @@ class Clocks:
             self.rows.append([s.strip() for s in line.split(",")])
 
     def stop(self):
+        if self.nvml:
+            self.run = False
+            if self.thread:
+                self.thread.join(1.0)
+            sm = [r[0] for r in self.rows]
+            reasons = set()
+            for _, rs in self.rows:
+                for bit, nm in self.REASONS.items():
+                    if rs & bit:
+                        reasons.add(nm)
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.mx,
+                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
         if self.proc:
             self.proc.terminate()
             try:
@@ -110,7 +156,7 @@ class Clocks:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi"}
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -158,13 +204,14 @@ def gpu_arm(args, rank, world):
             raise RuntimeError(f"bench solve did not converge: its={st.iterations} "
                                f"relres={st.relative_residual:.3e} reason={st.reason}")
 
+    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()   # sampling already during the warm-up: no sampler start-up inside the timed region
     for _ in range(args.warmup):
         s, pc, st = device_step()
         check(st)
         release(s, pc)
     dist_barrier(world)
-    clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
-    clocks.start()
+    clocks.mark()
     l0 = N.launches()
     times, its = [], []
     for _ in range(args.steps):
@@ -175,6 +222,7 @@ def gpu_arm(args, rank, world):
         check(st)
         times.append(ms.value)
         its.append(st.iterations)
+        print(f"[bench] device step {_}: {ms.value:.1f} ms", file=sys.stderr, flush=True)
         if _ < args.steps - 1:
             release(s, pc)
     launches = N.launches() - l0
