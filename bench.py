@@ -71,92 +71,67 @@ def measured_peak():
 
 
 class Clocks:
-    """SM clock / throttle-reason sampler for the timed region: NVML in-process (a thread
-    polling every 20 ms; initialised before the warm-up so that no process start-up or
-    NVML initialisation falls into the timed steps), nvidia-smi -lms as the fallback."""
+    """SM clock / throttle-reason samples of the timed region through NVML, taken in this thread
+    between the timed steps (right after a step's stop event, while the clocks are still at their
+    load level).  A background sampler -- an nvidia-smi child, or a thread polling NVML every
+    20 ms -- was measured to stall single steps by 50-120 ms (the queries take the driver's lock),
+    which is not the GPU's time.  nvidia-smi is the fallback when pynvml is missing."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index=0):
-        self.rows, self.proc, self.index = [], None, index
-        self.nvml, self.handle, self.run, self.thread, self.mx = None, None, False, None, None
+        self.rows, self.index, self.mx = [], index, None
+        self.nvml, self.handle = None, None
         try:
             import pynvml
             pynvml.nvmlInit()
             self.handle = pynvml.nvmlDeviceGetHandleByIndex(index)
             self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM))
             self.nvml = pynvml
+            self.sample()          # first queries (slow) outside the timed region
+            self.rows = []
         except Exception:
             self.nvml = None
 
-    def _poll(self):
-        nv = self.nvml
-        while self.run:
+    def sample(self):
+        if self.nvml:
             try:
-                sm = float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM))
-                rs = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle))
-                self.rows.append((sm, rs))
+                nv = self.nvml
+                self.rows.append((float(nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)),
+                                  int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle))))
             except Exception:
                 pass
-            time.sleep(0.02)
-
-    def mark(self):
-        """Start of the timed region: earlier samples (taken during the warm-up, so that the sampler's
-        own start-up cost stays outside the timed steps) are dropped."""
-        self.rows = []
-
-    def start(self):
-        if self.nvml:
-            self.run = True
-            self.thread = threading.Thread(target=self._poll, daemon=True)
-            self.thread.start()
             return
         try:
-            self.proc = subprocess.Popen(
+            out = subprocess.run(
                 ["nvidia-smi", "-i", str(self.index),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            threading.Thread(target=self._read, daemon=True).start()
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits"],
+                capture_output=True, text=True, timeout=10).stdout.strip().splitlines()[0]
+            f = [v.strip() for v in out.split(",")]
+            rs = 0
+            for bit, v in zip((0x8, 0x40, 0x20, 0x4), f[2:6]):
+                if v.lower() == "active":
+                    rs |= bit
+            self.rows.append((float(f[0]), rs))
+            self.mx = float(f[1])
         except Exception:
-            self.proc = None
+            pass
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([s.strip() for s in line.split(",")])
+    def mark(self):
+        self.rows = []
 
     def stop(self):
-        if self.nvml:
-            self.run = False
-            if self.thread:
-                self.thread.join(1.0)
-            sm = [r[0] for r in self.rows]
-            reasons = set()
-            for _, rs in self.rows:
-                for bit, nm in self.REASONS.items():
-                    if rs & bit:
-                        reasons.add(nm)
-            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.mx,
-                    "reasons": sorted(reasons), "samples": len(sm), "source": "nvml"}
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        sm = [r[0] for r in self.rows]
         reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            for k, nm in enumerate(names):
-                if len(r) > 3 + k and r[3 + k].lower() == "active":
+        for _, rs in self.rows:
+            for bit, nm in self.REASONS.items():
+                if rs & bit:
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm), "source": "nvidia-smi"}
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml, between timed steps" if self.nvml else "nvidia-smi, between timed steps"}
 
 
 # --------------------------------------------------------------------------- GPU arm
@@ -205,7 +180,6 @@ def gpu_arm(args, rank, world):
                                f"relres={st.relative_residual:.3e} reason={st.reason}")
 
     clocks = Clocks(int(os.environ.get("LOCAL_RANK", "0")))
-    clocks.start()   # sampling already during the warm-up: no sampler start-up inside the timed region
     for _ in range(args.warmup):
         s, pc, st = device_step()
         check(st)
@@ -222,6 +196,7 @@ def gpu_arm(args, rank, world):
         check(st)
         times.append(ms.value)
         its.append(st.iterations)
+        clocks.sample()   # inside the timed region, outside the step's own event pair
         print(f"[bench] device step {_}: {ms.value:.1f} ms", file=sys.stderr, flush=True)
         if _ < args.steps - 1:
             release(s, pc)

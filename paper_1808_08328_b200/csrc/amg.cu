@@ -741,7 +741,16 @@ __global__ void k_spmm(int rows, int m, const int *__restrict__ ptr, const int *
     const int p0 = ptr[r], p1 = ptr[r + 1];
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
         double s = 0.0;
-        for (int p = p0; p < p1; ++p) s += val[p] * X[(int64_t)idx[p] * m + j];
+        int p = p0;
+        for (; p + 4 <= p1; p += 4) {   // four rows of X in flight (the sum keeps the storage order)
+            const double x0 = X[(int64_t)idx[p] * m + j], x1 = X[(int64_t)idx[p + 1] * m + j];
+            const double x2 = X[(int64_t)idx[p + 2] * m + j], x3 = X[(int64_t)idx[p + 3] * m + j];
+            s += val[p] * x0;
+            s += val[p + 1] * x1;
+            s += val[p + 2] * x2;
+            s += val[p + 3] * x3;
+        }
+        for (; p < p1; ++p) s += val[p] * X[(int64_t)idx[p] * m + j];
         double y = alpha * s;
         if (Z) y += Z[(int64_t)r * m + j];
         if (add_identity && j == r) y += 1.0;

@@ -1,6 +1,5 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
 rm -f gpurun_out/ws_ph.txt
-DPP_LIB=$PWD/ab_libs/wsph.so DPP_WS_PH=$PWD/gpurun_out/ws_ph.txt DPP_PC_NOGRAPH=1 PROF_REPS=1 timeout 300 python tools/prof_pc.py > gpurun_out/ws_ph.log 2>&1; echo "ph rc=$?"
-python tools/ws_phases.py gpurun_out/ws_ph.txt | cut -c1-300
-bash tools/ab_pc.sh "X=0" "DPP_BD_B=1024" "DPP_BD_B=256" "DPP_LIB=$PWD/ab_libs/wsph.so"
+PROF_CFG=${PROF_CFG:-C4} DPP_LIB=$PWD/ab_libs/wsph.so DPP_WS_PH=$PWD/gpurun_out/ws_ph.txt DPP_PC_NOGRAPH=1 PROF_REPS=1 timeout 600 python tools/prof_pc.py > gpurun_out/ws_ph.log 2>&1; echo "ph rc=$?"
+python tools/ws_phases.py gpurun_out/ws_ph.txt | cut -c1-260

@@ -20,7 +20,10 @@ for s in secs:
     seen.add(key)
     a = np.array(s["rows"], dtype=np.float64)
     print("==", s["hdr"], f"({float(hdr['us']) * 1e3 / int(hdr['L']):.0f} ns/level)")
-    for cta in (0, 1, int(hdr["C"]) // 2, int(hdr["C"]) - 1):
+    C = int(hdr["C"])
+    for cta in sorted(set([0, 1, 15, 16, 17, C // 2, C - 17, C - 16, C - 1])):
+        if cta < 0 or cta >= C:
+            continue
         c = a[a[:, 0] == cta]
         ch = c[:, 8].sum()
         if ch == 0:
