@@ -1307,6 +1307,12 @@ __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
         pc = pnx;
 #ifdef DPP_WS_PH
         ph[6] += 1;
+        {
+            unsigned long long gt;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+            if (ci == 0) ph[3] = gt;   // first chunk of this warp solved (ns)
+            ph[4] = gt;                // last one
+        }
 #endif
         GS_PH(2, pt);
     }
@@ -2252,6 +2258,12 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
             CK(cudaMemsetAsync(x, 0xFF, sizeof(double) * (size_t)T.n, st));
             cfg.gridDim = dim3(P.C * T.ncomp, 1, 1);
             at[0].val.clusterDim.x = 16;
+            if (TraceScope::on() && !c->capturing) {
+                int nact = -1;
+                cudaOccupancyMaxActiveClusters(&nact, k_trsv_gs, &cfg);
+                std::fprintf(stderr, "[dpp-trace]   gs launch n=%d: %d clusters of 16, %zu B shared per CTA, co-resident clusters %d\n",
+                             T.n, P.C / 16, (size_t)cfg.dynamicSmemBytes, nact);
+            }
         }
         CK(cudaLaunchKernelEx(&cfg, k_trsv_gs, T.n / T.ncomp, T.ncomp, P.chunk, P.hmax, P.C, (int)T.backward, B, O,
                               (const int *)P.sstart.p, multi ? (const unsigned long long *)P.imp.p : nullptr,
