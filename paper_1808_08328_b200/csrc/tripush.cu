@@ -1093,7 +1093,7 @@ __global__ void __launch_bounds__(512, 1)
 // Same partition, halo / push tables, level-sorted right-aligned rows, NaN-sentinel readiness
 // and arithmetic (four partial sums per row) as k_trsv_ws.
 //
-// chunk (16-byte aligned segments): int4 {groups, w, np, 0} | u16 local row[w] | f64 1/diag[w] |
+// chunk (16-byte aligned segments): int4 {groups, w, np, level} | u16 local row[w] | f64 1/diag[w] |
 //   int (p0 << 4 | npush)[w] | int2 first two push entries[w] | int push[np] |
 //   groups x { u16 code[w][4] | f64 val[4][w] }
 #ifndef DPP_GS_WARPS_MAX
@@ -1118,6 +1118,9 @@ __host__ __device__ inline size_t gs_smem(int chunk, int hmax) {   // x slice | 
 #ifdef DPP_WS_PH
 // phase build: per (CTA, warp) cycles summed over its chunks {head, loads + groups, tail, -, -, polls, chunks, -}
 __device__ unsigned long long *g_ws_ph = nullptr;
+// CTA 0 only: per (warp, chunk) {level, t last group entered, t its inputs were there, t x stored} (clock64)
+__device__ unsigned long long *g_ws_hop = nullptr;
+constexpr int GS_HOP_MAX = 256;
 #define GS_PH(i, t0_) { const unsigned long long t_ = clock64(); ph[i] += t_ - (t0_); (t0_) = t_; }
 #else
 #define GS_PH(i, t0_)
@@ -1212,6 +1215,10 @@ __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
 #endif
     for (int ci = 0; ci < NCH; ++ci) {
         const int ng = hd.x, w = hd.y, np = hd.z;
+#ifdef DPP_WS_PH
+        const int hd_lev = hd.w;
+        unsigned long long hop1 = 0, hop2 = 0, hop3 = 0;
+#endif
         DPP_DCHECK(w >= 1 && w <= 32 && ng >= 0 && np >= 0);
         const bool act = lane < w;
         const int row = act ? rown : 0;
@@ -1266,6 +1273,7 @@ __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
                 long long spins = 0;
 #ifdef DPP_WS_PH
                 pq = clock64();
+                if (g0 + j == ng - 1) hop1 = pq;
 #endif
                 // the sentinel is the only stored value whose high word is all ones (a computed NaN is
                 // stored as the canonical quiet NaN), and 8-byte shared accesses are single transactions
@@ -1281,7 +1289,11 @@ __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
                     if (++spins > (1ll << 26)) __trap();
                 }
 #ifdef DPP_WS_PH
-                ph[5] += clock64() - pq;
+                {
+                    const unsigned long long tq = clock64();
+                    ph[5] += tq - pq;
+                    if (g0 + j == ng - 1) hop2 = tq;
+                }
 #endif
                 s0 = fma(v[j][0], xv[0], s0);
                 s1 = fma(v[j][1], xv[1], s1);
@@ -1294,6 +1306,9 @@ __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
             double xr = (bq - ((s0 + s1) + (s2 + s3))) * dq;   // dq = 1/t_ii
             if (__double2hiint(xr) == -1) xr = __longlong_as_double(0x7ff8000000000000ll);   // a NaN that looks pending
             st_vol_shared(xh_s + 8u * (unsigned)row, xr);
+#ifdef DPP_WS_PH
+            hop3 = clock64();
+#endif
             const int p0 = pinf >> 4, pn = pinf & 15;
             for (int u = 0; u < pn; ++u) {
                 const int pe = u < 2 ? (int)(p2 >> (32 * u)) : pl[p0 + u];
@@ -1307,6 +1322,10 @@ __global__ void __launch_bounds__(32 * GS_WARPS_MAX, 1)
         pc = pnx;
 #ifdef DPP_WS_PH
         ph[6] += 1;
+        if (lane == 0 && g_ws_hop && blockIdx.x == 0 && ci < GS_HOP_MAX) {
+            unsigned long long *o = g_ws_hop + ((size_t)wid * GS_HOP_MAX + ci) * 4;
+            o[0] = (unsigned long long)hd_lev; o[1] = hop1; o[2] = hop2; o[3] = hop3;
+        }
         {
             unsigned long long gt;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
@@ -1657,7 +1676,7 @@ __global__ void k_gs_fill(int n, int chunk, int chunkp, int zero_code, int nchun
         const int r = perm[q], owner = r / chunk;
         const int a0 = ptr[r], len = ptr[r + 1] - a0, pad = 4 * ngr - len;
         const int hs = hstart[owner], he = hstart[owner + 1];
-        if (lane == 0) *reinterpret_cast<int4 *>(B) = make_int4(ngr, w, np, 0);
+        if (lane == 0) *reinterpret_cast<int4 *>(B) = make_int4(ngr, w, np, lev[r]);   // .w: the chunk's level (instrumented builds)
         reinterpret_cast<unsigned short *>(B + 16)[lane] = (unsigned short)(r - owner * chunk);
         reinterpret_cast<double *>(B + gs_off_dq(w))[lane] = diag ? 1.0 / diag[r] : 1.0;
         const int p0 = rpp[q] - rpp[q0], pn = rpp[q + 1] - rpp[q];
@@ -2241,7 +2260,7 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
         cfg.dynamicSmemBytes = gs_smem(P.chunk, P.hmax);
 #ifdef DPP_WS_PH
         static const char *ph_pathw = std::getenv("DPP_WS_PH");
-        unsigned long long *phw = nullptr;
+        unsigned long long *phw = nullptr, *hopb = nullptr;
         const size_t nphw = (size_t)P.C * T.ncomp * (P.threads / 32) * 8;
         cudaEvent_t pe0w = nullptr, pe1w = nullptr;
         if (ph_pathw && *ph_pathw && !c->capturing) {
@@ -2249,6 +2268,9 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
             CK(cudaMalloc((void **)&phw, nphw * 8));
             CK(cudaMemset(phw, 0, nphw * 8));
             CK(cudaMemcpyToSymbol(g_ws_ph, &phw, sizeof(phw)));
+            CK(cudaMalloc((void **)&hopb, sizeof(unsigned long long) * 32 * GS_HOP_MAX * 4));
+            CK(cudaMemset(hopb, 0, sizeof(unsigned long long) * 32 * GS_HOP_MAX * 4));
+            CK(cudaMemcpyToSymbol(g_ws_hop, &hopb, sizeof(hopb)));
             cudaEventCreate(&pe0w); cudaEventCreate(&pe1w);
             cudaEventRecord(pe0w, st);
         }
@@ -2282,6 +2304,22 @@ void trsv_push(Ctx *c, const Tri &T, const double *b, double *x, const double *x
             cudaFree(phw);
             if (FILE *f = std::fopen(ph_pathw, "a")) {
                 const int nwv = P.threads / 32;
+                {
+                    std::vector<unsigned long long> hh((size_t)32 * GS_HOP_MAX * 4);
+                    CK(cudaMemcpy(hh.data(), hopb, hh.size() * 8, cudaMemcpyDeviceToHost));
+                    unsigned long long *zz = nullptr;
+                    CK(cudaMemcpyToSymbol(g_ws_hop, &zz, sizeof(zz)));
+                    cudaFree(hopb);
+                    std::string hp = std::string(ph_pathw) + ".hop";
+                    if (FILE *fh = std::fopen(hp.c_str(), "a")) {
+                        std::fprintf(fh, "# gs n=%d C=%d ncomp=%d L=%d warps=%d\n", T.n, P.C, T.ncomp, P.L, nwv);
+                        for (size_t i = 0; i < hh.size() / 4; ++i)
+                            if (hh[i * 4 + 3])
+                                std::fprintf(fh, "%zu %zu %llu %llu %llu %llu\n", i / GS_HOP_MAX, i % GS_HOP_MAX, hh[i * 4],
+                                             hh[i * 4 + 1], hh[i * 4 + 2], hh[i * 4 + 3]);
+                        std::fclose(fh);
+                    }
+                }
                 std::fprintf(f, "# gs n=%d C=%d ncomp=%d L=%d warps=%d us=%.2f\n", T.n, P.C, T.ncomp, P.L, nwv, ms * 1e3);
                 for (size_t i = 0; i < nphw / 8; ++i) {
                     const unsigned long long *o = &h[i * 8];

@@ -1,5 +1,4 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
-DPP_TRACE=1 TRACE_STEPS=3 timeout 300 python tools/trace_step.py 2>&1 | grep -E "tail_collapse|^step" | tail -6
-timeout 300 python tools/ws_check.py 16 "DPP_AMG_TAIL=0" "X=0" 2>&1 | tail -2
-bash tools/bench3.sh
+bash tools/ab_pc.sh "X=0" "X=1"
+timeout 300 python tools/ws_check.py 16 "DPP_PU_MODE=flow" "X=0" "DPP_GS_MIN_CLUSTERS=2" 2>&1 | tail -3
