@@ -294,6 +294,8 @@ DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
     // the facet arrays (80 % of the image for TET meshes) follow only when a formulation uses them
     const Part fparts[7] = {pcf, pfv, pfp, pfm, pcs, pfn, pfs};
     for (int q = 0; q < 7; ++q) { d->foff[q] = fparts[q].off; d->fbytes[q] = fparts[q].bytes; }
+    // cell Jacobian inverses for the trace / field queries; every assembly recomputes them inside
+    // its own timing, as the reference does (assembly.py:154-158)
     d->Jinv.alloc((size_t)d->C * d->dim * d->dim, c->s);
     if (d->C) {
         k_geom<<<grid_for(d->C, 128, c->sms), 128, 0, c->s>>>(d->C, d->dim, d->kind, d->nn, d->verts.p,
@@ -1677,6 +1679,10 @@ int dpp_assemble_ext(dpp_ctx *ctx, dpp_mesh *mm, int formulation, const dpp_para
             mp = &dev_mesh(c, hm);
         }
         DevMesh &m = *mp;
+        if (m.C) {   // cell geometry, inside the assembly's own timing
+            k_geom<<<grid_for(m.C, 128, c->sms), 128, 0, c->s>>>(m.C, m.dim, m.kind, m.nn, m.verts.p, m.cells.p, m.Jinv.p);
+            launched(c);
+        }
         auto S = std::make_unique<dpp_system>();
         S->ctx = c;
         if (formulation == DPP_HDIV) {
