@@ -1,4 +1,3 @@
 #!/bin/bash
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
-bash tools/ab_pc.sh "X=0" "X=1"
-timeout 300 python tools/ws_check.py 16 "DPP_PU_MODE=flow" "X=0" "DPP_GS_MIN_CLUSTERS=2" 2>&1 | tail -3
+for e in "X=0" "DPP_AGG_DEV_MIN=2048" "DPP_AGG_DEV_MIN=512" "X=1" "DPP_AGG_DEV_MIN=2048"; do echo "== $e"; env $e timeout 600 python bench.py --steps 8 --warmup 3 --no-cpu-baseline --no-c3 --no-c4 --no-fast 2>/dev/null | tail -1 | python -c "import sys,json; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['config']['ksp'])"; done
