@@ -494,7 +494,7 @@ def main():
         "data": "synthetic (structured mesh + manufactured solution, as the reference)",
         "config": {"workload": CONFIG["workload"], "dof": r["dof"], "ksp": r["its"][-1],
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "l2": "inputs (K 405 MB stored) larger than L2; roofline profile flushes L2"},
+                   "l2": "inputs (K 405 MB stored) larger than L2; roofline profile flushes L2 between launches (256 MiB written, then read back so no write-backs drain into the timed kernel)"},
         "gpu_launches": int(r["launches"] / max(args.steps, 1)),
         "clocks": r["clocks"],
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -31,6 +31,17 @@ static dpp_csr *borrow(Ctx *c, const Csr &A) {
     return &v->h;
 }
 
+// reads n 16-byte words and keeps the compiler from dropping the loads (the store never happens
+// for a memset pattern): the read half of dpp_profile_step's L2 flush
+__global__ void k_read_sink(const int4 *p, size_t n, int *sink) {
+    int acc = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const int4 v = p[i];
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x5a5a5a5b) *sink = acc;
+}
+
 extern "C" {
 
 const char *dpp_last_error(void) { return last_error_ref().c_str(); }
@@ -467,6 +478,14 @@ int dpp_solve(dpp_ctx *ctx, dpp_system *s, dpp_pc *pc, double rtol, int max_iter
 int dpp_profile_step(dpp_ctx *ctx, dpp_system *s, dpp_pc *pc, int reps, int flush_l2,
                      dpp_step_profile *out) {
     return guard([&] {
+        // L2 flush between timed launches: 256 MiB written, then read back -- the read pass evicts the
+        // dirty lines the write left behind, so the timed kernel starts on a cold *and clean* L2 (with
+        // only the write, ~120 MB of write-backs drained during the 50 us SpMV and inflated it by ~10 us)
+        auto flush = [&](Ctx *c, char *junk, size_t fl, int v) {
+            if (!fl) return;
+            CK(cudaMemsetAsync(junk, v & 0xff, fl, c->s));
+            k_read_sink<<<c->sms * 8, 256, 0, c->s>>>(reinterpret_cast<const int4 *>(junk), fl / 16, (int *)junk);
+        };
         Ctx *c = &ctx->c;
         const Csr &Kc = system_Kc(c, s);
         const int64_t n = Kc.rows;
@@ -483,7 +502,7 @@ int dpp_profile_step(dpp_ctx *ctx, dpp_system *s, dpp_pc *pc, int reps, int flus
         pc_apply_dev(pc, pc_in(pc), pc_out(pc));
         CK(cudaStreamSynchronize(c->s));
         for (int r = 0; r < reps; ++r) {
-            if (fl) CK(cudaMemsetAsync(junk.p, r & 0xff, fl, c->s));
+            flush(c, junk.p, fl, r);
             CK(cudaEventRecord(a, c->s));
             spmv(c, Kc, x.p, pc_in(pc));
             CK(cudaEventRecord(b, c->s));
@@ -491,7 +510,7 @@ int dpp_profile_step(dpp_ctx *ctx, dpp_system *s, dpp_pc *pc, int reps, int flus
             float ms;
             CK(cudaEventElapsedTime(&ms, a, b));
             t_spmv += ms;
-            if (fl) CK(cudaMemsetAsync(junk.p, (r + 1) & 0xff, fl, c->s));
+            flush(c, junk.p, fl, r + 1);
             CK(cudaEventRecord(a, c->s));
             pc_apply_dev(pc, pc_in(pc), pc_out(pc));
             CK(cudaEventRecord(b, c->s));
