@@ -1758,7 +1758,7 @@ bool try_push(Ctx *c, Tri &T, const DBuf<int> &lev, int L, int C) {
     const int chunk = (n + C - 1) / C;
     const int nblk = C * L;
     if (chunk >= (1 << 16)) return false;   // local row index in 16 bits of the row header
-    if (C > 16 && gs_smem(chunk, 1024) > PU_SMEM_LIMIT) return false;   // before any work: the x slice alone is too large
+    if (p16(8LL * chunk) + 8192 > (long long)PU_SMEM_LIMIT) return false;   // before any work: the x slice alone is too large
     const Csr &S = T.strict;
     // rows grouped by (owner CTA, level)
     DBuf<int> key(n, c->s), skey(n, c->s), rows(n, c->s), perm(n, c->s), lp((size_t)nblk + 1, c->s);

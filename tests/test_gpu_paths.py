@@ -14,6 +14,8 @@ bars: solution within 1e-9 relative, iterations within +-2.
   DPP_PU_MODE=ws              warp-stream sweeps (lane per row, per-warp TMA rings) everywhere
   DPP_AMG_TAIL=0              launch-by-launch V-cycle on the small tail levels (no dense collapse)
   DPP_SGS_PLAIN=1             Gauss-Seidel half-sweeps with the literal residual b - A x (four SpMVs per level)
+  DPP_BD_MAX=0 DPP_GBD_ROW=1  global block-dense sweeps (two launches per 512-row block) on the first AMG level
+  DPP_BD_INV=sparse           diagonal-block / dense-level inverses by sparse substitution (not the blocked GEMMs)
   DPP_PU_MODE=lvl             level-mbarrier cluster sweeps (k_trsv_lvl: level teams, SELL chunks)
   DPP_PU_FLOW=0               level-synchronous push-exchange cluster sweeps (k_trsv_push)
   DPP_NO_PUSH=1               barrier-per-level cluster sweeps (tricluster.cu)
@@ -55,6 +57,8 @@ VARIANTS = {
     "warp_stream": {"DPP_PU_MODE": "ws"},
     "no_tail_collapse": {"DPP_AMG_TAIL": "0"},
     "plain_sgs_residuals": {"DPP_SGS_PLAIN": "1"},
+    "global_block_dense": {"DPP_BD_MAX": "0", "DPP_GBD_ROW": "1"},
+    "sparse_block_inverses": {"DPP_BD_INV": "sparse"},
     "level_mbarrier": {"DPP_PU_MODE": "lvl"},
     "level_sync_push": {"DPP_PU_FLOW": "0"},
     "pull_cluster": {"DPP_NO_PUSH": "1"},
