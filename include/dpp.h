@@ -82,6 +82,12 @@ int dpp_csr_plan(dpp_csr *A, int kind);
 
 /* ---- mesh (mesh.py:73-277): numbering is bit-exact with the reference ----- */
 int dpp_mesh_generate(int dim, int kind, int n_div, dpp_mesh **out);
+/* generate_unit_mesh (mesh.py:206-277) with _build_facets / _facet_geometry / jacobians
+ * (mesh.py:106-185) run on the device: vertices, cells, the facet sort-unique (radix sorts of
+ * packed sorted-vertex keys), cell / facet adjacency, normals, measures and J are built in HBM
+ * (the mesh's device image) and the host arrays are read back from it; same arrays bit for bit
+ * as dpp_mesh_generate.  The mesh is bound to ctx's device. */
+int dpp_mesh_generate_device(dpp_ctx *ctx, int dim, int kind, int n_div, dpp_mesh **out);
 int dpp_mesh_from_arrays(int dim, int kind, int n_div, int64_t n_vertices,
                          const double *vertices_host, int64_t n_cells, const int64_t *cells_host,
                          dpp_mesh **out);

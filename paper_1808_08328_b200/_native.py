@@ -78,6 +78,7 @@ SIGNATURES = {
     "dpp_spmv": [P, P, P, P],
     "dpp_csr_plan": [P, I32],
     "dpp_mesh_generate": [I32, I32, I32, PP],
+    "dpp_mesh_generate_device": [P, I32, I32, I32, PP],
     "dpp_mesh_from_arrays": [I32, I32, I32, I64, P, I64, P, PP],
     "dpp_mesh_counts": [P, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)],
     "dpp_mesh_export": [P] + [P] * 11,

@@ -296,15 +296,17 @@ DevMesh &dev_mesh(Ctx *c, HostMesh &m) {
     for (int q = 0; q < 7; ++q) { d->foff[q] = fparts[q].off; d->fbytes[q] = fparts[q].bytes; }
     // cell Jacobian inverses for the trace / field queries; every assembly recomputes them inside
     // its own timing, as the reference does (assembly.py:154-158)
-    d->Jinv.alloc((size_t)d->C * d->dim * d->dim, c->s);
-    if (d->C) {
-        k_geom<<<grid_for(d->C, 128, c->sms), 128, 0, c->s>>>(d->C, d->dim, d->kind, d->nn, d->verts.p,
-                                                           d->cells.p, d->Jinv.p);
-        launched(c);
-    }
+    cell_jinv(c, *d);
     CK(cudaStreamSynchronize(c->s));
     m.dev = d;
     return *d;
+}
+
+void cell_jinv(Ctx *c, DevMesh &d) {
+    if (d.Jinv.n != (size_t)d.C * d.dim * d.dim) d.Jinv.alloc((size_t)d.C * d.dim * d.dim, c->s);
+    if (!d.C) return;
+    k_geom<<<grid_for(d.C, 128, c->sms), 128, 0, c->s>>>(d.C, d.dim, d.kind, d.nn, d.verts.p, d.cells.p, d.Jinv.p);
+    launched(c);
 }
 
 void ensure_facets(Ctx *c, HostMesh &hm, DevMesh &d) {

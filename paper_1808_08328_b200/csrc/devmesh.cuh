@@ -22,6 +22,10 @@ struct DevMesh {
 DevMesh &dev_mesh(Ctx *c, HostMesh &m);
 // facet arrays (H(div), DG-VMS, facet queries; CG-VMS assembly needs none)
 void ensure_facets(Ctx *c, HostMesh &hm, DevMesh &d);
+// cell Jacobian inverses (numpy.linalg.inv roundings) from the device vertices / cells
+void cell_jinv(Ctx *c, DevMesh &d);
+// the whole structured mesh built in HBM (devmesh.cu); the host arrays are read back from it
+void generate_on_device(Ctx *c, HostMesh &m, int dim, int kind, int n);
 
 }  // namespace dpp
 

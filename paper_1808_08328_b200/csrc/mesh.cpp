@@ -45,7 +45,7 @@ int local_facet(int kind, int f, int k) {
 }
 
 // numpy.linalg.det of a small matrix (row-major, modified in place)
-static double np_det(double *a, int d) {
+double np_det(double *a, int d) {
     double sign = 1.0;
     for (int k = 0; k < d; ++k) {
         int p = k;

@@ -37,5 +37,7 @@ int kind_nodes(int kind);
 int kind_facets(int kind);
 int kind_facet_nodes(int kind);
 int local_facet(int kind, int f, int k);
+// numpy.linalg.det of a d x d matrix (row-major, destroyed): getrf + sign * exp(sum log|u_ii|)
+double np_det(double *a, int d);
 
 }  // namespace dpp

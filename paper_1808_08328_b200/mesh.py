@@ -1,14 +1,17 @@
 """Structured meshes (drop-in for dppflow.mesh, reference mesh.py).
 
-Numbering is produced by libdpp's native mesh builder (csrc/mesh.cpp) and is
-bit-exact with the reference (mesh.py:206-277, :106-167); the Mesh object
-exposes the same numpy arrays and keeps the native handle that the device
-assembler uploads to HBM.
+Numbering is produced by libdpp -- on the device (csrc/devmesh.cu: closed-form
+vertices / cells, radix-sorted facet tuples, adjacency and geometry kernels) or,
+without a GPU or for user-supplied cells, by the host builder (csrc/mesh.cpp) --
+and is bit-exact with the reference (mesh.py:206-277, :106-167); the Mesh object
+exposes the same numpy arrays and keeps the native handle whose device image the
+assembler reads.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from enum import Enum
 
@@ -165,8 +168,39 @@ def generate_unit_mesh(dim: int, cell_kind, n_div: int) -> Mesh:
     if cell_kind.dim != dim:
         raise ValueError(f"cell kind {cell_kind.value} is {cell_kind.dim}D, requested dim={dim}")
     h = C.c_void_p()
-    N.call("dpp_mesh_generate", dim, N.KINDS[cell_kind.value], n_div, C.byref(h))
+    ctx = _mesh_ctx()
+    if ctx is not None:
+        # built in HBM (csrc/devmesh.cu); the numpy arrays are read back from the device image
+        N.call("dpp_mesh_generate_device", ctx, dim, N.KINDS[cell_kind.value], n_div, C.byref(h))
+    else:
+        N.call("dpp_mesh_generate", dim, N.KINDS[cell_kind.value], n_div, C.byref(h))
     return Mesh(dim, cell_kind, n_div, None, None, _handle=h)
+
+
+def _mesh_ctx():
+    """Where generate_unit_mesh numbers the mesh: $DPP_MESH = device | host | auto (default).
+
+    auto: on the device when there is one; a box without a GPU can still number a mesh with the
+    host builder (csrc/mesh.cpp, the same arrays bit for bit) -- assembling it needs the device.
+    """
+    mode = os.environ.get("DPP_MESH", "auto")
+    if mode == "host":
+        return None
+    if mode not in ("auto", "device"):
+        raise ValueError(f"DPP_MESH={mode!r}: expected device, host or auto")
+    global _NO_DEVICE
+    if mode == "auto" and _NO_DEVICE:
+        return None
+    try:
+        return N.ctx()
+    except N.DeviceUnavailable:
+        if mode == "device":
+            raise
+        _NO_DEVICE = True
+        return None
+
+
+_NO_DEVICE = False
 
 
 def facet_adjacency(mesh: Mesh):
