@@ -253,6 +253,29 @@ int dpp_gmres(dpp_ctx *ctx, const dpp_csr *A, dpp_apply_fn A_cb, void *A_user, d
 int dpp_solve(dpp_ctx *ctx, dpp_system *s, dpp_pc *pc, double rtol, int max_iter, int restart,
               double *x_host, dpp_krylov_stats *stats, double *history_host, int history_cap);
 
+/* ---- row-sharded SpMV over NVLink peer memory (NON-PARITY extension) ----
+ * The reference's SpMV is scipy's csr_matvec on the whole matrix (linalg.py:27-32).  Here rank p
+ * (one process per GPU) owns a contiguous row block of K and the matching slice of every vector;
+ * slices live in IPC-exportable buffers that the other ranks map, and the SpMV kernel loads
+ * off-rank entries of x directly through the peer mappings (no all-gather, no halo copy).
+ * Columns are 32-bit codes: owner << 29 | offset in the owner's slice (<= 8 ranks).  Row sums are
+ * lane-parallel: equal to csr_matvec up to the order of additions, so outside the parity contract. */
+typedef struct dpp_peerbuf dpp_peerbuf;
+typedef struct dpp_shard dpp_shard;
+int dpp_peerbuf_create(dpp_ctx *ctx, int64_t n, dpp_peerbuf **out);
+int dpp_peerbuf_export(const dpp_peerbuf *b, unsigned char *handle64);       /* cudaIpcMemHandle_t */
+int dpp_peerbuf_open(dpp_ctx *ctx, const unsigned char *handle64, int64_t n, dpp_peerbuf **out);
+int dpp_peerbuf_write(dpp_peerbuf *b, const double *host, int64_t n);
+int dpp_peerbuf_read(const dpp_peerbuf *b, double *host, int64_t n);
+int dpp_peerbuf_destroy(dpp_peerbuf *b);
+int dpp_shard_create(dpp_ctx *ctx, int rows, int64_t nnz, const int32_t *indptr, const uint32_t *codes,
+                     const double *values, int nseg, const int64_t *seg_len, dpp_shard **out);
+/* y[0:rows] = K[rows of this rank, :] x, x given as nseg slices (own buffer or mapped peers) */
+int dpp_shard_spmv(dpp_ctx *ctx, const dpp_shard *sh, dpp_peerbuf *const *xseg, dpp_peerbuf *y);
+int dpp_shard_profile(dpp_ctx *ctx, const dpp_shard *sh, dpp_peerbuf *const *xseg, dpp_peerbuf *y, int reps,
+                      double *ms_per_call, double *bytes_per_call);
+int dpp_shard_destroy(dpp_shard *sh);
+
 /* ---- measurement: CUDA-event timing of the Arnoldi-step kernels ----------- */
 typedef struct {
     double spmv_ms, pc_ms;           /* mean per call over reps */

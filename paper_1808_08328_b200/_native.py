@@ -121,6 +121,16 @@ SIGNATURES = {
     "dpp_gmres": [P, P, APPLY_FN, P, P, APPLY_FN, P, I64, P, P, P, D, I32, I32,
                   C.POINTER(KrylovStatsC), P, I32],
     "dpp_solve": [P, P, P, D, I32, I32, P, C.POINTER(KrylovStatsC), P, I32],
+    "dpp_peerbuf_create": [P, I64, PP],
+    "dpp_peerbuf_export": [P, P],
+    "dpp_peerbuf_open": [P, P, I64, PP],
+    "dpp_peerbuf_write": [P, P, I64],
+    "dpp_peerbuf_read": [P, P, I64],
+    "dpp_peerbuf_destroy": [P],
+    "dpp_shard_create": [P, I32, I64, P, P, P, I32, P, PP],
+    "dpp_shard_spmv": [P, P, C.POINTER(P), P],
+    "dpp_shard_profile": [P, P, C.POINTER(P), P, I32, C.POINTER(D), C.POINTER(D)],
+    "dpp_shard_destroy": [P],
     "dpp_profile_step": [P, P, P, I32, I32, C.POINTER(StepProfile)],
 }
 
