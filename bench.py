@@ -27,7 +27,8 @@ torchrun environment re-launches itself under torch.distributed.run (N replicas)
 The line also carries BASELINE config 3 as stated (c3_solve: per-cell permeability + no-flow
 walls, the extension; --no-c3 skips it) and the config-4 sweep (DG-VMS TET 32^3: 100 SpMV +
 100 PC applies, c4_sweep; --no-c4 skips it) and, labelled NON-PARITY, the same C2 step with
-the preconditioner's triangular solves as Jacobi sweeps (fast_mode; --no-fast skips it).
+the preconditioner's triangular solves as Jacobi sweeps (fast_mode; --no-fast skips it), and the
+SURVEY 8(f) components measured on C2 (mesh_generate, sharded_spmv; --no-extras skips them).
 """
 
 from __future__ import annotations
@@ -347,6 +348,60 @@ def c4_sweep():
     return out
 
 
+def extras():
+    """SURVEY 8(f) components next to the hot path, measured on the metric's config (C2):
+    mesh numbering on the device against the host builder (outside the reference's timed region;
+    both include the read-back / export of the numpy arrays), and the row-sharded SpMV kernel
+    (NON-PARITY extension) with all four shards of K on this one GPU."""
+    import ctypes as C
+
+    import scipy.sparse as sp
+
+    import paper_1808_08328_b200 as dpp
+    from paper_1808_08328_b200 import _native as N
+    from paper_1808_08328_b200 import sharded as S
+    from paper_1808_08328_b200.mesh import Mesh
+    cfg = CONFIG
+    kind = N.KINDS[cfg["kind"]]
+    t = {"device": [], "host": []}
+    for _ in range(3):
+        for name, fn, args in (("device", "dpp_mesh_generate_device", (N.ctx(),)), ("host", "dpp_mesh_generate", ())):
+            h = C.c_void_p()
+            t0 = time.perf_counter()
+            N.call(fn, *args, cfg["dim"], kind, cfg["n"], C.byref(h))
+            m = Mesh(cfg["dim"], cfg["kind"], cfg["n"], None, None, _handle=h)
+            t[name].append(1e3 * (time.perf_counter() - t0))
+            del m
+    out = {"mesh_generate": {"workload": f"{cfg['kind']} {cfg['n']}^{cfg['dim']} mesh, arrays exported to numpy",
+                             "device_ms": min(t["device"]), "host_builder_ms": min(t["host"])}}
+    p = dpp.DppParameters(k2=cfg["k2"], gamma_b=(0.0, 0.0, 0.0))
+    mesh = dpp.generate_unit_mesh(cfg["dim"], cfg["kind"], cfg["n"])
+    bs = dpp.assemble(mesh, cfg["formulation"], p, dpp.boundary_data(dpp.manufactured_solution(cfg["dim"], p), mesh))
+    K = sp.csr_matrix(dpp.monolithic_view(bs)[0])
+    K.eliminate_zeros()
+    x = np.random.default_rng(0).standard_normal(K.shape[0])
+    peak, _ = measured_peak()
+    out["sharded_spmv"] = {
+        "label": "NON-PARITY extension: row-sharded SpMV(K), off-rank x read through peer mappings; "
+                 "4 shards on this one GPU, launched one after another", "ranks": 4}
+    orders = {"field_major": None,
+              "node_interleaved": S.node_interleaved_order(bs.device().sizes, (cfg["dim"], 1, cfg["dim"], 1))}
+    for name, perm in orders.items():
+        op = S.LocalShards(K, 4, perm=perm)
+        err = float(np.abs(op.matvec(x) - K @ x).max() / np.abs(K).dot(np.abs(x)).max())
+        if not err <= 1e-13:
+            raise SystemExit(f"bench: sharded SpMV ({name}) differs from csr_matvec by {err:.2e}")
+        prof = op.profile(reps=50)
+        out["sharded_spmv"][name] = {
+            "rel_err_vs_csr_matvec": err,
+            "ms_per_shard": [a for a, _ in prof],
+            "gbs_per_shard": [b / a / 1e6 for a, b in prof],
+            "frac_of_peak_min": min(b / a / 1e6 for a, b in prof) / peak,
+            "off_rank_entry_share": [pl.halo_entries / max(len(pl.values), 1) for pl in op.plans]}
+        del op
+    return out
+
+
 def _sizes(sysh):
     import ctypes as C
 
@@ -437,6 +492,7 @@ def main():
     ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c4", action="store_true", help="skip the config-4 SpMV / PC-apply sweep")
+    ap.add_argument("--no-extras", action="store_true", help="skip the mesh-generation / sharded-SpMV fields")
     ap.add_argument("--no-c3", action="store_true", help="skip the config-3 solve")
     ap.add_argument("--no-fast", action="store_true", help="skip the non-parity fast-mode C2 step")
     args = ap.parse_args()
@@ -514,6 +570,8 @@ def main():
         line["c3_solve"] = c3_solve()
     if not args.no_c4 and world == 1:
         line["c4_sweep"] = c4_sweep()
+    if not args.no_extras and world == 1:
+        line.update(extras())
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline()
     print(json.dumps(line))

@@ -49,6 +49,28 @@ def partition_rows(indptr, world: int) -> np.ndarray:
     return starts
 
 
+def node_interleaved_order(sizes, per_node) -> np.ndarray:
+    """perm[new] = old index: the DoFs of node v of every field next to each other.
+
+    The reference orders K field by field, (u1, p1, u2, p2) (assembly.py:102-108), so a contiguous
+    row block holds one field of the whole mesh and most of its columns belong to other ranks.
+    For nodal formulations (CG-VMS: per_node = (dim, 1, dim, 1), velocity DoF = node * dim +
+    component) this order makes a row block a slab of the mesh and only the slab faces couple
+    ranks.  Apply it as K[perm][:, perm]; vectors permute the same way (x_new = x[perm]).
+    """
+    sizes = [int(n) for n in sizes]
+    per_node = [int(k) for k in per_node]
+    if len(sizes) != len(per_node) or any(k < 1 for k in per_node):
+        raise ValueError("one positive DoF count per node for every field")
+    nodes = {n // k for n, k in zip(sizes, per_node)}
+    if len(nodes) != 1 or any(n % k for n, k in zip(sizes, per_node)):
+        raise ValueError("fields do not share one node set (not a nodal formulation)")
+    V = nodes.pop()
+    off = np.concatenate(([0], np.cumsum(sizes)[:-1]))
+    cols = [off[f] + np.arange(V)[:, None] * k + np.arange(k)[None, :] for f, k in enumerate(per_node)]
+    return np.concatenate(cols, axis=1).ravel().astype(np.int64)
+
+
 def encode_columns(indices, starts) -> np.ndarray:
     """uint32 codes `owner << 29 | offset in the owner's slice` for global column indices."""
     starts = np.asarray(starts, dtype=np.int64)
@@ -177,11 +199,17 @@ class ShardedOperator:
     builds this rank's shard and maps every peer's x slice; without a group it is the
     single-rank operator.  Every rank passes the same global matrix (or one with at least its own
     rows filled: only rows [starts[rank], starts[rank+1]) are read when `starts` is given).
+    With `perm` the operator is K[perm][:, perm] and every slice is in that ordering.
     """
 
-    def __init__(self, A, group=None, starts=None):
+    def __init__(self, A, group=None, starts=None, perm=None):
         self.group = group
         self.rank, self.world = _rank_world(group)
+        if perm is not None:
+            perm = np.asarray(perm, dtype=np.int64)
+            A = sp.csr_matrix(sp.csr_matrix(A)[perm][:, perm])
+            A.sort_indices()
+        self.perm = perm
         self.plan = ShardPlan.from_global(A, self.rank, self.world, starts)
         self.shard = _DeviceShard(self.plan)
         seg = self.plan.seg_len()
@@ -235,10 +263,16 @@ class LocalShards:
 
     For checking the plan and the kernel where only one GPU is at hand, and for timing the kernel
     with its coded-column loads; launches run one after another and never wait on one another.
+    `perm` (e.g. `node_interleaved_order`) reorders the operator first; `matvec` still takes and
+    returns vectors in the caller's ordering.
     """
 
-    def __init__(self, A, world: int, starts=None):
+    def __init__(self, A, world: int, starts=None, perm=None):
         A = sp.csr_matrix(A)
+        self.perm = None if perm is None else np.asarray(perm, dtype=np.int64)
+        if self.perm is not None:
+            A = sp.csr_matrix(A[self.perm][:, self.perm])
+            A.sort_indices()
         self.world = world
         self.plans = [ShardPlan.from_global(A, p, world, starts) for p in range(world)]
         self.starts = self.plans[0].starts
@@ -249,9 +283,16 @@ class LocalShards:
         x = N.f64(x)
         if x.shape != (int(self.starts[-1]),):
             raise ValueError(f"dimension mismatch: {x.shape}")
+        if self.perm is not None:
+            x = np.ascontiguousarray(x[self.perm])
         for p, b in enumerate(self.xsegs):
             b.write(x[self.starts[p]:self.starts[p + 1]])
-        return np.concatenate([s.spmv(self.xsegs).read(s.plan.rows) for s in self.shards])
+        y = np.concatenate([s.spmv(self.xsegs).read(s.plan.rows) for s in self.shards])
+        if self.perm is not None:
+            out = np.empty_like(y)
+            out[self.perm] = y
+            return out
+        return y
 
     def profile(self, reps=20):
         return [s.profile(self.xsegs, reps) for s in self.shards]

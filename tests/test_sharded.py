@@ -97,6 +97,17 @@ def test_plans_reassemble_the_product(world):
         S.ShardPlan.from_global(A, 2, 2)
 
 
+def test_node_interleaved_order_groups_a_nodes_dofs():
+    perm = S.node_interleaved_order([6, 3, 6, 3], (2, 1, 2, 1))     # 3 nodes, dim 2
+    assert sorted(perm.tolist()) == list(range(18))
+    assert perm[:6].tolist() == [0, 1, 6, 9, 10, 15]                # node 0: u1x u1y p1 u2x u2y p2
+    assert perm[6:12].tolist() == [2, 3, 7, 11, 12, 16]
+    with pytest.raises(ValueError):
+        S.node_interleaved_order([6, 4, 6, 3], (2, 1, 2, 1))
+    with pytest.raises(ValueError):
+        S.node_interleaved_order([6, 3], (2, 1, 2))
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -202,6 +213,13 @@ def test_sharded_k_of_an_assembled_system():
     assert np.abs(op.matvec(x) - K @ x).max() <= _bound(K, x)
     for ms, by in op.profile(reps=5):
         assert ms > 0 and by > 0
+    # node-interleaved ordering: row blocks become slabs of the mesh, far fewer off-rank entries
+    sizes = bs.device().sizes
+    opi = S.LocalShards(K, 4, perm=S.node_interleaved_order(sizes, (3, 1, 3, 1)))
+    assert np.abs(opi.matvec(x) - K @ x).max() <= _bound(K, x)
+    off = sum(pl.halo_entries for pl in op.plans) / K.nnz
+    offi = sum(pl.halo_entries for pl in opi.plans) / K.nnz
+    assert offi < 0.25 * off, (off, offi)
 
 
 @pytest.mark.gpu

@@ -5,9 +5,9 @@
 #   3. full capture of the dominant kernels (push sweeps, block-dense sweep, SpMV)
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "bench rc=$?"
-python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-c3 --no-c4 --no-fast > gpurun_out/prof_bench_plain.log 2>&1 && \
+python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-c3 --no-c4 --no-fast --no-extras > gpurun_out/prof_bench_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/bench_launches.csv \
-    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-c3 --no-c4 --no-fast > gpurun_out/prof_bench_ncu.log 2>&1
+    python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-c3 --no-c4 --no-fast --no-extras > gpurun_out/prof_bench_ncu.log 2>&1
 echo "launch list rc=$?"
 PROF_REPS=1 python tools/prof_pc.py > gpurun_out/prof_pc_plain.log 2>&1 && \
 PROF_REPS=1 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \

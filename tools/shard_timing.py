@@ -17,12 +17,13 @@ K.eliminate_zeros()            # the zero-free K the SELL plan stores too
 x = np.random.default_rng(0).standard_normal(K.shape[0])
 ref = K @ x
 print(f"K: {K.shape[0]} rows, {K.nnz} entries")
-for world in (1, 2, 4, 8):
-    op = S.LocalShards(K, world)
+perm = S.node_interleaved_order(bs.device().sizes, (3, 1, 3, 1))
+for world, pm in [(w, q) for q in (None, perm) for w in (1, 2, 4, 8)]:
+    op = S.LocalShards(K, world, perm=pm)
     err = np.abs(op.matvec(x) - ref).max() / np.abs(K).dot(np.abs(x)).max()
     prof = op.profile(reps=50)
     halo = [pl.halo_entries / max(len(pl.values), 1) for pl in op.plans]
     ms = [a for a, _ in prof]
     gbs = [b / a / 1e6 for a, b in prof]
-    print(f"world {world}: err {err:.1e}  ms/launch max {max(ms):.4f}  GB/s per shard {min(gbs):.0f}-{max(gbs):.0f}"
+    print(f"{'field-major' if pm is None else 'node-interleaved'} world {world}: err {err:.1e}  ms/launch max {max(ms):.4f}  GB/s per shard {min(gbs):.0f}-{max(gbs):.0f}"
           f"  off-rank entries {100 * min(halo):.1f}-{100 * max(halo):.1f} %  rows {np.diff(op.starts).tolist()}")
