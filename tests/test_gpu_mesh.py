@@ -85,6 +85,37 @@ def test_device_mesh_is_bitwise_the_host_builder(dim, kind, n):
           f"host {1e3 * (t2 - t1):.1f} ms")
 
 
+@pytest.mark.parametrize("dim,kind,n", [(2, "tri", 300), (2, "quad", 257), (3, "tet", 48), (3, "hex", 72)])
+def test_device_mesh_properties_beyond_the_config_sizes(dim, kind, n):
+    """Size-independent checks where no reference answer is at hand: closed-form counts, facets in
+    lexicographic order without duplicates, plus = lower cell, consistent cell <-> facet tables,
+    closed cells (sum of outward measure-weighted normals = 0) and det J = dim! x cell volume."""
+    m = device_mesh(dim, kind, n)
+    F = {"tri": 3 * n * n + 2 * n, "quad": 2 * n * (n + 1), "tet": 12 * n ** 3 + 6 * n * n,
+         "hex": 3 * n * n * (n + 1)}[kind]
+    nb = {"tri": 4 * n, "quad": 4 * n, "tet": 12 * n * n, "hex": 6 * n * n}[kind]
+    assert m.n_vertices == (n + 1) ** dim and m.n_facets == F and len(m.boundary_facets) == nb
+    fv = m.facet_vertex_ids
+    assert np.all(np.diff(fv, axis=1) > 0)                       # sorted tuples
+    order = np.lexsort(fv.T[::-1])
+    assert np.array_equal(order, np.arange(F))                   # lexicographic, hence unique ...
+    assert np.all(np.any(fv[1:] != fv[:-1], axis=1))             # ... and no duplicates
+    inner = m.facet_minus >= 0
+    assert np.all(m.facet_plus[inner] < m.facet_minus[inner])
+    nf = m.cell_facets.shape[1]
+    cells = np.repeat(np.arange(m.n_cells), nf)
+    cf, cs = m.cell_facets.ravel(), m.cell_facet_signs.ravel()
+    assert np.array_equal(m.facet_plus[cf[cs > 0]], cells[cs > 0])
+    assert np.array_equal(m.facet_minus[cf[cs < 0]], cells[cs < 0])
+    assert np.count_nonzero(cs > 0) == F and np.count_nonzero(cs < 0) == F - nb
+    flux = np.zeros((m.n_cells, dim))
+    np.add.at(flux, cells, (cs * m.facet_measures[cf])[:, None] * m.facet_normals[cf])
+    assert np.abs(flux).max() < 1e-14
+    J, det = m.jacobians()
+    ref = {"tri": 0.5, "quad": 1.0, "tet": 1.0 / 6.0, "hex": 1.0}[kind]
+    assert np.all(det > 0) and abs(det.sum() * ref - 1.0) < 1e-12   # the cells tile the unit domain
+
+
 def test_device_mesh_feeds_the_assembly_without_an_upload():
     """A device-generated mesh is already resident: the assembly uploads nothing for it and gives
     the blocks of the host-numbered mesh bit for bit (H(div) reads the facet arrays too)."""
