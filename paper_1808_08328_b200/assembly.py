@@ -104,7 +104,12 @@ class BlockSystem:
         return {"u1": self.f1_u, "p1": self.f1_p, "u2": self.f2_u, "p2": self.f2_p}
 
     def split_solution(self, x: np.ndarray) -> dict:
-        return {name: x[idx] for name, idx in self.index_sets().items()}
+        # the index sets are contiguous ranges: copies of slices (the reference's x[idx] also copies)
+        out, start = {}, 0
+        for name, n in self.field_sizes.items():
+            out[name] = np.array(x[start:start + n])
+            start += n
+        return out
 
     def device(self) -> DeviceSystem:
         """The HBM copy of this system (uploaded from the scipy blocks on first use)."""
